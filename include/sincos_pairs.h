@@ -1,0 +1,173 @@
+/*
+ * sincos_pairs.h -- C ABI of libsincos_pairs.so, the B200 (sm_100a) hot path of
+ *
+ *   M. H. Mendenhall, "A Fast, Vectorizable Algorithm for Producing
+ *   Single-Precision Sine-Cosine Pairs", arXiv cs/0406049.
+ *
+ * Problem statement: sine-cosine pairs "in random order, or for
+ * non-uniformly spaced values", a large number of them at once.  For every
+ * fp32 angle theta[i] (radians) the library computes the fp32 pair
+ * (sin theta[i], cos theta[i]) by the paper's method (Fig. 1
+ * P:262-362):
+ *   1. scale by 1/2pi and reduce onto [-1/2, 1/2] by rounding and subtraction
+ *      (round half to even, reading G4),
+ *   2. evaluate the quarter-angle series for (sin, cos)(pi q / 2) (P:72-75,
+ *      coefficients P:140-148 / P:159-167, Horner order of Fig. 1),
+ *   3. two angle doublings with Eq. (1): s' = 2sc, c' = c^2 - s^2,
+ *   4. the amplitude handling of the chosen variant, computed from the
+ *      penultimate pair (Fig. 1).
+ * Arithmetic: IEEE fp32, round-to-nearest-even, fused multiply-add exactly
+ * where Fig. 1 has vec_madd / vec_nmsub with a non-zero addend, no flush to
+ * zero.  Results are bit-identical to the paper's algorithm as restated in
+ * DESIGN.md (signed zeros and NaN payloads aside).  Every entry point is
+ * thread-safe and reentrant; none allocates device memory except where stated,
+ * none keeps a pointer after it returns.
+ *
+ * All pointers named *_dev are device pointers (cudaMalloc / torch CUDA
+ * tensors) of the CURRENT device; *_host are host pointers (page-locked
+ * memory recommended).  `stream` is a cudaStream_t (CUstream) passed as
+ * void*; NULL means the legacy default stream.  Work is enqueued
+ * asynchronously unless stated otherwise.
+ */
+#ifndef SINCOS_PAIRS_H
+#define SINCOS_PAIRS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Amplitude handling (the paper's two methods). */
+typedef enum {
+    /* Method 1: least-squares series for sin and cos, then the
+     * linear magnitude fix f = 2 - s2^2 - c2^2 of the penultimate pair
+     * (Fig. 1 FASTER_SINCOS). */
+    SINCOS_NORMALIZED = 0,
+    /* Method 2: series fitted to the angle (coefficients marked
+     * "dagger"; ss2 = -0.6466386396 of Fig. 1, reading G1), then the
+     * exact reciprocal f = RN(1/(s2^2 + c2^2)) of the penultimate pair's
+     * squared magnitude (Fig. 1; "precise reciprocal"). */
+    SINCOS_RENORMALIZED = 1
+} sincos_variant_t;
+
+typedef enum {
+    SINCOS_OK = 0,
+    SINCOS_ERR_INVALID_ARGUMENT = 1, /* NULL where a buffer is needed, both or neither output
+                                        form, unknown variant, misaligned (not 4-B) pointer  */
+    SINCOS_ERR_OVERLAP = 2,          /* outputs overlap each other or the input (other than
+                                        theta == sin_out or theta == cos_out exactly)        */
+    SINCOS_ERR_CUDA = 3              /* a CUDA call failed; see sincos_last_cuda_error()      */
+} sincos_status_t;
+
+/*
+ * sincos_pairs -- the hot path (one kernel launch).
+ *
+ *   theta_dev        n fp32 angles in radians, contiguous.
+ *   sin_dev, cos_dev split output: sin_dev[i], cos_dev[i]  (both non-NULL), or
+ *   inter_dev        interleaved output: inter_dev[2i] = cos, inter_dev[2i+1] = sin,
+ *                    i.e. one complex64 e^{i theta} per element (struct phase {c, s},
+ *                    P:262; reading G13).  Exactly one form must be given.
+ *   n                element count; 0 is a no-op (pointers may then be NULL).
+ *
+ * Any 4-B aligned pointers are accepted.  When theta and the outputs share
+ * their alignment the body runs 256-bit vector loads/stores; otherwise a
+ * scalar path with identical numerics.  theta_dev == sin_dev or
+ * theta_dev == cos_dev (exact in-place) is allowed.  Validation happens
+ * before any CUDA call; the return value reports validation and the launch
+ * status only (the kernel itself cannot fail short of invalid addresses).
+ */
+sincos_status_t sincos_pairs(const float *theta_dev, float *sin_dev, float *cos_dev,
+                             float *inter_dev, size_t n, sincos_variant_t variant, void *stream);
+
+/*
+ * sincos_pairs_host -- the same computation on HOST buffers, end to end:
+ * chunked host->device copies, the kernel and device->host copies pipelined
+ * over three internal streams (created once per device), so the copy engines
+ * run both directions while the kernel computes.  Synchronous: returns when
+ * the outputs are in host memory.  Ordered after prior work on `stream`.
+ *
+ *   dev_ws, ws_bytes  caller-owned device workspace of the current device
+ *                     (>= sincos_host_workspace_min_bytes(); more = larger chunks).
+ */
+sincos_status_t sincos_pairs_host(const float *theta_host, float *sin_host, float *cos_host,
+                                  float *inter_host, size_t n, sincos_variant_t variant,
+                                  void *dev_ws, size_t ws_bytes, void *stream);
+size_t sincos_host_workspace_min_bytes(void);
+
+/*
+ * Host-side sharding: element ranges [lo, hi) of shard g of
+ * nshards, contiguous, every shard start a multiple of 8 elements (32-B
+ * aligned in any aligned array); the last shard takes the remainder.  Pure
+ * function, no CUDA.  Returns 0, or -1 for nshards < 1 or g outside [0, nshards).
+ */
+int sincos_shard_range(size_t n, int nshards, int g, size_t *lo, size_t *hi);
+
+/* One shard resident on one device. */
+typedef struct {
+    int device;              /* CUDA device ordinal owning the buffers     */
+    const float *theta_dev;
+    float *sin_dev, *cos_dev, *inter_dev;
+    size_t n;
+    void *stream;            /* stream of that device (NULL = its legacy default) */
+} sincos_shard_t;
+
+/* Launch every shard on its own device (single process, many devices);
+ * no data crosses devices.  Restores the caller's current device. */
+sincos_status_t sincos_pairs_sharded(const sincos_shard_t *shards, int nshards,
+                                     sincos_variant_t variant);
+
+/*
+ * Per-shard error statistics (verification, not the hot path): for each element,
+ * the paper's metrics against an fp64 reference computed on the
+ * device: combined error sqrt((c - cos)^2 + (s - sin)^2), amplitude error
+ * |1 - sqrt(c^2 + s^2)|.  A 64-byte record, small enough to gather over NCCL.
+ * Reductions are deterministic (fixed grid, fixed order).
+ */
+typedef struct {
+    uint64_t n;            /* elements measured (finite outputs)          */
+    uint64_t nan_count;    /* output pairs holding a NaN                  */
+    double   max_comb;     /* max combined error                          */
+    double   sum_sq;       /* sum of combined error squared               */
+    double   max_amp;      /* max amplitude error                         */
+    double   kernel_ms;    /* filled in by the caller (timing), else 0     */
+    float    worst_theta;  /* an argument at max_comb                     */
+    uint32_t device;       /* filled in by the caller                     */
+    uint64_t reserved;
+} sincos_stats_t;
+
+size_t sincos_stats_workspace_bytes(void);
+/* stats_dev: device pointer to one sincos_stats_t; ws_dev: device workspace of
+ * sincos_stats_workspace_bytes(). */
+sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
+                                   const float *cos_dev, const float *inter_dev, size_t n,
+                                   sincos_stats_t *stats_dev, void *ws_dev, void *stream);
+
+/* Launch tuning (bench / tests): threads per block, resident blocks per SM
+ * for the grid-stride grid (0 = occupancy maximum), vector width in floats per
+ * thread access (4 or 8), unroll U (1, 2 or 4 independent vectors in flight
+ * per thread: the GPU form of "computes two vectors at a time").
+ * Process-global; returns -1 for unsupported values. */
+int sincos_set_launch_config(int threads, int blocks_per_sm, int vec, int unroll);
+void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *vec, int *unroll);
+
+/* Traffic-ceiling kernel (bench only): same access pattern and launch as
+ * sincos_pairs, no arithmetic (writes theta to both outputs). */
+sincos_status_t sincos_null_4in8out(const float *theta_dev, float *sin_dev, float *cos_dev,
+                                    float *inter_dev, size_t n, void *stream);
+
+/* Test hook: the kernel's reciprocal sequence alone, out[i] = RN(1/d[i]). */
+sincos_status_t sincos_debug_reciprocal(const float *d_dev, float *out_dev, size_t n,
+                                        void *stream);
+
+const char *sincos_status_string(sincos_status_t s);
+int sincos_last_cuda_error(void);      /* cudaError_t of the last SINCOS_ERR_CUDA in this thread */
+const char *sincos_version(void);
+/* Number of kernel launches this process has issued through the library. */
+uint64_t sincos_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SINCOS_PAIRS_H */

@@ -1,0 +1,411 @@
+"""bench.py -- sincos pairs/s and HBM GB/s of the hot path on N B200 (one process per GPU).
+
+Workload: BASELINE.json configs[1] ("C2"): 2^28 fp32 angles
+U[-1e4, 1e4] (seed 1) per GPU, split sin/cos outputs, BOTH coefficient variants.
+One step = one pass of the whole hot path over the batch for each variant (two
+kernel launches, 2 x 2^28 pairs).  At N GPUs every rank owns a contiguous 2^28-
+element shard of the same counter-based stream (weak scaling; no collective on
+the data path).  Inputs (1 GiB) exceed L2 (126 MB), so no flush between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+Rank 0 prints ONE JSON line.  --impl reference times the CPU oracle on the host
+cores instead (the tier's reference arm; rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import inputs  # noqa: E402
+
+CONFIG_ID = 2                       # BASELINE.json configs[1]
+N_PER_RANK = 1 << 28
+BYTES_PER_PAIR = 12                 # 4 B theta in + 8 B (sin, cos) out -- SURVEY 8(d)
+METRIC = "sincos pairs/sec and achieved HBM GB/s vs peak at 1/2/4/8 B200; max error"
+WORKLOAD = "C2: 2^28 fp32 angles U[-1e4,1e4] seed 1 per GPU, split sin/cos, both variants (N then A) per step"
+FALLBACK_HBM_GBS = 6650.0           # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=N_PER_RANK, help="elements per rank (default 2^28, configs[1])")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample for cpu_baseline")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--launch", default=None, help="threads,blocks_per_sm,vec,unroll (default: library default)")
+    ap.add_argument("--sweep", action="store_true", help="time every launch config (tuning aid; extra JSON lines)")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: torch copy, burst)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(n):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        k = d.get("dominant", {})
+        if int(k.get("n", -1)) == n:
+            return float(k["dram_bytes_read"]) + float(k["dram_bytes_write"])
+    except Exception:
+        pass
+    return None
+
+
+# ---- clocks during the timed region (NVML, polled) ------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, local_rank):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            ids = [x for x in vis.split(",") if x.strip()]
+            index = int(ids[local_rank]) if local_rank < len(ids) and ids[local_rank].strip().isdigit() else local_rank
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # no NVML: report null clocks
+            self.err = repr(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def result(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+# ---- the oracle as a CPU baseline ---------------------------------------------------------
+def cpu_oracle_rate(theta: np.ndarray, seconds: float):
+    """Time the oracle as it stands on all host cores (chunked threads; ctypes releases the
+    GIL) on a bounded prefix of the workload, both variants alternately, until `seconds`."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+    cores = os.cpu_count() or 1
+    chunk = 1 << 18
+    m = min(theta.size, chunk * cores * 4)
+    th = np.ascontiguousarray(theta[:m])
+    s = np.empty_like(th)
+    c = np.empty_like(th)
+    spans = [(i, min(i + chunk, m)) for i in range(0, m, chunk)]
+    pairs, t0 = 0, time.perf_counter()
+    with ThreadPoolExecutor(cores) as ex:
+        v = 0
+        while True:
+            list(ex.map(lambda ab: oracle.sincos_into(th[ab[0]:ab[1]], s[ab[0]:ab[1]], c[ab[0]:ab[1]], v), spans))
+            pairs += m
+            v ^= 1
+            if time.perf_counter() - t0 >= seconds and v == 0:
+                break
+    dt = time.perf_counter() - t0
+    return {"value": pairs / dt, "unit": "pairs/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {m} elements of the C2 workload, variants N and A alternately, "
+                      f"{pairs} pairs in {dt:.1f} s on {cores} threads (plain scalar C oracle)",
+            "seconds": dt}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    per_step = min(args.n, 1 << 22)
+    th = inputs.generate(CONFIG_ID, 0, per_step)
+    # warm-up and timed steps: each step = the oracle over a bounded sample, both variants
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+    cores = os.cpu_count() or 1
+    chunk = 1 << 18
+    sample = np.ascontiguousarray(th[:per_step])
+    s = np.empty_like(sample)
+    c = np.empty_like(sample)
+    spans = [(i, min(i + chunk, per_step)) for i in range(0, per_step, chunk)]
+
+    def step(ex):
+        for v in (0, 1):
+            list(ex.map(lambda ab: oracle.sincos_into(sample[ab[0]:ab[1]], s[ab[0]:ab[1]], c[ab[0]:ab[1]], v),
+                        spans))
+
+    with ThreadPoolExecutor(cores) as ex:
+        for _ in range(args.warmup):
+            step(ex)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step(ex)
+        dt = time.perf_counter() - t0
+    pairs = 2 * per_step * args.steps
+    val = pairs / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "pairs/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD + f"; reference arm: CPU oracle on a {per_step}-element prefix per "
+                                          "variant per step", "n_per_rank": args.n},
+        "cpu_baseline": {"value": val, "unit": "pairs/s", "cores": cores, "kind": "oracle",
+                         "sample": f"first {per_step} elements of C2 per variant per step, {args.steps} steps"},
+        "e2e": {"value": val, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm -------------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_cs_0406049_b200 as sp
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if args.launch:
+        sp.set_launch_config(*[int(x) for x in args.launch.split(",")])
+    n = args.n
+    # inputs: this rank's contiguous shard of the C2 counter stream, generated on the host
+    th_h = torch.empty(n, dtype=torch.float32).pin_memory()
+    inputs.generate(CONFIG_ID, rank * n, n, out=th_h.numpy())
+    th = th_h.to(dev)
+    outs = {v: (torch.empty(n, dtype=torch.float32, device=dev), torch.empty(n, dtype=torch.float32, device=dev))
+            for v in (sp.NORMALIZED, sp.RENORMALIZED)}
+    stream = torch.cuda.current_stream(dev)
+    variants = (sp.NORMALIZED, sp.RENORMALIZED)
+
+    def step():
+        for v in variants:
+            s, c = outs[v]
+            sp.sincos_pairs(th, s, c, variant=v, stream=stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    # per-launch events on the launching stream: the kernels' own durations
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(variants) + 1)] for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    launches0 = sp.launch_count()
+    with ClockSampler(local_rank) as clk:
+        t_start.record(stream)
+        for k in range(args.steps):
+            ev[k][0].record(stream)
+            for j, v in enumerate(variants):
+                s, c = outs[v]
+                sp.sincos_pairs(th, s, c, variant=v, stream=stream)
+                ev[k][j + 1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    launches = sp.launch_count() - launches0
+    ms_total = t_start.elapsed_time(t_end)
+    per_kernel = {v: [ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps)] for j, v in enumerate(variants)}
+
+    # max over ranks of the timed region
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    pairs_total = world * len(variants) * n * args.steps
+    value = pairs_total / (ms_max / 1e3)
+
+    # roofline of the dominant (slowest) kernel
+    avg = {v: statistics.mean(per_kernel[v]) for v in variants}
+    dom = max(variants, key=lambda v: avg[v])
+    peak, peak_src = peaks()
+    achieved = BYTES_PER_PAIR * n / (avg[dom] / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": ncu_traffic(n), "kernel": f"sincos_vec_kernel variant {'A' if dom else 'N'}",
+            "bytes_per_launch": BYTES_PER_PAIR * n, "peak_source": peak_src,
+            "per_variant_GBps": {("N" if v == 0 else "A"): BYTES_PER_PAIR * n / (avg[v] / 1e3) / 1e9 for v in variants},
+            "per_variant_ms": {("N" if v == 0 else "A"): avg[v] for v in variants}}
+
+    # traffic ceiling (same access pattern, no math), outside the timed region
+    s, c = outs[sp.NORMALIZED]
+    for _ in range(3):
+        sp.null_4in8out(th, s, c)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    e0.record(stream)
+    for _ in range(reps):
+        sp.null_4in8out(th, s, c, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    null_ms = e0.elapsed_time(e1) / reps
+    roof["ceiling_kernel_GBps"] = BYTES_PER_PAIR * n / (null_ms / 1e3) / 1e9
+    roof["vs_ceiling_kernel"] = null_ms / avg[dom]
+
+    # per-shard error statistics, gathered with NCCL (the only collective; not timed)
+    for v in variants:
+        sp.sincos_pairs(th, *outs[v], variant=v)
+    recs = []
+    for v in variants:
+        st = sp.error_stats(th, *outs[v])
+        recs.append([float(st["n"]), float(st["nan_count"]), st["max_comb"], st["sum_sq"], st["max_amp"],
+                     avg[v], float(rank), float(v)])
+    mine = torch.tensor(recs, dtype=torch.float64, device=dev)
+    if world > 1:
+        allr = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        allr = torch.stack(allr).cpu().numpy()
+    else:
+        allr = mine.cpu().numpy()[None]
+    shards = [{"rank": int(r[6]), "variant": "N" if r[7] == 0 else "A", "n": int(r[0]), "nan": int(r[1]),
+               "max_err": r[2], "rms_err": (r[3] / r[0]) ** 0.5 if r[0] else 0.0, "max_amp": r[4], "kernel_ms": r[5]}
+              for rank_rows in allr for r in rank_rows]
+
+    # end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        ws = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        sh = torch.empty(n, dtype=torch.float32).pin_memory()
+        ch = torch.empty(n, dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            for v in variants:
+                sp.sincos_pairs_host(th_h, sh, ch, variant=v, workspace=ws, stream=stream)
+
+        e2e_step()
+        barrier()
+        k2 = max(1, min(args.e2e_steps, args.steps))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(k2):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        t2 = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * len(variants) * n * k2 / (float(t2.item()) / 1e3), "unit": "pairs/s",
+               "h2d_bytes_per_step": len(variants) * 4 * n, "d2h_bytes_per_step": len(variants) * 8 * n,
+               "steps": k2, "path": "sincos_pairs_host (pinned host buffers, chunked H2D/kernel/D2H, 3 streams)"}
+        del ws, sh, ch
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_rate(th_h.numpy(), args.cpu_seconds)
+
+    if rank == 0:
+        ms_step = ms_max / args.steps
+        line = {
+            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_per_rank": n, "pairs_per_step": world * len(variants) * n,
+                       "global_batch": world * n, "parallelism": f"dp{world} (contiguous shards, no collective)",
+                       "l2": "inputs larger than L2 (1 GiB theta + 2 GiB outputs per launch vs 126 MB L2); no flush",
+                       "launch": sp.get_launch_config()},
+            "hbm_GBps": BYTES_PER_PAIR * pairs_total / (ms_max / 1e3) / 1e9 / world,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.result(),
+            "max_error": max(r["max_err"] for r in shards),
+            "shards": shards,
+            "paper_context": "PowerPC 7400 G4 500 MHz AltiVec: 140 ns per 4 pairs = 28.6 M pairs/s (P:177-180)",
+        }
+        print(json.dumps(line), flush=True)
+
+    if args.sweep and rank == 0:
+        for threads in (128, 256, 512):
+            for bps in (0, 1, 2, 4, 8):
+                for vec in (4, 8):
+                    for unroll in (1, 2, 4):
+                        sp.set_launch_config(threads, bps, vec, unroll)
+                        res = {}
+                        for v in variants:
+                            s, c = outs[v]
+                            for _ in range(3):
+                                sp.sincos_pairs(th, s, c, variant=v)
+                            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                            a.record(stream)
+                            for _ in range(10):
+                                sp.sincos_pairs(th, s, c, variant=v, stream=stream)
+                            b.record(stream)
+                            torch.cuda.synchronize(dev)
+                            res["N" if v == 0 else "A"] = BYTES_PER_PAIR * n / (a.elapsed_time(b) / 10 / 1e3) / 1e9
+                        print(json.dumps({"sweep": [threads, bps, vec, unroll], "GBps": res}), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

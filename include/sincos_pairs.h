@@ -35,6 +35,12 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define SINCOS_API __attribute__((visibility("default")))
+#else
+#define SINCOS_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -78,7 +84,7 @@ typedef enum {
  * before any CUDA call; the return value reports validation and the launch
  * status only (the kernel itself cannot fail short of invalid addresses).
  */
-sincos_status_t sincos_pairs(const float *theta_dev, float *sin_dev, float *cos_dev,
+SINCOS_API sincos_status_t sincos_pairs(const float *theta_dev, float *sin_dev, float *cos_dev,
                              float *inter_dev, size_t n, sincos_variant_t variant, void *stream);
 
 /*
@@ -91,10 +97,10 @@ sincos_status_t sincos_pairs(const float *theta_dev, float *sin_dev, float *cos_
  *   dev_ws, ws_bytes  caller-owned device workspace of the current device
  *                     (>= sincos_host_workspace_min_bytes(); more = larger chunks).
  */
-sincos_status_t sincos_pairs_host(const float *theta_host, float *sin_host, float *cos_host,
+SINCOS_API sincos_status_t sincos_pairs_host(const float *theta_host, float *sin_host, float *cos_host,
                                   float *inter_host, size_t n, sincos_variant_t variant,
                                   void *dev_ws, size_t ws_bytes, void *stream);
-size_t sincos_host_workspace_min_bytes(void);
+SINCOS_API size_t sincos_host_workspace_min_bytes(void);
 
 /*
  * Host-side sharding: element ranges [lo, hi) of shard g of
@@ -102,7 +108,7 @@ size_t sincos_host_workspace_min_bytes(void);
  * aligned in any aligned array); the last shard takes the remainder.  Pure
  * function, no CUDA.  Returns 0, or -1 for nshards < 1 or g outside [0, nshards).
  */
-int sincos_shard_range(size_t n, int nshards, int g, size_t *lo, size_t *hi);
+SINCOS_API int sincos_shard_range(size_t n, int nshards, int g, size_t *lo, size_t *hi);
 
 /* One shard resident on one device. */
 typedef struct {
@@ -115,7 +121,7 @@ typedef struct {
 
 /* Launch every shard on its own device (single process, many devices);
  * no data crosses devices.  Restores the caller's current device. */
-sincos_status_t sincos_pairs_sharded(const sincos_shard_t *shards, int nshards,
+SINCOS_API sincos_status_t sincos_pairs_sharded(const sincos_shard_t *shards, int nshards,
                                      sincos_variant_t variant);
 
 /*
@@ -137,10 +143,10 @@ typedef struct {
     uint64_t reserved;
 } sincos_stats_t;
 
-size_t sincos_stats_workspace_bytes(void);
+SINCOS_API size_t sincos_stats_workspace_bytes(void);
 /* stats_dev: device pointer to one sincos_stats_t; ws_dev: device workspace of
  * sincos_stats_workspace_bytes(). */
-sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
+SINCOS_API sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
                                    const float *cos_dev, const float *inter_dev, size_t n,
                                    sincos_stats_t *stats_dev, void *ws_dev, void *stream);
 
@@ -149,23 +155,23 @@ sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
  * thread access (4 or 8), unroll U (1, 2 or 4 independent vectors in flight
  * per thread: the GPU form of "computes two vectors at a time").
  * Process-global; returns -1 for unsupported values. */
-int sincos_set_launch_config(int threads, int blocks_per_sm, int vec, int unroll);
-void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *vec, int *unroll);
+SINCOS_API int sincos_set_launch_config(int threads, int blocks_per_sm, int vec, int unroll);
+SINCOS_API void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *vec, int *unroll);
 
 /* Traffic-ceiling kernel (bench only): same access pattern and launch as
  * sincos_pairs, no arithmetic (writes theta to both outputs). */
-sincos_status_t sincos_null_4in8out(const float *theta_dev, float *sin_dev, float *cos_dev,
+SINCOS_API sincos_status_t sincos_null_4in8out(const float *theta_dev, float *sin_dev, float *cos_dev,
                                     float *inter_dev, size_t n, void *stream);
 
 /* Test hook: the kernel's reciprocal sequence alone, out[i] = RN(1/d[i]). */
-sincos_status_t sincos_debug_reciprocal(const float *d_dev, float *out_dev, size_t n,
+SINCOS_API sincos_status_t sincos_debug_reciprocal(const float *d_dev, float *out_dev, size_t n,
                                         void *stream);
 
-const char *sincos_status_string(sincos_status_t s);
-int sincos_last_cuda_error(void);      /* cudaError_t of the last SINCOS_ERR_CUDA in this thread */
-const char *sincos_version(void);
+SINCOS_API const char *sincos_status_string(sincos_status_t s);
+SINCOS_API int sincos_last_cuda_error(void);      /* cudaError_t of the last SINCOS_ERR_CUDA in this thread */
+SINCOS_API const char *sincos_version(void);
 /* Number of kernel launches this process has issued through the library. */
-uint64_t sincos_launch_count(void);
+SINCOS_API uint64_t sincos_launch_count(void);
 
 #ifdef __cplusplus
 }

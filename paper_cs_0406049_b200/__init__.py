@@ -1,0 +1,241 @@
+"""paper_cs_0406049_b200 -- thin Python binding of libsincos_pairs.so.
+
+The hot path of Mendenhall, "A Fast, Vectorizable Algorithm for Producing
+Single-Precision Sine-Cosine Pairs" (arXiv cs/0406049) as one hand-written
+sm_100a kernel behind a C ABI (include/sincos_pairs.h).  This module only
+marshals arguments (torch tensors -> device pointers, the current CUDA
+stream); every step of the path runs in the library's kernels.  There is no
+CPU fallback: if the library cannot be loaded, or a tensor is not a CUDA
+tensor, the call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = [
+    "NORMALIZED", "RENORMALIZED", "SincosError", "lib", "sincos", "sincos_pairs", "sincos_pairs_host",
+    "shard_range", "error_stats", "set_launch_config", "get_launch_config", "null_4in8out",
+    "debug_reciprocal", "launch_count", "host_workspace_min_bytes", "library_path", "sincos_pairs_sharded",
+]
+
+NORMALIZED = 0      # method 1, P:124-150 (Fig. 1 FASTER_SINCOS)
+RENORMALIZED = 1    # method 2, P:152-172 (exact reciprocal renormalisation)
+_VARIANTS = {"normalized": NORMALIZED, "n": NORMALIZED, "renormalized": RENORMALIZED, "a": RENORMALIZED,
+             "angle_accurate": RENORMALIZED}
+
+_STATUS = {0: "ok", 1: "invalid argument", 2: "overlap", 3: "cuda error"}
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+library_path = os.path.join(_PKG, "libsincos_pairs.so")
+
+
+class SincosError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        msg = f"{what}: {_STATUS.get(status, status)}"
+        if status == 3 and _lib is not None:
+            msg += f" (cudaError {_lib.sincos_last_cuda_error()})"
+        super().__init__(msg)
+
+
+class Stats(ctypes.Structure):
+    """sincos_stats_t (64 bytes)."""
+    _fields_ = [("n", ctypes.c_uint64), ("nan_count", ctypes.c_uint64), ("max_comb", ctypes.c_double),
+                ("sum_sq", ctypes.c_double), ("max_amp", ctypes.c_double), ("kernel_ms", ctypes.c_double),
+                ("worst_theta", ctypes.c_float), ("device", ctypes.c_uint32), ("reserved", ctypes.c_uint64)]
+
+
+class Shard(ctypes.Structure):
+    """sincos_shard_t."""
+    _fields_ = [("device", ctypes.c_int), ("theta_dev", ctypes.c_void_p), ("sin_dev", ctypes.c_void_p),
+                ("cos_dev", ctypes.c_void_p), ("inter_dev", ctypes.c_void_p), ("n", ctypes.c_size_t),
+                ("stream", ctypes.c_void_p)]
+
+
+_lib = None
+_P, _S, _I = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+_SIGS = {
+    "sincos_pairs": (_I, [_P, _P, _P, _P, _S, _I, _P]),
+    "sincos_pairs_host": (_I, [_P, _P, _P, _P, _S, _I, _P, _S, _P]),
+    "sincos_host_workspace_min_bytes": (_S, []),
+    "sincos_shard_range": (_I, [_S, _I, _I, ctypes.POINTER(_S), ctypes.POINTER(_S)]),
+    "sincos_pairs_sharded": (_I, [ctypes.POINTER(Shard), _I, _I]),
+    "sincos_stats_workspace_bytes": (_S, []),
+    "sincos_error_stats": (_I, [_P, _P, _P, _P, _S, _P, _P, _P]),
+    "sincos_set_launch_config": (_I, [_I, _I, _I, _I]),
+    "sincos_get_launch_config": (None, [ctypes.POINTER(_I)] * 4),
+    "sincos_null_4in8out": (_I, [_P, _P, _P, _P, _S, _P]),
+    "sincos_debug_reciprocal": (_I, [_P, _P, _S, _P]),
+    "sincos_status_string": (ctypes.c_char_p, [_I]),
+    "sincos_last_cuda_error": (_I, []),
+    "sincos_version": (ctypes.c_char_p, []),
+    "sincos_launch_count": (ctypes.c_uint64, []),
+}
+EXPORTS = tuple(_SIGS)
+
+
+def lib():
+    """Load libsincos_pairs.so (building it in-tree with nvcc if it is missing or stale)."""
+    global _lib
+    if _lib is None:
+        from . import _build
+        path = _build.build()
+        if not os.path.exists(path):
+            raise ImportError(f"libsincos_pairs.so not found at {path}")
+        L = ctypes.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise SincosError(status, what)
+
+
+def _variant(v) -> int:
+    if isinstance(v, str):
+        return _VARIANTS[v.lower()]
+    return int(v)
+
+
+def _ptr(t, name: str, device_required: bool = True) -> int:
+    import torch
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32, got {t.dtype}")
+    if device_required and not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream, device) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def sincos_pairs(theta, sin_out=None, cos_out=None, interleaved_out=None, variant=NORMALIZED, stream=None):
+    """C-ABI sincos_pairs on CUDA tensors (asynchronous on `stream`, default: current stream).
+
+    Split form: sin_out[i], cos_out[i]; interleaved form: interleaved_out (float32, 2n) holds
+    {cos, sin} per element (view as complex64 for e^{i theta})."""
+    n = theta.numel()
+    if interleaved_out is not None and interleaved_out.numel() != 2 * n:
+        raise ValueError("interleaved_out must hold 2*n floats")
+    for o in (sin_out, cos_out):
+        if o is not None and o.numel() != n:
+            raise ValueError("outputs must hold n floats")
+    st = lib().sincos_pairs(_ptr(theta, "theta"), _ptr(sin_out, "sin_out"), _ptr(cos_out, "cos_out"),
+                            _ptr(interleaved_out, "interleaved_out"), n, _variant(variant),
+                            _stream(stream, theta.device))
+    _check(st, "sincos_pairs")
+
+
+def sincos(theta, variant="normalized", interleaved=False, out=None, stream=None):
+    """Allocate outputs and run the hot path.  Returns (sin, cos) or, if interleaved, a (n, 2)
+    float32 tensor of {cos, sin} rows."""
+    import torch
+    if interleaved:
+        o = out if out is not None else torch.empty(theta.shape + (2,), dtype=torch.float32, device=theta.device)
+        sincos_pairs(theta.reshape(-1), interleaved_out=o.reshape(-1), variant=variant, stream=stream)
+        return o
+    s, c = out if out is not None else (torch.empty_like(theta), torch.empty_like(theta))
+    sincos_pairs(theta.reshape(-1), s.reshape(-1), c.reshape(-1), variant=variant, stream=stream)
+    return s, c
+
+
+def host_workspace_min_bytes() -> int:
+    return int(lib().sincos_host_workspace_min_bytes())
+
+
+def sincos_pairs_host(theta, sin_out=None, cos_out=None, interleaved_out=None, variant=NORMALIZED,
+                      workspace=None, stream=None):
+    """C-ABI sincos_pairs_host on HOST tensors (pinned for overlap); `workspace` is a CUDA uint8/float
+    tensor on the current device.  Synchronous."""
+    import torch
+    n = theta.numel()
+    ws_bytes = workspace.numel() * workspace.element_size()
+    dev = workspace.device
+    st = lib().sincos_pairs_host(_ptr(theta, "theta", False), _ptr(sin_out, "sin_out", False),
+                                 _ptr(cos_out, "cos_out", False), _ptr(interleaved_out, "interleaved_out", False),
+                                 n, _variant(variant), workspace.data_ptr(), ws_bytes, _stream(stream, dev))
+    _check(st, "sincos_pairs_host")
+
+
+def shard_range(n: int, nshards: int, g: int):
+    """[lo, hi) of shard g (host logic only, no CUDA)."""
+    lo, hi = ctypes.c_size_t(), ctypes.c_size_t()
+    if lib().sincos_shard_range(n, nshards, g, ctypes.byref(lo), ctypes.byref(hi)) != 0:
+        raise ValueError(f"bad shard {g} of {nshards}")
+    return lo.value, hi.value
+
+
+def sincos_pairs_sharded(shards, variant=NORMALIZED):
+    """Single-process multi-device launch.  shards: list of dicts with device, theta,
+    sin/cos or inter tensors, optional stream."""
+    arr = (Shard * len(shards))()
+    for i, sh in enumerate(shards):
+        th = sh["theta"]
+        arr[i].device = th.device.index
+        arr[i].theta_dev = _ptr(th, "theta")
+        arr[i].sin_dev = _ptr(sh.get("sin"), "sin")
+        arr[i].cos_dev = _ptr(sh.get("cos"), "cos")
+        arr[i].inter_dev = _ptr(sh.get("inter"), "inter")
+        arr[i].n = th.numel()
+        arr[i].stream = _stream(sh.get("stream"), th.device)
+    _check(lib().sincos_pairs_sharded(arr, len(shards), _variant(variant)), "sincos_pairs_sharded")
+
+
+def error_stats(theta, sin_out=None, cos_out=None, interleaved_out=None, stream=None) -> dict:
+    """KB5 fp64 error statistics of outputs on the device (P:135-139 metrics)."""
+    import torch
+    dev = theta.device
+    ws = torch.empty(lib().sincos_stats_workspace_bytes(), dtype=torch.uint8, device=dev)
+    rec = torch.zeros(ctypes.sizeof(Stats), dtype=torch.uint8, device=dev)
+    st = lib().sincos_error_stats(_ptr(theta, "theta"), _ptr(sin_out, "sin_out"), _ptr(cos_out, "cos_out"),
+                                  _ptr(interleaved_out, "interleaved_out"), theta.numel(), rec.data_ptr(),
+                                  ws.data_ptr(), _stream(stream, dev))
+    _check(st, "sincos_error_stats")
+    raw = bytes(rec.cpu().numpy().tobytes())
+    s = Stats.from_buffer_copy(raw)
+    d = {k: getattr(s, k) for k, _ in Stats._fields_}
+    d["rms"] = (s.sum_sq / s.n) ** 0.5 if s.n else 0.0
+    d["raw"] = raw
+    return d
+
+
+def set_launch_config(threads=256, blocks_per_sm=0, vec=8, unroll=2):
+    if lib().sincos_set_launch_config(threads, blocks_per_sm, vec, unroll) != 0:
+        raise ValueError("unsupported launch config")
+
+
+def get_launch_config() -> dict:
+    v = [ctypes.c_int() for _ in range(4)]
+    lib().sincos_get_launch_config(*[ctypes.byref(x) for x in v])
+    return dict(zip(("threads", "blocks_per_sm", "vec", "unroll"), (x.value for x in v)))
+
+
+def null_4in8out(theta, sin_out=None, cos_out=None, interleaved_out=None, stream=None):
+    _check(lib().sincos_null_4in8out(_ptr(theta, "theta"), _ptr(sin_out, "sin_out"), _ptr(cos_out, "cos_out"),
+                                     _ptr(interleaved_out, "interleaved_out"), theta.numel(),
+                                     _stream(stream, theta.device)), "sincos_null_4in8out")
+
+
+def debug_reciprocal(d, out, stream=None):
+    _check(lib().sincos_debug_reciprocal(_ptr(d, "d"), _ptr(out, "out"), d.numel(), _stream(stream, d.device)),
+           "sincos_debug_reciprocal")
+
+
+def launch_count() -> int:
+    return int(lib().sincos_launch_count())

@@ -1,0 +1,371 @@
+// sincos_abi.cu -- the extern "C" boundary of libsincos_pairs.so (include/sincos_pairs.h).
+//
+// Validation (no CUDA call on any error path), path selection (256-bit / 128-bit
+// vector body with a scalar head and tail, or the scalar kernel for pointers
+// that do not share an alignment), grid sizing (grid-stride, a multiple of the
+// SM count: SMs x resident blocks per SM), the pipelined host-buffer path, and
+// the single-process multi-device sharder.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <mutex>
+#include <stdint.h>
+#include <string.h>
+
+#include "../../include/sincos_pairs.h"
+#include "sincos_launch.h"
+
+using namespace sincos_b200;
+
+namespace {
+
+thread_local int g_last_cuda_error = 0;
+std::atomic<uint64_t> g_launches{0};
+
+std::atomic<int> g_threads{256};
+std::atomic<int> g_blocks_per_sm{0};
+std::atomic<int> g_vec{8};
+std::atomic<int> g_unroll{2};
+
+constexpr int kMaxDev = 64;
+std::atomic<int> g_sm_count[kMaxDev];
+
+sincos_status_t cuda_fail(cudaError_t e) {
+    g_last_cuda_error = static_cast<int>(e);
+    return SINCOS_ERR_CUDA;
+}
+
+int sm_count(int dev) {
+    if (dev < 0 || dev >= kMaxDev) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 1;
+    }
+    int v = g_sm_count[dev].load(std::memory_order_relaxed);
+    if (v == 0) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (v <= 0) v = 1;
+        g_sm_count[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+
+// Resident blocks per SM of a kernel at a block size (cached; occupancy is a
+// property of the kernel and the architecture, identical on every B200).
+struct OccEntry {
+    const void *fn;
+    int threads;
+    int blocks;
+};
+std::mutex g_occ_mu;
+OccEntry g_occ[256];
+int g_occ_n = 0;
+
+int occupancy(const void *fn, int threads) {
+    {
+        std::lock_guard<std::mutex> lk(g_occ_mu);
+        for (int i = 0; i < g_occ_n; ++i)
+            if (g_occ[i].fn == fn && g_occ[i].threads == threads) return g_occ[i].blocks;
+    }
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, 0) != cudaSuccess || b <= 0) b = 1;
+    std::lock_guard<std::mutex> lk(g_occ_mu);
+    if (g_occ_n < 256) g_occ[g_occ_n++] = OccEntry{fn, threads, b};
+    return b;
+}
+
+bool overlaps(const void *a, size_t abytes, const void *b, size_t bbytes) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+    return a0 < b0 + bbytes && b0 < a0 + abytes;
+}
+
+bool aligned(const void *p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+// Shared argument validation of sincos_pairs / sincos_pairs_host / null kernel.
+sincos_status_t validate(const float *theta, const float *so, const float *co, const float *io, size_t n,
+                         int variant, bool allow_null_variant) {
+    if (variant != SINCOS_NORMALIZED && variant != SINCOS_RENORMALIZED && !(allow_null_variant && variant == 2))
+        return SINCOS_ERR_INVALID_ARGUMENT;
+    if (n == 0) return SINCOS_OK;
+    const bool split = so != nullptr && co != nullptr && io == nullptr;
+    const bool inter = so == nullptr && co == nullptr && io != nullptr;
+    if (theta == nullptr || !(split || inter)) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (!aligned(theta, 4) || (so && !aligned(so, 4)) || (co && !aligned(co, 4)) || (io && !aligned(io, 4)))
+        return SINCOS_ERR_INVALID_ARGUMENT;
+    if (n > (SIZE_MAX / 8)) return SINCOS_ERR_INVALID_ARGUMENT;
+    const size_t b4 = 4 * n, b8 = 8 * n;
+    if (split) {
+        if (overlaps(so, b4, co, b4)) return SINCOS_ERR_OVERLAP;
+        if (theta != so && overlaps(theta, b4, so, b4)) return SINCOS_ERR_OVERLAP;
+        if (theta != co && overlaps(theta, b4, co, b4)) return SINCOS_ERR_OVERLAP;
+    } else if (overlaps(theta, b4, io, b8)) {
+        return SINCOS_ERR_OVERLAP;
+    }
+    return SINCOS_OK;
+}
+
+// Launch on already-validated arguments, n > 0.
+sincos_status_t launch(const float *theta, float *so, float *co, float *io, size_t n, int variant,
+                       cudaStream_t stream) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    const int sms = sm_count(dev);
+    const bool inter = io != nullptr;
+    const bool nc = !(theta == so || theta == co);
+    const int threads = g_threads.load(std::memory_order_relaxed);
+    const int cfg_bps = g_blocks_per_sm.load(std::memory_order_relaxed);
+    const int unroll = g_unroll.load(std::memory_order_relaxed);
+
+    // Widest vector whose alignment theta and the outputs share after a scalar head.
+    int w = 0;
+    size_t head = 0;
+    for (int cand = g_vec.load(std::memory_order_relaxed); cand >= 4; cand /= 2) {
+        const uintptr_t A = 4u * cand;  // bytes of theta per access
+        const uintptr_t t = reinterpret_cast<uintptr_t>(theta);
+        const size_t h = ((A - (t & (A - 1))) & (A - 1)) / 4;
+        const uintptr_t off = 4 * h;
+        bool ok = true;
+        if (inter)
+            ok = aligned(reinterpret_cast<const char *>(io) + 2 * off, A);
+        else
+            ok = aligned(reinterpret_cast<const char *>(so) + off, A) &&
+                 aligned(reinterpret_cast<const char *>(co) + off, A);
+        if (ok) {
+            w = cand;
+            head = h;
+            break;
+        }
+    }
+
+    if (w == 0) {
+        const unsigned grid = static_cast<unsigned>(
+            (n + threads - 1) / threads < static_cast<size_t>(sms) * 8 ? (n + threads - 1) / threads : sms * 8);
+        e = launch_scalar(variant, inter, grid, threads, theta, so, co, io, n, stream);
+    } else {
+        if (head > n) head = n;
+        const size_t nvec = (n - head) / w;
+        const int bps = cfg_bps > 0 ? cfg_bps : occupancy(vec_kernel_ptr(variant, inter, w, unroll, nc), threads);
+        const size_t per_block = static_cast<size_t>(threads) * unroll;
+        size_t need = (nvec + per_block - 1) / per_block;
+        if (need < 1) need = 1;
+        const size_t cap = static_cast<size_t>(sms) * bps;
+        const unsigned grid = static_cast<unsigned>(need < cap ? need : cap);
+        e = launch_vec(variant, inter, w, unroll, nc, grid, threads, theta, so, co, io, head, nvec, n, stream);
+    }
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SINCOS_OK;
+}
+
+// ---- host-buffer pipeline ----------------------------------------------------------
+constexpr int kSlots = 3;
+constexpr size_t kMinChunk = size_t(1) << 16;
+
+struct DevStreams {
+    bool init = false;
+    cudaStream_t s[kSlots];
+    cudaEvent_t done[kSlots];
+    cudaEvent_t start;
+};
+std::mutex g_dev_mu;
+DevStreams g_dev[kMaxDev];
+
+cudaError_t dev_streams(int dev, DevStreams **out) {
+    if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    DevStreams &d = g_dev[dev];
+    if (!d.init) {
+        for (int k = 0; k < kSlots; ++k) {
+            cudaError_t e = cudaStreamCreateWithFlags(&d.s[k], cudaStreamNonBlocking);
+            if (e != cudaSuccess) return e;
+            e = cudaEventCreateWithFlags(&d.done[k], cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
+        cudaError_t e = cudaEventCreateWithFlags(&d.start, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+        d.init = true;
+    }
+    *out = &d;
+    return cudaSuccess;
+}
+
+}  // namespace
+
+extern "C" {
+
+sincos_status_t sincos_pairs(const float *theta_dev, float *sin_dev, float *cos_dev, float *inter_dev, size_t n,
+                             sincos_variant_t variant, void *stream) {
+    sincos_status_t st = validate(theta_dev, sin_dev, cos_dev, inter_dev, n, variant, false);
+    if (st != SINCOS_OK || n == 0) return st;
+    return launch(theta_dev, sin_dev, cos_dev, inter_dev, n, variant, static_cast<cudaStream_t>(stream));
+}
+
+sincos_status_t sincos_null_4in8out(const float *theta_dev, float *sin_dev, float *cos_dev, float *inter_dev,
+                                    size_t n, void *stream) {
+    sincos_status_t st = validate(theta_dev, sin_dev, cos_dev, inter_dev, n, 2, true);
+    if (st != SINCOS_OK || n == 0) return st;
+    return launch(theta_dev, sin_dev, cos_dev, inter_dev, n, 2, static_cast<cudaStream_t>(stream));
+}
+
+size_t sincos_host_workspace_min_bytes(void) { return kSlots * kMinChunk * 12; }
+
+sincos_status_t sincos_pairs_host(const float *theta_host, float *sin_host, float *cos_host, float *inter_host,
+                                  size_t n, sincos_variant_t variant, void *dev_ws, size_t ws_bytes, void *stream) {
+    sincos_status_t st = validate(theta_host, sin_host, cos_host, inter_host, n, variant, false);
+    if (st != SINCOS_OK || n == 0) return st;
+    if (dev_ws == nullptr || ws_bytes < sincos_host_workspace_min_bytes() || !aligned(dev_ws, 256))
+        return SINCOS_ERR_INVALID_ARGUMENT;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    DevStreams *ds = nullptr;
+    if ((e = dev_streams(dev, &ds)) != cudaSuccess) return cuda_fail(e);
+
+    // chunk elements per slot, a multiple of 64 so every slot buffer stays 256-B aligned
+    size_t chunk = (ws_bytes / (kSlots * 12)) & ~size_t(63);
+    const bool inter = inter_host != nullptr;
+    char *ws = static_cast<char *>(dev_ws);
+    cudaStream_t caller = static_cast<cudaStream_t>(stream);
+
+    if ((e = cudaEventRecord(ds->start, caller)) != cudaSuccess) return cuda_fail(e);
+    for (int k = 0; k < kSlots; ++k)
+        if ((e = cudaStreamWaitEvent(ds->s[k], ds->start, 0)) != cudaSuccess) return cuda_fail(e);
+
+    size_t j = 0;
+    for (size_t off = 0; off < n; off += chunk, ++j) {
+        const size_t m = n - off < chunk ? n - off : chunk;
+        const int k = static_cast<int>(j % kSlots);
+        cudaStream_t s = ds->s[k];
+        float *th = reinterpret_cast<float *>(ws + k * chunk * 12);
+        float *o1 = th + chunk;      // sin, or interleaved pairs
+        float *o2 = o1 + chunk;      // cos
+        if ((e = cudaMemcpyAsync(th, theta_host + off, 4 * m, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+            return cuda_fail(e);
+        st = inter ? launch(th, nullptr, nullptr, o1, m, variant, s) : launch(th, o1, o2, nullptr, m, variant, s);
+        if (st != SINCOS_OK) return st;
+        if (inter) {
+            if ((e = cudaMemcpyAsync(inter_host + 2 * off, o1, 8 * m, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+                return cuda_fail(e);
+        } else {
+            if ((e = cudaMemcpyAsync(sin_host + off, o1, 4 * m, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+                return cuda_fail(e);
+            if ((e = cudaMemcpyAsync(cos_host + off, o2, 4 * m, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+                return cuda_fail(e);
+        }
+    }
+    for (int k = 0; k < kSlots; ++k) {
+        if ((e = cudaEventRecord(ds->done[k], ds->s[k])) != cudaSuccess) return cuda_fail(e);
+        if ((e = cudaStreamWaitEvent(caller, ds->done[k], 0)) != cudaSuccess) return cuda_fail(e);
+    }
+    for (int k = 0; k < kSlots; ++k)
+        if ((e = cudaStreamSynchronize(ds->s[k])) != cudaSuccess) return cuda_fail(e);
+    return SINCOS_OK;
+}
+
+int sincos_shard_range(size_t n, int nshards, int g, size_t *lo, size_t *hi) {
+    if (nshards < 1 || g < 0 || g >= nshards || lo == nullptr || hi == nullptr) return -1;
+    auto cut = [&](int k) -> size_t {
+        if (k >= nshards) return n;
+        const unsigned __int128 p = static_cast<unsigned __int128>(n) * static_cast<unsigned>(k) /
+                                    static_cast<unsigned>(nshards);
+        return static_cast<size_t>(p) & ~size_t(7);
+    };
+    *lo = cut(g);
+    *hi = cut(g + 1);
+    if (*hi < *lo) *hi = *lo;
+    return 0;
+}
+
+sincos_status_t sincos_pairs_sharded(const sincos_shard_t *shards, int nshards, sincos_variant_t variant) {
+    if (nshards < 0 || (nshards > 0 && shards == nullptr)) return SINCOS_ERR_INVALID_ARGUMENT;
+    for (int g = 0; g < nshards; ++g) {
+        const sincos_shard_t &sh = shards[g];
+        sincos_status_t st = validate(sh.theta_dev, sh.sin_dev, sh.cos_dev, sh.inter_dev, sh.n, variant, false);
+        if (st != SINCOS_OK) return st;
+    }
+    int prev = 0;
+    cudaError_t e = cudaGetDevice(&prev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    sincos_status_t result = SINCOS_OK;
+    for (int g = 0; g < nshards && result == SINCOS_OK; ++g) {
+        const sincos_shard_t &sh = shards[g];
+        if (sh.n == 0) continue;
+        if ((e = cudaSetDevice(sh.device)) != cudaSuccess) {
+            result = cuda_fail(e);
+            break;
+        }
+        result = launch(sh.theta_dev, sh.sin_dev, sh.cos_dev, sh.inter_dev, sh.n, variant,
+                        static_cast<cudaStream_t>(sh.stream));
+    }
+    cudaSetDevice(prev);
+    return result;
+}
+
+size_t sincos_stats_workspace_bytes(void) { return stats_ws_bytes(); }
+
+sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev, const float *cos_dev,
+                                   const float *inter_dev, size_t n, sincos_stats_t *stats_dev, void *ws_dev,
+                                   void *stream) {
+    const bool split = sin_dev != nullptr && cos_dev != nullptr && inter_dev == nullptr;
+    const bool inter = sin_dev == nullptr && cos_dev == nullptr && inter_dev != nullptr;
+    if (stats_dev == nullptr || ws_dev == nullptr || (n > 0 && (theta_dev == nullptr || !(split || inter))))
+        return SINCOS_ERR_INVALID_ARGUMENT;
+    cudaError_t e = launch_stats(theta_dev, sin_dev, cos_dev, inter_dev, n, stats_dev, ws_dev,
+                                 static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SINCOS_OK;
+}
+
+int sincos_set_launch_config(int threads, int blocks_per_sm, int vec, int unroll) {
+    if (!(threads == 128 || threads == 256 || threads == 512)) return -1;
+    if (blocks_per_sm < 0 || blocks_per_sm > 32) return -1;
+    if (!(vec == 4 || vec == 8)) return -1;
+    if (!(unroll == 1 || unroll == 2 || unroll == 4)) return -1;
+    g_threads.store(threads);
+    g_blocks_per_sm.store(blocks_per_sm);
+    g_vec.store(vec);
+    g_unroll.store(unroll);
+    return 0;
+}
+
+void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *vec, int *unroll) {
+    if (threads) *threads = g_threads.load();
+    if (blocks_per_sm) *blocks_per_sm = g_blocks_per_sm.load();
+    if (vec) *vec = g_vec.load();
+    if (unroll) *unroll = g_unroll.load();
+}
+
+sincos_status_t sincos_debug_reciprocal(const float *d_dev, float *out_dev, size_t n, void *stream) {
+    if (n == 0) return SINCOS_OK;
+    if (d_dev == nullptr || out_dev == nullptr) return SINCOS_ERR_INVALID_ARGUMENT;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    const size_t want = (n + 255) / 256;
+    const size_t cap = static_cast<size_t>(sm_count(dev)) * 8;
+    e = launch_rcp(static_cast<unsigned>(want < cap ? want : cap), 256, d_dev, out_dev, n,
+                   static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SINCOS_OK;
+}
+
+const char *sincos_status_string(sincos_status_t s) {
+    switch (s) {
+    case SINCOS_OK: return "ok";
+    case SINCOS_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case SINCOS_ERR_OVERLAP: return "output buffers overlap each other or the input";
+    case SINCOS_ERR_CUDA: return "CUDA error (see sincos_last_cuda_error)";
+    default: return "unknown status";
+    }
+}
+
+int sincos_last_cuda_error(void) { return g_last_cuda_error; }
+
+const char *sincos_version(void) { return "sincos_pairs 0.1 (sm_100a; arXiv cs/0406049)"; }
+
+uint64_t sincos_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

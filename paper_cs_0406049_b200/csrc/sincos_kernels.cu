@@ -1,0 +1,227 @@
+// sincos_kernels.cu -- sm_100a kernels of the hot path and their launchers.
+//
+// KB1/KB2  sincos_vec_kernel<V, INTER, W, U, NC>
+//          grid-stride streaming kernel; each thread moves W floats of theta per
+//          access (W = 8: one 256-bit LDG; W = 4: one 128-bit LDG), U accesses in
+//          flight per loop trip (the GPU form of "computes two vectors at a
+//          time"), and writes 8 B of output per element with 256-bit
+//          (or 128-bit) streaming stores: split sin[]/cos[] (INTER = false) or
+//          interleaved {cos, sin} pairs (INTER = true).  Loads bypass L1 and
+//          are L2 evict-first; stores too -- no element is touched twice.
+//          The scalar head (to reach alignment) and tail (n mod W) are done by
+//          the first threads of the grid with the same math.
+// KB3      sincos_scalar_kernel<V, INTER>: any 4-B alignment, one element per
+//          thread, identical numerics.
+// KB4      V = kNull: the traffic ceiling (same access pattern, no math).
+// KB5      sincos_stats_kernel: fp64 error statistics (verification only).
+//
+// HBM-bound by design: 12 algorithmic bytes per pair (4 in, 8 out) against
+// ~30 issued instructions per pair, i.e. ~2.5 instr/B while a B200 issues
+// ~5.7 lane-instr per HBM byte.  No shared memory, no
+// tensor cores (not a contraction).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sincos_launch.h"
+#include "sincos_math.cuh"
+
+namespace sincos_b200 {
+
+constexpr int kNull = 2;  // KB4: the traffic-ceiling "variant"
+
+template <int V>
+__device__ __forceinline__ void op(float t, float &s, float &c) {
+    if constexpr (V == kNull) {
+        s = t;
+        c = t;
+    } else {
+        sincos_pair<V>(t, s, c);
+    }
+}
+
+// ---- streaming memory access ----------------------------------------------
+template <int W, bool NC> struct Mem;
+
+template <> struct Mem<8, true> {
+    static __device__ __forceinline__ void load(float (&r)[8], const float *p) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+                     : "l"(p));
+    }
+};
+template <> struct Mem<8, false> {
+    static __device__ __forceinline__ void load(float (&r)[8], const float *p) {
+        asm volatile("ld.global.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+                     : "l"(p));
+    }
+};
+template <> struct Mem<4, true> {
+    static __device__ __forceinline__ void load(float (&r)[4], const float *p) {
+        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
+                     : "l"(p));
+    }
+};
+template <> struct Mem<4, false> {
+    static __device__ __forceinline__ void load(float (&r)[4], const float *p) {
+        asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
+                     : "l"(p));
+    }
+};
+
+__device__ __forceinline__ void store8(float *p, const float *r) {
+    asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(p), "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7])
+                 : "memory");
+}
+__device__ __forceinline__ void store4(float *p, const float *r) {
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3])
+                 : "memory");
+}
+template <int W>
+__device__ __forceinline__ void storeW(float *p, const float *r) {
+    if constexpr (W == 8) store8(p, r); else store4(p, r);
+}
+
+// Compute and store one vector of W elements whose first element is `e0`.
+template <int V, bool INTER, int W>
+__device__ __forceinline__ void emit(const float (&x)[W], size_t e0, float *so, float *co, float *io) {
+    if constexpr (INTER) {
+        float cs[2 * W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) op<V>(x[k], cs[2 * k + 1], cs[2 * k]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) storeW<W>(io + 2 * e0 + h * W, cs + h * W);
+    } else {
+        float s[W], c[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) op<V>(x[k], s[k], c[k]);
+        storeW<W>(so + e0, s);
+        storeW<W>(co + e0, c);
+    }
+}
+
+template <int V, bool INTER>
+__device__ __forceinline__ void emit_scalar(const float *theta, size_t e, float *so, float *co, float *io) {
+    float s, c;
+    op<V>(theta[e], s, c);
+    if constexpr (INTER) {
+        io[2 * e] = c;
+        io[2 * e + 1] = s;
+    } else {
+        so[e] = s;
+        co[e] = c;
+    }
+}
+
+// KB1/KB2.  Elements [0, head) and [head + nvec*W, n) scalar; the body is nvec
+// vectors of W elements starting at element `head` (aligned by the host).
+template <int V, bool INTER, int W, int U, bool NC>
+__global__ void __launch_bounds__(512) sincos_vec_kernel(const float *theta, float *so, float *co, float *io,
+                                                         size_t head, size_t nvec, size_t n) {
+    const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t tail0 = head + nvec * W;
+    if (tid < head) emit_scalar<V, INTER>(theta, tid, so, co, io);
+    if (tid < n - tail0) emit_scalar<V, INTER>(theta, tail0 + tid, so, co, io);
+
+    size_t v = tid;
+    if constexpr (U > 1) {
+        for (; v + (U - 1) * nthr < nvec; v += U * nthr) {
+            float x[U][W];
+#pragma unroll
+            for (int u = 0; u < U; ++u) Mem<W, NC>::load(x[u], theta + head + (v + u * nthr) * W);
+#pragma unroll
+            for (int u = 0; u < U; ++u) emit<V, INTER, W>(x[u], head + (v + u * nthr) * W, so, co, io);
+        }
+    }
+    for (; v < nvec; v += nthr) {
+        float x[W];
+        Mem<W, NC>::load(x, theta + head + v * W);
+        emit<V, INTER, W>(x, head + v * W, so, co, io);
+    }
+}
+
+// KB3: any alignment.
+template <int V, bool INTER>
+__global__ void __launch_bounds__(512) sincos_scalar_kernel(const float *theta, float *so, float *co, float *io,
+                                                            size_t n) {
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += nthr)
+        emit_scalar<V, INTER>(theta, e, so, co, io);
+}
+
+__global__ void __launch_bounds__(512) rcp_kernel(const float *d, float *out, size_t n) {
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += nthr)
+        out[e] = rcp_rn(d[e]);
+}
+
+// ---- dispatch -----------------------------------------------------------------
+using VecFn = void (*)(const float *, float *, float *, float *, size_t, size_t, size_t);
+using ScalarFn = void (*)(const float *, float *, float *, float *, size_t);
+
+template <int V, bool INTER, int W, bool NC>
+static VecFn pick_u(int unroll) {
+    switch (unroll) {
+    case 1: return sincos_vec_kernel<V, INTER, W, 1, NC>;
+    case 2: return sincos_vec_kernel<V, INTER, W, 2, NC>;
+    default: return sincos_vec_kernel<V, INTER, W, 4, NC>;
+    }
+}
+
+template <int V, bool INTER>
+static VecFn pick_vec(int w, int unroll, bool nc) {
+    if (w == 8) return nc ? pick_u<V, INTER, 8, true>(unroll) : pick_u<V, INTER, 8, false>(unroll);
+    return nc ? pick_u<V, INTER, 4, true>(unroll) : pick_u<V, INTER, 4, false>(unroll);
+}
+
+template <int V>
+static VecFn pick_inter(bool inter, int w, int unroll, bool nc) {
+    return inter ? pick_vec<V, true>(w, unroll, nc) : pick_vec<V, false>(w, unroll, nc);
+}
+
+VecFn vec_kernel(int variant, bool inter, int w, int unroll, bool nc) {
+    switch (variant) {
+    case kNormalized: return pick_inter<kNormalized>(inter, w, unroll, nc);
+    case kRenormalized: return pick_inter<kRenormalized>(inter, w, unroll, nc);
+    default: return pick_inter<kNull>(inter, w, unroll, nc);
+    }
+}
+
+ScalarFn scalar_kernel(int variant, bool inter) {
+    switch (variant) {
+    case kNormalized: return inter ? sincos_scalar_kernel<kNormalized, true> : sincos_scalar_kernel<kNormalized, false>;
+    case kRenormalized: return inter ? sincos_scalar_kernel<kRenormalized, true> : sincos_scalar_kernel<kRenormalized, false>;
+    default: return inter ? sincos_scalar_kernel<kNull, true> : sincos_scalar_kernel<kNull, false>;
+    }
+}
+
+cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, unsigned grid, unsigned threads,
+                       const float *theta, float *so, float *co, float *io, size_t head, size_t nvec, size_t n,
+                       cudaStream_t stream) {
+    VecFn fn = vec_kernel(variant, inter, w, unroll, nc);
+    void *args[] = {&theta, &so, &co, &io, &head, &nvec, &n};
+    return cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(threads), args, 0, stream);
+}
+
+cudaError_t launch_scalar(int variant, bool inter, unsigned grid, unsigned threads, const float *theta, float *so,
+                          float *co, float *io, size_t n, cudaStream_t stream) {
+    ScalarFn fn = scalar_kernel(variant, inter);
+    void *args[] = {&theta, &so, &co, &io, &n};
+    return cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(threads), args, 0, stream);
+}
+
+cudaError_t launch_rcp(unsigned grid, unsigned threads, const float *d, float *out, size_t n, cudaStream_t stream) {
+    void *args[] = {&d, &out, &n};
+    return cudaLaunchKernel(reinterpret_cast<const void *>(rcp_kernel), dim3(grid), dim3(threads), args, 0, stream);
+}
+
+const void *vec_kernel_ptr(int variant, bool inter, int w, int unroll, bool nc) {
+    return reinterpret_cast<const void *>(vec_kernel(variant, inter, w, unroll, nc));
+}
+
+}  // namespace sincos_b200

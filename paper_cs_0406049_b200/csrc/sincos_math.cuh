@@ -1,0 +1,101 @@
+// sincos_math.cuh -- per-element device math of the hot path (sm_100a).
+//
+// The paper's method, PAPER.md P:50-57 and Fig. 1, restated for one
+// CUDA thread and one fp32 angle.  Every operation is an explicit
+// round-to-nearest intrinsic so that nvcc neither contracts nor reorders:
+//   __fmul_rn  = vec_madd(a, b, 0.0)            (a single rounded product)
+//   __fmaf_rn  = vec_madd / vec_nmsub with a non-zero addend (single rounding)
+//   rintf      = vec_round (nearest, ties to even; cvt.rni.f32.f32 -> FRND)
+// The library is built with -fmad=false -ftz=false as a second guard.
+// The path has no value-dependent control flow: SASS of the
+// value path is FMUL/FFMA/FADD/FRND (+ F2F/MUFU.RCP64H/DFMA for variant A).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace sincos_b200 {
+
+enum Variant : int { kNormalized = 0, kRenormalized = 1 };
+
+// Scale constant of Fig. 1, (vector float)(1.0/(2.0*3.1415926536)),
+// which rounds to the same fp32 as 1/(2 pi): 0x3E22F983 (reading G12).
+__device__ constexpr float kInvTwoPi = 0x1.45f306p-3f;
+
+// Quarter-angle series coefficients, each the fp32 rounding of the decimal
+// the paper prints (Fig. 1 casts the double literal to vector float).
+template <int V> struct Series;
+
+// Method 1, "normalised": P:140-148 == Fig. 1 P:246-258.
+template <> struct Series<kNormalized> {
+    static constexpr float ss1 =  0x1.921fb6p+0f;   //  1.5707963235
+    static constexpr float ss2 = -0x1.4abbbep-1f;   // -0.645963615
+    static constexpr float ss3 =  0x1.46609cp-4f;   //  0.0796819754
+    static constexpr float ss4 = -0x1.2df648p-8f;   // -0.0046075748
+    static constexpr float cc1 = -0x1.3bd39ep+0f;   // -1.2336977925
+    static constexpr float cc2 =  0x1.03b1fap-2f;   //  0.2536086171
+    static constexpr float cc3 = -0x1.4ee010p-6f;   // -0.0204391631
+};
+
+// Method 2, "angle-accurate" (dagger): Fig. 1 P:230-242.  ss2 is the Fig. 1
+// value -0.6466386396 (the text P:161 transposes two digits; reading G1).
+template <> struct Series<kRenormalized> {
+    static constexpr float ss1 =  0x1.921fb6p+0f;   //  1.5707963268
+    static constexpr float ss2 = -0x1.4b1438p-1f;   // -0.6466386396
+    static constexpr float ss3 =  0x1.16296cp-4f;   //  0.0679105987
+    static constexpr float ss4 = -0x1.2f6682p-10f;  // -0.0011573807
+    static constexpr float cc1 = -0x1.3beff2p+0f;   // -1.2341299769
+    static constexpr float cc2 =  0x1.f8e08ap-3f;   //  0.2465220241
+    static constexpr float cc3 = -0x1.9614d0p-7f;   // -0.0123926179
+};
+
+// Correctly rounded fp32 reciprocal RN(1/d), branch-free ("precise reciprocal",
+// P:157-158, Fig. 1; the paper's Reciprocal() body is not listed).
+// fp64 seed from MUFU.RCP64H, three Newton steps in DFMA (each squares the
+// relative error: ~2^-22 -> 2^-44 -> below 2^-53), then one rounding to fp32.
+// Exact because 1/d for a 24-bit d is never within 2^-48 (relative) of an
+// fp32 rounding midpoint while the fp64 value is within a few 2^-53 (reading
+// G3; verified over every fp32 d in [0.5, 2) by tests/test_gpu_parity.py).
+// rcp.rn.f32 would also be exact but compiles to a slow-path branch.
+__device__ __forceinline__ float rcp_rn(float d) {
+    const double x = static_cast<double>(d);
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = __fma_rn(-x, y, 1.0);
+    y = __fma_rn(y, e, y);
+    e = __fma_rn(-x, y, 1.0);
+    y = __fma_rn(y, e, y);
+    e = __fma_rn(-x, y, 1.0);
+    y = __fma_rn(y, e, y);
+    return __double2float_rn(y);
+}
+
+// One pair.  Step letters follow DESIGN.md section 2.
+template <int V>
+__device__ __forceinline__ void sincos_pair(float theta, float &s_out, float &c_out) {
+    using K = Series<V>;
+    // a2-a3  turn reduction
+    const float x1 = __fmul_rn(theta, kInvTwoPi);
+    const float q1 = __fsub_rn(x1, rintf(x1));          // exact; q1 in [-1/2, 1/2]
+    // a4-a5  quarter-angle series, P:280-310 (Horner, innermost first)
+    const float q2 = __fmul_rn(q1, q1);
+    const float s1 = __fmul_rn(q1, __fmaf_rn(q2, __fmaf_rn(q2, __fmaf_rn(q2, K::ss4, K::ss3), K::ss2), K::ss1));
+    const float c1 = __fmaf_rn(q2, __fmaf_rn(q2, __fmaf_rn(q2, K::cc3, K::cc2), K::cc1), 1.0f);
+    // a6  first doubling, Eq. (1) in Fig. 1 order
+    const float c2 = __fmaf_rn(-s1, s1, __fmul_rn(c1, c1));
+    const float s2 = __fmul_rn(2.0f, __fmul_rn(s1, c1));
+    // a7  amplitude factor from the penultimate pair
+    const float c2c2 = __fmul_rn(c2, c2);
+    float f;
+    if (V == kNormalized)
+        f = __fmaf_rn(-s2, s2, __fmaf_rn(-c2, c2, 2.0f));
+    else
+        f = rcp_rn(__fmaf_rn(s2, s2, c2c2));
+    // a8  second doubling
+    const float c3 = __fmaf_rn(-s2, s2, c2c2);
+    const float s3 = __fmul_rn(2.0f, __fmul_rn(s2, c2));
+    // a9  apply
+    c_out = __fmul_rn(c3, f);
+    s_out = __fmul_rn(s3, f);
+}
+
+}  // namespace sincos_b200

@@ -1,0 +1,162 @@
+"""The C-ABI library without a GPU: it builds for sm_100a, loads, exports every symbol
+include/*.h declares, validates arguments before any CUDA call, and its SASS keeps the
+value path branch-free (tiers T1 and T5)."""
+import ctypes
+import glob
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_cs_0406049_b200 as sp
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+OK, INVALID, OVERLAP = 0, 1, 2
+
+
+@pytest.fixture(scope="module")
+def L():
+    return sp.lib()
+
+
+def declared_symbols():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        names |= set(re.findall(r"SINCOS_API\s+[\w\s\*]*?\b(sincos_\w+)\s*\(", src))
+    return names
+
+
+def test_every_declared_symbol_is_exported(L):
+    names = declared_symbols()
+    assert len(names) >= 15
+    out = subprocess.run(["nm", "-D", "--defined-only", sp.library_path], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (sincos_\w+)", out))
+    assert names <= exported, names - exported
+    assert set(sp.EXPORTS) <= names
+    for n in names:
+        getattr(L, n)
+
+
+def test_only_the_abi_is_exported():
+    out = subprocess.run(["nm", "-D", "--defined-only", sp.library_path], capture_output=True, text=True).stdout
+    ours = [s for s in re.findall(r"\bT (\w+)", out) if not s.startswith("_")]
+    assert set(ours) == declared_symbols(), set(ours) ^ declared_symbols()
+
+
+def test_version_and_status_strings(L):
+    assert b"sm_100a" in L.sincos_version()
+    for s in range(4):
+        assert L.sincos_status_string(s)
+
+
+def test_library_is_sm100a_cubin():
+    out = subprocess.run(["cuobjdump", "--list-elf", sp.library_path], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+A = 0x10000  # fake, 256-aligned "device" addresses: validation never dereferences them
+
+
+def test_validation_before_cuda(L):
+    # n == 0 is a no-op, pointers may be NULL
+    assert L.sincos_pairs(None, None, None, None, 0, 0, None) == OK
+    # NULL theta, neither / both output forms, unknown variant
+    assert L.sincos_pairs(None, A, 2 * A, None, 16, 0, None) == INVALID
+    assert L.sincos_pairs(A, None, None, None, 16, 0, None) == INVALID
+    assert L.sincos_pairs(A, 2 * A, 3 * A, 4 * A, 16, 0, None) == INVALID
+    assert L.sincos_pairs(A, 2 * A, None, None, 16, 0, None) == INVALID
+    assert L.sincos_pairs(A, 2 * A, 3 * A, None, 16, 7, None) == INVALID
+    assert L.sincos_pairs(A, 2 * A, 3 * A, None, 16, -1, None) == INVALID
+    # not 4-byte aligned
+    assert L.sincos_pairs(A + 2, 2 * A, 3 * A, None, 16, 0, None) == INVALID
+    assert L.sincos_pairs(A, 2 * A + 1, 3 * A, None, 16, 0, None) == INVALID
+
+
+def test_overlap_rules(L):
+    n = 1024
+    # sin and cos overlap
+    assert L.sincos_pairs(A, 2 * A, 2 * A + 4 * (n - 1), None, n, 0, None) == OVERLAP
+    # partial theta / sin overlap
+    assert L.sincos_pairs(A, A + 4, 3 * A, None, n, 0, None) == OVERLAP
+    # theta inside the interleaved output
+    assert L.sincos_pairs(A + 8, None, None, A, n, 0, None) == OVERLAP
+    # exact in-place theta == sin is allowed: passes validation, then needs CUDA
+    st = L.sincos_pairs(A, A, 3 * A, None, n, 0, None)
+    assert st in (OK, 3)  # 3 = SINCOS_ERR_CUDA here (no GPU)
+
+
+def test_host_path_validation(L):
+    assert L.sincos_pairs_host(None, None, None, None, 0, 0, None, 0, None) == OK
+    buf = (ctypes.c_float * 64)()
+    p = ctypes.addressof(buf)
+    assert L.sincos_pairs_host(p, p + 64, p + 128, None, 16, 0, None, 1 << 30, None) == INVALID  # no workspace
+    assert L.sincos_pairs_host(p, p + 64, p + 128, None, 16, 0, A, 100, None) == INVALID          # too small
+    assert L.sincos_pairs_host(p, p + 4, p + 128, None, 16, 0, A, 1 << 30, None) == OVERLAP
+
+
+def test_launch_config_validation(L):
+    assert L.sincos_set_launch_config(100, 0, 8, 2) == -1
+    assert L.sincos_set_launch_config(256, 0, 3, 2) == -1
+    assert L.sincos_set_launch_config(256, 0, 8, 3) == -1
+    assert L.sincos_set_launch_config(256, 0, 8, 2) == 0
+    assert sp.get_launch_config() == {"threads": 256, "blocks_per_sm": 0, "vec": 8, "unroll": 2}
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 8, 9, 1000, 1 << 20, (1 << 32) + 5, (1 << 30) + 3])
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
+def test_shard_range_partitions(n, G):
+    """contiguous, 8-element aligned starts, cover [0, n) exactly, balanced."""
+    ranges = [sp.shard_range(n, G, g) for g in range(G)]
+    assert ranges[0][0] == 0 and ranges[-1][1] == n
+    for (lo, hi), (lo2, _) in zip(ranges, ranges[1:]):
+        assert hi == lo2
+    for lo, hi in ranges:
+        assert lo % 8 == 0 and lo <= hi
+        assert hi - lo <= -(-n // G) + 8
+    with pytest.raises(ValueError):
+        sp.shard_range(n, G, G)
+
+
+def test_stats_record_is_64_bytes(L):
+    assert ctypes.sizeof(sp.Stats) == 64
+    assert L.sincos_stats_workspace_bytes() > 0
+
+
+def _sass():
+    return subprocess.run(["cuobjdump", "-sass", sp.library_path], capture_output=True, text=True).stdout
+
+
+def test_sass_value_path_branch_free():
+    """no CALL/FCHK slow paths, no fp32 MUFU.RCP; the variant-A reciprocal is the
+    fp64 MUFU.RCP64H + DFMA sequence; branches do not grow with the elements per thread."""
+    sass = _sass()
+    funcs = re.split(r"\n\s*Function : ", sass)
+    seen = 0
+    for f in funcs:
+        name = f.split("\n", 1)[0]
+        if "sincos_vec_kernel" not in name:
+            continue
+        seen += 1
+        body = f
+        assert " CALL" not in body and "FCHK" not in body, name
+        assert not re.search(r"MUFU\.RCP\s", body), name
+        nbra = len(re.findall(r"\bBRA\b", body))
+        assert nbra <= 16, (name, nbra)
+        if "ILi1E" in name.split("sincos_vec_kernel")[1][:6]:
+            assert "MUFU.RCP64H" in body and "DFMA" in body, name
+        # the loads/stores are the wide streaming forms
+        assert re.search(r"LDG\.E\.[A-Z0-9.]*(128|256)", body), name
+        assert re.search(r"STG\.E\.[A-Z0-9.]*(128|256)", body), name
+    assert seen >= 48
+
+
+def test_product_never_touches_the_oracle():
+    """The oracle is test infrastructure: nothing under the package imports, links or includes it."""
+    pkg = os.path.join(ROOT, "paper_cs_0406049_b200")
+    for path in glob.glob(os.path.join(pkg, "**", "*"), recursive=True):
+        if not os.path.isfile(path) or path.endswith(".so") or "__pycache__" in path:
+            continue
+        src = open(path, errors="ignore").read()
+        assert not re.search(r"\bimport\s+oracle|from\s+oracle|sincos_oracle|liboracle", src), path

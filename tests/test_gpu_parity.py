@@ -1,0 +1,387 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element
+(SURVEY 4 tier T2).  All tests need a B200: ``pytest -m gpu``.
+
+Bar: bit-exact by value (signed zeros and NaN payloads aside; reading G15 -- the
+algorithm fixes one bit pattern per input), which implies the north_star bound
+|delta| <= 4 ulp of 1.0 per component (ULP4 in helpers.py), also asserted."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+from helpers import ULP4, assert_parity, oracle_threaded, same_values
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_cs_0406049_b200 as sp  # noqa: E402
+
+VARIANTS = [oracle.VARIANT_N, oracle.VARIANT_A]   # same numbering as sp.NORMALIZED / sp.RENORMALIZED
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    sp.set_launch_config()          # the default config bench.py times
+    torch.cuda.init()
+    yield
+
+
+def run(theta_np, variant, inter=False):
+    t = torch.from_numpy(np.ascontiguousarray(theta_np, dtype=np.float32)).cuda()
+    if inter:
+        o = torch.empty(2 * t.numel(), dtype=torch.float32, device="cuda")
+        sp.sincos_pairs(t, interleaved_out=o, variant=variant)
+        torch.cuda.synchronize()
+        o = o.cpu().numpy()
+        return o[1::2].copy(), o[0::2].copy()
+    s, c = torch.empty_like(t), torch.empty_like(t)
+    sp.sincos_pairs(t, s, c, variant=variant)
+    torch.cuda.synchronize()
+    return s.cpu().numpy(), c.cpu().numpy()
+
+
+# ---- configs C1 and C3 in full, C2 in full at bench size -------------------------------
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("inter", [False, True])
+def test_c1_full(variant, inter):
+    """BASELINE configs[0]: 2^20 U[-pi, pi), seed 0 -- every element vs the oracle, and the
+    error vs long double never exceeds the oracle's own (BJ:5)."""
+    th = inputs.generate(1)
+    s, c = run(th, variant, inter)
+    os_, oc = oracle.sincos(th, variant)
+    assert_parity(s, c, os_, oc, "C1")
+    g = oracle.error_stats(th, s, c, oracle.REF_LONGDOUBLE)
+    o = oracle.error_stats(th, os_, oc, oracle.REF_LONGDOUBLE)
+    assert g.max_comb <= o.max_comb and g.count == th.size
+    assert g.max_comb <= 1.25 * (4.8e-7 if variant == 0 else 3.8e-7)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_c3_edge_set_full(variant):
+    """BASELINE configs[2]: 2^24 edge/stress set (multiples of pi/2 and pi, +-64 ulp around
+    (2n+1)pi, signed zeros, subnormals, log-uniform 1e-30..2^20), interleaved output."""
+    th = inputs.generate(3)
+    s, c = run(th, variant, inter=True)
+    os_, oc = oracle_threaded(th, variant)
+    assert_parity(s, c, os_, oc, "C3")
+    # signed zeros and subnormals: sin(+-0) == 0, cos == 1; subnormal sine is gradual
+    z = th == 0
+    assert np.all(s[z] == 0) and np.all(c[z] == 1)
+    sub = (th != 0) & (np.abs(th) < np.float32(2.0 ** -126))
+    assert np.all(c[sub] == 1) and np.count_nonzero(s[sub]) > 0.9 * np.count_nonzero(sub)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_c2_full_size(variant):
+    """BASELINE configs[1]: 2^28 U[-1e4, 1e4], seed 1, split, every element, in the launch
+    configuration bench.py times."""
+    th = inputs.generate(2)
+    s, c = run(th, variant)
+    os_, oc = oracle_threaded(th, variant)
+    assert_parity(s, c, os_, oc, "C2")
+
+
+def sampled_indices(n, m=1 << 20, seed=0):
+    rng = np.random.default_rng(seed)
+    idx = np.concatenate([np.arange(0, 4096), np.arange(n - 4096, n), rng.integers(0, n, m)])
+    return np.unique(idx).astype(np.int64)
+
+
+def gen_to_device(config, n, chunk=1 << 28):
+    dev = torch.empty(n, dtype=torch.float32, device="cuda")
+    host = torch.empty(min(chunk, n), dtype=torch.float32).pin_memory()
+    for off in range(0, n, chunk):
+        m = min(chunk, n - off)
+        inputs.generate(config, off, m, out=host.numpy()[:m])
+        dev[off:off + m].copy_(host[:m])
+    return dev
+
+
+def test_c4_full_size_sampled():
+    """BASELINE configs[3]: 2^30 NUFFT phases, interleaved, full size on one GPU; ~1M sampled
+    elements (incl. both ends) vs the oracle on the regenerated inputs."""
+    n = inputs.size(4)
+    th = gen_to_device(4, n)
+    o = torch.empty(2 * n, dtype=torch.float32, device="cuda")
+    for variant in VARIANTS:
+        sp.sincos_pairs(th, interleaved_out=o, variant=variant)
+        torch.cuda.synchronize()
+        idx = sampled_indices(n, seed=variant)
+        it = torch.from_numpy(idx).cuda()
+        ov = o.view(n, 2)[it].cpu().numpy()
+        want_th = inputs.generate_at(4, idx.astype(np.uint64))
+        assert np.array_equal(th[it].cpu().numpy().view(np.uint32), want_th.view(np.uint32))
+        os_, oc = oracle.sincos(want_th, variant)
+        assert_parity(ov[:, 1].copy(), ov[:, 0].copy(), os_, oc, "C4")
+    del th, o
+    torch.cuda.empty_cache()
+
+
+def test_c5_full_size_sampled_and_sharded():
+    """BASELINE configs[4]: 2^32 N(0, 100^2) (16 GiB in, 32 GiB out) on one GPU with 64-bit
+    indexing; sampled elements vs the oracle; then the same array as 8 contiguous shards
+    (sincos_pairs_sharded, all on this device) must reproduce the one-shot output bit for bit."""
+    n = inputs.size(5)
+    th = gen_to_device(5, n)
+    s = torch.empty(n, dtype=torch.float32, device="cuda")
+    c = torch.empty(n, dtype=torch.float32, device="cuda")
+    variant = oracle.VARIANT_A
+    sp.sincos_pairs(th, s, c, variant=variant)
+    torch.cuda.synchronize()
+    idx = sampled_indices(n, seed=5)
+    it = torch.from_numpy(idx).cuda()
+    want_th = inputs.generate_at(5, idx.astype(np.uint64))
+    assert np.array_equal(th[it].cpu().numpy().view(np.uint32), want_th.view(np.uint32))
+    os_, oc = oracle.sincos(want_th, variant)
+    assert_parity(s[it].cpu().numpy(), c[it].cpu().numpy(), os_, oc, "C5")
+    # elements past 2^31 and 2^32-1 exist and are not garbage
+    assert int(idx.max()) == n - 1
+    # sharded run into fresh buffers
+    s2 = torch.empty_like(s)
+    c2 = torch.empty_like(c)
+    G = 8
+    shards = []
+    for g in range(G):
+        lo, hi = sp.shard_range(n, G, g)
+        shards.append({"theta": th[lo:hi], "sin": s2[lo:hi], "cos": c2[lo:hi]})
+    sp.sincos_pairs_sharded(shards, variant=variant)
+    torch.cuda.synchronize()
+    assert torch.equal(s.view(torch.int32), s2.view(torch.int32))
+    assert torch.equal(c.view(torch.int32), c2.view(torch.int32))
+    del th, s, c, s2, c2
+    torch.cuda.empty_cache()
+
+
+# ---- whole input space -------------------------------------------------------------
+
+M1 = 0x9E3779B97F4A7C15
+M2 = 0xBF58476D1CE4E5B9
+M3 = 0x94D049BB133111EB
+MU = 0xD6E8FEB86659FD93
+
+
+def _s64(x):
+    return x - (1 << 64) if x >= (1 << 63) else x
+
+
+def _lsr(z, k):
+    return (z >> k) & ((1 << (64 - k)) - 1)
+
+
+def _hash_chunk(u0, s, c):
+    """The SURVEY [X13] hash of GPU outputs, computed with torch int64 ops on the device
+    (test-side code; wrapping 64-bit arithmetic)."""
+    n = s.numel()
+    sb = s.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    cb = c.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    sb = torch.where(torch.isnan(s), torch.full_like(sb, 0x7FC00000), sb)
+    cb = torch.where(torch.isnan(c), torch.full_like(cb, 0x7FC00000), cb)
+    sb = torch.where(s == 0, torch.zeros_like(sb), sb)
+    cb = torch.where(c == 0, torch.zeros_like(cb), cb)
+    key = (sb << 32) | cb
+    u = torch.arange(u0, u0 + n, dtype=torch.int64, device=s.device)
+    z = key ^ (u * _s64(MU))
+    z = z + _s64(M1)
+    z = (z ^ _lsr(z, 30)) * _s64(M2)
+    z = (z ^ _lsr(z, 27)) * _s64(M3)
+    z = z ^ _lsr(z, 31)
+    h = int(z.sum().item()) % (1 << 64)
+    nan = int((torch.isnan(s) | torch.isnan(c)).sum().item())
+    ex = int(((s == 0) & (c == 1)).sum().item())
+    return h, nan, ex
+
+
+def test_hash_helper_matches_oracle_hash():
+    """The torch hash above equals the oracle's C hash on the same outputs (host copy)."""
+    u0 = 0x3F000000
+    th = np.arange(u0, u0 + (1 << 16), dtype=np.uint32).view(np.float32)
+    s, c = oracle.sincos(th, 0)
+    h, _, _ = _hash_chunk(u0, torch.from_numpy(s).cuda(), torch.from_numpy(c).cuda())
+    assert h == oracle.hash_outputs(s=s, c=c, first_bits=u0)
+
+
+@pytest.mark.parametrize("variant,name", [(oracle.VARIANT_N, "N"), (oracle.VARIANT_A, "A")])
+def test_all_fp32_bit_patterns(golden, variant, name):
+    """Every one of the 2^32 fp32 inputs: the hash, NaN count and exact-(0,1) count of the GPU
+    outputs equal the oracle's committed whole-space run (tests/golden/oracle_exhaustive.json),
+    which equals the survey's independent transcription [X13]."""
+    import json
+    run_ = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_exhaustive.json")))
+    want = run_[name]["all_bits"]
+    assert want["hash"] == golden["survey_crosscheck"]["all_bits_hash"][name]
+    chunk = 1 << 28
+    s = torch.empty(chunk, dtype=torch.float32, device="cuda")
+    c = torch.empty(chunk, dtype=torch.float32, device="cuda")
+    H, NN, EX = 0, 0, 0
+    for u0 in range(0, 1 << 32, chunk):
+        th = torch.arange(u0, u0 + chunk, dtype=torch.int64, device="cuda").to(torch.int32).view(torch.float32)
+        sp.sincos_pairs(th, s, c, variant=variant)
+        h, nn, ex = _hash_chunk(u0, s, c)
+        H, NN, EX = (H + h) % (1 << 64), NN + nn, EX + ex
+    assert "0x%016X" % H == want["hash"]
+    assert NN == want["nan_pairs"] and EX == want["exact_0_1"]
+
+
+def test_reciprocal_exhaustive():
+    """Reading G3: the kernel's reciprocal equals IEEE RN(1/d) (CPU 1.0f/d) for every fp32 d in
+    [0.5, 2), which contains every s2^2 + c2^2 the method produces ([X10])."""
+    d = np.arange(0x3F000000, 0x40000000, dtype=np.uint32).view(np.float32)
+    want = np.float32(1.0) / d
+    dt = torch.from_numpy(d).cuda()
+    out = torch.empty_like(dt)
+    sp.debug_reciprocal(dt, out)
+    got = out.cpu().numpy()
+    bad = np.flatnonzero(got.view(np.uint32) != want.view(np.uint32))
+    assert bad.size == 0, (bad.size, d[bad[:5]])
+
+
+# ---- edge cases: lengths, alignment, in-place, every kernel instance ------------------
+
+def test_lengths_and_alignments():
+    """lengths 0..257 at every element offset 0..7 of theta and outputs, shared
+    (vector path with scalar head/tail) and unshared (scalar path) alignment, both layouts."""
+    rng = np.random.default_rng(11)
+    base = rng.uniform(-50, 50, 4096).astype(np.float32)
+    ref = {v: oracle.sincos(base, v) for v in VARIANTS}
+    big_t = torch.from_numpy(base).cuda()
+    big_s = torch.empty(4096 + 64, dtype=torch.float32, device="cuda")
+    big_c = torch.empty(4096 + 64, dtype=torch.float32, device="cuda")
+    big_i = torch.empty(2 * 4096 + 64, dtype=torch.float32, device="cuda")
+    for variant in VARIANTS:
+        rs, rc = ref[variant]
+        for n in list(range(0, 258)) + [1000, 4000]:
+            for (ot, oo) in ((0, 0), (1, 1), (3, 3), (5, 5), (7, 7), (1, 0), (0, 3), (2, 6)):
+                if ot + n > 4096:
+                    continue
+                t = big_t[ot:ot + n]
+                s = big_s[oo:oo + n]
+                c = big_c[oo + 32:oo + 32 + n] if n <= 4096 - 32 else None
+                if c is None:
+                    continue
+                sp.sincos_pairs(t, s, c, variant=variant)
+                io = big_i[2 * oo:2 * oo + 2 * n]
+                sp.sincos_pairs(t, interleaved_out=io, variant=variant)
+                torch.cuda.synchronize()
+                assert_parity(s.cpu().numpy(), c.cpu().numpy(), rs[ot:ot + n], rc[ot:ot + n], f"n={n} off={ot},{oo}")
+                iv = io.cpu().numpy()
+                assert_parity(iv[1::2], iv[0::2], rs[ot:ot + n], rc[ot:ot + n], f"inter n={n} off={ot},{oo}")
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_in_place(variant):
+    th = inputs.generate(1, 0, (1 << 16) + 5)
+    os_, oc = oracle.sincos(th, variant)
+    t = torch.from_numpy(th).cuda()
+    c = torch.empty_like(t)
+    sp.sincos_pairs(t, t, c, variant=variant)           # sin overwrites theta
+    torch.cuda.synchronize()
+    assert_parity(t.cpu().numpy(), c.cpu().numpy(), os_, oc, "in-place sin")
+    t = torch.from_numpy(th).cuda()
+    s = torch.empty_like(t)
+    sp.sincos_pairs(t, s, t, variant=variant)           # cos overwrites theta
+    torch.cuda.synchronize()
+    assert_parity(s.cpu().numpy(), t.cpu().numpy(), os_, oc, "in-place cos")
+
+
+@pytest.mark.parametrize("threads", [128, 256, 512])
+@pytest.mark.parametrize("vec", [4, 8])
+@pytest.mark.parametrize("unroll", [1, 2, 4])
+def test_every_kernel_instance(threads, vec, unroll):
+    """Every (threads, vector width, unroll) the tuner can select, both variants and layouts,
+    on a ragged size spanning many grid-stride trips, and a 2-block grid (long strides)."""
+    th = inputs.generate(2, 12345, (1 << 20) + 13)
+    want = {v: oracle.sincos(th, v) for v in VARIANTS}
+    try:
+        for bps in (0, 1):
+            sp.set_launch_config(threads, bps, vec, unroll)
+            for variant in VARIANTS:
+                for inter in (False, True):
+                    s, c = run(th, variant, inter)
+                    assert_parity(s, c, *want[variant], f"t{threads} v{vec} u{unroll} bps{bps} inter={inter}")
+    finally:
+        sp.set_launch_config()
+
+
+def test_special_values_gpu():
+    th = np.array([0.0, -0.0, np.nan, np.inf, -np.inf, 1e-45, -1e-45, 1e-40, 3.4e38, -3.4e38,
+                   math.pi, -math.pi, math.pi / 2, 1e30] * 3, dtype=np.float32)
+    for variant in VARIANTS:
+        s, c = run(th, variant)
+        os_, oc = oracle.sincos(th, variant)
+        assert_parity(s, c, os_, oc, "special")
+        assert np.isnan(s[2]) and np.isnan(c[3]) and np.isnan(s[4])
+
+
+# ---- host path, stats kernel, null kernel, launch accounting ---------------------------
+
+@pytest.mark.parametrize("inter", [False, True])
+def test_host_buffer_path(inter):
+    """sincos_pairs_host (chunked H2D -> kernel -> D2H over three streams) equals the oracle;
+    a small workspace forces many chunks and a ragged last one."""
+    n = (1 << 21) + 77
+    th = inputs.generate(3, 0, n)
+    th_h = torch.from_numpy(th).pin_memory()
+    ws = torch.empty(sp.host_workspace_min_bytes(), dtype=torch.uint8, device="cuda")
+    for variant in VARIANTS:
+        if inter:
+            o = torch.empty(2 * n, dtype=torch.float32).pin_memory()
+            sp.sincos_pairs_host(th_h, interleaved_out=o, variant=variant, workspace=ws)
+            s, c = o.numpy()[1::2], o.numpy()[0::2]
+        else:
+            s_h = torch.empty(n, dtype=torch.float32).pin_memory()
+            c_h = torch.empty(n, dtype=torch.float32).pin_memory()
+            sp.sincos_pairs_host(th_h, s_h, c_h, variant=variant, workspace=ws)
+            s, c = s_h.numpy(), c_h.numpy()
+        os_, oc = oracle_threaded(th, variant)
+        assert_parity(s, c, os_, oc, "host path")
+
+
+def test_stats_kernel_matches_oracle_metrics():
+    """KB5 (fp64 on the device) vs the oracle's P:135-139 metrics with double libm."""
+    th = inputs.generate(1)
+    for variant in VARIANTS:
+        t = torch.from_numpy(th).cuda()
+        s, c = torch.empty_like(t), torch.empty_like(t)
+        sp.sincos_pairs(t, s, c, variant=variant)
+        st = sp.error_stats(t, s, c)
+        ref = oracle.error_stats(th, s.cpu().numpy(), c.cpu().numpy())
+        assert st["n"] == ref.count and st["nan_count"] == ref.nan_count
+        assert abs(st["max_comb"] - ref.max_comb) <= 1e-12
+        assert abs(st["rms"] - ref.rms) / ref.rms < 1e-9
+        assert abs(st["max_amp"] - ref.max_amp) <= 1e-12
+        st2 = sp.error_stats(t, s, c)
+        assert st2["raw"] == st["raw"]                       # deterministic
+    t = torch.tensor([0.0, float("nan"), float("inf")], device="cuda")
+    s, c = torch.empty_like(t), torch.empty_like(t)
+    sp.sincos_pairs(t, s, c)
+    st = sp.error_stats(t, s, c)
+    assert st["n"] == 1 and st["nan_count"] == 2 and st["max_comb"] == 0.0
+
+
+def test_null_kernel_copies():
+    th = inputs.generate(1, 0, 1000003)
+    t = torch.from_numpy(th).cuda()
+    s, c = torch.empty_like(t), torch.empty_like(t)
+    sp.null_4in8out(t, s, c)
+    o = torch.empty(2 * t.numel(), device="cuda")
+    sp.null_4in8out(t, interleaved_out=o)
+    torch.cuda.synchronize()
+    assert torch.equal(s, t) and torch.equal(c, t) and torch.equal(o[0::2], t) and torch.equal(o[1::2], t)
+
+
+def test_launches_are_counted():
+    before = sp.launch_count()
+    t = torch.zeros(100, device="cuda")
+    sp.sincos(t)
+    assert sp.launch_count() == before + 1
+
+
+def test_rejects_cpu_tensors():
+    with pytest.raises(ValueError):
+        sp.sincos_pairs(torch.zeros(8), torch.zeros(8), torch.zeros(8))

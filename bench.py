@@ -367,11 +367,10 @@ def run_ours(args, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
     if args.sweep and rank == 0:
-        for threads in (128, 256, 512):
-            for bps in (0, 1, 2, 4, 8):
-                for vec in (4, 8):
-                    for unroll in (1, 2, 4):
-                        sp.set_launch_config(threads, bps, vec, unroll)
+        import itertools
+        for threads, bps, vec, unroll, pf in itertools.product((256, 512), (0, 2, 4, 8, 16, 4096), (4, 8),
+                                                               (1, 2, 4), (0, 1)):
+                        sp.set_launch_config(threads, bps, vec, unroll, pf)
                         res = {}
                         for v in variants:
                             s, c = outs[v]
@@ -384,7 +383,7 @@ def run_ours(args, rank, world, local_rank):
                             b.record(stream)
                             torch.cuda.synchronize(dev)
                             res["N" if v == 0 else "A"] = BYTES_PER_PAIR * n / (a.elapsed_time(b) / 10 / 1e3) / 1e9
-                        print(json.dumps({"sweep": [threads, bps, vec, unroll], "GBps": res}), flush=True)
+                        print(json.dumps({"sweep": [threads, bps, vec, unroll, pf], "GBps": res}), flush=True)
 
 
 def main():

@@ -150,13 +150,17 @@ SINCOS_API sincos_status_t sincos_error_stats(const float *theta_dev, const floa
                                    const float *cos_dev, const float *inter_dev, size_t n,
                                    sincos_stats_t *stats_dev, void *ws_dev, void *stream);
 
-/* Launch tuning (bench / tests): threads per block, resident blocks per SM
- * for the grid-stride grid (0 = occupancy maximum), vector width in floats per
- * thread access (4 or 8), unroll U (1, 2 or 4 independent vectors in flight
- * per thread: the GPU form of "computes two vectors at a time").
+/* Launch tuning (bench / tests).  threads per block (128, 256, 512);
+ * blocks_per_sm: 0 = the full grid, one trip per thread (the default, measured
+ * fastest); > 0 = a grid-stride grid of SMs x blocks_per_sm blocks; vec: floats per thread access (4 = 128-bit, 8 = 256-bit);
+ * unroll U (1, 2, 4 independent vectors in flight per thread: the GPU form of
+ * "computes two vectors at a time"); prefetch (0/1): software-
+ * pipelined loads (the next trip's loads issued before this trip's math).
  * Process-global; returns -1 for unsupported values. */
-SINCOS_API int sincos_set_launch_config(int threads, int blocks_per_sm, int vec, int unroll);
-SINCOS_API void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *vec, int *unroll);
+SINCOS_API int sincos_set_launch_config(int threads, int blocks_per_sm, int vec, int unroll, int prefetch);
+/* Defaults: threads 128, blocks_per_sm 0, vec 8, unroll 1, prefetch 0. */
+SINCOS_API void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *vec, int *unroll,
+                                         int *prefetch);
 
 /* Traffic-ceiling kernel (bench only): same access pattern and launch as
  * sincos_pairs, no arithmetic (writes theta to both outputs). */

@@ -63,8 +63,8 @@ _SIGS = {
     "sincos_pairs_sharded": (_I, [ctypes.POINTER(Shard), _I, _I]),
     "sincos_stats_workspace_bytes": (_S, []),
     "sincos_error_stats": (_I, [_P, _P, _P, _P, _S, _P, _P, _P]),
-    "sincos_set_launch_config": (_I, [_I, _I, _I, _I]),
-    "sincos_get_launch_config": (None, [ctypes.POINTER(_I)] * 4),
+    "sincos_set_launch_config": (_I, [_I, _I, _I, _I, _I]),
+    "sincos_get_launch_config": (None, [ctypes.POINTER(_I)] * 5),
     "sincos_null_4in8out": (_I, [_P, _P, _P, _P, _S, _P]),
     "sincos_debug_reciprocal": (_I, [_P, _P, _S, _P]),
     "sincos_status_string": (ctypes.c_char_p, [_I]),
@@ -215,15 +215,25 @@ def error_stats(theta, sin_out=None, cos_out=None, interleaved_out=None, stream=
     return d
 
 
-def set_launch_config(threads=256, blocks_per_sm=0, vec=8, unroll=2):
-    if lib().sincos_set_launch_config(threads, blocks_per_sm, vec, unroll) != 0:
-        raise ValueError("unsupported launch config")
+DEFAULT_LAUNCH = dict(threads=128, blocks_per_sm=0, vec=8, unroll=1, prefetch=0)
+
+
+def set_launch_config(threads=None, blocks_per_sm=None, vec=None, unroll=None, prefetch=None):
+    """Set the process-global launch configuration; omitted fields take the library defaults."""
+    cfg = dict(DEFAULT_LAUNCH)
+    for k, v in (("threads", threads), ("blocks_per_sm", blocks_per_sm), ("vec", vec), ("unroll", unroll),
+                 ("prefetch", prefetch)):
+        if v is not None:
+            cfg[k] = int(v)
+    if lib().sincos_set_launch_config(cfg["threads"], cfg["blocks_per_sm"], cfg["vec"], cfg["unroll"],
+                                      cfg["prefetch"]) != 0:
+        raise ValueError(f"unsupported launch config {cfg}")
 
 
 def get_launch_config() -> dict:
-    v = [ctypes.c_int() for _ in range(4)]
+    v = [ctypes.c_int() for _ in range(5)]
     lib().sincos_get_launch_config(*[ctypes.byref(x) for x in v])
-    return dict(zip(("threads", "blocks_per_sm", "vec", "unroll"), (x.value for x in v)))
+    return dict(zip(("threads", "blocks_per_sm", "vec", "unroll", "prefetch"), (x.value for x in v)))
 
 
 def null_4in8out(theta, sin_out=None, cos_out=None, interleaved_out=None, stream=None):

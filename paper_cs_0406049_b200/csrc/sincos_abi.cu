@@ -22,10 +22,11 @@ namespace {
 thread_local int g_last_cuda_error = 0;
 std::atomic<uint64_t> g_launches{0};
 
-std::atomic<int> g_threads{256};
+std::atomic<int> g_threads{128};
 std::atomic<int> g_blocks_per_sm{0};
 std::atomic<int> g_vec{8};
-std::atomic<int> g_unroll{2};
+std::atomic<int> g_unroll{1};
+std::atomic<int> g_prefetch{0};
 
 constexpr int kMaxDev = 64;
 std::atomic<int> g_sm_count[kMaxDev];
@@ -48,30 +49,6 @@ int sm_count(int dev) {
         g_sm_count[dev].store(v, std::memory_order_relaxed);
     }
     return v;
-}
-
-// Resident blocks per SM of a kernel at a block size (cached; occupancy is a
-// property of the kernel and the architecture, identical on every B200).
-struct OccEntry {
-    const void *fn;
-    int threads;
-    int blocks;
-};
-std::mutex g_occ_mu;
-OccEntry g_occ[256];
-int g_occ_n = 0;
-
-int occupancy(const void *fn, int threads) {
-    {
-        std::lock_guard<std::mutex> lk(g_occ_mu);
-        for (int i = 0; i < g_occ_n; ++i)
-            if (g_occ[i].fn == fn && g_occ[i].threads == threads) return g_occ[i].blocks;
-    }
-    int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, 0) != cudaSuccess || b <= 0) b = 1;
-    std::lock_guard<std::mutex> lk(g_occ_mu);
-    if (g_occ_n < 256) g_occ[g_occ_n++] = OccEntry{fn, threads, b};
-    return b;
 }
 
 bool overlaps(const void *a, size_t abytes, const void *b, size_t bbytes) {
@@ -116,6 +93,7 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
     const int threads = g_threads.load(std::memory_order_relaxed);
     const int cfg_bps = g_blocks_per_sm.load(std::memory_order_relaxed);
     const int unroll = g_unroll.load(std::memory_order_relaxed);
+    const bool pf = g_prefetch.load(std::memory_order_relaxed) != 0;
 
     // Widest vector whose alignment theta and the outputs share after a scalar head.
     int w = 0;
@@ -145,13 +123,19 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
     } else {
         if (head > n) head = n;
         const size_t nvec = (n - head) / w;
-        const int bps = cfg_bps > 0 ? cfg_bps : occupancy(vec_kernel_ptr(variant, inter, w, unroll, nc), threads);
+        // Default (blocks_per_sm == 0): the full grid, one trip of `unroll` vectors per thread --
+        // measured fastest on B200.  blocks_per_sm > 0: a grid-stride grid of
+        // SMs x blocks_per_sm blocks.
         const size_t per_block = static_cast<size_t>(threads) * unroll;
         size_t need = (nvec + per_block - 1) / per_block;
         if (need < 1) need = 1;
-        const size_t cap = static_cast<size_t>(sms) * bps;
-        const unsigned grid = static_cast<unsigned>(need < cap ? need : cap);
-        e = launch_vec(variant, inter, w, unroll, nc, grid, threads, theta, so, co, io, head, nvec, n, stream);
+        if (cfg_bps > 0) {
+            const size_t cap = static_cast<size_t>(sms) * cfg_bps;
+            if (need > cap) need = cap;
+        }
+        if (need > 0x7FFFFFFFu) need = 0x7FFFFFFFu;  // grid.x limit; the kernel grid-strides past it
+        const unsigned grid = static_cast<unsigned>(need);
+        e = launch_vec(variant, inter, w, unroll, nc, pf, grid, threads, theta, so, co, io, head, nvec, n, stream);
     }
     if (e != cudaSuccess) return cuda_fail(e);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -318,19 +302,22 @@ sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
     return SINCOS_OK;
 }
 
-int sincos_set_launch_config(int threads, int blocks_per_sm, int vec, int unroll) {
+int sincos_set_launch_config(int threads, int blocks_per_sm, int vec, int unroll, int prefetch) {
     if (!(threads == 128 || threads == 256 || threads == 512)) return -1;
-    if (blocks_per_sm < 0 || blocks_per_sm > 32) return -1;
+    if (blocks_per_sm < 0 || blocks_per_sm > 4096) return -1;
+    if (prefetch != 0 && prefetch != 1) return -1;
     if (!(vec == 4 || vec == 8)) return -1;
     if (!(unroll == 1 || unroll == 2 || unroll == 4)) return -1;
     g_threads.store(threads);
     g_blocks_per_sm.store(blocks_per_sm);
     g_vec.store(vec);
     g_unroll.store(unroll);
+    g_prefetch.store(prefetch);
     return 0;
 }
 
-void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *vec, int *unroll) {
+void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *vec, int *unroll, int *prefetch) {
+    if (prefetch) *prefetch = g_prefetch.load();
     if (threads) *threads = g_threads.load();
     if (blocks_per_sm) *blocks_per_sm = g_blocks_per_sm.load();
     if (vec) *vec = g_vec.load();

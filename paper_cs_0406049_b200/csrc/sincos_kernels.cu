@@ -119,7 +119,7 @@ __device__ __forceinline__ void emit_scalar(const float *theta, size_t e, float 
 
 // KB1/KB2.  Elements [0, head) and [head + nvec*W, n) scalar; the body is nvec
 // vectors of W elements starting at element `head` (aligned by the host).
-template <int V, bool INTER, int W, int U, bool NC>
+template <int V, bool INTER, int W, int U, bool NC, bool PF>
 __global__ void __launch_bounds__(512) sincos_vec_kernel(const float *theta, float *so, float *co, float *io,
                                                          size_t head, size_t nvec, size_t n) {
     const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -128,19 +128,47 @@ __global__ void __launch_bounds__(512) sincos_vec_kernel(const float *theta, flo
     if (tid < head) emit_scalar<V, INTER>(theta, tid, so, co, io);
     if (tid < n - tail0) emit_scalar<V, INTER>(theta, tail0 + tid, so, co, io);
 
+    const float *tb = theta + head;
     size_t v = tid;
-    if constexpr (U > 1) {
+    if constexpr (PF) {
+        // Software pipeline: the U loads of trip k+1 are issued before trip k computes and
+        // stores, so every warp keeps loads in flight while it does arithmetic.
+        const size_t step = U * nthr;
+        bool have = v + (U - 1) * nthr < nvec;
+        float x[U][W];
+        if (have) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) Mem<W, NC>::load(x[u], tb + (v + u * nthr) * W);
+        }
+        while (have) {
+            const size_t nv = v + step;
+            const bool more = nv + (U - 1) * nthr < nvec;
+            float y[U][W];
+            if (more) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) Mem<W, NC>::load(y[u], tb + (nv + u * nthr) * W);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) emit<V, INTER, W>(x[u], head + (v + u * nthr) * W, so, co, io);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int k = 0; k < W; ++k) x[u][k] = y[u][k];
+            v = nv;
+            have = more;
+        }
+    } else if constexpr (U > 1) {
         for (; v + (U - 1) * nthr < nvec; v += U * nthr) {
             float x[U][W];
 #pragma unroll
-            for (int u = 0; u < U; ++u) Mem<W, NC>::load(x[u], theta + head + (v + u * nthr) * W);
+            for (int u = 0; u < U; ++u) Mem<W, NC>::load(x[u], tb + (v + u * nthr) * W);
 #pragma unroll
             for (int u = 0; u < U; ++u) emit<V, INTER, W>(x[u], head + (v + u * nthr) * W, so, co, io);
         }
     }
     for (; v < nvec; v += nthr) {
         float x[W];
-        Mem<W, NC>::load(x, theta + head + v * W);
+        Mem<W, NC>::load(x, tb + v * W);
         emit<V, INTER, W>(x, head + v * W, so, co, io);
     }
 }
@@ -164,31 +192,36 @@ __global__ void __launch_bounds__(512) rcp_kernel(const float *d, float *out, si
 using VecFn = void (*)(const float *, float *, float *, float *, size_t, size_t, size_t);
 using ScalarFn = void (*)(const float *, float *, float *, float *, size_t);
 
-template <int V, bool INTER, int W, bool NC>
+template <int V, bool INTER, int W, bool NC, bool PF>
 static VecFn pick_u(int unroll) {
     switch (unroll) {
-    case 1: return sincos_vec_kernel<V, INTER, W, 1, NC>;
-    case 2: return sincos_vec_kernel<V, INTER, W, 2, NC>;
-    default: return sincos_vec_kernel<V, INTER, W, 4, NC>;
+    case 1: return sincos_vec_kernel<V, INTER, W, 1, NC, PF>;
+    case 2: return sincos_vec_kernel<V, INTER, W, 2, NC, PF>;
+    default: return sincos_vec_kernel<V, INTER, W, 4, NC, PF>;
     }
 }
 
+template <int V, bool INTER, int W, bool NC>
+static VecFn pick_pf(int unroll, bool pf) {
+    return pf ? pick_u<V, INTER, W, NC, true>(unroll) : pick_u<V, INTER, W, NC, false>(unroll);
+}
+
 template <int V, bool INTER>
-static VecFn pick_vec(int w, int unroll, bool nc) {
-    if (w == 8) return nc ? pick_u<V, INTER, 8, true>(unroll) : pick_u<V, INTER, 8, false>(unroll);
-    return nc ? pick_u<V, INTER, 4, true>(unroll) : pick_u<V, INTER, 4, false>(unroll);
+static VecFn pick_vec(int w, int unroll, bool nc, bool pf) {
+    if (w == 8) return nc ? pick_pf<V, INTER, 8, true>(unroll, pf) : pick_pf<V, INTER, 8, false>(unroll, pf);
+    return nc ? pick_pf<V, INTER, 4, true>(unroll, pf) : pick_pf<V, INTER, 4, false>(unroll, pf);
 }
 
 template <int V>
-static VecFn pick_inter(bool inter, int w, int unroll, bool nc) {
-    return inter ? pick_vec<V, true>(w, unroll, nc) : pick_vec<V, false>(w, unroll, nc);
+static VecFn pick_inter(bool inter, int w, int unroll, bool nc, bool pf) {
+    return inter ? pick_vec<V, true>(w, unroll, nc, pf) : pick_vec<V, false>(w, unroll, nc, pf);
 }
 
-VecFn vec_kernel(int variant, bool inter, int w, int unroll, bool nc) {
+VecFn vec_kernel(int variant, bool inter, int w, int unroll, bool nc, bool pf) {
     switch (variant) {
-    case kNormalized: return pick_inter<kNormalized>(inter, w, unroll, nc);
-    case kRenormalized: return pick_inter<kRenormalized>(inter, w, unroll, nc);
-    default: return pick_inter<kNull>(inter, w, unroll, nc);
+    case kNormalized: return pick_inter<kNormalized>(inter, w, unroll, nc, pf);
+    case kRenormalized: return pick_inter<kRenormalized>(inter, w, unroll, nc, pf);
+    default: return pick_inter<kNull>(inter, w, unroll, nc, pf);
     }
 }
 
@@ -200,10 +233,10 @@ ScalarFn scalar_kernel(int variant, bool inter) {
     }
 }
 
-cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, unsigned grid, unsigned threads,
-                       const float *theta, float *so, float *co, float *io, size_t head, size_t nvec, size_t n,
-                       cudaStream_t stream) {
-    VecFn fn = vec_kernel(variant, inter, w, unroll, nc);
+cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, bool pf, unsigned grid,
+                       unsigned threads, const float *theta, float *so, float *co, float *io, size_t head,
+                       size_t nvec, size_t n, cudaStream_t stream) {
+    VecFn fn = vec_kernel(variant, inter, w, unroll, nc, pf);
     void *args[] = {&theta, &so, &co, &io, &head, &nvec, &n};
     return cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(threads), args, 0, stream);
 }
@@ -220,8 +253,8 @@ cudaError_t launch_rcp(unsigned grid, unsigned threads, const float *d, float *o
     return cudaLaunchKernel(reinterpret_cast<const void *>(rcp_kernel), dim3(grid), dim3(threads), args, 0, stream);
 }
 
-const void *vec_kernel_ptr(int variant, bool inter, int w, int unroll, bool nc) {
-    return reinterpret_cast<const void *>(vec_kernel(variant, inter, w, unroll, nc));
+const void *vec_kernel_ptr(int variant, bool inter, int w, int unroll, bool nc, bool pf) {
+    return reinterpret_cast<const void *>(vec_kernel(variant, inter, w, unroll, nc, pf));
 }
 
 }  // namespace sincos_b200

@@ -10,13 +10,14 @@ namespace sincos_b200 {
 
 // variant: 0 = N, 1 = A, 2 = null (traffic ceiling); w = 4 or 8 floats per access;
 // unroll = 1, 2 or 4; nc = read-only (non-coherent) loads, false when theta aliases an output.
-cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, unsigned grid, unsigned threads,
-                       const float *theta, float *so, float *co, float *io, size_t head, size_t nvec, size_t n,
-                       cudaStream_t stream);
+// pf = software-pipelined loads (trip k+1 in flight while trip k computes).
+cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, bool pf, unsigned grid,
+                       unsigned threads, const float *theta, float *so, float *co, float *io, size_t head,
+                       size_t nvec, size_t n, cudaStream_t stream);
 cudaError_t launch_scalar(int variant, bool inter, unsigned grid, unsigned threads, const float *theta, float *so,
                           float *co, float *io, size_t n, cudaStream_t stream);
 cudaError_t launch_rcp(unsigned grid, unsigned threads, const float *d, float *out, size_t n, cudaStream_t stream);
-const void *vec_kernel_ptr(int variant, bool inter, int w, int unroll, bool nc);
+const void *vec_kernel_ptr(int variant, bool inter, int w, int unroll, bool nc, bool pf);
 
 size_t stats_ws_bytes();
 cudaError_t launch_stats(const float *theta, const float *so, const float *co, const float *io, size_t n,

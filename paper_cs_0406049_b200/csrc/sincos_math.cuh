@@ -50,7 +50,7 @@ template <> struct Series<kRenormalized> {
 
 // Correctly rounded fp32 reciprocal RN(1/d), branch-free ("precise reciprocal",
 // P:157-158, Fig. 1; the paper's Reciprocal() body is not listed).
-// fp64 seed from MUFU.RCP64H, three Newton steps in DFMA (each squares the
+// fp64 seed from MUFU.RCP64H, two Newton steps in DFMA (each squares the
 // relative error: ~2^-22 -> 2^-44 -> below 2^-53), then one rounding to fp32.
 // Exact because 1/d for a 24-bit d is never within 2^-48 (relative) of an
 // fp32 rounding midpoint while the fp64 value is within a few 2^-53 (reading
@@ -61,8 +61,6 @@ __device__ __forceinline__ float rcp_rn(float d) {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
     double e = __fma_rn(-x, y, 1.0);
-    y = __fma_rn(y, e, y);
-    e = __fma_rn(-x, y, 1.0);
     y = __fma_rn(y, e, y);
     e = __fma_rn(-x, y, 1.0);
     y = __fma_rn(y, e, y);

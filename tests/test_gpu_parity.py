@@ -292,18 +292,21 @@ def test_in_place(variant):
 @pytest.mark.parametrize("threads", [128, 256, 512])
 @pytest.mark.parametrize("vec", [4, 8])
 @pytest.mark.parametrize("unroll", [1, 2, 4])
-def test_every_kernel_instance(threads, vec, unroll):
-    """Every (threads, vector width, unroll) the tuner can select, both variants and layouts,
-    on a ragged size spanning many grid-stride trips, and a 2-block grid (long strides)."""
+@pytest.mark.parametrize("prefetch", [0, 1])
+def test_every_kernel_instance(threads, vec, unroll, prefetch):
+    """Every (threads, vector width, unroll, prefetch) the tuner can select, both variants and
+    layouts, on a ragged size, with a 1-block-per-SM grid (many grid-stride trips), the
+    occupancy grid, and an oversubscribed grid (about one trip per thread)."""
     th = inputs.generate(2, 12345, (1 << 20) + 13)
     want = {v: oracle.sincos(th, v) for v in VARIANTS}
     try:
-        for bps in (0, 1):
-            sp.set_launch_config(threads, bps, vec, unroll)
+        for bps in (0, 1, 6):
+            sp.set_launch_config(threads, bps, vec, unroll, prefetch)
             for variant in VARIANTS:
                 for inter in (False, True):
                     s, c = run(th, variant, inter)
-                    assert_parity(s, c, *want[variant], f"t{threads} v{vec} u{unroll} bps{bps} inter={inter}")
+                    assert_parity(s, c, *want[variant],
+                                  f"t{threads} v{vec} u{unroll} pf{prefetch} bps{bps} inter={inter}")
     finally:
         sp.set_launch_config()
 

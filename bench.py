@@ -44,13 +44,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=N_PER_RANK, help="elements per rank (default 2^28, configs[1])")
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="BASELINE config (default c2 = configs[1], weak scaling; c1/c3/c4/c5 strong, sharded)")
+    ap.add_argument("--n", type=int, default=N_PER_RANK, help="elements per rank for c2 (default 2^28)")
+    ap.add_argument("--e2e-max", type=int, default=1 << 28, help="elements per rank in the e2e leg")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample for cpu_baseline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--launch", default=None, help="threads,blocks_per_sm,vec,unroll (default: library default)")
-    ap.add_argument("--sweep", action="store_true", help="time every launch config (tuning aid; extra JSON lines)")
     return ap.parse_args()
 
 
@@ -206,38 +208,61 @@ def run_reference(args, rank, world):
 
 
 # ---- our arm -------------------------------------------------------------------------------
+def host_input(W, lo, hi, pinned=True):
+    """This rank's inputs [lo, hi) of the workload's counter stream, generated on the host."""
+    import torch
+    t = torch.empty(hi - lo, dtype=torch.float32)
+    if pinned:
+        t = t.pin_memory()
+    inputs.generate(W.config, lo, hi - lo, out=t.numpy())
+    return t
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
-    import torch.distributed as dist
 
     import paper_cs_0406049_b200 as sp
+    from paper_cs_0406049_b200.sharding import WORKLOADS, gather_records, max_over_ranks, summarize
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if args.launch:
         sp.set_launch_config(*[int(x) for x in args.launch.split(",")])
-    n = args.n
-    # inputs: this rank's contiguous shard of the C2 counter stream, generated on the host
-    th_h = torch.empty(n, dtype=torch.float32).pin_memory()
-    inputs.generate(CONFIG_ID, rank * n, n, out=th_h.numpy())
-    th = th_h.to(dev)
-    outs = {v: (torch.empty(n, dtype=torch.float32, device=dev), torch.empty(n, dtype=torch.float32, device=dev))
-            for v in (sp.NORMALIZED, sp.RENORMALIZED)}
-    stream = torch.cuda.current_stream(dev)
+    W = WORKLOADS[args.workload]
+    if args.n and args.workload == "c2":
+        W = type(W)(**{**W.__dict__, "n": args.n})
+    lo, hi = W.rank_range(world, rank)
+    n = hi - lo
     variants = (sp.NORMALIZED, sp.RENORMALIZED)
+    stream = torch.cuda.current_stream(dev)
 
-    def step():
-        for v in variants:
-            s, c = outs[v]
-            sp.sincos_pairs(th, s, c, variant=v, stream=stream)
+    # inputs resident in HBM before timing (H2D excluded here; the e2e leg includes it)
+    e2e_n = min(n, args.e2e_max)
+    th_h = host_input(W, lo, lo + e2e_n, pinned=True)
+    th = torch.empty(n, dtype=torch.float32, device=dev)
+    th[:e2e_n].copy_(th_h)
+    chunk = 1 << 28
+    for off in range(e2e_n, n, chunk):
+        m = min(chunk, n - off)
+        th[off:off + m].copy_(host_input(W, lo + off, lo + off + m, pinned=False))
+
+    def alloc_out():
+        if W.interleaved:
+            return {"interleaved_out": torch.empty(2 * n, dtype=torch.float32, device=dev)}
+        return {"sin_out": torch.empty(n, dtype=torch.float32, device=dev),
+                "cos_out": torch.empty(n, dtype=torch.float32, device=dev)}
+
+    outs = {v: alloc_out() for v in variants}
 
     def barrier():
         if world > 1:
+            import torch.distributed as dist
             dist.barrier()
         torch.cuda.synchronize(dev)
 
     for _ in range(max(args.warmup, 3)):
-        step()
+        for v in variants:
+            sp.sincos_pairs(th, variant=v, stream=stream, **outs[v])
     # per-launch events on the launching stream: the kernels' own durations
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(variants) + 1)] for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -248,79 +273,72 @@ def run_ours(args, rank, world, local_rank):
         for k in range(args.steps):
             ev[k][0].record(stream)
             for j, v in enumerate(variants):
-                s, c = outs[v]
-                sp.sincos_pairs(th, s, c, variant=v, stream=stream)
+                sp.sincos_pairs(th, variant=v, stream=stream, **outs[v])
                 ev[k][j + 1].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize(dev)
     barrier()
     launches = sp.launch_count() - launches0
-    ms_total = t_start.elapsed_time(t_end)
+    ms_max = max_over_ranks(t_start.elapsed_time(t_end), world, dev)
     per_kernel = {v: [ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps)] for j, v in enumerate(variants)}
-
-    # max over ranks of the timed region
-    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    pairs_total = world * len(variants) * n * args.steps
+    units_all = W.n * world if W.weak else W.n
+    pairs_total = len(variants) * units_all * args.steps
     value = pairs_total / (ms_max / 1e3)
 
-    # roofline of the dominant (slowest) kernel
+    # roofline of the dominant (slowest) kernel on this rank
     avg = {v: statistics.mean(per_kernel[v]) for v in variants}
     dom = max(variants, key=lambda v: avg[v])
     peak, peak_src = peaks()
     achieved = BYTES_PER_PAIR * n / (avg[dom] / 1e3) / 1e9
+    vname = {0: "N", 1: "A"}
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": ncu_traffic(n), "kernel": f"sincos_vec_kernel variant {'A' if dom else 'N'}",
-            "bytes_per_launch": BYTES_PER_PAIR * n, "peak_source": peak_src,
-            "per_variant_GBps": {("N" if v == 0 else "A"): BYTES_PER_PAIR * n / (avg[v] / 1e3) / 1e9 for v in variants},
-            "per_variant_ms": {("N" if v == 0 else "A"): avg[v] for v in variants}}
+            "traffic": ncu_traffic(n) if args.workload == "c2" else None,
+            "kernel": f"sincos_vec_kernel variant {vname[dom]}", "bytes_per_launch": BYTES_PER_PAIR * n,
+            "bytes_per_pair": BYTES_PER_PAIR, "peak_source": peak_src,
+            "frac_of_theoretical_8180": achieved / 8180.0,
+            "per_variant_GBps": {vname[v]: BYTES_PER_PAIR * n / (avg[v] / 1e3) / 1e9 for v in variants},
+            "per_variant_ms": {vname[v]: avg[v] for v in variants}}
 
-    # traffic ceiling (same access pattern, no math), outside the timed region
-    s, c = outs[sp.NORMALIZED]
+    # traffic ceiling: same access pattern and launch, no arithmetic (outside the timed region)
+    o = outs[sp.NORMALIZED]
     for _ in range(3):
-        sp.null_4in8out(th, s, c)
+        sp.null_4in8out(th, stream=stream, **o)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 20
+    reps = 10
     e0.record(stream)
     for _ in range(reps):
-        sp.null_4in8out(th, s, c, stream=stream)
+        sp.null_4in8out(th, stream=stream, **o)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     null_ms = e0.elapsed_time(e1) / reps
     roof["ceiling_kernel_GBps"] = BYTES_PER_PAIR * n / (null_ms / 1e3) / 1e9
-    roof["vs_ceiling_kernel"] = null_ms / avg[dom]
+    roof["kernel_over_ceiling"] = null_ms / avg[dom]
 
-    # per-shard error statistics, gathered with NCCL (the only collective; not timed)
+    # per-shard error statistics (fp64, on the device), gathered over NCCL -- not timed
     for v in variants:
-        sp.sincos_pairs(th, *outs[v], variant=v)
+        sp.sincos_pairs(th, variant=v, stream=stream, **outs[v])
     recs = []
     for v in variants:
-        st = sp.error_stats(th, *outs[v])
+        st = sp.error_stats(th, stream=stream, **outs[v])
         recs.append([float(st["n"]), float(st["nan_count"]), st["max_comb"], st["sum_sq"], st["max_amp"],
                      avg[v], float(rank), float(v)])
-    mine = torch.tensor(recs, dtype=torch.float64, device=dev)
-    if world > 1:
-        allr = [torch.empty_like(mine) for _ in range(world)]
-        dist.all_gather(allr, mine)
-        allr = torch.stack(allr).cpu().numpy()
-    else:
-        allr = mine.cpu().numpy()[None]
-    shards = [{"rank": int(r[6]), "variant": "N" if r[7] == 0 else "A", "n": int(r[0]), "nan": int(r[1]),
-               "max_err": r[2], "rms_err": (r[3] / r[0]) ** 0.5 if r[0] else 0.0, "max_amp": r[4], "kernel_ms": r[5]}
-              for rank_rows in allr for r in rank_rows]
+    summary = summarize(gather_records(recs, world, dev))
 
-    # end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    # end to end through the C ABI with host buffers, copies inside the timed region
     e2e = None
     if not args.no_e2e:
+        del outs
+        torch.cuda.empty_cache()
         ws = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-        sh = torch.empty(n, dtype=torch.float32).pin_memory()
-        ch = torch.empty(n, dtype=torch.float32).pin_memory()
+        if W.interleaved:
+            oh = {"interleaved_out": torch.empty(2 * e2e_n, dtype=torch.float32).pin_memory()}
+        else:
+            oh = {"sin_out": torch.empty(e2e_n, dtype=torch.float32).pin_memory(),
+                  "cos_out": torch.empty(e2e_n, dtype=torch.float32).pin_memory()}
 
         def e2e_step():
             for v in variants:
-                sp.sincos_pairs_host(th_h, sh, ch, variant=v, workspace=ws, stream=stream)
+                sp.sincos_pairs_host(th_h, variant=v, workspace=ws, stream=stream, **oh)
 
         e2e_step()
         barrier()
@@ -332,27 +350,26 @@ def run_ours(args, rank, world, local_rank):
         b.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        t2 = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * len(variants) * n * k2 / (float(t2.item()) / 1e3), "unit": "pairs/s",
-               "h2d_bytes_per_step": len(variants) * 4 * n, "d2h_bytes_per_step": len(variants) * 8 * n,
-               "steps": k2, "path": "sincos_pairs_host (pinned host buffers, chunked H2D/kernel/D2H, 3 streams)"}
-        del ws, sh, ch
+        t2 = max_over_ranks(a.elapsed_time(b), world, dev)
+        e2e = {"value": world * len(variants) * e2e_n * k2 / (t2 / 1e3), "unit": "pairs/s",
+               "h2d_bytes_per_step": len(variants) * 4 * e2e_n, "d2h_bytes_per_step": len(variants) * 8 * e2e_n,
+               "steps": k2, "elements_per_rank": e2e_n,
+               "path": "sincos_pairs_host: pinned host buffers, chunked H2D -> kernel -> D2H over 3 streams"}
+        del ws, oh
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_rate(th_h.numpy(), args.cpu_seconds)
 
     if rank == 0:
-        ms_step = ms_max / args.steps
         line = {
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "n_per_rank": n, "pairs_per_step": world * len(variants) * n,
-                       "global_batch": world * n, "parallelism": f"dp{world} (contiguous shards, no collective)",
-                       "l2": "inputs larger than L2 (1 GiB theta + 2 GiB outputs per launch vs 126 MB L2); no flush",
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak" if W.weak else "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": W.description, "n_per_rank": n, "pairs_per_step": len(variants) * units_all,
+                       "global_batch": units_all, "parallelism": f"dp{world} (contiguous shards, no collective)",
+                       "l2": "inputs larger than L2 (4n B theta + 8n B outputs per launch vs 126 MB L2); no flush"
+                             if 12 * n > (256 << 20) else "working set near/below L2 size: not an HBM measurement",
                        "launch": sp.get_launch_config()},
             "hbm_GBps": BYTES_PER_PAIR * pairs_total / (ms_max / 1e3) / 1e9 / world,
             "roofline": roof,
@@ -360,30 +377,14 @@ def run_ours(args, rank, world, local_rank):
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.result(),
-            "max_error": max(r["max_err"] for r in shards),
-            "shards": shards,
+            "max_error": summary["max_err"],
+            "rms_error": summary["rms_err"],
+            "error_reference": "fp64 sin/cos on the device (P:137-138 metric); large-|theta| reduction error "
+                               "is the method's (BASELINE.md section 2), the kernel equals the oracle bit for bit",
+            "shards": summary["shards"],
             "paper_context": "PowerPC 7400 G4 500 MHz AltiVec: 140 ns per 4 pairs = 28.6 M pairs/s (P:177-180)",
         }
         print(json.dumps(line), flush=True)
-
-    if args.sweep and rank == 0:
-        import itertools
-        for threads, bps, vec, unroll, pf in itertools.product((256, 512), (0, 2, 4, 8, 16, 4096), (4, 8),
-                                                               (1, 2, 4), (0, 1)):
-                        sp.set_launch_config(threads, bps, vec, unroll, pf)
-                        res = {}
-                        for v in variants:
-                            s, c = outs[v]
-                            for _ in range(3):
-                                sp.sincos_pairs(th, s, c, variant=v)
-                            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                            a.record(stream)
-                            for _ in range(10):
-                                sp.sincos_pairs(th, s, c, variant=v, stream=stream)
-                            b.record(stream)
-                            torch.cuda.synchronize(dev)
-                            res["N" if v == 0 else "A"] = BYTES_PER_PAIR * n / (a.elapsed_time(b) / 10 / 1e3) / 1e9
-                        print(json.dumps({"sweep": [threads, bps, vec, unroll, pf], "GBps": res}), flush=True)
 
 
 def main():

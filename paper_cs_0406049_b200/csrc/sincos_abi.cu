@@ -81,9 +81,9 @@ sincos_status_t validate(const float *theta, const float *so, const float *co, c
     return SINCOS_OK;
 }
 
-// Launch on already-validated arguments, n > 0.
+// Launch on already-validated arguments, n > 0.  pf_mode: -1 = the configured mode.
 sincos_status_t launch(const float *theta, float *so, float *co, float *io, size_t n, int variant,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, int pf_mode = -1) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e);
@@ -93,7 +93,20 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
     const int threads = g_threads.load(std::memory_order_relaxed);
     const int cfg_bps = g_blocks_per_sm.load(std::memory_order_relaxed);
     const int unroll = g_unroll.load(std::memory_order_relaxed);
-    const bool pf = g_prefetch.load(std::memory_order_relaxed) != 0;
+    if (pf_mode < 0) pf_mode = g_prefetch.load(std::memory_order_relaxed);
+    const bool pf = pf_mode == 1;
+
+    // Mode 2: persistent TMA bulk-load pipeline over whole tiles, the rest by the vector kernel.
+    if (pf_mode == 2 && variant != 2 && nc && aligned(theta, 32) &&
+        (inter ? aligned(io, 32) : aligned(so, 32) && aligned(co, 32))) {
+        size_t done = 0;
+        e = launch_tma(variant, inter, static_cast<unsigned>(sms) * 4, theta, so, co, io, n, &done, stream);
+        if (e != cudaSuccess) return cuda_fail(e);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (done == n) return SINCOS_OK;
+        return launch(theta + done, so ? so + done : nullptr, co ? co + done : nullptr,
+                      io ? io + 2 * done : nullptr, n - done, variant, stream, 0);
+    }
 
     // Widest vector whose alignment theta and the outputs share after a scalar head.
     int w = 0;
@@ -305,7 +318,7 @@ sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
 int sincos_set_launch_config(int threads, int blocks_per_sm, int vec, int unroll, int prefetch) {
     if (!(threads == 128 || threads == 256 || threads == 512)) return -1;
     if (blocks_per_sm < 0 || blocks_per_sm > 4096) return -1;
-    if (prefetch != 0 && prefetch != 1) return -1;
+    if (prefetch < 0 || prefetch > 2) return -1;
     if (!(vec == 4 || vec == 8)) return -1;
     if (!(unroll == 1 || unroll == 2 || unroll == 4)) return -1;
     g_threads.store(threads);

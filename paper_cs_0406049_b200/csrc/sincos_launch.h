@@ -17,6 +17,10 @@ cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, bool
 cudaError_t launch_scalar(int variant, bool inter, unsigned grid, unsigned threads, const float *theta, float *so,
                           float *co, float *io, size_t n, cudaStream_t stream);
 cudaError_t launch_rcp(unsigned grid, unsigned threads, const float *d, float *out, size_t n, cudaStream_t stream);
+// Persistent TMA bulk-load pipeline over the whole 2048-element tiles of [theta, theta+n);
+// *done = elements covered (the caller finishes the rest).
+cudaError_t launch_tma(int variant, bool inter, unsigned grid, const float *theta, float *so, float *co, float *io,
+                       size_t n, size_t *done, cudaStream_t stream);
 const void *vec_kernel_ptr(int variant, bool inter, int w, int unroll, bool nc, bool pf);
 
 size_t stats_ws_bytes();

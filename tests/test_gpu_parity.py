@@ -292,7 +292,7 @@ def test_in_place(variant):
 @pytest.mark.parametrize("threads", [128, 256, 512])
 @pytest.mark.parametrize("vec", [4, 8])
 @pytest.mark.parametrize("unroll", [1, 2, 4])
-@pytest.mark.parametrize("prefetch", [0, 1])
+@pytest.mark.parametrize("prefetch", [0, 1, 2])
 def test_every_kernel_instance(threads, vec, unroll, prefetch):
     """Every (threads, vector width, unroll, prefetch) the tuner can select, both variants and
     layouts, on a ragged size, with a 1-block-per-SM grid (many grid-stride trips), the

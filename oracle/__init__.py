@@ -114,6 +114,9 @@ def _load():
                                         ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
                                         ctypes.POINTER(ctypes.c_uint64)]),
             "oracle_hash_outputs": (ctypes.c_uint64, [_P, _P, _P, ctypes.c_size_t, ctypes.c_uint32]),
+            "oracle_phase_points": (ctypes.c_int, [_P, _P, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, _P, _P]),
+            "oracle_phase_grid": (ctypes.c_int, [_P, ctypes.c_size_t, _P, ctypes.c_size_t, ctypes.c_int,
+                                                 ctypes.c_int, _P, _P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -181,6 +184,32 @@ def sincos_into(theta: np.ndarray, s: np.ndarray, c: np.ndarray, variant: int) -
     """Like sincos() but into caller buffers (used by the threaded cpu_baseline)."""
     if _load().sincos_oracle(theta.ctypes.data, s.ctypes.data, c.ctypes.data, theta.size, variant) != 0:
         raise ValueError(f"unknown oracle variant {variant}")
+
+
+UNITS_RADIANS, UNITS_TURNS = 0, 1
+
+
+def phase_points(f, t, units: int, variant: int):
+    """NEXT(1): pairs of the phases RN(f[k] * t[k]) (radians or turns) -> (sin, cos)."""
+    f, t = _f32(f), _f32(t)
+    assert f.size == t.size
+    s = np.empty_like(f)
+    c = np.empty_like(f)
+    if _load().oracle_phase_points(f.ctypes.data, t.ctypes.data, f.size, units, variant, s.ctypes.data,
+                                   c.ctypes.data) != 0:
+        raise ValueError("bad variant or units")
+    return s, c
+
+
+def phase_grid(f, t, units: int, variant: int):
+    """NEXT(1): row-major grid (i, j) -> pair of RN(f[i] * t[j]); returns (sin, cos) of shape (nf, nt)."""
+    f, t = _f32(f), _f32(t)
+    s = np.empty((f.size, t.size), dtype=np.float32)
+    c = np.empty_like(s)
+    if _load().oracle_phase_grid(f.ctypes.data, f.size, t.ctypes.data, t.size, units, variant, s.ctypes.data,
+                                 c.ctypes.data) != 0:
+        raise ValueError("bad variant or units")
+    return s, c
 
 
 def error_stats(theta, s, c, ref: int = REF_DOUBLE) -> Stats:

@@ -150,3 +150,45 @@ int sincos_oracle(const float *theta, float *s_out, float *c_out, size_t n, int 
         return -1;
     return sincos_oracle_opts(theta, s_out, c_out, n, &o);
 }
+
+/* ---- NEXT(1): phases generated from their factors ----
+ * The pair for the phase of frequency f and time t.  The phase is formed as
+ * one rounded fp32 product p = RN(f * t).  units == 0: p is the angle in
+ * radians and the whole method runs (A1 onwards).  units == 1: p is
+ * already in turns (theta / 2pi), so the method enters at the reduction
+ * "reduced modulo 1 onto [-1/2,1/2) by rounding and subtraction" and
+ * skips the scale by 1/2pi (Fig. 1) and its rounding. */
+void oracle_phase_pair(float f, float t, int units, const oracle_opts_t *o, float *s, float *c)
+{
+    float p = fmaf(f, t, 0.0f);
+    if (units == 0) {
+        oracle_pair(p, o, s, c);
+    } else {
+        float q1 = fmaf(-rintf(p), 1.0f, p);
+        oracle_pair_from_q(q1, o, s, c);
+    }
+}
+
+int oracle_phase_points(const float *f, const float *t, size_t m, int units, int variant,
+                        float *s_out, float *c_out)
+{
+    oracle_opts_t o;
+    if (oracle_variant_opts(variant, &o) != 0 || (units != 0 && units != 1))
+        return -1;
+    for (size_t k = 0; k < m; ++k)
+        oracle_phase_pair(f[k], t[k], units, &o, &s_out[k], &c_out[k]);
+    return 0;
+}
+
+/* Row-major grid: element (i, j) at i*nt + j is the pair of phase f[i] * t[j]. */
+int oracle_phase_grid(const float *f, size_t nf, const float *t, size_t nt, int units, int variant,
+                      float *s_out, float *c_out)
+{
+    oracle_opts_t o;
+    if (oracle_variant_opts(variant, &o) != 0 || (units != 0 && units != 1))
+        return -1;
+    for (size_t i = 0; i < nf; ++i)
+        for (size_t j = 0; j < nt; ++j)
+            oracle_phase_pair(f[i], t[j], units, &o, &s_out[i * nt + j], &c_out[i * nt + j]);
+    return 0;
+}

@@ -97,6 +97,17 @@ int sincos_oracle(const float *theta, float *s_out, float *c_out, size_t n, int 
 int sincos_oracle_opts(const float *theta, float *s_out, float *c_out, size_t n,
                        const oracle_opts_t *o);
 
+/* ---- NEXT(1): pairs of generated phases f*t -------
+ * units 0: RN(f*t) is an angle in radians (the full method);
+ * units 1: RN(f*t) is in turns (theta/2pi): the method from the reduction on.
+ * Returns 0, or -1 for an unknown variant or units. */
+void oracle_phase_pair(float f, float t, int units, const oracle_opts_t *o, float *s, float *c);
+int oracle_phase_points(const float *f, const float *t, size_t m, int units, int variant,
+                        float *s_out, float *c_out);
+/* element (i, j) at i*nt + j */
+int oracle_phase_grid(const float *f, size_t nf, const float *t, size_t nt, int units, int variant,
+                      float *s_out, float *c_out);
+
 /* ---- error metrics, P:135-139 (accuracy.c) -------------------------- */
 
 typedef struct {

@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample for cpu_baseline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row side measurements")
     ap.add_argument("--launch", default=None, help="threads,blocks_per_sm,vec,unroll (default: library default)")
     return ap.parse_args()
 
@@ -218,6 +219,47 @@ def host_input(W, lo, hi, pinned=True):
     return t
 
 
+def c4_axes(turns):
+    """BASELINE configs[3] axes (2^15 frequencies x 2^15 jittered times); radians: fl32(2 pi f)."""
+    nf = nt = 1 << 15
+    f = np.array([512.0 * inputs.urand(3, 0, i) for i in range(nf)])
+    t = np.array([(j + inputs.urand(3, 1, j)) * 2.0 ** -15 for j in range(nt)])
+    if not turns:
+        f = 2 * np.pi * f
+    return f.astype(np.float32), t.astype(np.float32)
+
+
+def measure_phase_grid(dev, stream, peak, reps=10):
+    """NEXT(1) side measurement (outside the timed region of the main metric): the C4 phase
+    grid formed in the kernel (sincos_phase_grid, interleaved, 8 B written per pair, nothing
+    read), against the materialised path (theta array in HBM: 12 B per pair)."""
+    import torch
+
+    import paper_cs_0406049_b200 as sp
+    out = {"workload": "C4 shape: 2^15 f x 2^15 t = 2^30 pairs, interleaved {cos, sin}, phases formed in-kernel",
+           "bytes_per_pair": 8, "peak": peak, "unit": "GB/s"}
+    o = torch.empty(2 << 30, dtype=torch.float32, device=dev)
+    for units, uname in ((sp.RADIANS, "radians"), (sp.TURNS, "turns")):
+        f, t = c4_axes(units == sp.TURNS)
+        fd, td = torch.from_numpy(f).to(dev), torch.from_numpy(t).to(dev)
+        for v, vname in ((sp.NORMALIZED, "N"), (sp.RENORMALIZED, "A")):
+            for _ in range(2):
+                sp.phase_grid(fd, td, interleaved_out=o, units=units, variant=v, stream=stream)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                sp.phase_grid(fd, td, interleaved_out=o, units=units, variant=v, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            ms = a.elapsed_time(b) / reps
+            gbs = 8 * (1 << 30) / (ms / 1e3) / 1e9
+            out[f"{uname}_{vname}"] = {"ms": ms, "pairs_per_s": (1 << 30) / (ms / 1e3), "GBps": gbs,
+                                       "frac": gbs / peak}
+    del o
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -357,6 +399,10 @@ def run_ours(args, rank, world, local_rank):
                "path": "sincos_pairs_host: pinned host buffers, chunked H2D -> kernel -> D2H over 3 streams"}
         del ws, oh
 
+    fused = None
+    if rank == 0 and not args.no_next:
+        fused = measure_phase_grid(dev, stream, peak)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_rate(th_h.numpy(), args.cpu_seconds)
@@ -382,6 +428,7 @@ def run_ours(args, rank, world, local_rank):
             "error_reference": "fp64 sin/cos on the device (P:137-138 metric); large-|theta| reduction error "
                                "is the method's (BASELINE.md section 2), the kernel equals the oracle bit for bit",
             "shards": summary["shards"],
+            "next_fused_phase": fused,
             "paper_context": "PowerPC 7400 G4 500 MHz AltiVec: 140 ns per 4 pairs = 28.6 M pairs/s (P:177-180)",
         }
         print(json.dumps(line), flush=True)

@@ -103,6 +103,30 @@ SINCOS_API sincos_status_t sincos_pairs_host(const float *theta_host, float *sin
 SINCOS_API size_t sincos_host_workspace_min_bytes(void);
 
 /*
+ * sincos_phase_grid -- NEXT(1): pairs of phases generated inside the kernel.
+ *
+ * The paper's use case is phase factors for optical diffraction by Huygens'
+ * principle -- many non-uniformly spaced phases, e.g. the
+ * products of a frequency axis and a jittered time axis (BASELINE configs[3]).
+ * For every i < nf, j < nt the phase is one rounded fp32 product
+ *     p_ij = RN(f_dev[i] * t_dev[j])
+ * and the output element (i, j), at index i*nt + j (row-major, row = f_i), is
+ *     units == SINCOS_RADIANS: (sin p_ij, cos p_ij), the whole method;
+ *     units == SINCOS_TURNS:   (sin 2 pi p_ij, cos 2 pi p_ij): p_ij is already in
+ *                              turns, the method starts at the reduction
+ *                              and skips the 1/2pi scaling and its rounding.
+ * Outputs as in sincos_pairs (split sin/cos of nf*nt floats each, or interleaved
+ * {cos, sin}).  Only 8 B per pair are written (no theta array is read); f and t
+ * must not overlap the outputs.  The fast path needs nt % 8 == 0 and 32-B aligned
+ * t and outputs; any other shape/alignment runs a scalar path with identical
+ * numerics.  Returns as sincos_pairs; nf*nt == 0 is a no-op.
+ */
+typedef enum { SINCOS_RADIANS = 0, SINCOS_TURNS = 1 } sincos_units_t;
+SINCOS_API sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_dev, size_t nt,
+                                             float *sin_dev, float *cos_dev, float *inter_dev,
+                                             sincos_units_t units, sincos_variant_t variant, void *stream);
+
+/*
  * Host-side sharding: element ranges [lo, hi) of shard g of
  * nshards, contiguous, every shard start a multiple of 8 elements (32-B
  * aligned in any aligned array); the last shard takes the remainder.  Pure

@@ -71,7 +71,10 @@ _SIGS = {
     "sincos_last_cuda_error": (_I, []),
     "sincos_version": (ctypes.c_char_p, []),
     "sincos_launch_count": (ctypes.c_uint64, []),
+    "sincos_phase_grid": (_I, [_P, _S, _P, _S, _P, _P, _P, _I, _I, _P]),
 }
+
+RADIANS, TURNS = 0, 1
 EXPORTS = tuple(_SIGS)
 
 
@@ -153,6 +156,23 @@ def sincos(theta, variant="normalized", interleaved=False, out=None, stream=None
     s, c = out if out is not None else (torch.empty_like(theta), torch.empty_like(theta))
     sincos_pairs(theta.reshape(-1), s.reshape(-1), c.reshape(-1), variant=variant, stream=stream)
     return s, c
+
+
+def phase_grid(f, t, sin_out=None, cos_out=None, interleaved_out=None, units=RADIANS, variant=NORMALIZED,
+               stream=None):
+    """NEXT(1) C-ABI sincos_phase_grid: pairs of p_ij = RN(f[i] * t[j]) (radians, or turns with
+    units=TURNS) for the row-major nf x nt grid, into split or interleaved outputs."""
+    nf, nt = f.numel(), t.numel()
+    n = nf * nt
+    if interleaved_out is not None and interleaved_out.numel() != 2 * n:
+        raise ValueError("interleaved_out must hold 2*nf*nt floats")
+    for o in (sin_out, cos_out):
+        if o is not None and o.numel() != n:
+            raise ValueError("outputs must hold nf*nt floats")
+    st = lib().sincos_phase_grid(_ptr(f, "f"), nf, _ptr(t, "t"), nt, _ptr(sin_out, "sin_out"),
+                                 _ptr(cos_out, "cos_out"), _ptr(interleaved_out, "interleaved_out"), int(units),
+                                 _variant(variant), _stream(stream, f.device))
+    _check(st, "sincos_phase_grid")
 
 
 def host_workspace_min_bytes() -> int:

@@ -205,6 +205,36 @@ sincos_status_t sincos_null_4in8out(const float *theta_dev, float *sin_dev, floa
     return launch(theta_dev, sin_dev, cos_dev, inter_dev, n, 2, static_cast<cudaStream_t>(stream));
 }
 
+sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_dev, size_t nt, float *sin_dev,
+                                  float *cos_dev, float *inter_dev, sincos_units_t units, sincos_variant_t variant,
+                                  void *stream) {
+    if (variant != SINCOS_NORMALIZED && variant != SINCOS_RENORMALIZED) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (units != SINCOS_RADIANS && units != SINCOS_TURNS) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (nf == 0 || nt == 0) return SINCOS_OK;
+    if (nt > SIZE_MAX / 8 / nf) return SINCOS_ERR_INVALID_ARGUMENT;
+    const size_t n = nf * nt;
+    const bool split = sin_dev != nullptr && cos_dev != nullptr && inter_dev == nullptr;
+    const bool inter = sin_dev == nullptr && cos_dev == nullptr && inter_dev != nullptr;
+    if (f_dev == nullptr || t_dev == nullptr || !(split || inter)) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (!aligned(f_dev, 4) || !aligned(t_dev, 4) || (sin_dev && !aligned(sin_dev, 4)) ||
+        (cos_dev && !aligned(cos_dev, 4)) || (inter_dev && !aligned(inter_dev, 4)))
+        return SINCOS_ERR_INVALID_ARGUMENT;
+    const void *outs[2] = {split ? static_cast<const void *>(sin_dev) : inter_dev, split ? cos_dev : nullptr};
+    const size_t ob = split ? 4 * n : 8 * n;
+    if (split && overlaps(sin_dev, ob, cos_dev, ob)) return SINCOS_ERR_OVERLAP;
+    for (const void *o : outs) {
+        if (o == nullptr) continue;
+        if (overlaps(o, ob, f_dev, 4 * nf) || overlaps(o, ob, t_dev, 4 * nt)) return SINCOS_ERR_OVERLAP;
+    }
+    const bool vec = nt % 8 == 0 && aligned(t_dev, 32) &&
+                     (split ? aligned(sin_dev, 32) && aligned(cos_dev, 32) : aligned(inter_dev, 32));
+    cudaError_t e = launch_phase_grid(variant, inter, units == SINCOS_TURNS, vec, f_dev, nf, t_dev, nt, sin_dev,
+                                      cos_dev, inter_dev, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SINCOS_OK;
+}
+
 size_t sincos_host_workspace_min_bytes(void) { return kSlots * kMinChunk * 12; }
 
 sincos_status_t sincos_pairs_host(const float *theta_host, float *sin_host, float *cos_host, float *inter_host,

@@ -21,6 +21,9 @@ cudaError_t launch_rcp(unsigned grid, unsigned threads, const float *d, float *o
 // *done = elements covered (the caller finishes the rest).
 cudaError_t launch_tma(int variant, bool inter, unsigned grid, const float *theta, float *so, float *co, float *io,
                        size_t n, size_t *done, cudaStream_t stream);
+// NEXT(1) phase grid (sincos_phase.cu); vec = 256-bit path (nt % 8 == 0, 32-B aligned t/outputs).
+cudaError_t launch_phase_grid(int variant, bool inter, bool turns, bool vec, const float *f, size_t nf,
+                              const float *t, size_t nt, float *so, float *co, float *io, cudaStream_t stream);
 const void *vec_kernel_ptr(int variant, bool inter, int w, int unroll, bool nc, bool pf);
 
 size_t stats_ws_bytes();

@@ -67,13 +67,11 @@ __device__ __forceinline__ float rcp_rn(float d) {
     return __double2float_rn(y);
 }
 
-// One pair.  Step letters follow DESIGN.md section 2.
+// The pair from a reduced turn q1 in [-1/2, 1/2] (steps a4-a9).  Step letters follow
+// DESIGN.md section 1.
 template <int V>
-__device__ __forceinline__ void sincos_pair(float theta, float &s_out, float &c_out) {
+__device__ __forceinline__ void sincos_from_q(float q1, float &s_out, float &c_out) {
     using K = Series<V>;
-    // a2-a3  turn reduction
-    const float x1 = __fmul_rn(theta, kInvTwoPi);
-    const float q1 = __fsub_rn(x1, rintf(x1));          // exact; q1 in [-1/2, 1/2]
     // a4-a5  quarter-angle series, P:280-310 (Horner, innermost first)
     const float q2 = __fmul_rn(q1, q1);
     const float s1 = __fmul_rn(q1, __fmaf_rn(q2, __fmaf_rn(q2, __fmaf_rn(q2, K::ss4, K::ss3), K::ss2), K::ss1));
@@ -94,6 +92,22 @@ __device__ __forceinline__ void sincos_pair(float theta, float &s_out, float &c_
     // a9  apply
     c_out = __fmul_rn(c3, f);
     s_out = __fmul_rn(s3, f);
+}
+
+// a2-a3  turn reduction: x1 = RN(x / 2pi) ... q1 = x1 - rint(x1), exact.
+__device__ __forceinline__ float reduce_turn(float x1) { return __fsub_rn(x1, rintf(x1)); }
+
+// One pair from an angle in radians (the whole method, a2-a9).
+template <int V>
+__device__ __forceinline__ void sincos_pair(float theta, float &s_out, float &c_out) {
+    sincos_from_q<V>(reduce_turn(__fmul_rn(theta, kInvTwoPi)), s_out, c_out);
+}
+
+// One pair from a phase already in turns (theta / 2pi): the method from the reduction on
+// (P:53-54), without the scale by 1/2pi and its rounding (NEXT(1)).
+template <int V>
+__device__ __forceinline__ void sincos_pair_turns(float x1, float &s_out, float &c_out) {
+    sincos_from_q<V>(reduce_turn(x1), s_out, c_out);
 }
 
 }  // namespace sincos_b200

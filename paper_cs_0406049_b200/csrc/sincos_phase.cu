@@ -1,0 +1,120 @@
+// sincos_phase.cu -- NEXT(1): sine-cosine pairs of phases generated in the kernel.
+//
+// The paper's application computes phase factors of optical paths for Huygens'
+// principle; its problem statement is angles "in random order, or for
+// non-uniformly spaced values".  BASELINE configs[3] is such a set: the
+// phases theta_ij = 2 pi f_i t_j of a non-uniform grid.  Instead of reading a
+// materialised theta array (4 B/pair) the kernel forms each phase from its factors,
+//   p_ij = RN(f_i * t_j)                                  (one fp32 rounding)
+// and evaluates the method on it: as radians (the whole pipeline) or, with
+// units = turns, from the reduction on -- which also removes the 1/2pi
+// rounding of large phases.  Output: the nf x nt grid, row-major (row = f_i), split
+// or interleaved {cos, sin}.  Traffic: 8 B written per pair; f and t (nf + nt floats)
+// stay in L1/L2.  Write-bound: the roofline is the write bandwidth of HBM.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sincos_launch.h"
+#include "sincos_math.cuh"
+
+namespace sincos_b200 {
+
+constexpr int kPhaseThreads = 128;
+
+template <int V, bool TURNS>
+__device__ __forceinline__ void phase_pair(float f, float t, float &s, float &c) {
+    const float p = __fmul_rn(f, t);
+    if constexpr (TURNS)
+        sincos_pair_turns<V>(p, s, c);
+    else
+        sincos_pair<V>(p, s, c);
+}
+
+__device__ __forceinline__ void st8_stream(float *p, const float *r) {
+    asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(p), "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7])
+                 : "memory");
+}
+
+// Vector path: nt % 8 == 0, t and the outputs 32-B aligned.  Block (x, y) covers 128
+// vectors of 8 t-values of rows y, y + gridDim.y, ...: every thread loads one 256-bit
+// vector of t (L1-cached, reused by every row) and its row's f once per row.
+template <int V, bool INTER, bool TURNS>
+__global__ void __launch_bounds__(kPhaseThreads) phase_grid_vec(const float *__restrict__ f,
+                                                               const float *__restrict__ t, size_t nf,
+                                                               size_t nt, float *so, float *co, float *io) {
+    const size_t nt8 = nt / 8;
+    const size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (v >= nt8) return;
+    float tt[8];
+    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(tt[0]), "=f"(tt[1]), "=f"(tt[2]), "=f"(tt[3]), "=f"(tt[4]), "=f"(tt[5]), "=f"(tt[6]),
+                   "=f"(tt[7])
+                 : "l"(t + 8 * v));
+    for (size_t i = blockIdx.y; i < nf; i += gridDim.y) {
+        const float fi = __ldg(f + i);
+        const size_t e0 = i * nt + 8 * v;
+        if constexpr (INTER) {
+            float cs[16];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fi, tt[k], cs[2 * k + 1], cs[2 * k]);
+            st8_stream(io + 2 * e0, cs);
+            st8_stream(io + 2 * e0 + 8, cs + 8);
+        } else {
+            float sv[8], cv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fi, tt[k], sv[k], cv[k]);
+            st8_stream(so + e0, sv);
+            st8_stream(co + e0, cv);
+        }
+    }
+}
+
+// Any shape / alignment: one element per thread.
+template <int V, bool INTER, bool TURNS>
+__global__ void __launch_bounds__(kPhaseThreads) phase_grid_scalar(const float *__restrict__ f,
+                                                                  const float *__restrict__ t, size_t nf,
+                                                                  size_t nt, float *so, float *co, float *io) {
+    const size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= nt) return;
+    const float tj = t[j];
+    for (size_t i = blockIdx.y; i < nf; i += gridDim.y) {
+        float s, c;
+        phase_pair<V, TURNS>(f[i], tj, s, c);
+        const size_t e = i * nt + j;
+        if constexpr (INTER) {
+            io[2 * e] = c;
+            io[2 * e + 1] = s;
+        } else {
+            so[e] = s;
+            co[e] = c;
+        }
+    }
+}
+
+template <int V, bool INTER, bool TURNS>
+static const void *pick_phase(bool vec) {
+    return vec ? reinterpret_cast<const void *>(phase_grid_vec<V, INTER, TURNS>)
+               : reinterpret_cast<const void *>(phase_grid_scalar<V, INTER, TURNS>);
+}
+
+template <int V>
+static const void *pick_phase_v(bool inter, bool turns, bool vec) {
+    if (inter) return turns ? pick_phase<V, true, true>(vec) : pick_phase<V, true, false>(vec);
+    return turns ? pick_phase<V, false, true>(vec) : pick_phase<V, false, false>(vec);
+}
+
+cudaError_t launch_phase_grid(int variant, bool inter, bool turns, bool vec, const float *f, size_t nf,
+                              const float *t, size_t nt, float *so, float *co, float *io, cudaStream_t stream) {
+    const void *fn = variant == kNormalized ? pick_phase_v<kNormalized>(inter, turns, vec)
+                                            : pick_phase_v<kRenormalized>(inter, turns, vec);
+    const size_t cols = vec ? nt / 8 : nt;
+    const size_t gx = (cols + kPhaseThreads - 1) / kPhaseThreads;
+    const size_t gy = nf < 65535 ? nf : 65535;
+    if (gx == 0 || gx > 0x7FFFFFFFu) return cudaErrorInvalidValue;
+    void *args[] = {&f, &t, &nf, &nt, &so, &co, &io};
+    return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)), dim3(kPhaseThreads),
+                            args, 0, stream);
+}
+
+}  // namespace sincos_b200

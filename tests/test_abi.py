@@ -87,6 +87,22 @@ def test_overlap_rules(L):
     assert st in (OK, 3)  # 3 = SINCOS_ERR_CUDA here (no GPU)
 
 
+def test_phase_grid_validation(L):
+    """NEXT(1) sincos_phase_grid: same conventions, checked before any CUDA call."""
+    f, t = A, 2 * A
+    assert L.sincos_phase_grid(None, 0, None, 5, None, None, None, 0, 0, None) == OK       # empty grid
+    assert L.sincos_phase_grid(f, 4, t, 8, 3 * A, 4 * A, None, 2, 0, None) == INVALID       # bad units
+    assert L.sincos_phase_grid(f, 4, t, 8, 3 * A, 4 * A, None, 0, 5, None) == INVALID       # bad variant
+    assert L.sincos_phase_grid(None, 4, t, 8, 3 * A, 4 * A, None, 0, 0, None) == INVALID    # no f
+    assert L.sincos_phase_grid(f, 4, t, 8, 3 * A, None, None, 0, 0, None) == INVALID        # half a split form
+    assert L.sincos_phase_grid(f, 4, t, 8, 3 * A, 4 * A, 5 * A, 1, 0, None) == INVALID      # both forms
+    assert L.sincos_phase_grid(f, 1 << 40, t, 1 << 40, 3 * A, 4 * A, None, 0, 0, None) == INVALID  # overflow
+    assert L.sincos_phase_grid(f, 4, t, 8, f + 4, 4 * A, None, 0, 0, None) == OVERLAP       # output over f
+    assert L.sincos_phase_grid(f, 4, t, 8, None, None, t - 16, 1, 0, None) == OVERLAP       # output over t
+    assert L.sincos_phase_grid(f, 4, t, 8, 3 * A, 3 * A + 64, None, 0, 0, None) == OVERLAP  # sin over cos
+    assert L.sincos_phase_grid(f, 4, t, 8, 3 * A, 4 * A, None, 0, 0, None) in (OK, 3)       # valid: needs CUDA
+
+
 def test_host_path_validation(L):
     assert L.sincos_pairs_host(None, None, None, None, 0, 0, None, 0, None) == OK
     buf = (ctypes.c_float * 64)()
@@ -100,7 +116,7 @@ def test_launch_config_validation(L):
     assert L.sincos_set_launch_config(100, 0, 8, 2, 0) == -1
     assert L.sincos_set_launch_config(256, 0, 3, 2, 0) == -1
     assert L.sincos_set_launch_config(256, 0, 8, 3, 0) == -1
-    assert L.sincos_set_launch_config(256, 0, 8, 2, 2) == -1
+    assert L.sincos_set_launch_config(256, 0, 8, 2, 3) == -1
     assert L.sincos_set_launch_config(256, -1, 8, 2, 0) == -1
     assert L.sincos_set_launch_config(512, 16, 4, 4, 1) == 0
     assert sp.get_launch_config() == {"threads": 512, "blocks_per_sm": 16, "vec": 4, "unroll": 4, "prefetch": 1}

@@ -1,0 +1,109 @@
+"""GPU parity of NEXT(1), sincos_phase_grid (pairs of phases f_i * t_j formed in the kernel),
+against the oracle's phase functions: bit-exact by value.  ``pytest -m gpu``."""
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+from helpers import assert_parity
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_cs_0406049_b200 as sp  # noqa: E402
+
+R, T = 0, 1
+COMBOS = [(u, v) for u in (R, T) for v in (0, 1)]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+
+
+def c4_axes(nf=1 << 15, nt=1 << 15, turns=False):
+    """BASELINE configs[3] axes: f_i = 512 u(3,0,i), t_j = (j + u(3,1,j)) 2^-15 (jittered,
+    sorted); in radians the row factor is fl32(2 pi f_i)."""
+    f = np.array([512.0 * inputs.urand(3, 0, i) for i in range(nf)])
+    t = np.array([(j + inputs.urand(3, 1, j)) * 2.0 ** -15 for j in range(nt)])
+    if not turns:
+        f = 2 * np.pi * f
+    return f.astype(np.float32), t.astype(np.float32)
+
+
+@pytest.mark.parametrize("units,variant", COMBOS)
+@pytest.mark.parametrize("shape", [(37, 53), (100, 1024), (3, 8), (1, 1), (5, 7)])
+@pytest.mark.parametrize("inter", [False, True])
+def test_small_grids_full(units, variant, shape, inter):
+    nf, nt = shape
+    rng = np.random.default_rng(nf * 1000 + nt)
+    f = rng.uniform(0, 400, nf).astype(np.float32)
+    t = rng.uniform(-1, 1, nt).astype(np.float32)
+    ws, wc = oracle.phase_grid(f, t, units, variant)
+    fd, td = torch.from_numpy(f).cuda(), torch.from_numpy(t).cuda()
+    if inter:
+        o = torch.empty(2 * nf * nt, device="cuda")
+        sp.phase_grid(fd, td, interleaved_out=o, units=units, variant=variant)
+        o = o.cpu().numpy()
+        gs, gc = o[1::2], o[0::2]
+    else:
+        s = torch.empty(nf * nt, device="cuda")
+        c = torch.empty(nf * nt, device="cuda")
+        sp.phase_grid(fd, td, s, c, units=units, variant=variant)
+        gs, gc = s.cpu().numpy(), c.cpu().numpy()
+    assert_parity(gs, gc, ws.ravel(), wc.ravel(), f"phase {shape} units={units} v={variant}")
+
+
+@pytest.mark.parametrize("units,variant", COMBOS)
+def test_misaligned_outputs_use_the_scalar_path(units, variant):
+    nf, nt = 64, 256
+    rng = np.random.default_rng(9)
+    f = rng.uniform(0, 400, nf).astype(np.float32)
+    t = rng.uniform(0, 1, nt).astype(np.float32)
+    ws, wc = oracle.phase_grid(f, t, units, variant)
+    fd, td = torch.from_numpy(f).cuda(), torch.from_numpy(t).cuda()
+    big = torch.empty(2 * nf * nt + 8, device="cuda")
+    s, c = big[1:1 + nf * nt], big[nf * nt + 3:2 * nf * nt + 3]
+    sp.phase_grid(fd, td, s, c, units=units, variant=variant)
+    assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws.ravel(), wc.ravel(), "misaligned")
+    tbig = torch.empty(nt + 1, device="cuda")
+    tbig[1:] = td
+    s2, c2 = torch.empty(nf * nt, device="cuda"), torch.empty(nf * nt, device="cuda")
+    sp.phase_grid(fd, tbig[1:], s2, c2, units=units, variant=variant)       # t not 32-B aligned
+    assert_parity(s2.cpu().numpy(), c2.cpu().numpy(), ws.ravel(), wc.ravel(), "misaligned t")
+
+
+@pytest.mark.parametrize("units,variant", COMBOS)
+def test_c4_full_size_sampled(units, variant):
+    """The C4 shape (2^15 x 2^15 = 2^30 pairs, interleaved, 8 GiB) at full size; ~1M sampled
+    elements and whole first/last rows against the oracle's pointwise phase pairs."""
+    nf = nt = 1 << 15
+    f, t = c4_axes(nf, nt, turns=units == T)
+    fd, td = torch.from_numpy(f).cuda(), torch.from_numpy(t).cuda()
+    o = torch.empty(2 * nf * nt, device="cuda")
+    sp.phase_grid(fd, td, interleaved_out=o, units=units, variant=variant)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(units * 2 + variant)
+    idx = np.unique(np.concatenate([np.arange(nt), np.arange(nf * nt - nt, nf * nt),
+                                    rng.integers(0, nf * nt, 1 << 20)])).astype(np.int64)
+    ov = o.view(-1, 2)[torch.from_numpy(idx).cuda()].cpu().numpy()
+    ws, wc = oracle.phase_points(f[idx // nt], t[idx % nt], units, variant)
+    assert_parity(ov[:, 1].copy(), ov[:, 0].copy(), ws, wc, "C4 phase grid")
+    del o
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_radians_equals_the_materialised_path(variant):
+    """Product-level consistency: the fused grid in radians equals sincos_pairs on the
+    materialised fp32 outer product (torch fp32 multiply = RN(f t)), bit for bit."""
+    f, t = c4_axes(1 << 10, 1 << 12)
+    fd, td = torch.from_numpy(f).cuda(), torch.from_numpy(t).cuda()
+    th = torch.outer(fd, td).reshape(-1).contiguous()
+    s1, c1 = sp.sincos(th, variant=variant)
+    s2, c2 = torch.empty_like(th), torch.empty_like(th)
+    sp.phase_grid(fd, td, s2, c2, units=R, variant=variant)
+    torch.cuda.synchronize()
+    assert torch.equal(s1, s2) and torch.equal(c1, c2)

@@ -117,6 +117,8 @@ def _load():
             "oracle_phase_points": (ctypes.c_int, [_P, _P, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, _P, _P]),
             "oracle_phase_grid": (ctypes.c_int, [_P, ctypes.c_size_t, _P, ctypes.c_size_t, ctypes.c_int,
                                                  ctypes.c_int, _P, _P]),
+            "oracle_nudft": (ctypes.c_int, [_P, ctypes.c_size_t, _P, _P, ctypes.c_size_t, ctypes.c_int,
+                                            ctypes.c_int, _P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -210,6 +212,21 @@ def phase_grid(f, t, units: int, variant: int):
                                  c.ctypes.data) != 0:
         raise ValueError("bad variant or units")
     return s, c
+
+
+def nudft(f, t, a, units: int, variant: int) -> np.ndarray:
+    """NEXT(2): F_k = sum_j a_j e^{i p_kj}, p_kj = RN(f_k t_j), pairs by the method, products and
+    sums in double.  a: complex64 array (or interleaved float32); returns complex128 (nf,)."""
+    f, t = _f32(f), _f32(t)
+    a = np.ascontiguousarray(a)
+    a = a.view(np.float32) if np.iscomplexobj(a) else _f32(a)
+    a = np.ascontiguousarray(a.astype(np.float32, copy=False))
+    assert a.size == 2 * t.size
+    out = np.empty(2 * f.size, dtype=np.float64)
+    if _load().oracle_nudft(f.ctypes.data, f.size, t.ctypes.data, a.ctypes.data, t.size, units, variant,
+                            out.ctypes.data) != 0:
+        raise ValueError("bad variant or units")
+    return out.view(np.complex128)
 
 
 def error_stats(theta, s, c, ref: int = REF_DOUBLE) -> Stats:

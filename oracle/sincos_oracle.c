@@ -180,6 +180,34 @@ int oracle_phase_points(const float *f, const float *t, size_t m, int units, int
     return 0;
 }
 
+/* ---- NEXT(2): the consumer of the pairs -- a direct non-uniform Fourier / Huygens sum
+ * ("rapid computation of optical diffraction patterns via Huygens'
+ * principle"):
+ *     F_k = sum_j a_j (cos p_kj + i sin p_kj),   p_kj = RN(f_k t_j)
+ * with the pairs of oracle_phase_pair (radians or turns) and the complex products
+ * and the sum in double (the plain definition; a = interleaved {re, im} float
+ * pairs, out = interleaved {re, im} doubles). */
+int oracle_nudft(const float *f, size_t nf, const float *t, const float *a, size_t nt, int units,
+                 int variant, double *out)
+{
+    oracle_opts_t o;
+    if (oracle_variant_opts(variant, &o) != 0 || (units != 0 && units != 1))
+        return -1;
+    for (size_t k = 0; k < nf; ++k) {
+        double re = 0.0, im = 0.0;
+        for (size_t j = 0; j < nt; ++j) {
+            float s, c;
+            oracle_phase_pair(f[k], t[j], units, &o, &s, &c);
+            const double ar = a[2 * j], ai = a[2 * j + 1];
+            re += ar * (double)c - ai * (double)s;
+            im += ar * (double)s + ai * (double)c;
+        }
+        out[2 * k] = re;
+        out[2 * k + 1] = im;
+    }
+    return 0;
+}
+
 /* Row-major grid: element (i, j) at i*nt + j is the pair of phase f[i] * t[j]. */
 int oracle_phase_grid(const float *f, size_t nf, const float *t, size_t nt, int units, int variant,
                       float *s_out, float *c_out)

@@ -108,6 +108,13 @@ int oracle_phase_points(const float *f, const float *t, size_t m, int units, int
 int oracle_phase_grid(const float *f, size_t nf, const float *t, size_t nt, int units, int variant,
                       float *s_out, float *c_out);
 
+/* ---- NEXT(2): direct non-uniform Fourier / Huygens sum ------
+ * out[k] = sum_j a_j * (cos p_kj + i sin p_kj), p_kj = RN(f_k t_j) (units as
+ * above); a: nt interleaved {re, im} floats; out: nf interleaved {re, im}
+ * doubles, products and sums in double.  Returns 0 or -1. */
+int oracle_nudft(const float *f, size_t nf, const float *t, const float *a, size_t nt, int units,
+                 int variant, double *out);
+
 /* ---- error metrics, P:135-139 (accuracy.c) -------------------------- */
 
 typedef struct {

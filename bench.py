@@ -260,6 +260,56 @@ def measure_phase_grid(dev, stream, peak, reps=10):
     return out
 
 
+ALU_PEAK_OPS = 148 * 128 * 1.965e9   # FP32-pipe lane-ops/s at the max SM clock (FMA = 1 op)
+# algorithmic FP32-pipe ops per term of the fused sum, variant N: the phase product (1), the
+# method (11 FMUL + 10 FFMA + 1 FADD + 1 FRND = 23; turns skips the 1/2pi FMUL), the complex MAC (4)
+NUDFT_OPS = {"radians": 28, "turns": 27}
+
+
+def measure_nudft(dev, stream, reps=5):
+    """NEXT(2) side measurement: the fused Huygens / non-uniform Fourier sum at the C4 shape
+    (2^15 frequencies x 2^15 jittered times = 2^30 terms, random complex amplitudes).  FP32-ALU
+    bound: achieved = algorithmic FP32-pipe ops/s vs 148 SMs x 128 lanes x 1.965 GHz.  The same
+    fused kernel with CUDA's sincosf (sincospif in turns) and __sincosf is timed as context."""
+    import torch
+
+    import paper_cs_0406049_b200 as sp
+    nf = nt = 1 << 15
+    rng = np.random.default_rng(7)
+    a = torch.from_numpy((rng.normal(size=nt) + 1j * rng.normal(size=nt)).astype(np.complex64)).to(dev)
+    out = torch.empty(nf, dtype=torch.complex64, device=dev)
+    ws = torch.empty(sp.lib().sincos_nudft_workspace_bytes(nf, nt), dtype=torch.uint8, device=dev)
+    res = {"workload": "C4 shape: 2^15 f x 2^15 t = 2^30 terms, complex64 amplitudes", "bound": "alu",
+           "peak_ops_per_s": ALU_PEAK_OPS, "ops_per_term": NUDFT_OPS}
+    ks = torch.arange(0, nf, nf // 16, device=dev)
+    asum = float(a.abs().sum())
+    for units, uname in ((sp.RADIANS, "radians"), (sp.TURNS, "turns")):
+        f, t = c4_axes(units == sp.TURNS)
+        fd, td = torch.from_numpy(f).to(dev), torch.from_numpy(t).to(dev)
+        # fp64 reference of 16 sampled outputs (torch, complex128): sum_j a_j exp(i p_kj) with the
+        # same rounded phases p_kj = RN(f_k t_j) -- measures each variant's pair error
+        p = (fd[ks, None] * td[None, :]).double()
+        ang = p if units == sp.RADIANS else 2 * np.pi * (p - torch.round(p))
+        ref = (a.to(torch.complex128)[None, :] * torch.exp(1j * ang)).sum(dim=1)
+        for v, vname in ((sp.NORMALIZED, "N"), (sp.RENORMALIZED, "A"), (sp.CMP_LIBM_SINCOSF, "cuda_sincosf"),
+                         (sp.CMP_INTRINSIC_SINCOSF, "cuda___sincosf")):
+            sp.nudft(fd, td, a, out=out, units=units, variant=v, workspace=ws, stream=stream)
+            err = float((out[ks].to(torch.complex128) - ref).abs().max()) / asum
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                sp.nudft(fd, td, a, out=out, units=units, variant=v, workspace=ws, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms = e0.elapsed_time(e1) / reps
+            terms = (nf * nt) / (ms / 1e3)
+            r = {"ms": ms, "terms_per_s": terms, "max_err_over_sum_abs_a": err}
+            if vname == "N":
+                r["alu_frac"] = terms * NUDFT_OPS[uname] / ALU_PEAK_OPS
+            res[f"{uname}_{vname}"] = r
+    return res
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -402,6 +452,9 @@ def run_ours(args, rank, world, local_rank):
     fused = None
     if rank == 0 and not args.no_next:
         fused = measure_phase_grid(dev, stream, peak)
+        nudft_res = measure_nudft(dev, stream)
+    else:
+        nudft_res = None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -429,6 +482,7 @@ def run_ours(args, rank, world, local_rank):
                                "is the method's (BASELINE.md section 2), the kernel equals the oracle bit for bit",
             "shards": summary["shards"],
             "next_fused_phase": fused,
+            "next_fused_nudft": nudft_res,
             "paper_context": "PowerPC 7400 G4 500 MHz AltiVec: 140 ns per 4 pairs = 28.6 M pairs/s (P:177-180)",
         }
         print(json.dumps(line), flush=True)

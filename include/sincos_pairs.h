@@ -127,6 +127,30 @@ SINCOS_API sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, cons
                                              sincos_units_t units, sincos_variant_t variant, void *stream);
 
 /*
+ * sincos_nudft -- NEXT(2): the pairs' consumer fused with them, a direct
+ * non-uniform Fourier / Huygens sum (the diffraction application of P:203-206):
+ *     out[k] = sum_{j < nt} a[j] * (cos p_kj + i sin p_kj),   p_kj = RN(f[k] * t[j]),
+ * p in radians or turns as in sincos_phase_grid, pairs bit-identical to it.
+ *   a_dev    nt complex64 amplitudes, interleaved {re, im} (8-B aligned)
+ *   out_dev  nf complex64 results, interleaved {re, im} (8-B aligned)
+ *   ws_dev   device workspace of >= sincos_nudft_workspace_bytes(nf, nt) bytes
+ *            (8-B aligned), not overlapping anything else
+ * Arithmetic: complex products and per-chunk sums in fp32 with FMA (chunks of
+ * sincos_nudft_chunk(nt) consecutive terms, summed in order), the chunk partials
+ * added in fp64 in chunk order, rounded once to fp32: deterministic.  Error bound
+ * against the exact sum of the same pairs:
+ *   |out[k] - F_k| <= (chunk + 2) * 2^-24 * sum_j |a_j| + 2^-24 |F_k|.
+ * Two launches (partials, reduction).  nf == 0 is a no-op; nt == 0 zeroes out.
+ * variant: SINCOS_NORMALIZED / SINCOS_RENORMALIZED, or -- for comparison only --
+ * 3 = CUDA libm sincosf (sincospif in turns), 4 = the __sincosf intrinsic.
+ */
+SINCOS_API size_t sincos_nudft_chunk(size_t nt);
+SINCOS_API size_t sincos_nudft_workspace_bytes(size_t nf, size_t nt);
+SINCOS_API sincos_status_t sincos_nudft(const float *f_dev, size_t nf, const float *t_dev, const float *a_dev,
+                                        size_t nt, float *out_dev, sincos_units_t units, int variant,
+                                        void *ws_dev, size_t ws_bytes, void *stream);
+
+/*
  * Host-side sharding: element ranges [lo, hi) of shard g of
  * nshards, contiguous, every shard start a multiple of 8 elements (32-B
  * aligned in any aligned array); the last shard takes the remainder.  Pure

@@ -72,7 +72,13 @@ _SIGS = {
     "sincos_version": (ctypes.c_char_p, []),
     "sincos_launch_count": (ctypes.c_uint64, []),
     "sincos_phase_grid": (_I, [_P, _S, _P, _S, _P, _P, _P, _I, _I, _P]),
+    "sincos_nudft_chunk": (_S, [_S]),
+    "sincos_nudft_workspace_bytes": (_S, [_S, _S]),
+    "sincos_nudft": (_I, [_P, _S, _P, _P, _S, _P, _I, _I, _P, _S, _P]),
 }
+
+CMP_LIBM_SINCOSF = 3      # comparison only: CUDA libm sincosf / sincospif in the fused sum
+CMP_INTRINSIC_SINCOSF = 4  # comparison only: __sincosf
 
 RADIANS, TURNS = 0, 1
 EXPORTS = tuple(_SIGS)
@@ -173,6 +179,32 @@ def phase_grid(f, t, sin_out=None, cos_out=None, interleaved_out=None, units=RAD
                                  _ptr(cos_out, "cos_out"), _ptr(interleaved_out, "interleaved_out"), int(units),
                                  _variant(variant), _stream(stream, f.device))
     _check(st, "sincos_phase_grid")
+
+
+def nudft_chunk(nt: int) -> int:
+    return int(lib().sincos_nudft_chunk(nt))
+
+
+def nudft(f, t, a, out=None, units=RADIANS, variant=NORMALIZED, workspace=None, stream=None):
+    """NEXT(2) C-ABI sincos_nudft: out[k] = sum_j a[j] e^{i RN(f[k] t[j])} (complex64 a, out;
+    float32 f, t; CUDA tensors).  Returns out."""
+    import torch
+    nf, nt = f.numel(), t.numel()
+    if a.dtype == torch.complex64:
+        a = torch.view_as_real(a)
+    if a.numel() != 2 * nt:
+        raise ValueError("a must hold nt complex values")
+    if out is None:
+        out = torch.empty(nf, dtype=torch.complex64, device=f.device)
+    o = torch.view_as_real(out) if out.dtype == torch.complex64 else out
+    need = int(lib().sincos_nudft_workspace_bytes(nf, nt))
+    if workspace is None:
+        workspace = torch.empty(max(need, 8), dtype=torch.uint8, device=f.device)
+    st = lib().sincos_nudft(_ptr(f, "f"), nf, _ptr(t, "t"), _ptr(a.contiguous(), "a"), nt, _ptr(o, "out"),
+                            int(units), _variant(variant), workspace.data_ptr(),
+                            workspace.numel() * workspace.element_size(), _stream(stream, f.device))
+    _check(st, "sincos_nudft")
+    return out
 
 
 def host_workspace_min_bytes() -> int:

@@ -235,6 +235,40 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
     return SINCOS_OK;
 }
 
+size_t sincos_nudft_chunk(size_t nt) { return nudft_chunk(nt); }
+
+size_t sincos_nudft_workspace_bytes(size_t nf, size_t nt) { return nudft_ws_bytes(nf, nt); }
+
+sincos_status_t sincos_nudft(const float *f_dev, size_t nf, const float *t_dev, const float *a_dev, size_t nt,
+                             float *out_dev, sincos_units_t units, int variant, void *ws_dev, size_t ws_bytes,
+                             void *stream) {
+    if (variant < 0 || variant > 4) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (units != SINCOS_RADIANS && units != SINCOS_TURNS) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (nf == 0) return SINCOS_OK;
+    if (f_dev == nullptr || out_dev == nullptr || !aligned(f_dev, 4) || !aligned(out_dev, 8))
+        return SINCOS_ERR_INVALID_ARGUMENT;
+    if (nf > SIZE_MAX / 16 || nt > SIZE_MAX / 16) return SINCOS_ERR_INVALID_ARGUMENT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (overlaps(out_dev, 8 * nf, f_dev, 4 * nf)) return SINCOS_ERR_OVERLAP;
+    if (nt == 0) {
+        cudaError_t e = cudaMemsetAsync(out_dev, 0, 8 * nf, s);
+        return e == cudaSuccess ? SINCOS_OK : cuda_fail(e);
+    }
+    if (t_dev == nullptr || a_dev == nullptr || ws_dev == nullptr || !aligned(t_dev, 4) || !aligned(a_dev, 8) ||
+        !aligned(ws_dev, 8))
+        return SINCOS_ERR_INVALID_ARGUMENT;
+    const size_t need = nudft_ws_bytes(nf, nt);
+    if (ws_bytes < need) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (overlaps(out_dev, 8 * nf, t_dev, 4 * nt) || overlaps(out_dev, 8 * nf, a_dev, 8 * nt) ||
+        overlaps(ws_dev, need, out_dev, 8 * nf) || overlaps(ws_dev, need, f_dev, 4 * nf) ||
+        overlaps(ws_dev, need, t_dev, 4 * nt) || overlaps(ws_dev, need, a_dev, 8 * nt))
+        return SINCOS_ERR_OVERLAP;
+    cudaError_t e = launch_nudft(variant, units == SINCOS_TURNS, f_dev, nf, t_dev, a_dev, nt, out_dev, ws_dev, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    return SINCOS_OK;
+}
+
 size_t sincos_host_workspace_min_bytes(void) { return kSlots * kMinChunk * 12; }
 
 sincos_status_t sincos_pairs_host(const float *theta_host, float *sin_host, float *cos_host, float *inter_host,

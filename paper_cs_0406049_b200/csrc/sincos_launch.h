@@ -24,6 +24,11 @@ cudaError_t launch_tma(int variant, bool inter, unsigned grid, const float *thet
 // NEXT(1) phase grid (sincos_phase.cu); vec = 256-bit path (nt % 8 == 0, 32-B aligned t/outputs).
 cudaError_t launch_phase_grid(int variant, bool inter, bool turns, bool vec, const float *f, size_t nf,
                               const float *t, size_t nt, float *so, float *co, float *io, cudaStream_t stream);
+// NEXT(2) fused non-uniform Fourier sum (sincos_nudft.cu); variant 3/4 = comparison sincosf.
+size_t nudft_chunk(size_t nt);
+size_t nudft_ws_bytes(size_t nf, size_t nt);
+cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, const float *t, const float *a,
+                         size_t nt, float *out, void *ws, cudaStream_t stream);
 const void *vec_kernel_ptr(int variant, bool inter, int w, int unroll, bool nc, bool pf);
 
 size_t stats_ws_bytes();

@@ -50,21 +50,20 @@ template <> struct Series<kRenormalized> {
 
 // Correctly rounded fp32 reciprocal RN(1/d), branch-free ("precise reciprocal",
 // P:157-158, Fig. 1; the paper's Reciprocal() body is not listed).
-// fp64 seed from MUFU.RCP64H, two Newton steps in DFMA (each squares the
-// relative error: ~2^-22 -> 2^-44 -> below 2^-53), then one rounding to fp32.
-// Exact because 1/d for a 24-bit d is never within 2^-48 (relative) of an
-// fp32 rounding midpoint while the fp64 value is within a few 2^-53 (reading
-// G3; verified over every fp32 d in [0.5, 2) by tests/test_gpu_parity.py).
-// rcp.rn.f32 would also be exact but compiles to a slow-path branch.
+// MUFU.RCP seed (rcp.approx.ftz.f32) and one Newton step in FMA: the residual
+// e = 1 - d*y0 is exact in fp32 for a seed within an ulp, and y0 + y0*e rounds once.
+// On sm_100a this sequence returns RN(1/d) for EVERY fp32 d in [0.5, 2) -- including
+// the near-midpoint case d = 1 - 2^-24 -- verified exhaustively on the B200
+// (tools/rcp_probe.cu; tests/test_gpu_parity.py::test_reciprocal_exhaustive), and the
+// method only produces d = s2^2 + c2^2 in [0.9975, 1.0000002] (SURVEY [X10]; the
+// all-2^32-input hash test covers every d that occurs).  3 instructions, branch-free;
+// rcp.rn.f32 would also be exact but compiles to a slow-path branch, and the fp64
+// Newton sequence used before costs 8 instructions (F2F, MUFU.RCP64H, 4 DFMA, F2F).
 __device__ __forceinline__ float rcp_rn(float d) {
-    const double x = static_cast<double>(d);
-    double y;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    double e = __fma_rn(-x, y, 1.0);
-    y = __fma_rn(y, e, y);
-    e = __fma_rn(-x, y, 1.0);
-    y = __fma_rn(y, e, y);
-    return __double2float_rn(y);
+    float y0;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y0) : "f"(d));
+    const float e = __fmaf_rn(-d, y0, 1.0f);
+    return __fmaf_rn(y0, e, y0);
 }
 
 // The pair from a reduced turn q1 in [-1/2, 1/2] (steps a4-a9).  Step letters follow

@@ -1,0 +1,158 @@
+// sincos_nudft.cu -- NEXT(2): the consumer of the pairs, fused.
+//
+// "The author has been applying this method to the rapid computation of optical
+// diffraction patterns via Huygens' principle": a sum of many unit
+// phasors of non-uniformly spaced phases weighted by complex amplitudes,
+//     F_k = sum_j a_j (cos p_kj + i sin p_kj),     p_kj = RN(f_k * t_j),
+// i.e. a direct non-uniform Fourier sum.  The pairs are evaluated by the paper's
+// method in registers and consumed at once -- none reaches HBM -- so the kernel is
+// bound by the FP32 pipe, not by memory: per term 1 FMUL (the phase) + the method
+// (~23 FP32-pipe ops + FRND, N) + 4 FFMA (complex multiply-accumulate).
+//
+// Layout: block (x, y) owns kKPerBlock frequencies (kKPerThread per thread, strided by
+// the block size so the partial stores coalesce) and chunk y of kChunk consecutive
+// terms j.  The chunk's (t_j, a_j) are staged through shared memory in tiles and read
+// by all threads as broadcasts.  Each thread accumulates its kKPerThread complex sums
+// over the chunk in fp32 (kChunk terms, sequential), writes the partial to the
+// workspace, and a second kernel adds the partials of all chunks in fp64 in chunk
+// order (deterministic) and rounds to complex64.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sincos_launch.h"
+#include "sincos_math.cuh"
+
+namespace sincos_b200 {
+
+constexpr int kNuThreads = 128;
+constexpr int kKPerThread = 4;
+constexpr int kKPerBlock = kNuThreads * kKPerThread;
+constexpr int kTileJ = 256;
+
+// Comparison "variants" for the bench only (not the paper's method): CUDA's libm
+// sincosf (accurate, with a slow path for large arguments) and the __sincosf intrinsic.
+constexpr int kLibmSincosf = 3;
+constexpr int kIntrinsicSincosf = 4;
+
+template <int V, bool TURNS>
+__device__ __forceinline__ void term_pair(float f, float t, float &s, float &c) {
+    const float p = __fmul_rn(f, t);
+    if constexpr (V == kLibmSincosf) {
+        if constexpr (TURNS) sincospif(2.0f * p, &s, &c); else sincosf(p, &s, &c);
+    } else if constexpr (V == kIntrinsicSincosf) {
+        __sincosf(TURNS ? 6.28318530717958647692f * p : p, &s, &c);
+    } else if constexpr (TURNS) {
+        sincos_pair_turns<V>(p, s, c);
+    } else {
+        sincos_pair<V>(p, s, c);
+    }
+}
+
+template <int V, bool TURNS>
+__global__ void __launch_bounds__(kNuThreads) nudft_partial(const float *__restrict__ f, size_t nf,
+                                                            const float *__restrict__ t,
+                                                            const float2 *__restrict__ a, size_t nt,
+                                                            size_t chunk, float2 *__restrict__ part) {
+    __shared__ float st[kTileJ];
+    __shared__ float2 sa[kTileJ];
+    const size_t k0 = static_cast<size_t>(blockIdx.x) * kKPerBlock + threadIdx.x;
+    const size_t j0 = static_cast<size_t>(blockIdx.y) * chunk;
+    const size_t j1 = j0 + chunk < nt ? j0 + chunk : nt;
+    float fk[kKPerThread], re[kKPerThread], im[kKPerThread];
+#pragma unroll
+    for (int m = 0; m < kKPerThread; ++m) {
+        const size_t k = k0 + m * kNuThreads;
+        fk[m] = k < nf ? f[k] : 0.0f;
+        re[m] = 0.0f;
+        im[m] = 0.0f;
+    }
+    for (size_t jt = j0; jt < j1; jt += kTileJ) {
+        const int len = static_cast<int>(j1 - jt < kTileJ ? j1 - jt : kTileJ);
+        __syncthreads();
+        for (int q = threadIdx.x; q < len; q += kNuThreads) {
+            st[q] = t[jt + q];
+            sa[q] = a[jt + q];
+        }
+        __syncthreads();
+        for (int q = 0; q < len; ++q) {
+            const float tj = st[q];
+            const float2 aj = sa[q];
+#pragma unroll
+            for (int m = 0; m < kKPerThread; ++m) {
+                float s, c;
+                term_pair<V, TURNS>(fk[m], tj, s, c);
+                // (ar + i ai)(c + i s) accumulated with single-rounding FMAs
+                re[m] = __fmaf_rn(aj.x, c, re[m]);
+                re[m] = __fmaf_rn(-aj.y, s, re[m]);
+                im[m] = __fmaf_rn(aj.x, s, im[m]);
+                im[m] = __fmaf_rn(aj.y, c, im[m]);
+            }
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < kKPerThread; ++m) {
+        const size_t k = k0 + m * kNuThreads;
+        if (k < nf) part[static_cast<size_t>(blockIdx.y) * nf + k] = make_float2(re[m], im[m]);
+    }
+}
+
+__global__ void __launch_bounds__(256) nudft_reduce(const float2 *__restrict__ part, size_t nf, size_t nchunks,
+                                                    float2 *__restrict__ out) {
+    const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= nf) return;
+    double re = 0.0, im = 0.0;
+    for (size_t c = 0; c < nchunks; ++c) {
+        const float2 p = part[c * nf + k];
+        re += p.x;
+        im += p.y;
+    }
+    out[k] = make_float2(__double2float_rn(re), __double2float_rn(im));
+}
+
+size_t nudft_chunk(size_t nt) {
+    // terms per thread per chunk: enough chunks to fill the GPU, long enough to amortise
+    // the partial sums; a multiple of the shared-memory tile
+    size_t chunk = 1024;
+    if (nt < 4 * chunk) chunk = kTileJ;
+    return chunk;
+}
+
+size_t nudft_ws_bytes(size_t nf, size_t nt) {
+    const size_t chunk = nudft_chunk(nt);
+    const size_t nchunks = (nt + chunk - 1) / chunk;
+    return nchunks * nf * sizeof(float2);
+}
+
+template <int V>
+static const void *pick_nudft(bool turns) {
+    return turns ? reinterpret_cast<const void *>(nudft_partial<V, true>)
+                 : reinterpret_cast<const void *>(nudft_partial<V, false>);
+}
+
+cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, const float *t, const float *a,
+                         size_t nt, float *out, void *ws, cudaStream_t stream) {
+    size_t chunk = nudft_chunk(nt);
+    const size_t nchunks = (nt + chunk - 1) / chunk;
+    const size_t gx = (nf + kKPerBlock - 1) / kKPerBlock;
+    if (gx > 0x7FFFFFFFu || nchunks > 65535) return cudaErrorInvalidValue;
+    const void *fn;
+    switch (variant) {
+    case kNormalized: fn = pick_nudft<kNormalized>(turns); break;
+    case kRenormalized: fn = pick_nudft<kRenormalized>(turns); break;
+    case kLibmSincosf: fn = pick_nudft<kLibmSincosf>(turns); break;
+    default: fn = pick_nudft<kIntrinsicSincosf>(turns); break;
+    }
+    const float2 *a2 = reinterpret_cast<const float2 *>(a);
+    float2 *part = static_cast<float2 *>(ws);
+    void *args[] = {&f, &nf, &t, &a2, &nt, &chunk, &part};
+    cudaError_t e = cudaLaunchKernel(fn, dim3(static_cast<unsigned>(gx), static_cast<unsigned>(nchunks)),
+                                     dim3(kNuThreads), args, 0, stream);
+    if (e != cudaSuccess) return e;
+    float2 *o = reinterpret_cast<float2 *>(out);
+    size_t nch = nchunks;
+    void *rargs[] = {&part, &nf, &nch, &o};
+    return cudaLaunchKernel(reinterpret_cast<const void *>(nudft_reduce),
+                            dim3(static_cast<unsigned>((nf + 255) / 256)), dim3(256), rargs, 0, stream);
+}
+
+}  // namespace sincos_b200

@@ -1,0 +1,121 @@
+"""GPU parity of NEXT(2), sincos_nudft (the fused Huygens / non-uniform Fourier sum), against
+the oracle's nudft (same pairs, products and sums in double).  ``pytest -m gpu``.
+
+The pairs are bit-identical to the method; the fused sum rounds differently from the
+oracle's double sum, so the bar is the bound the header derives from the arithmetic:
+  |out_k - F_k| <= (chunk + 2) 2^-24 sum_j |a_j| + 2^-24 |F_k|."""
+import numpy as np
+import pytest
+
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_cs_0406049_b200 as sp  # noqa: E402
+
+U = 2.0 ** -24
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+
+
+def rand_complex(rng, n):
+    return (rng.normal(size=n) + 1j * rng.normal(size=n)).astype(np.complex64)
+
+
+def run(f, t, a, units, variant):
+    out = sp.nudft(torch.from_numpy(f).cuda(), torch.from_numpy(t).cuda(), torch.from_numpy(a).cuda(),
+                   units=units, variant=variant)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.complex128)
+
+
+def bound(a, F, nt):
+    return (sp.nudft_chunk(nt) + 2) * U * np.abs(a).sum() + U * np.abs(F)
+
+
+@pytest.mark.parametrize("units", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("shape", [(300, 1000), (1, 1), (513, 257), (1024, 5000)])
+def test_random_problems_within_bound(units, variant, shape):
+    nf, nt = shape
+    rng = np.random.default_rng(nf + nt)
+    f = rng.uniform(0, 512 if units else 3000, nf).astype(np.float32)
+    t = np.sort(rng.uniform(0, 1, nt)).astype(np.float32)
+    a = rand_complex(rng, nt)
+    got = run(f, t, a, units, variant)
+    want = oracle.nudft(f, t, a, units, variant)
+    assert np.all(np.abs(got - want) <= bound(a, want, nt))
+
+
+@pytest.mark.parametrize("units", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1])
+def test_single_amplitude_is_exactly_the_pair(units, variant):
+    """a = e_j0: every product and partial sum is exact, so out_k is the method's pair of
+    (f_k, t_j0) bit for bit (the fused path evaluates the same pairs as sincos_phase_grid)."""
+    rng = np.random.default_rng(5)
+    nf, nt = 700, 3000
+    f = rng.uniform(0, 400, nf).astype(np.float32)
+    t = rng.uniform(-1, 1, nt).astype(np.float32)
+    a = np.zeros(nt, np.complex64)
+    a[1234] = 1
+    got = run(f, t, a, units, variant)
+    s, c = oracle.phase_points(f, np.full(nf, t[1234], np.float32), units, variant)
+    assert np.array_equal(got.real, c.astype(np.float64)) and np.array_equal(got.imag, s.astype(np.float64))
+
+
+def test_uniform_grid_matches_fft():
+    """LIBRARY: t_j = j/N in turns, f_k = k -> the DFT; torch.fft on the GPU as the reference,
+    within the method's pair error times sum|a| plus the summation bound."""
+    N = 4096
+    rng = np.random.default_rng(6)
+    a = rand_complex(rng, N)
+    f = np.arange(N, dtype=np.float32)
+    t = (np.arange(N) / N).astype(np.float32)
+    got = run(f, t, a, 1, 0)
+    want = N * torch.fft.ifft(torch.from_numpy(a.astype(np.complex128)).cuda()).cpu().numpy()
+    assert np.all(np.abs(got - want) <= 4.9e-7 * np.abs(a).sum() + bound(a, want, N))
+
+
+@pytest.mark.parametrize("units", [0, 1])
+def test_c4_scale_sampled(units):
+    """The C4 shape (2^15 frequencies x 2^15 jittered times, 2^30 terms), 64 sampled k vs the
+    oracle."""
+    nf = nt = 1 << 15
+    rng = np.random.default_rng(7)
+    f = (512 * rng.random(nf)).astype(np.float32)
+    if not units:
+        f = (2 * np.pi * f.astype(np.float64)).astype(np.float32)
+    t = ((np.arange(nt) + rng.random(nt)) * 2.0 ** -15).astype(np.float32)
+    a = rand_complex(rng, nt)
+    got = run(f, t, a, units, 0)
+    ks = np.unique(np.concatenate([[0, nf - 1], rng.integers(0, nf, 62)]))
+    want = oracle.nudft(f[ks], t, a, units, 0)
+    assert np.all(np.abs(got[ks] - want) <= bound(a, want, nt))
+
+
+def test_edges():
+    f = torch.rand(10, device="cuda")
+    out = torch.full((10,), 7 + 7j, dtype=torch.complex64, device="cuda")
+    sp.nudft(f, torch.empty(0, device="cuda"), torch.empty(0, dtype=torch.complex64, device="cuda"), out=out)
+    torch.cuda.synchronize()
+    assert torch.all(out == 0)
+    sp.nudft(torch.empty(0, device="cuda"), torch.rand(5, device="cuda"),
+             torch.zeros(5, dtype=torch.complex64, device="cuda"))
+
+
+@pytest.mark.parametrize("variant", [sp.CMP_LIBM_SINCOSF, sp.CMP_INTRINSIC_SINCOSF])
+def test_comparison_variants_run(variant):
+    """The bench's comparison kernels (CUDA sincosf / __sincosf in the same fused sum) are sane."""
+    rng = np.random.default_rng(8)
+    f = rng.uniform(0, 50, 256).astype(np.float32)
+    t = rng.uniform(0, 1, 2048).astype(np.float32)
+    a = rand_complex(rng, 2048)
+    got = run(f, t, a, 1, variant)
+    want = oracle.nudft(f, t, a, 1, 0)
+    assert np.all(np.abs(got - want) <= 1e-3 * np.abs(a).sum())

@@ -103,6 +103,33 @@ SINCOS_API sincos_status_t sincos_pairs_host(const float *theta_host, float *sin
 SINCOS_API size_t sincos_host_workspace_min_bytes(void);
 
 /*
+ * sincos_pairs_method -- NEXT(3): the method with caller-supplied series and doubling
+ * count ("after n iterations ... two options for computing the raw pair.
+ * These options differ in the fitting algorithm used to find the coefficients").
+ *   s1 = RN(q * (ss[0] + q2 (ss[1] + ... q2 ss[n_ss-1])))   Horner, innermost first
+ *   c1 = 1 + q2 (cc[0] + q2 (cc[1] + ... q2 cc[n_cc-1]))     (1 when n_cc == 0)
+ * with q the reduced turn (steps a2-a3 unchanged), then `doublings` Eq. (1) doublings and
+ * the amplitude handling `fix` taken from the penultimate pair: 0 = linear
+ * f = 2 - s^2 - c^2 (method 1), 1 = exact reciprocal 1/(s^2 + c^2) (method 2; exact
+ * for penultimate magnitudes^2 in [0.5, 2), i.e. any usable fit), 3 = none.
+ * The paper's two methods are {its coefficients, n_ss 4, n_cc 3, doublings 2, fix 0/1}
+ * and give bit-identical results to sincos_pairs.  Same buffers, alignment and error
+ * conventions as sincos_pairs (in-place not supported).  `method` is a host pointer,
+ * read before return.
+ */
+typedef struct {
+    float ss[8];
+    int n_ss;        /* 1..8 */
+    float cc[8];
+    int n_cc;        /* 0..8 */
+    int doublings;   /* 0..8; fix requires >= 1 */
+    int fix;         /* 0 linear, 1 reciprocal, 3 none */
+} sincos_method_t;
+SINCOS_API sincos_status_t sincos_pairs_method(const float *theta_dev, float *sin_dev, float *cos_dev,
+                                               float *inter_dev, size_t n, const sincos_method_t *method,
+                                               void *stream);
+
+/*
  * sincos_phase_grid -- NEXT(1): pairs of phases generated inside the kernel.
  *
  * The paper's use case is phase factors for optical diffraction by Huygens'

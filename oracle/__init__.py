@@ -84,6 +84,29 @@ class Stats(ctypes.Structure):
         return d
 
 
+class Method(ctypes.Structure):
+    """oracle_method_t (NEXT(3)): any series degrees, doubling count and fix."""
+    _fields_ = [("ss", ctypes.c_float * 8), ("n_ss", ctypes.c_int), ("cc", ctypes.c_float * 8),
+                ("n_cc", ctypes.c_int), ("doublings", ctypes.c_int), ("fix", ctypes.c_int)]
+
+
+def make_method(ss, cc, doublings=2, fix=FIX_LINEAR_PENULTIMATE) -> Method:
+    m = Method()
+    for i, v in enumerate(ss):
+        m.ss[i] = float(np.float32(v))
+    for i, v in enumerate(cc):
+        m.cc[i] = float(np.float32(v))
+    m.n_ss, m.n_cc, m.doublings, m.fix = len(ss), len(cc), doublings, fix
+    return m
+
+
+def paper_method(variant: int) -> Method:
+    """The paper's method (variant N or A) as a general Method."""
+    o = opts(variant)
+    k = o.coeffs
+    return make_method([k.ss1, k.ss2, k.ss3, k.ss4], [k.cc1, k.cc2, k.cc3], o.doublings, o.fix)
+
+
 _lib = None
 _P = ctypes.c_void_p
 
@@ -119,6 +142,12 @@ def _load():
                                                  ctypes.c_int, _P, _P]),
             "oracle_nudft": (ctypes.c_int, [_P, ctypes.c_size_t, _P, _P, ctypes.c_size_t, ctypes.c_int,
                                             ctypes.c_int, _P]),
+            "oracle_method_pair_from_q": (ctypes.c_int, [ctypes.c_float, ctypes.POINTER(Method),
+                                                         ctypes.POINTER(ctypes.c_float),
+                                                         ctypes.POINTER(ctypes.c_float)]),
+            "oracle_method_sincos": (ctypes.c_int, [_P, _P, _P, ctypes.c_size_t, ctypes.POINTER(Method)]),
+            "oracle_method_sweep_q": (None, [ctypes.POINTER(Method), ctypes.c_uint32, ctypes.c_uint32,
+                                             ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(Stats)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -227,6 +256,32 @@ def nudft(f, t, a, units: int, variant: int) -> np.ndarray:
                             out.ctypes.data) != 0:
         raise ValueError("bad variant or units")
     return out.view(np.complex128)
+
+
+def method_pair_from_q(q: float, m: Method):
+    s, c = ctypes.c_float(), ctypes.c_float()
+    if _load().oracle_method_pair_from_q(q, ctypes.byref(m), ctypes.byref(s), ctypes.byref(c)) != 0:
+        raise ValueError("invalid method")
+    return s.value, c.value
+
+
+def method_sincos(theta, m: Method):
+    """NEXT(3): the general method over an array -> (sin, cos)."""
+    theta = _f32(theta)
+    s = np.empty_like(theta)
+    c = np.empty_like(theta)
+    if _load().oracle_method_sincos(theta.ctypes.data, s.ctypes.data, c.ctypes.data, theta.size,
+                                    ctypes.byref(m)) != 0:
+        raise ValueError("invalid method")
+    return s, c
+
+
+def method_sweep_q(m: Method, lo_bits: int = 0, hi_bits: int = 0x3F000000, stride: int = 1,
+                   nthreads: int = 0) -> Stats:
+    """Kernel-only error stats of a method over fp32 q in [0, 1/2] (every `stride`-th pattern)."""
+    st = Stats()
+    _load().oracle_method_sweep_q(ctypes.byref(m), lo_bits, hi_bits, stride, nthreads, ctypes.byref(st))
+    return st
 
 
 def error_stats(theta, s, c, ref: int = REF_DOUBLE) -> Stats:

@@ -188,6 +188,43 @@ void oracle_sweep_bits(const oracle_opts_t *o, int mode, uint32_t lo_bits, uint3
     free(part);
 }
 
+/* NEXT(3): kernel-only stats of a general method over fp32 q = bits(u), u = lo, lo+stride, ...
+ * <= hi, vs sin/cos(2 pi q) in double.  Fixed chunks merged in order (thread-count independent). */
+void oracle_method_sweep_q(const oracle_method_t *m, uint32_t lo_bits, uint32_t hi_bits, uint32_t stride,
+                           int nthreads, oracle_stats_t *st)
+{
+    if (stride == 0)
+        stride = 1;
+    uint64_t total = ((uint64_t)hi_bits - lo_bits) / stride + 1;
+    uint64_t nchunks = (total + SWEEP_CHUNK - 1) / SWEEP_CHUNK;
+    oracle_stats_t *part = (oracle_stats_t *)calloc(nchunks, sizeof(oracle_stats_t));
+#ifdef _OPENMP
+    if (nthreads > 0)
+        omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+    for (int64_t ch = 0; ch < (int64_t)nchunks; ++ch) {
+        oracle_stats_t *p = &part[ch];
+        stats_init(p);
+        uint64_t k0 = (uint64_t)ch * SWEEP_CHUNK, k1 = k0 + SWEEP_CHUNK;
+        if (k1 > total)
+            k1 = total;
+        for (uint64_t k = k0; k < k1; ++k) {
+            float x = u2f((uint32_t)(lo_bits + k * stride));
+            float s, c;
+            double rs, rc;
+            long double rsl, rcl;
+            oracle_method_pair_from_q(x, m, &s, &c);
+            ref_pair(2.0 * M_PI * (double)x, 0.0L, ORACLE_REF_DOUBLE, &rs, &rc, &rsl, &rcl);
+            stats_add(p, x, s, c, rs, rc, rsl, rcl, ORACLE_REF_DOUBLE);
+        }
+    }
+    stats_init(st);
+    for (uint64_t ch = 0; ch < nchunks; ++ch)
+        stats_merge(st, &part[ch]);
+    free(part);
+}
+
 /* SplitMix64 finalizer with its additive pre-step (SURVEY 8(c) hash definition). */
 static inline uint64_t hash_mix64(uint64_t x)
 {

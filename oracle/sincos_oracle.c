@@ -151,6 +151,59 @@ int sincos_oracle(const float *theta, float *s_out, float *c_out, size_t n, int 
     return sincos_oracle_opts(theta, s_out, c_out, n, &o);
 }
 
+/* ---- NEXT(3): any series degrees and doubling count ------------- */
+static int method_valid(const oracle_method_t *m)
+{
+    if (m->n_ss < 1 || m->n_ss > ORACLE_MAX_TERMS || m->n_cc < 0 || m->n_cc > ORACLE_MAX_TERMS)
+        return 0;
+    if (m->doublings < 0 || m->doublings > 8)
+        return 0;
+    if (m->fix == ORACLE_FIX_NONE)
+        return 1;
+    return (m->fix == ORACLE_FIX_LINEAR_PENULTIMATE || m->fix == ORACLE_FIX_RECIPROCAL) && m->doublings >= 1;
+}
+
+int oracle_method_pair_from_q(float q1, const oracle_method_t *m, float *s_out, float *c_out)
+{
+    if (!method_valid(m))
+        return -1;
+    float q2 = fmaf(q1, q1, 0.0f);
+    float ps = m->ss[m->n_ss - 1];                       /* Horner, innermost first */
+    for (int i = m->n_ss - 2; i >= 0; --i)
+        ps = fmaf(q2, ps, m->ss[i]);
+    float s = fmaf(q1, ps, 0.0f);
+    float c = 1.0f;
+    if (m->n_cc > 0) {
+        float pc = m->cc[m->n_cc - 1];
+        for (int i = m->n_cc - 2; i >= 0; --i)
+            pc = fmaf(q2, pc, m->cc[i]);
+        c = fmaf(q2, pc, 1.0f);
+    }
+    float fix = 1.0f;
+    for (int i = 0; i < m->doublings; ++i) {
+        if (i == m->doublings - 1) {                     /* the penultimate pair */
+            if (m->fix == ORACLE_FIX_LINEAR_PENULTIMATE)
+                fix = fmaf(-s, s, fmaf(-c, c, 2.0f));
+            else if (m->fix == ORACLE_FIX_RECIPROCAL)
+                fix = 1.0f / fmaf(s, s, fmaf(c, c, 0.0f));
+        }
+        oracle_double_angle(s, c, ORACLE_DOUBLING_EQ1, &s, &c);
+    }
+    *c_out = fmaf(c, fix, 0.0f);
+    *s_out = fmaf(s, fix, 0.0f);
+    return 0;
+}
+
+int oracle_method_sincos(const float *theta, float *s_out, float *c_out, size_t n,
+                         const oracle_method_t *m)
+{
+    if (!method_valid(m))
+        return -1;
+    for (size_t i = 0; i < n; ++i)
+        oracle_method_pair_from_q(oracle_reduce_turns(theta[i]), m, &s_out[i], &c_out[i]);
+    return 0;
+}
+
 /* ---- NEXT(1): phases generated from their factors ----
  * The pair for the phase of frequency f and time t.  The phase is formed as
  * one rounded fp32 product p = RN(f * t).  units == 0: p is the angle in

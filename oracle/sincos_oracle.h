@@ -97,6 +97,30 @@ int sincos_oracle(const float *theta, float *s_out, float *c_out, size_t n, int 
 int sincos_oracle_opts(const float *theta, float *s_out, float *c_out, size_t n,
                        const oracle_opts_t *o);
 
+/* ---- NEXT(3): the method with any series degrees and doubling count --------
+ * "the form of (1) produces a pair (after n iterations) ... there are two
+ * options for computing the raw pair. These options differ in the fitting algorithm
+ * used to find the coefficients".  Series (Horner, innermost first, as Fig. 1):
+ *   s1 = RN(q * (ss[0] + q2 (ss[1] + ... q2 ss[n_ss-1])))        (n_ss >= 1)
+ *   c1 = 1 + q2 (cc[0] + q2 (cc[1] + ... q2 cc[n_cc-1]))          (n_cc >= 0; 1 if 0)
+ * then `doublings` Eq. (1) doublings, the fix from the penultimate pair (Fig. 1
+ * order; needs doublings >= 1) or none.  For n_ss = 4, n_cc = 3, doublings = 2 it
+ * is exactly oracle_pair_from_q with the same coefficients. */
+#define ORACLE_MAX_TERMS 8
+typedef struct {
+    float ss[ORACLE_MAX_TERMS];
+    int n_ss;
+    float cc[ORACLE_MAX_TERMS];
+    int n_cc;
+    int doublings;    /* 0 .. 8 */
+    int fix;          /* ORACLE_FIX_LINEAR_PENULTIMATE, ORACLE_FIX_RECIPROCAL or ORACLE_FIX_NONE */
+} oracle_method_t;
+
+/* Returns 0, or -1 for an invalid method. */
+int oracle_method_pair_from_q(float q1, const oracle_method_t *m, float *s, float *c);
+int oracle_method_sincos(const float *theta, float *s_out, float *c_out, size_t n,
+                         const oracle_method_t *m);
+
 /* ---- NEXT(1): pairs of generated phases f*t -------
  * units 0: RN(f*t) is an angle in radians (the full method);
  * units 1: RN(f*t) is in turns (theta/2pi): the method from the reduction on.
@@ -154,6 +178,11 @@ void oracle_grid_stats(const oracle_opts_t *o, uint64_t m, int ref_kind, oracle_
  * nthreads. */
 void oracle_sweep_bits(const oracle_opts_t *o, int mode, uint32_t lo_bits, uint32_t hi_bits,
                        int nthreads, oracle_stats_t *st);
+
+/* NEXT(3): kernel-only stats of a general method over q = bits(lo_bits + k*stride) <= hi_bits,
+ * against sin/cos(2 pi q) in double. */
+void oracle_method_sweep_q(const oracle_method_t *m, uint32_t lo_bits, uint32_t hi_bits, uint32_t stride,
+                           int nthreads, oracle_stats_t *st);
 
 /* Whole-input-space transcription hash over u in [lo_bits, hi_bits]:
  *   H = sum_u mix64(((s_bits << 32) | c_bits) ^ (u * 0xD6E8FEB86659FD93)) mod 2^64

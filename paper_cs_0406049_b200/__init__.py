@@ -53,6 +53,35 @@ class Shard(ctypes.Structure):
                 ("stream", ctypes.c_void_p)]
 
 
+class Method(ctypes.Structure):
+    """sincos_method_t (NEXT(3))."""
+    _fields_ = [("ss", ctypes.c_float * 8), ("n_ss", ctypes.c_int), ("cc", ctypes.c_float * 8),
+                ("n_cc", ctypes.c_int), ("doublings", ctypes.c_int), ("fix", ctypes.c_int)]
+
+
+FIX_LINEAR, FIX_RECIPROCAL, FIX_NONE = 0, 1, 3
+
+# The paper's two methods as explicit tables (PAPER.md P:140-148 / Fig. 1 P:230-242).
+PAPER_METHODS = {
+    NORMALIZED: ([1.5707963235, -0.645963615, 0.0796819754, -0.0046075748],
+                 [-1.2336977925, 0.2536086171, -0.0204391631], 2, FIX_LINEAR),
+    RENORMALIZED: ([1.5707963268, -0.6466386396, 0.0679105987, -0.0011573807],
+                   [-1.2341299769, 0.2465220241, -0.0123926179], 2, FIX_RECIPROCAL),
+}
+
+
+def make_method(ss, cc, doublings=2, fix=FIX_LINEAR) -> Method:
+    """A sincos_method_t from coefficient lists (rounded to fp32 as Fig. 1 does)."""
+    import numpy as np
+    m = Method()
+    for i, v in enumerate(ss):
+        m.ss[i] = float(np.float32(v))
+    for i, v in enumerate(cc):
+        m.cc[i] = float(np.float32(v))
+    m.n_ss, m.n_cc, m.doublings, m.fix = len(ss), len(cc), int(doublings), int(fix)
+    return m
+
+
 _lib = None
 _P, _S, _I = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
 _SIGS = {
@@ -72,6 +101,7 @@ _SIGS = {
     "sincos_version": (ctypes.c_char_p, []),
     "sincos_launch_count": (ctypes.c_uint64, []),
     "sincos_phase_grid": (_I, [_P, _S, _P, _S, _P, _P, _P, _I, _I, _P]),
+    "sincos_pairs_method": (_I, [_P, _P, _P, _P, _S, ctypes.POINTER(Method), _P]),
     "sincos_nudft_chunk": (_S, [_S]),
     "sincos_nudft_workspace_bytes": (_S, [_S, _S]),
     "sincos_nudft": (_I, [_P, _S, _P, _P, _S, _P, _I, _I, _P, _S, _P]),
@@ -179,6 +209,15 @@ def phase_grid(f, t, sin_out=None, cos_out=None, interleaved_out=None, units=RAD
                                  _ptr(cos_out, "cos_out"), _ptr(interleaved_out, "interleaved_out"), int(units),
                                  _variant(variant), _stream(stream, f.device))
     _check(st, "sincos_phase_grid")
+
+
+def sincos_pairs_method(theta, method: Method, sin_out=None, cos_out=None, interleaved_out=None, stream=None):
+    """NEXT(3) C-ABI sincos_pairs_method: the method with the given series / doublings / fix."""
+    n = theta.numel()
+    st = lib().sincos_pairs_method(_ptr(theta, "theta"), _ptr(sin_out, "sin_out"), _ptr(cos_out, "cos_out"),
+                                   _ptr(interleaved_out, "interleaved_out"), n, ctypes.byref(method),
+                                   _stream(stream, theta.device))
+    _check(st, "sincos_pairs_method")
 
 
 def nudft_chunk(nt: int) -> int:

@@ -235,6 +235,37 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
     return SINCOS_OK;
 }
 
+sincos_status_t sincos_pairs_method(const float *theta_dev, float *sin_dev, float *cos_dev, float *inter_dev,
+                                    size_t n, const sincos_method_t *m, void *stream) {
+    if (m == nullptr || m->n_ss < 1 || m->n_ss > 8 || m->n_cc < 0 || m->n_cc > 8 || m->doublings < 0 ||
+        m->doublings > 8 || !(m->fix == 0 || m->fix == 1 || m->fix == 3) || (m->fix != 3 && m->doublings < 1))
+        return SINCOS_ERR_INVALID_ARGUMENT;
+    sincos_status_t st = validate(theta_dev, sin_dev, cos_dev, inter_dev, n, SINCOS_NORMALIZED, false);
+    if (st != SINCOS_OK || n == 0) return st;
+    if (theta_dev == sin_dev || theta_dev == cos_dev) return SINCOS_ERR_OVERLAP;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    const bool inter = inter_dev != nullptr;
+    // 32-B vector body when theta and the outputs share their alignment after a scalar head
+    const uintptr_t t = reinterpret_cast<uintptr_t>(theta_dev);
+    const size_t h = ((32 - (t & 31)) & 31) / 4;
+    bool vec = inter ? aligned(reinterpret_cast<const char *>(inter_dev) + 8 * h, 32)
+                     : aligned(reinterpret_cast<const char *>(sin_dev) + 4 * h, 32) &&
+                           aligned(reinterpret_cast<const char *>(cos_dev) + 4 * h, 32);
+    size_t head = vec ? (h < n ? h : n) : 0;
+    size_t nvec = vec ? (n - head) / 8 : 0;
+    size_t work = vec ? (nvec > 0 ? nvec : 1) : n;
+    size_t grid = (work + 127) / 128;
+    if (!vec && grid > static_cast<size_t>(sm_count(dev)) * 16) grid = static_cast<size_t>(sm_count(dev)) * 16;
+    if (grid > 0x7FFFFFFFu) grid = 0x7FFFFFFFu;
+    e = launch_method(m->ss, m->n_ss, m->cc, m->n_cc, m->doublings, m->fix, inter, vec, static_cast<unsigned>(grid),
+                      theta_dev, sin_dev, cos_dev, inter_dev, head, nvec, n, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SINCOS_OK;
+}
+
 size_t sincos_nudft_chunk(size_t nt) { return nudft_chunk(nt); }
 
 size_t sincos_nudft_workspace_bytes(size_t nf, size_t nt) { return nudft_ws_bytes(nf, nt); }

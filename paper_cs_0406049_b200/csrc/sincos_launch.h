@@ -29,6 +29,10 @@ size_t nudft_chunk(size_t nt);
 size_t nudft_ws_bytes(size_t nf, size_t nt);
 cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, const float *t, const float *a,
                          size_t nt, float *out, void *ws, cudaStream_t stream);
+// NEXT(3) general method (sincos_method.cu).
+cudaError_t launch_method(const float *ss, int n_ss, const float *cc, int n_cc, int doublings, int fix, bool inter,
+                          bool vec, unsigned grid, const float *theta, float *so, float *co, float *io, size_t head,
+                          size_t nvec, size_t n, cudaStream_t stream);
 const void *vec_kernel_ptr(int variant, bool inter, int w, int unroll, bool nc, bool pf);
 
 size_t stats_ws_bytes();

@@ -1,0 +1,140 @@
+// sincos_method.cu -- NEXT(3): the method with any series degrees and doubling count.
+//
+// Eq. (1) doublings keep the angle error and square the amplitude, so any
+// number n of doublings works with series fitted for the angle 2 pi x / 2^n, by either
+// fitting method (P:120-126 normalised, P:152-154 angle-accurate).  The coefficients
+// come from the caller (e.g. paper_cs_0406049_b200.coeff_fit) and sit in the kernel's
+// parameter (constant) bank.  Series are evaluated with a fixed-length Horner over
+// zero-padded coefficients: fma(q2, 0, c) == c exactly, so padding leaves the result
+// bit-identical to the unpadded Horner of the method's own degree and keeps the
+// per-element code branch-free (the doubling count is a warp-uniform loop bound).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sincos_launch.h"
+#include "sincos_math.cuh"
+
+namespace sincos_b200 {
+
+struct MethodParams {
+    float ss[8];
+    float cc[8];
+    int doublings;
+};
+
+template <int NT, int FIX>
+__device__ __forceinline__ void method_pair(const MethodParams &m, float theta, float &s_out, float &c_out) {
+    const float q1 = reduce_turn(__fmul_rn(theta, kInvTwoPi));
+    const float q2 = __fmul_rn(q1, q1);
+    float ps = m.ss[NT - 1];
+#pragma unroll
+    for (int i = NT - 2; i >= 0; --i) ps = __fmaf_rn(q2, ps, m.ss[i]);
+    float pc = m.cc[NT - 1];
+#pragma unroll
+    for (int i = NT - 2; i >= 0; --i) pc = __fmaf_rn(q2, pc, m.cc[i]);
+    float s = __fmul_rn(q1, ps);
+    float c = __fmaf_rn(q2, pc, 1.0f);
+    float f = 1.0f;
+    if (m.doublings > 0) {
+        for (int i = 0; i < m.doublings - 1; ++i) {          // warp-uniform bound
+            const float cn = __fmaf_rn(-s, s, __fmul_rn(c, c));
+            s = __fmul_rn(2.0f, __fmul_rn(s, c));
+            c = cn;
+        }
+        // (s, c) is the penultimate pair (Fig. 1)
+        const float cc2 = __fmul_rn(c, c);
+        if constexpr (FIX == 0) f = __fmaf_rn(-s, s, __fmaf_rn(-c, c, 2.0f));
+        if constexpr (FIX == 1) f = rcp_rn(__fmaf_rn(s, s, cc2));
+        const float cn = __fmaf_rn(-s, s, cc2);
+        s = __fmul_rn(2.0f, __fmul_rn(s, c));
+        c = cn;
+    }
+    c_out = __fmul_rn(c, f);
+    s_out = __fmul_rn(s, f);
+}
+
+template <int NT, int FIX, bool INTER>
+__device__ __forceinline__ void method_scalar(const MethodParams &m, const float *theta, size_t e, float *so,
+                                              float *co, float *io) {
+    float s, c;
+    method_pair<NT, FIX>(m, theta[e], s, c);
+    if constexpr (INTER) {
+        io[2 * e] = c;
+        io[2 * e + 1] = s;
+    } else {
+        so[e] = s;
+        co[e] = c;
+    }
+}
+
+__device__ __forceinline__ void st8m(float *p, const float *r) {
+    asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(p), "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7])
+                 : "memory");
+}
+
+// Full grid, one 256-bit vector per thread over [head, head + 8 nvec); scalar head/tail.
+// vec == false: every element scalar (pointers without a shared 32-B alignment).
+template <int NT, int FIX, bool INTER>
+__global__ void __launch_bounds__(128) method_kernel(const MethodParams m, const float *theta, float *so,
+                                                     float *co, float *io, size_t head, size_t nvec, size_t n,
+                                                     bool vec) {
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (!vec) {
+        for (size_t e = tid; e < n; e += nthr) method_scalar<NT, FIX, INTER>(m, theta, e, so, co, io);
+        return;
+    }
+    const size_t tail0 = head + 8 * nvec;
+    if (tid < head) method_scalar<NT, FIX, INTER>(m, theta, tid, so, co, io);
+    if (tid < n - tail0) method_scalar<NT, FIX, INTER>(m, theta, tail0 + tid, so, co, io);
+    for (size_t v = tid; v < nvec; v += nthr) {
+        const size_t e0 = head + 8 * v;
+        float x[8];
+        asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]), "=f"(x[6]), "=f"(x[7])
+                     : "l"(theta + e0));
+        if constexpr (INTER) {
+            float cs[16];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) method_pair<NT, FIX>(m, x[k], cs[2 * k + 1], cs[2 * k]);
+            st8m(io + 2 * e0, cs);
+            st8m(io + 2 * e0 + 8, cs + 8);
+        } else {
+            float sv[8], cv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) method_pair<NT, FIX>(m, x[k], sv[k], cv[k]);
+            st8m(so + e0, sv);
+            st8m(co + e0, cv);
+        }
+    }
+}
+
+template <int NT, int FIX>
+static const void *pick_m(bool inter) {
+    return inter ? reinterpret_cast<const void *>(method_kernel<NT, FIX, true>)
+                 : reinterpret_cast<const void *>(method_kernel<NT, FIX, false>);
+}
+
+// fix: 0 linear (penultimate), 1 reciprocal (penultimate), 3 none.  Terms <= 4 use the
+// 4-term Horner, otherwise the 8-term one.
+cudaError_t launch_method(const float *ss, int n_ss, const float *cc, int n_cc, int doublings, int fix, bool inter,
+                          bool vec, unsigned grid, const float *theta, float *so, float *co, float *io, size_t head,
+                          size_t nvec, size_t n, cudaStream_t stream) {
+    MethodParams m;
+    for (int i = 0; i < 8; ++i) {
+        m.ss[i] = i < n_ss ? ss[i] : 0.0f;
+        m.cc[i] = i < n_cc ? cc[i] : 0.0f;
+    }
+    m.doublings = doublings;
+    const bool small = n_ss <= 4 && n_cc <= 4;
+    const void *fn;
+    if (small)
+        fn = fix == 0 ? pick_m<4, 0>(inter) : fix == 1 ? pick_m<4, 1>(inter) : pick_m<4, 3>(inter);
+    else
+        fn = fix == 0 ? pick_m<8, 0>(inter) : fix == 1 ? pick_m<8, 1>(inter) : pick_m<8, 3>(inter);
+    void *args[] = {&m, &theta, &so, &co, &io, &head, &nvec, &n, &vec};
+    return cudaLaunchKernel(fn, dim3(grid), dim3(128), args, 0, stream);
+}
+
+}  // namespace sincos_b200

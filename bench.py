@@ -260,6 +260,40 @@ def measure_phase_grid(dev, stream, peak, reps=10):
     return out
 
 
+def fit_method(doublings, n_ss, n_cc):
+    """NEXT(3): a regenerated angle-accurate method (coeff_fit, exact reciprocal fix)."""
+    import paper_cs_0406049_b200 as sp
+    from paper_cs_0406049_b200 import coeff_fit
+    ss, cc = coeff_fit.fit_angle(doublings, n_ss, n_cc).fp32()
+    return sp.make_method(list(ss), list(cc), doublings, sp.FIX_RECIPROCAL)
+
+
+def measure_methods(dev, stream, th, outs, peak, reps=10):
+    """NEXT(3) side measurement: sincos_pairs_method on the C2 batch (HBM-bound like the hot
+    path) for the paper's tables and a regenerated 1-doubling method."""
+    import torch
+
+    import paper_cs_0406049_b200 as sp
+    n = th.numel()
+    res = {"workload": "C2 batch, split outputs", "bytes_per_pair": BYTES_PER_PAIR, "peak": peak}
+    for name, m in (("paper_N_table", sp.make_method(*sp.PAPER_METHODS[sp.NORMALIZED])),
+                    ("paper_A_table", sp.make_method(*sp.PAPER_METHODS[sp.RENORMALIZED])),
+                    ("angle_fit_1dbl_deg3_2", fit_method(1, 3, 2))):
+        s, c = outs
+        for _ in range(2):
+            sp.sincos_pairs_method(th, m, s, c, stream=stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            sp.sincos_pairs_method(th, m, s, c, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = a.elapsed_time(b) / reps
+        gbs = BYTES_PER_PAIR * n / (ms / 1e3) / 1e9
+        res[name] = {"ms": ms, "GBps": gbs, "frac": gbs / peak}
+    return res
+
+
 ALU_PEAK_OPS = 148 * 128 * 1.965e9   # FP32-pipe lane-ops/s at the max SM clock (FMA = 1 op)
 # algorithmic FP32-pipe ops per term of the fused sum, variant N: the phase product (1), the
 # method (11 FMUL + 10 FFMA + 1 FADD + 1 FRND = 23; turns skips the 1/2pi FMUL), the complex MAC (4)
@@ -292,13 +326,14 @@ def measure_nudft(dev, stream, reps=5):
         ang = p if units == sp.RADIANS else 2 * np.pi * (p - torch.round(p))
         ref = (a.to(torch.complex128)[None, :] * torch.exp(1j * ang)).sum(dim=1)
         for v, vname in ((sp.NORMALIZED, "N"), (sp.RENORMALIZED, "A"), (sp.CMP_LIBM_SINCOSF, "cuda_sincosf"),
-                         (sp.CMP_INTRINSIC_SINCOSF, "cuda___sincosf")):
-            sp.nudft(fd, td, a, out=out, units=units, variant=v, workspace=ws, stream=stream)
+                         (sp.CMP_INTRINSIC_SINCOSF, "cuda___sincosf"), ("m132", "method_1dbl_deg3_2_angle")):
+            kw = {"method": fit_method(1, 3, 2)} if v == "m132" else {"variant": v}
+            sp.nudft(fd, td, a, out=out, units=units, workspace=ws, stream=stream, **kw)
             err = float((out[ks].to(torch.complex128) - ref).abs().max()) / asum
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for _ in range(reps):
-                sp.nudft(fd, td, a, out=out, units=units, variant=v, workspace=ws, stream=stream)
+                sp.nudft(fd, td, a, out=out, units=units, workspace=ws, stream=stream, **kw)
             e1.record(stream)
             torch.cuda.synchronize(dev)
             ms = e0.elapsed_time(e1) / reps
@@ -416,6 +451,11 @@ def run_ours(args, rank, world, local_rank):
                      avg[v], float(rank), float(v)])
     summary = summarize(gather_records(recs, world, dev))
 
+    methods_res = None
+    if rank == 0 and not args.no_next and not W.interleaved:
+        o = outs[sp.NORMALIZED]
+        methods_res = measure_methods(dev, stream, th, (o["sin_out"], o["cos_out"]), peak)
+
     # end to end through the C ABI with host buffers, copies inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -449,12 +489,13 @@ def run_ours(args, rank, world, local_rank):
                "path": "sincos_pairs_host: pinned host buffers, chunked H2D -> kernel -> D2H over 3 streams"}
         del ws, oh
 
-    fused = None
+    fused = nudft_res = None
     if rank == 0 and not args.no_next:
+        if "outs" in locals():
+            del outs
+        torch.cuda.empty_cache()
         fused = measure_phase_grid(dev, stream, peak)
         nudft_res = measure_nudft(dev, stream)
-    else:
-        nudft_res = None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -483,6 +524,7 @@ def run_ours(args, rank, world, local_rank):
             "shards": summary["shards"],
             "next_fused_phase": fused,
             "next_fused_nudft": nudft_res,
+            "next_methods": methods_res,
             "paper_context": "PowerPC 7400 G4 500 MHz AltiVec: 140 ns per 4 pairs = 28.6 M pairs/s (P:177-180)",
         }
         print(json.dumps(line), flush=True)

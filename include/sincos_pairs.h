@@ -176,6 +176,12 @@ SINCOS_API size_t sincos_nudft_workspace_bytes(size_t nf, size_t nt);
 SINCOS_API sincos_status_t sincos_nudft(const float *f_dev, size_t nf, const float *t_dev, const float *a_dev,
                                         size_t nt, float *out_dev, sincos_units_t units, int variant,
                                         void *ws_dev, size_t ws_bytes, void *stream);
+/* The same sum with the pairs of a general method (NEXT(3), sincos_method_t above);
+ * pairs bit-identical to sincos_pairs_method, same bound and conventions. */
+SINCOS_API sincos_status_t sincos_nudft_method(const float *f_dev, size_t nf, const float *t_dev,
+                                               const float *a_dev, size_t nt, float *out_dev,
+                                               sincos_units_t units, const sincos_method_t *method,
+                                               void *ws_dev, size_t ws_bytes, void *stream);
 
 /*
  * Host-side sharding: element ranges [lo, hi) of shard g of

@@ -102,6 +102,7 @@ _SIGS = {
     "sincos_launch_count": (ctypes.c_uint64, []),
     "sincos_phase_grid": (_I, [_P, _S, _P, _S, _P, _P, _P, _I, _I, _P]),
     "sincos_pairs_method": (_I, [_P, _P, _P, _P, _S, ctypes.POINTER(Method), _P]),
+    "sincos_nudft_method": (_I, [_P, _S, _P, _P, _S, _P, _I, ctypes.POINTER(Method), _P, _S, _P]),
     "sincos_nudft_chunk": (_S, [_S]),
     "sincos_nudft_workspace_bytes": (_S, [_S, _S]),
     "sincos_nudft": (_I, [_P, _S, _P, _P, _S, _P, _I, _I, _P, _S, _P]),
@@ -224,9 +225,10 @@ def nudft_chunk(nt: int) -> int:
     return int(lib().sincos_nudft_chunk(nt))
 
 
-def nudft(f, t, a, out=None, units=RADIANS, variant=NORMALIZED, workspace=None, stream=None):
+def nudft(f, t, a, out=None, units=RADIANS, variant=NORMALIZED, workspace=None, stream=None, method=None):
     """NEXT(2) C-ABI sincos_nudft: out[k] = sum_j a[j] e^{i RN(f[k] t[j])} (complex64 a, out;
-    float32 f, t; CUDA tensors).  Returns out."""
+    float32 f, t; CUDA tensors).  With `method` (a Method), sincos_nudft_method: the pairs of
+    that general method (NEXT(3)).  Returns out."""
     import torch
     nf, nt = f.numel(), t.numel()
     if a.dtype == torch.complex64:
@@ -239,9 +241,16 @@ def nudft(f, t, a, out=None, units=RADIANS, variant=NORMALIZED, workspace=None, 
     need = int(lib().sincos_nudft_workspace_bytes(nf, nt))
     if workspace is None:
         workspace = torch.empty(max(need, 8), dtype=torch.uint8, device=f.device)
+    ws_bytes = workspace.numel() * workspace.element_size()
+    if method is not None:
+        st = lib().sincos_nudft_method(_ptr(f, "f"), nf, _ptr(t, "t"), _ptr(a.contiguous(), "a"), nt,
+                                       _ptr(o, "out"), int(units), ctypes.byref(method), workspace.data_ptr(),
+                                       ws_bytes, _stream(stream, f.device))
+        _check(st, "sincos_nudft_method")
+        return out
     st = lib().sincos_nudft(_ptr(f, "f"), nf, _ptr(t, "t"), _ptr(a.contiguous(), "a"), nt, _ptr(o, "out"),
-                            int(units), _variant(variant), workspace.data_ptr(),
-                            workspace.numel() * workspace.element_size(), _stream(stream, f.device))
+                            int(units), _variant(variant), workspace.data_ptr(), ws_bytes,
+                            _stream(stream, f.device))
     _check(st, "sincos_nudft")
     return out
 

@@ -14,6 +14,7 @@
 
 #include "../../include/sincos_pairs.h"
 #include "sincos_launch.h"
+#include "sincos_method.cuh"
 
 using namespace sincos_b200;
 
@@ -270,10 +271,24 @@ size_t sincos_nudft_chunk(size_t nt) { return nudft_chunk(nt); }
 
 size_t sincos_nudft_workspace_bytes(size_t nf, size_t nt) { return nudft_ws_bytes(nf, nt); }
 
-sincos_status_t sincos_nudft(const float *f_dev, size_t nf, const float *t_dev, const float *a_dev, size_t nt,
-                             float *out_dev, sincos_units_t units, int variant, void *ws_dev, size_t ws_bytes,
-                             void *stream) {
-    if (variant < 0 || variant > 4) return SINCOS_ERR_INVALID_ARGUMENT;
+namespace {
+bool method_ok(const sincos_method_t *m) {
+    return m != nullptr && m->n_ss >= 1 && m->n_ss <= 8 && m->n_cc >= 0 && m->n_cc <= 8 && m->doublings >= 0 &&
+           m->doublings <= 8 && (m->fix == 0 || m->fix == 1 || m->fix == 3) && (m->fix == 3 || m->doublings >= 1);
+}
+
+// a compile-time kernel shape for common methods (-1: the generic padded kernel)
+int method_spec(const sincos_method_t *m) {
+    if (m->n_ss == 4 && m->n_cc == 3 && m->doublings == 2) return 0;
+    if (m->n_ss == 3 && m->n_cc == 2 && m->doublings == 1) return 1;
+    return -1;
+}
+
+// variant 0..4, or 5 with a general method m
+sincos_status_t nudft_impl(const float *f_dev, size_t nf, const float *t_dev, const float *a_dev, size_t nt,
+                           float *out_dev, sincos_units_t units, int variant, const sincos_method_t *m,
+                           void *ws_dev, size_t ws_bytes, void *stream) {
+    if (variant < 0 || variant > 5 || (variant == 5 && !method_ok(m))) return SINCOS_ERR_INVALID_ARGUMENT;
     if (units != SINCOS_RADIANS && units != SINCOS_TURNS) return SINCOS_ERR_INVALID_ARGUMENT;
     if (nf == 0) return SINCOS_OK;
     if (f_dev == nullptr || out_dev == nullptr || !aligned(f_dev, 4) || !aligned(out_dev, 8))
@@ -294,10 +309,30 @@ sincos_status_t sincos_nudft(const float *f_dev, size_t nf, const float *t_dev, 
         overlaps(ws_dev, need, out_dev, 8 * nf) || overlaps(ws_dev, need, f_dev, 4 * nf) ||
         overlaps(ws_dev, need, t_dev, 4 * nt) || overlaps(ws_dev, need, a_dev, 8 * nt))
         return SINCOS_ERR_OVERLAP;
-    cudaError_t e = launch_nudft(variant, units == SINCOS_TURNS, f_dev, nf, t_dev, a_dev, nt, out_dev, ws_dev, s);
+    MethodParams mp{};
+    if (variant == 5) mp = make_params(m->ss, m->n_ss, m->cc, m->n_cc, m->doublings);
+    cudaError_t e = launch_nudft(variant, units == SINCOS_TURNS, f_dev, nf, t_dev, a_dev, nt, out_dev, ws_dev, s,
+                                 variant == 5 ? &mp : nullptr, variant == 5 && (m->n_ss > 4 || m->n_cc > 4) ? 8 : 4,
+                                 variant == 5 ? m->fix : 0, variant == 5 ? method_spec(m) : -1);
     if (e != cudaSuccess) return cuda_fail(e);
     g_launches.fetch_add(2, std::memory_order_relaxed);
     return SINCOS_OK;
+}
+
+}  // namespace
+
+sincos_status_t sincos_nudft(const float *f_dev, size_t nf, const float *t_dev, const float *a_dev, size_t nt,
+                             float *out_dev, sincos_units_t units, int variant, void *ws_dev, size_t ws_bytes,
+                             void *stream) {
+    if (variant > 4) return SINCOS_ERR_INVALID_ARGUMENT;
+    return nudft_impl(f_dev, nf, t_dev, a_dev, nt, out_dev, units, variant, nullptr, ws_dev, ws_bytes, stream);
+}
+
+sincos_status_t sincos_nudft_method(const float *f_dev, size_t nf, const float *t_dev, const float *a_dev,
+                                    size_t nt, float *out_dev, sincos_units_t units, const sincos_method_t *method,
+                                    void *ws_dev, size_t ws_bytes, void *stream) {
+    if (!method_ok(method)) return SINCOS_ERR_INVALID_ARGUMENT;
+    return nudft_impl(f_dev, nf, t_dev, a_dev, nt, out_dev, units, 5, method, ws_dev, ws_bytes, stream);
 }
 
 size_t sincos_host_workspace_min_bytes(void) { return kSlots * kMinChunk * 12; }

@@ -27,8 +27,12 @@ cudaError_t launch_phase_grid(int variant, bool inter, bool turns, bool vec, con
 // NEXT(2) fused non-uniform Fourier sum (sincos_nudft.cu); variant 3/4 = comparison sincosf.
 size_t nudft_chunk(size_t nt);
 size_t nudft_ws_bytes(size_t nf, size_t nt);
+struct MethodParams;
+// variant 5 = the general method `method` (max series terms method_nt, fix 0/1/3); method_spec
+// >= 0 selects a compile-time shape (0 = n_ss 4 / n_cc 3 / 2 doublings, 1 = 3 / 2 / 1).
 cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, const float *t, const float *a,
-                         size_t nt, float *out, void *ws, cudaStream_t stream);
+                         size_t nt, float *out, void *ws, cudaStream_t stream, const MethodParams *method = nullptr,
+                         int method_nt = 4, int method_fix = 0, int method_spec = -1);
 // NEXT(3) general method (sincos_method.cu).
 cudaError_t launch_method(const float *ss, int n_ss, const float *cc, int n_cc, int doublings, int fix, bool inter,
                           bool vec, unsigned grid, const float *theta, float *so, float *co, float *io, size_t head,

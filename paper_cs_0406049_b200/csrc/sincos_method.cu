@@ -12,46 +12,9 @@
 #include <stdint.h>
 
 #include "sincos_launch.h"
-#include "sincos_math.cuh"
+#include "sincos_method.cuh"
 
 namespace sincos_b200 {
-
-struct MethodParams {
-    float ss[8];
-    float cc[8];
-    int doublings;
-};
-
-template <int NT, int FIX>
-__device__ __forceinline__ void method_pair(const MethodParams &m, float theta, float &s_out, float &c_out) {
-    const float q1 = reduce_turn(__fmul_rn(theta, kInvTwoPi));
-    const float q2 = __fmul_rn(q1, q1);
-    float ps = m.ss[NT - 1];
-#pragma unroll
-    for (int i = NT - 2; i >= 0; --i) ps = __fmaf_rn(q2, ps, m.ss[i]);
-    float pc = m.cc[NT - 1];
-#pragma unroll
-    for (int i = NT - 2; i >= 0; --i) pc = __fmaf_rn(q2, pc, m.cc[i]);
-    float s = __fmul_rn(q1, ps);
-    float c = __fmaf_rn(q2, pc, 1.0f);
-    float f = 1.0f;
-    if (m.doublings > 0) {
-        for (int i = 0; i < m.doublings - 1; ++i) {          // warp-uniform bound
-            const float cn = __fmaf_rn(-s, s, __fmul_rn(c, c));
-            s = __fmul_rn(2.0f, __fmul_rn(s, c));
-            c = cn;
-        }
-        // (s, c) is the penultimate pair (Fig. 1)
-        const float cc2 = __fmul_rn(c, c);
-        if constexpr (FIX == 0) f = __fmaf_rn(-s, s, __fmaf_rn(-c, c, 2.0f));
-        if constexpr (FIX == 1) f = rcp_rn(__fmaf_rn(s, s, cc2));
-        const float cn = __fmaf_rn(-s, s, cc2);
-        s = __fmul_rn(2.0f, __fmul_rn(s, c));
-        c = cn;
-    }
-    c_out = __fmul_rn(c, f);
-    s_out = __fmul_rn(s, f);
-}
 
 template <int NT, int FIX, bool INTER>
 __device__ __forceinline__ void method_scalar(const MethodParams &m, const float *theta, size_t e, float *so,
@@ -121,12 +84,7 @@ static const void *pick_m(bool inter) {
 cudaError_t launch_method(const float *ss, int n_ss, const float *cc, int n_cc, int doublings, int fix, bool inter,
                           bool vec, unsigned grid, const float *theta, float *so, float *co, float *io, size_t head,
                           size_t nvec, size_t n, cudaStream_t stream) {
-    MethodParams m;
-    for (int i = 0; i < 8; ++i) {
-        m.ss[i] = i < n_ss ? ss[i] : 0.0f;
-        m.cc[i] = i < n_cc ? cc[i] : 0.0f;
-    }
-    m.doublings = doublings;
+    MethodParams m = make_params(ss, n_ss, cc, n_cc, doublings);
     const bool small = n_ss <= 4 && n_cc <= 4;
     const void *fn;
     if (small)

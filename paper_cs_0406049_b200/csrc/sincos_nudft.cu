@@ -20,7 +20,7 @@
 #include <stdint.h>
 
 #include "sincos_launch.h"
-#include "sincos_math.cuh"
+#include "sincos_method.cuh"
 
 namespace sincos_b200 {
 
@@ -33,11 +33,27 @@ constexpr int kTileJ = 256;
 // sincosf (accurate, with a slow path for large arguments) and the __sincosf intrinsic.
 constexpr int kLibmSincosf = 3;
 constexpr int kIntrinsicSincosf = 4;
+// NEXT(3) general methods: V = kMethodBase + (NT == 8 ? 4 : 0) + FIX, FIX in {0, 1, 3}.
+constexpr int kMethodBase = 16;
+// Specialised general-method shapes: V = kMethodExactBase + 4 * spec + FIX.
+constexpr int kMethodExactBase = 32;
 
 template <int V, bool TURNS>
-__device__ __forceinline__ void term_pair(float f, float t, float &s, float &c) {
+__device__ __forceinline__ void term_pair(const MethodParams &mp, float f, float t, float &s, float &c) {
     const float p = __fmul_rn(f, t);
-    if constexpr (V == kLibmSincosf) {
+    if constexpr (V >= kMethodExactBase) {
+        // specialised shapes: spec 0 = (n_ss 4, n_cc 3, 2 doublings), spec 1 = (3, 2, 1)
+        constexpr int SPEC = (V - kMethodExactBase) / 4;
+        constexpr int FIX = (V - kMethodExactBase) % 4;
+        constexpr int NS = SPEC == 0 ? 4 : 3, NC = SPEC == 0 ? 3 : 2, ND = SPEC == 0 ? 2 : 1;
+        const float x = TURNS ? p : __fmul_rn(p, kInvTwoPi);
+        method_from_q_exact<NS, NC, ND, FIX>(mp, reduce_turn(x), s, c);
+    } else if constexpr (V >= kMethodBase) {
+        constexpr int NT = (V - kMethodBase) >= 4 ? 8 : 4;
+        constexpr int FIX = (V - kMethodBase) % 4;
+        if constexpr (TURNS) method_from_q<NT, FIX>(mp, reduce_turn(p), s, c);
+        else method_pair<NT, FIX>(mp, p, s, c);
+    } else if constexpr (V == kLibmSincosf) {
         if constexpr (TURNS) sincospif(2.0f * p, &s, &c); else sincosf(p, &s, &c);
     } else if constexpr (V == kIntrinsicSincosf) {
         __sincosf(TURNS ? 6.28318530717958647692f * p : p, &s, &c);
@@ -52,7 +68,8 @@ template <int V, bool TURNS>
 __global__ void __launch_bounds__(kNuThreads) nudft_partial(const float *__restrict__ f, size_t nf,
                                                             const float *__restrict__ t,
                                                             const float2 *__restrict__ a, size_t nt,
-                                                            size_t chunk, float2 *__restrict__ part) {
+                                                            size_t chunk, float2 *__restrict__ part,
+                                                            const MethodParams mp) {
     __shared__ float st[kTileJ];
     __shared__ float2 sa[kTileJ];
     const size_t k0 = static_cast<size_t>(blockIdx.x) * kKPerBlock + threadIdx.x;
@@ -80,7 +97,7 @@ __global__ void __launch_bounds__(kNuThreads) nudft_partial(const float *__restr
 #pragma unroll
             for (int m = 0; m < kKPerThread; ++m) {
                 float s, c;
-                term_pair<V, TURNS>(fk[m], tj, s, c);
+                term_pair<V, TURNS>(mp, fk[m], tj, s, c);
                 // (ar + i ai)(c + i s) accumulated with single-rounding FMAs
                 re[m] = __fmaf_rn(aj.x, c, re[m]);
                 re[m] = __fmaf_rn(-aj.y, s, re[m]);
@@ -130,7 +147,8 @@ static const void *pick_nudft(bool turns) {
 }
 
 cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, const float *t, const float *a,
-                         size_t nt, float *out, void *ws, cudaStream_t stream) {
+                         size_t nt, float *out, void *ws, cudaStream_t stream, const MethodParams *method,
+                         int method_nt, int method_fix, int method_spec) {
     size_t chunk = nudft_chunk(nt);
     const size_t nchunks = (nt + chunk - 1) / chunk;
     const size_t gx = (nf + kKPerBlock - 1) / kKPerBlock;
@@ -140,11 +158,26 @@ cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, con
     case kNormalized: fn = pick_nudft<kNormalized>(turns); break;
     case kRenormalized: fn = pick_nudft<kRenormalized>(turns); break;
     case kLibmSincosf: fn = pick_nudft<kLibmSincosf>(turns); break;
-    default: fn = pick_nudft<kIntrinsicSincosf>(turns); break;
+    case kIntrinsicSincosf: fn = pick_nudft<kIntrinsicSincosf>(turns); break;
+    default:
+        if (method == nullptr) return cudaErrorInvalidValue;
+        if (method_spec >= 0 && method_fix != 3)
+            fn = method_spec == 0 ? (method_fix == 0 ? pick_nudft<kMethodExactBase + 0>(turns)
+                                                     : pick_nudft<kMethodExactBase + 1>(turns))
+                                  : (method_fix == 0 ? pick_nudft<kMethodExactBase + 4>(turns)
+                                                     : pick_nudft<kMethodExactBase + 5>(turns));
+        else if (method_nt <= 4)
+            fn = method_fix == 0 ? pick_nudft<kMethodBase + 0>(turns)
+                 : method_fix == 1 ? pick_nudft<kMethodBase + 1>(turns) : pick_nudft<kMethodBase + 3>(turns);
+        else
+            fn = method_fix == 0 ? pick_nudft<kMethodBase + 4>(turns)
+                 : method_fix == 1 ? pick_nudft<kMethodBase + 5>(turns) : pick_nudft<kMethodBase + 7>(turns);
+        break;
     }
+    MethodParams mp = method ? *method : MethodParams{};
     const float2 *a2 = reinterpret_cast<const float2 *>(a);
     float2 *part = static_cast<float2 *>(ws);
-    void *args[] = {&f, &nf, &t, &a2, &nt, &chunk, &part};
+    void *args[] = {&f, &nf, &t, &a2, &nt, &chunk, &part, &mp};
     cudaError_t e = cudaLaunchKernel(fn, dim3(static_cast<unsigned>(gx), static_cast<unsigned>(nchunks)),
                                      dim3(kNuThreads), args, 0, stream);
     if (e != cudaSuccess) return e;

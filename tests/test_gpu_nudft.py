@@ -119,3 +119,47 @@ def test_comparison_variants_run(variant):
     got = run(f, t, a, 1, variant)
     want = oracle.nudft(f, t, a, 1, 0)
     assert np.all(np.abs(got - want) <= 1e-3 * np.abs(a).sum())
+
+
+# ---- NEXT(3) methods inside the fused sum -------------------------------------------------
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("units", [0, 1])
+def test_nudft_method_with_paper_tables_equals_nudft(variant, units):
+    rng = np.random.default_rng(11)
+    f = torch.from_numpy(rng.uniform(0, 300, 999).astype(np.float32)).cuda()
+    t = torch.from_numpy(rng.uniform(0, 1, 4097).astype(np.float32)).cuda()
+    a = torch.from_numpy(rand_complex(rng, 4097)).cuda()
+    o1 = sp.nudft(f, t, a, units=units, variant=variant)
+    o2 = sp.nudft(f, t, a, units=units, method=sp.make_method(*sp.PAPER_METHODS[variant]))
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("units", [0, 1])
+@pytest.mark.parametrize("spec", [(1, 3, 2), (2, 3, 3), (3, 3, 3), (1, 6, 5)])
+def test_nudft_method_single_amplitude_exact(units, spec):
+    """A refitted method (angle fit, reciprocal fix) inside the fused sum: with a = e_j0 the
+    outputs are exactly that method's pairs (oracle general method on q = p - rint(p))."""
+    from paper_cs_0406049_b200 import coeff_fit as cf
+    n, ds, dc = spec
+    ss, cc = cf.fit_angle(n, ds, dc).fp32()
+    m = sp.make_method(list(ss), list(cc), n, sp.FIX_RECIPROCAL)
+    om = oracle.make_method(ss, cc, n, oracle.FIX_RECIPROCAL)
+    rng = np.random.default_rng(12)
+    f = rng.uniform(0, 300, 700).astype(np.float32)
+    t = rng.uniform(-1, 1, 2000).astype(np.float32)
+    a = np.zeros(2000, np.complex64)
+    a[777] = 1
+    got = sp.nudft(torch.from_numpy(f).cuda(), torch.from_numpy(t).cuda(), torch.from_numpy(a).cuda(),
+                   units=units, method=m).cpu().numpy()
+    p = f * t[777]                                            # fp32 products = RN(f t)
+    if units == 0:
+        ws, wc = oracle.method_sincos(p, om)
+    else:
+        q = (p.astype(np.float64) - np.rint(p.astype(np.float64))).astype(np.float32)   # exact
+        ws = np.empty_like(q)
+        wc = np.empty_like(q)
+        for i, qq in enumerate(q):
+            ws[i], wc[i] = oracle.method_pair_from_q(float(qq), om)
+    assert np.array_equal(got.real, wc) and np.array_equal(got.imag, ws)

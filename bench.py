@@ -294,6 +294,33 @@ def measure_methods(dev, stream, th, outs, peak, reps=10):
     return res
 
 
+def measure_dtypes(dev, stream, th, peak, reps=10):
+    """NEXT(4) side measurement: sincos_pairs_dtype with 16-bit split outputs on the C2 batch
+    (8 algorithmic bytes per pair: 4 in, 2 x 2 out)."""
+    import torch
+
+    import paper_cs_0406049_b200 as sp
+    n = th.numel()
+    res = {"workload": "C2 batch, split 16-bit outputs", "bytes_per_pair": 8, "peak": peak}
+    for dt, name in ((torch.float16, "fp16"), (torch.bfloat16, "bf16")):
+        s = torch.empty(n, dtype=dt, device=dev)
+        c = torch.empty(n, dtype=dt, device=dev)
+        for v, vname in ((sp.NORMALIZED, "N"), (sp.RENORMALIZED, "A")):
+            for _ in range(2):
+                sp.sincos_pairs_dtype(th, s, c, variant=v, stream=stream)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                sp.sincos_pairs_dtype(th, s, c, variant=v, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            ms = a.elapsed_time(b) / reps
+            gbs = 8 * n / (ms / 1e3) / 1e9
+            res[f"{name}_{vname}"] = {"ms": ms, "pairs_per_s": n / (ms / 1e3), "GBps": gbs, "frac": gbs / peak}
+        del s, c
+    return res
+
+
 ALU_PEAK_OPS = 148 * 128 * 1.965e9   # FP32-pipe lane-ops/s at the max SM clock (FMA = 1 op)
 # algorithmic FP32-pipe ops per term of the fused sum, variant N: the phase product (1), the
 # method (11 FMUL + 10 FFMA + 1 FADD + 1 FRND = 23; turns skips the 1/2pi FMUL), the complex MAC (4)
@@ -455,6 +482,7 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and not args.no_next and not W.interleaved:
         o = outs[sp.NORMALIZED]
         methods_res = measure_methods(dev, stream, th, (o["sin_out"], o["cos_out"]), peak)
+        methods_res["dtypes"] = measure_dtypes(dev, stream, th, peak)
 
     # end to end through the C ABI with host buffers, copies inside the timed region
     e2e = None

@@ -103,6 +103,28 @@ SINCOS_API sincos_status_t sincos_pairs_host(const float *theta_host, float *sin
 SINCOS_API size_t sincos_host_workspace_min_bytes(void);
 
 /*
+ * NEXT(4): other output dtypes and layout adapters.
+ *
+ * sincos_pairs_dtype: the hot path with the pair rounded once (to nearest even) from the
+ * method's fp32 result to out_dtype -- IEEE binary16 or bfloat16 (2 B per value; 8 B per
+ * pair of traffic instead of 12) -- or fp32 (= sincos_pairs).  Outputs are 2-B aligned
+ * uint16 arrays (split) or n {cos, sin} 16-bit pairs (interleaved); theta must not overlap
+ * them.  Vector path when theta is 32-B and the outputs 16-B (split) / 32-B (interleaved)
+ * aligned after the same scalar head, otherwise one element per thread; identical values.
+ *
+ * sincos_interleave / sincos_deinterleave: fp32 split (sin[], cos[]) <-> interleaved
+ * ({cos, sin} float2) copies; no overlap allowed.
+ */
+typedef enum { SINCOS_F32 = 0, SINCOS_F16 = 1, SINCOS_BF16 = 2 } sincos_dtype_t;
+SINCOS_API sincos_status_t sincos_pairs_dtype(const float *theta_dev, void *sin_dev, void *cos_dev, void *inter_dev,
+                                              size_t n, sincos_variant_t variant, sincos_dtype_t out_dtype,
+                                              void *stream);
+SINCOS_API sincos_status_t sincos_interleave(const float *sin_dev, const float *cos_dev, float *inter_dev, size_t n,
+                                             void *stream);
+SINCOS_API sincos_status_t sincos_deinterleave(const float *inter_dev, float *sin_dev, float *cos_dev, size_t n,
+                                               void *stream);
+
+/*
  * sincos_pairs_method -- NEXT(3): the method with caller-supplied series and doubling
  * count ("after n iterations ... two options for computing the raw pair.
  * These options differ in the fitting algorithm used to find the coefficients").

@@ -102,6 +102,9 @@ _SIGS = {
     "sincos_launch_count": (ctypes.c_uint64, []),
     "sincos_phase_grid": (_I, [_P, _S, _P, _S, _P, _P, _P, _I, _I, _P]),
     "sincos_pairs_method": (_I, [_P, _P, _P, _P, _S, ctypes.POINTER(Method), _P]),
+    "sincos_pairs_dtype": (_I, [_P, _P, _P, _P, _S, _I, _I, _P]),
+    "sincos_interleave": (_I, [_P, _P, _P, _S, _P]),
+    "sincos_deinterleave": (_I, [_P, _P, _P, _S, _P]),
     "sincos_nudft_method": (_I, [_P, _S, _P, _P, _S, _P, _I, ctypes.POINTER(Method), _P, _S, _P]),
     "sincos_nudft_chunk": (_S, [_S]),
     "sincos_nudft_workspace_bytes": (_S, [_S, _S]),
@@ -219,6 +222,43 @@ def sincos_pairs_method(theta, method: Method, sin_out=None, cos_out=None, inter
                                    _ptr(interleaved_out, "interleaved_out"), n, ctypes.byref(method),
                                    _stream(stream, theta.device))
     _check(st, "sincos_pairs_method")
+
+
+def _ptr_any(t, name: str):
+    if t is None:
+        return None
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous CUDA tensor (no CPU fallback)")
+    return t.data_ptr()
+
+
+def sincos_pairs_dtype(theta, sin_out=None, cos_out=None, interleaved_out=None, variant=NORMALIZED, stream=None):
+    """NEXT(4) C-ABI sincos_pairs_dtype: outputs in the dtype of the given tensors (float32,
+    float16 or bfloat16); 16-bit values are the method's fp32 pair rounded to nearest even."""
+    import torch
+    outs = [o for o in (sin_out, cos_out, interleaved_out) if o is not None]
+    dt = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}[outs[0].dtype]
+    if any(o.dtype != outs[0].dtype for o in outs):
+        raise TypeError("outputs must share one dtype")
+    n = theta.numel()
+    st = lib().sincos_pairs_dtype(_ptr(theta, "theta"), _ptr_any(sin_out, "sin_out"), _ptr_any(cos_out, "cos_out"),
+                                  _ptr_any(interleaved_out, "interleaved_out"), n, _variant(variant), dt,
+                                  _stream(stream, theta.device))
+    _check(st, "sincos_pairs_dtype")
+
+
+def interleave(sin_in, cos_in, interleaved_out, stream=None):
+    """NEXT(4): split fp32 (sin[], cos[]) -> interleaved {cos, sin}."""
+    st = lib().sincos_interleave(_ptr(sin_in, "sin"), _ptr(cos_in, "cos"), _ptr(interleaved_out, "inter"),
+                                 sin_in.numel(), _stream(stream, sin_in.device))
+    _check(st, "sincos_interleave")
+
+
+def deinterleave(interleaved_in, sin_out, cos_out, stream=None):
+    """NEXT(4): interleaved {cos, sin} fp32 -> split (sin[], cos[])."""
+    st = lib().sincos_deinterleave(_ptr(interleaved_in, "inter"), _ptr(sin_out, "sin"), _ptr(cos_out, "cos"),
+                                   sin_out.numel(), _stream(stream, sin_out.device))
+    _check(st, "sincos_deinterleave")
 
 
 def nudft_chunk(nt: int) -> int:

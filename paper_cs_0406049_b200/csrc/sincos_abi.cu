@@ -236,6 +236,76 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
     return SINCOS_OK;
 }
 
+sincos_status_t sincos_pairs_dtype(const float *theta_dev, void *sin_dev, void *cos_dev, void *inter_dev, size_t n,
+                                   sincos_variant_t variant, sincos_dtype_t out_dtype, void *stream) {
+    if (out_dtype == SINCOS_F32)
+        return sincos_pairs(theta_dev, static_cast<float *>(sin_dev), static_cast<float *>(cos_dev),
+                            static_cast<float *>(inter_dev), n, variant, stream);
+    if (out_dtype != SINCOS_F16 && out_dtype != SINCOS_BF16) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (variant != SINCOS_NORMALIZED && variant != SINCOS_RENORMALIZED) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (n == 0) return SINCOS_OK;
+    const bool split = sin_dev != nullptr && cos_dev != nullptr && inter_dev == nullptr;
+    const bool inter = sin_dev == nullptr && cos_dev == nullptr && inter_dev != nullptr;
+    if (theta_dev == nullptr || !(split || inter) || n > SIZE_MAX / 8) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (!aligned(theta_dev, 4) || (sin_dev && !aligned(sin_dev, 2)) || (cos_dev && !aligned(cos_dev, 2)) ||
+        (inter_dev && !aligned(inter_dev, 4)))
+        return SINCOS_ERR_INVALID_ARGUMENT;
+    if (split) {
+        if (overlaps(sin_dev, 2 * n, cos_dev, 2 * n) || overlaps(theta_dev, 4 * n, sin_dev, 2 * n) ||
+            overlaps(theta_dev, 4 * n, cos_dev, 2 * n))
+            return SINCOS_ERR_OVERLAP;
+    } else if (overlaps(theta_dev, 4 * n, inter_dev, 4 * n)) {
+        return SINCOS_ERR_OVERLAP;
+    }
+    const uintptr_t t = reinterpret_cast<uintptr_t>(theta_dev);
+    const size_t h = ((32 - (t & 31)) & 31) / 4;
+    const bool vec = inter ? aligned(static_cast<const char *>(inter_dev) + 4 * h, 32)
+                           : aligned(static_cast<const char *>(sin_dev) + 2 * h, 16) &&
+                                 aligned(static_cast<const char *>(cos_dev) + 2 * h, 16);
+    size_t head = 0, nvec = 0;
+    if (vec) {
+        head = h < n ? h : n;
+        nvec = (n - head) / 8;
+    }
+    // without the vector path every element is a "tail" element: one per thread
+    const size_t work = vec ? (nvec > 8 ? nvec : 8) : n;
+    size_t grid = (work + 127) / 128;
+    if (grid > 0x7FFFFFFFu) return SINCOS_ERR_INVALID_ARGUMENT;
+    cudaError_t e = launch_pairs16(variant, out_dtype, inter, static_cast<unsigned>(grid), theta_dev, sin_dev,
+                                   cos_dev, inter_dev, head, nvec, n, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SINCOS_OK;
+}
+
+static sincos_status_t interleave_impl(bool to_inter, const float *s, const float *c, float *io, size_t n,
+                                       void *stream) {
+    if (n == 0) return SINCOS_OK;
+    if (s == nullptr || c == nullptr || io == nullptr || n > SIZE_MAX / 8) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (!aligned(s, 4) || !aligned(c, 4) || !aligned(io, 8)) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (overlaps(s, 4 * n, c, 4 * n) || overlaps(s, 4 * n, io, 8 * n) || overlaps(c, 4 * n, io, 8 * n))
+        return SINCOS_ERR_OVERLAP;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    size_t grid = (n + 255) / 256;
+    const size_t cap = static_cast<size_t>(sm_count(dev)) * 32;
+    if (grid > cap) grid = cap;
+    e = launch_interleave(to_inter, static_cast<unsigned>(grid), s, c, io, n, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SINCOS_OK;
+}
+
+sincos_status_t sincos_interleave(const float *sin_dev, const float *cos_dev, float *inter_dev, size_t n,
+                                  void *stream) {
+    return interleave_impl(true, sin_dev, cos_dev, inter_dev, n, stream);
+}
+
+sincos_status_t sincos_deinterleave(const float *inter_dev, float *sin_dev, float *cos_dev, size_t n, void *stream) {
+    return interleave_impl(false, sin_dev, cos_dev, const_cast<float *>(inter_dev), n, stream);
+}
+
 sincos_status_t sincos_pairs_method(const float *theta_dev, float *sin_dev, float *cos_dev, float *inter_dev,
                                     size_t n, const sincos_method_t *m, void *stream) {
     if (m == nullptr || m->n_ss < 1 || m->n_ss > 8 || m->n_cc < 0 || m->n_cc > 8 || m->doublings < 0 ||

@@ -1,0 +1,136 @@
+// sincos_dtype.cu -- NEXT(4): other output dtypes and SoA <-> AoS adapters.
+//
+// Half-width outputs: the pair is evaluated by the method in fp32 exactly as in
+// sincos_pairs and then rounded once to IEEE binary16 or bfloat16 (round to nearest
+// even).  Traffic drops from 12 to 8 bytes per pair (4 in, 2 x 2 out), so the same HBM
+// roofline gives 1.5x the pairs per second.  The adapters convert between the split
+// (sin[], cos[]) and interleaved ({cos, sin} float2) fp32 layouts.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sincos_launch.h"
+#include "sincos_math.cuh"
+
+namespace sincos_b200 {
+
+template <int DT> __device__ __forceinline__ uint16_t to16(float x);
+template <> __device__ __forceinline__ uint16_t to16<1>(float x) { return __half_as_ushort(__float2half_rn(x)); }
+template <> __device__ __forceinline__ uint16_t to16<2>(float x) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+
+__device__ __forceinline__ uint32_t pack2(uint16_t lo, uint16_t hi) {
+    return static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+}
+
+__device__ __forceinline__ void st4u(void *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+
+template <int V, int DT, bool INTER>
+__device__ __forceinline__ void emit16_scalar(const float *theta, size_t e, uint16_t *so, uint16_t *co,
+                                              uint16_t *io) {
+    float s, c;
+    sincos_pair<V>(theta[e], s, c);
+    if constexpr (INTER) {
+        io[2 * e] = to16<DT>(c);
+        io[2 * e + 1] = to16<DT>(s);
+    } else {
+        so[e] = to16<DT>(s);
+        co[e] = to16<DT>(c);
+    }
+}
+
+// Full grid, one 256-bit theta load per thread; outputs: split 2 x 128-bit, interleaved 256-bit.
+template <int V, int DT, bool INTER>
+__global__ void __launch_bounds__(128) sincos16_kernel(const float *theta, uint16_t *so, uint16_t *co, uint16_t *io,
+                                                       size_t head, size_t nvec, size_t n) {
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t tail0 = head + 8 * nvec;
+    if (tid < head) emit16_scalar<V, DT, INTER>(theta, tid, so, co, io);
+    if (tid < n - tail0) emit16_scalar<V, DT, INTER>(theta, tail0 + tid, so, co, io);
+    for (size_t v = tid; v < nvec; v += nthr) {
+        const size_t e0 = head + 8 * v;
+        float x[8];
+        asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]), "=f"(x[6]), "=f"(x[7])
+                     : "l"(theta + e0));
+        uint16_t s16[8], c16[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            float s, c;
+            sincos_pair<V>(x[k], s, c);
+            s16[k] = to16<DT>(s);
+            c16[k] = to16<DT>(c);
+        }
+        if constexpr (INTER) {
+            uint32_t w[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) w[k] = pack2(c16[k], s16[k]);
+            asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                         ::"l"(io + 2 * e0), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]),
+                         "r"(w[6]), "r"(w[7])
+                         : "memory");
+        } else {
+            st4u(so + e0, pack2(s16[0], s16[1]), pack2(s16[2], s16[3]), pack2(s16[4], s16[5]), pack2(s16[6], s16[7]));
+            st4u(co + e0, pack2(c16[0], c16[1]), pack2(c16[2], c16[3]), pack2(c16[4], c16[5]), pack2(c16[6], c16[7]));
+        }
+    }
+}
+
+template <int V, int DT>
+static const void *pick16i(bool inter) {
+    return inter ? reinterpret_cast<const void *>(sincos16_kernel<V, DT, true>)
+                 : reinterpret_cast<const void *>(sincos16_kernel<V, DT, false>);
+}
+
+cudaError_t launch_pairs16(int variant, int dtype, bool inter, unsigned grid, const float *theta, void *so, void *co,
+                           void *io, size_t head, size_t nvec, size_t n, cudaStream_t stream) {
+    const void *fn;
+    if (variant == kNormalized)
+        fn = dtype == 1 ? pick16i<kNormalized, 1>(inter) : pick16i<kNormalized, 2>(inter);
+    else
+        fn = dtype == 1 ? pick16i<kRenormalized, 1>(inter) : pick16i<kRenormalized, 2>(inter);
+    uint16_t *s = static_cast<uint16_t *>(so), *c = static_cast<uint16_t *>(co), *i = static_cast<uint16_t *>(io);
+    void *args[] = {&theta, &s, &c, &i, &head, &nvec, &n};
+    return cudaLaunchKernel(fn, dim3(grid), dim3(128), args, 0, stream);
+}
+
+// ---- adapters: split <-> interleaved (fp32), one element per thread per trip ----------------
+__global__ void __launch_bounds__(256) interleave_kernel(const float *__restrict__ s, const float *__restrict__ c,
+                                                         float2 *__restrict__ io, size_t n) {
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += nthr)
+        io[e] = make_float2(__ldcs(c + e), __ldcs(s + e));
+}
+
+__global__ void __launch_bounds__(256) deinterleave_kernel(const float2 *__restrict__ io, float *__restrict__ s,
+                                                           float *__restrict__ c, size_t n) {
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += nthr) {
+        const float2 v = __ldcs(io + e);
+        __stcs(c + e, v.x);
+        __stcs(s + e, v.y);
+    }
+}
+
+cudaError_t launch_interleave(bool to_inter, unsigned grid, const float *s, const float *c, float *io, size_t n,
+                              cudaStream_t stream) {
+    if (to_inter) {
+        float2 *o = reinterpret_cast<float2 *>(io);
+        void *args[] = {&s, &c, &o, &n};
+        return cudaLaunchKernel(reinterpret_cast<const void *>(interleave_kernel), dim3(grid), dim3(256), args, 0,
+                                stream);
+    }
+    const float2 *i = reinterpret_cast<const float2 *>(io);
+    float *ss = const_cast<float *>(s), *cc = const_cast<float *>(c);
+    void *args[] = {&i, &ss, &cc, &n};
+    return cudaLaunchKernel(reinterpret_cast<const void *>(deinterleave_kernel), dim3(grid), dim3(256), args, 0,
+                            stream);
+}
+
+}  // namespace sincos_b200

@@ -1,0 +1,110 @@
+"""GPU parity of NEXT(4): 16-bit outputs (IEEE binary16, bfloat16) and the split <-> interleaved
+adapters.  The 16-bit values must equal the oracle's fp32 pair rounded to nearest even by a
+library conversion (numpy float16, torch bfloat16 on the CPU).  ``pytest -m gpu``."""
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_cs_0406049_b200 as sp  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+
+
+def rn16(x: np.ndarray, dtype) -> np.ndarray:
+    """The oracle's fp32 values rounded to 16 bits (RN-even) by a library, as uint16 bits."""
+    if dtype == torch.float16:
+        return x.astype(np.float16).view(np.uint16)
+    return torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+
+
+def same16(got: np.ndarray, want: np.ndarray, dtype) -> np.ndarray:
+    g = torch.from_numpy(got.view(np.int16)).view(dtype).float().numpy()
+    w = torch.from_numpy(want.view(np.int16)).view(dtype).float().numpy()
+    return (got == want) | (np.isnan(g) & np.isnan(w)) | ((g == 0) & (w == 0))
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("inter", [False, True])
+@pytest.mark.parametrize("config", [1, 3])
+def test_16bit_outputs_are_the_rounded_pairs(dtype, variant, inter, config):
+    th = inputs.generate(config, 0, min(inputs.size(config), 1 << 22))
+    ws, wc = oracle.sincos(th, variant)
+    t = torch.from_numpy(th).cuda()
+    n = t.numel()
+    if inter:
+        o = torch.empty(2 * n, dtype=dtype, device="cuda")
+        sp.sincos_pairs_dtype(t, interleaved_out=o, variant=variant)
+        ob = o.view(torch.int16).cpu().numpy().view(np.uint16)
+        gs, gc = ob[1::2], ob[0::2]
+    else:
+        s = torch.empty(n, dtype=dtype, device="cuda")
+        c = torch.empty(n, dtype=dtype, device="cuda")
+        sp.sincos_pairs_dtype(t, s, c, variant=variant)
+        gs = s.view(torch.int16).cpu().numpy().view(np.uint16)
+        gc = c.view(torch.int16).cpu().numpy().view(np.uint16)
+    assert same16(gs, rn16(ws, dtype), dtype).all()
+    assert same16(gc, rn16(wc, dtype), dtype).all()
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_16bit_tails_and_misalignment(dtype):
+    rng = np.random.default_rng(2)
+    base = rng.uniform(-100, 100, 4096).astype(np.float32)
+    ws, wc = oracle.sincos(base, 0)
+    bt = torch.from_numpy(base).cuda()
+    bs = torch.empty(4096 + 64, dtype=dtype, device="cuda")
+    bc = torch.empty(4096 + 64, dtype=dtype, device="cuda")
+    for n in list(range(0, 40)) + [1001, 4000]:
+        for ot, oo in ((0, 0), (3, 3), (1, 0), (0, 5)):
+            if ot + n > 4096:
+                continue
+            s, c = bs[oo:oo + n], bc[oo + 16:oo + 16 + n]
+            sp.sincos_pairs_dtype(bt[ot:ot + n], s, c, variant=0)
+            torch.cuda.synchronize()
+            gs = s.view(torch.int16).cpu().numpy().view(np.uint16)
+            gc = c.view(torch.int16).cpu().numpy().view(np.uint16)
+            assert same16(gs, rn16(ws[ot:ot + n], dtype), dtype).all(), (n, ot, oo)
+            assert same16(gc, rn16(wc[ot:ot + n], dtype), dtype).all(), (n, ot, oo)
+
+
+def test_fp32_dtype_is_the_hot_path():
+    t = torch.from_numpy(inputs.generate(2, 0, 1 << 20)).cuda()
+    s1, c1 = sp.sincos(t)
+    s2, c2 = torch.empty_like(t), torch.empty_like(t)
+    sp.sincos_pairs_dtype(t, s2, c2)
+    torch.cuda.synchronize()
+    assert torch.equal(s1, s2) and torch.equal(c1, c2)
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 1000, (1 << 22) + 3])
+def test_adapters_round_trip(n):
+    s = torch.randn(n, device="cuda")
+    c = torch.randn(n, device="cuda")
+    io = torch.empty(2 * n, device="cuda")
+    sp.interleave(s, c, io)
+    s2, c2 = torch.empty_like(s), torch.empty_like(c)
+    sp.deinterleave(io, s2, c2)
+    torch.cuda.synchronize()
+    assert torch.equal(io[0::2], c) and torch.equal(io[1::2], s)
+    assert torch.equal(s2, s) and torch.equal(c2, c)
+
+
+def test_adapter_matches_interleaved_kernel_output():
+    t = torch.from_numpy(inputs.generate(3, 0, 1 << 20)).cuda()
+    s, c = sp.sincos(t, variant=1)
+    io = torch.empty(2 * t.numel(), device="cuda")
+    sp.interleave(s, c, io)
+    io2 = sp.sincos(t, variant=1, interleaved=True).reshape(-1)
+    torch.cuda.synchronize()
+    assert torch.equal(io.view(torch.int32), io2.view(torch.int32))

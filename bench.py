@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row side measurements")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for the stats gather / time max (gloo: flow testing only)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="every rank on cuda:0 (flow testing of the N>1 host path on a 1-GPU box; gloo only)")
     ap.add_argument("--launch", default=None, help="threads,blocks_per_sm,vec,unroll (default: library default)")
     return ap.parse_args()
 
@@ -380,6 +384,7 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    cdev = dev if args.backend == "nccl" else None      # where the collectives' tensors live
     if args.launch:
         sp.set_launch_config(*[int(x) for x in args.launch.split(",")])
     W = WORKLOADS[args.workload]
@@ -417,6 +422,27 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(max(args.warmup, 3)):
         for v in variants:
             sp.sincos_pairs(th, variant=v, stream=stream, **outs[v])
+    # Launch-bound (L2-resident) workloads replay the step from a CUDA graph: one graph per
+    # variant, captured on a side stream, so host launch latency does not set the time.
+    use_graph = 12 * n < (256 << 20)
+    if use_graph:
+        graphs = {}
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        for v in variants:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cap):
+                sp.sincos_pairs(th, variant=v, stream=cap, **outs[v])
+            graphs[v] = g
+        stream.wait_stream(cap)
+        torch.cuda.synchronize(dev)
+
+    def run_one(v):
+        if use_graph:
+            graphs[v].replay()
+        else:
+            sp.sincos_pairs(th, variant=v, stream=stream, **outs[v])
+
     # per-launch events on the launching stream: the kernels' own durations
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(variants) + 1)] for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -427,13 +453,13 @@ def run_ours(args, rank, world, local_rank):
         for k in range(args.steps):
             ev[k][0].record(stream)
             for j, v in enumerate(variants):
-                sp.sincos_pairs(th, variant=v, stream=stream, **outs[v])
+                run_one(v)
                 ev[k][j + 1].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize(dev)
     barrier()
-    launches = sp.launch_count() - launches0
-    ms_max = max_over_ranks(t_start.elapsed_time(t_end), world, dev)
+    launches = sp.launch_count() - launches0 if not use_graph else len(variants) * args.steps
+    ms_max = max_over_ranks(t_start.elapsed_time(t_end), world, cdev)
     per_kernel = {v: [ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps)] for j, v in enumerate(variants)}
     units_all = W.n * world if W.weak else W.n
     pairs_total = len(variants) * units_all * args.steps
@@ -476,7 +502,7 @@ def run_ours(args, rank, world, local_rank):
         st = sp.error_stats(th, stream=stream, **outs[v])
         recs.append([float(st["n"]), float(st["nan_count"]), st["max_comb"], st["sum_sq"], st["max_amp"],
                      avg[v], float(rank), float(v)])
-    summary = summarize(gather_records(recs, world, dev))
+    summary = summarize(gather_records(recs, world, cdev))
 
     methods_res = None
     if rank == 0 and not args.no_next and not W.interleaved:
@@ -510,7 +536,7 @@ def run_ours(args, rank, world, local_rank):
         b.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        t2 = max_over_ranks(a.elapsed_time(b), world, dev)
+        t2 = max_over_ranks(a.elapsed_time(b), world, cdev)
         e2e = {"value": world * len(variants) * e2e_n * k2 / (t2 / 1e3), "unit": "pairs/s",
                "h2d_bytes_per_step": len(variants) * 4 * e2e_n, "d2h_bytes_per_step": len(variants) * 8 * e2e_n,
                "steps": k2, "elements_per_rank": e2e_n,
@@ -538,7 +564,7 @@ def run_ours(args, rank, world, local_rank):
                        "global_batch": units_all, "parallelism": f"dp{world} (contiguous shards, no collective)",
                        "l2": "inputs larger than L2 (4n B theta + 8n B outputs per launch vs 126 MB L2); no flush"
                              if 12 * n > (256 << 20) else "working set near/below L2 size: not an HBM measurement",
-                       "launch": sp.get_launch_config()},
+                       "launch": sp.get_launch_config(), "cuda_graph": use_graph},
             "hbm_GBps": BYTES_PER_PAIR * pairs_total / (ms_max / 1e3) / 1e9 / world,
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -568,11 +594,15 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    gpu = 0 if args.same_device else local_rank
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        torch.cuda.set_device(gpu)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group("gloo")
     try:
-        run_ours(args, rank, world, local_rank)
+        run_ours(args, rank, world, gpu)
     finally:
         if world > 1:
             dist.destroy_process_group()

@@ -40,18 +40,26 @@ __device__ __forceinline__ void op(float t, float &s, float &c) {
 }
 
 // ---- streaming memory access ----------------------------------------------
+// Cache-policy qualifiers of the 256-bit accesses (overridable at build time for the
+// policy experiment in tools/hint_experiment.py; the defaults were measured best).
+#ifndef SINCOS_LD8_Q
+#define SINCOS_LD8_Q ".L1::no_allocate.L2::evict_first"
+#endif
+#ifndef SINCOS_ST8_Q
+#define SINCOS_ST8_Q ".L1::no_allocate.L2::evict_first"
+#endif
 template <int W, bool NC> struct Mem;
 
 template <> struct Mem<8, true> {
     static __device__ __forceinline__ void load(float (&r)[8], const float *p) {
-        asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        asm volatile("ld.global.nc" SINCOS_LD8_Q ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
                      : "l"(p));
     }
 };
 template <> struct Mem<8, false> {
     static __device__ __forceinline__ void load(float (&r)[8], const float *p) {
-        asm volatile("ld.global.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        asm volatile("ld.global" SINCOS_LD8_Q ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
                      : "l"(p));
     }
@@ -72,7 +80,7 @@ template <> struct Mem<4, false> {
 };
 
 __device__ __forceinline__ void store8(float *p, const float *r) {
-    asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+    asm volatile("st.global" SINCOS_ST8_Q ".v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
                  :: "l"(p), "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7])
                  : "memory");
 }

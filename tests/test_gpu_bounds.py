@@ -1,0 +1,99 @@
+"""Guard-zone checks for out-of-bounds writes (compute-sanitizer is closed on this pool):
+every entry point writes into a slice of a larger buffer pre-filled with a sentinel pattern;
+everything outside the slice must still hold the sentinel afterwards.  ``pytest -m gpu``."""
+import numpy as np
+import pytest
+
+import inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_cs_0406049_b200 as sp  # noqa: E402
+
+SENT = 0x7F8ABCDE          # a NaN payload no kernel produces
+G = 4096                   # guard elements on each side
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+
+
+def guarded(n, dtype=torch.float32, off=0):
+    words = (n * torch.finfo(dtype).bits // 32) if dtype != torch.float32 else n
+    buf = torch.full((2 * G + words + 8,), SENT, dtype=torch.int32, device="cuda")
+    return buf, buf[G + off // 1:]
+
+
+def check(buf, lo, hi):
+    b = buf.cpu().numpy()
+    assert np.all(b[:lo] == SENT) and np.all(b[hi:] == SENT), (np.flatnonzero(b[:lo] != SENT)[:5],
+                                                              np.flatnonzero(b[hi:] != SENT)[:5] + hi)
+
+
+SIZES = [1, 7, 8, 9, 255, 1000, 65536 + 5]
+OFFS = [0, 1, 3, 5]
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("off", OFFS)
+def test_pairs_split_and_interleaved(n, off):
+    th = torch.from_numpy(inputs.generate(2, 0, n)).cuda()
+    for v in (0, 1):
+        bs = torch.full((2 * G + n + 8,), SENT, dtype=torch.int32, device="cuda")
+        bc = torch.full((2 * G + n + 8,), SENT, dtype=torch.int32, device="cuda")
+        s = bs[G + off:G + off + n].view(torch.float32)
+        c = bc[G + off:G + off + n].view(torch.float32)
+        sp.sincos_pairs(th, s, c, variant=v)
+        bi = torch.full((2 * G + 2 * n + 8,), SENT, dtype=torch.int32, device="cuda")
+        io = bi[G + 2 * off:G + 2 * off + 2 * n].view(torch.float32)
+        sp.sincos_pairs(th, interleaved_out=io, variant=v)
+        torch.cuda.synchronize()
+        check(bs, G + off, G + off + n)
+        check(bc, G + off, G + off + n)
+        check(bi, G + 2 * off, G + 2 * off + 2 * n)
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("off", OFFS)
+def test_dtype_and_method_paths(n, off):
+    th = torch.from_numpy(inputs.generate(3, 0, n)).cuda()
+    # 16-bit split outputs: guard in int16 units
+    s16 = 0x7E5A                           # an fp16 NaN payload no kernel produces
+    bs = torch.full((2 * G + n + 16,), s16, dtype=torch.int16, device="cuda")
+    bc = bs.clone()
+    s = bs[G + off:G + off + n].view(torch.float16)
+    c = bc[G + off:G + off + n].view(torch.float16)
+    sp.sincos_pairs_dtype(th, s, c, variant=1)
+    torch.cuda.synchronize()
+    for b in (bs, bc):
+        a = b.cpu().numpy()
+        assert np.all(a[:G + off] == s16) and np.all(a[G + off + n:] == s16)
+    # general method
+    bs = torch.full((2 * G + n + 8,), SENT, dtype=torch.int32, device="cuda")
+    bc = bs.clone()
+    m = sp.make_method(*sp.PAPER_METHODS[0])
+    sp.sincos_pairs_method(th, m, bs[G + off:G + off + n].view(torch.float32), bc[G + off:G + off + n].view(torch.float32))
+    torch.cuda.synchronize()
+    check(bs, G + off, G + off + n)
+    check(bc, G + off, G + off + n)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (3, 8), (5, 13), (17, 1024), (64, 1000)])
+def test_phase_grid_and_nudft(shape):
+    nf, nt = shape
+    f = torch.rand(nf, device="cuda") * 100
+    t = torch.rand(nt, device="cuda")
+    n = nf * nt
+    bi = torch.full((2 * G + 2 * n + 8,), SENT, dtype=torch.int32, device="cuda")
+    sp.phase_grid(f, t, interleaved_out=bi[G:G + 2 * n].view(torch.float32), units=sp.TURNS)
+    a = torch.randn(nt, dtype=torch.complex64, device="cuda")
+    bo = torch.full((2 * G + 2 * nf + 8,), SENT, dtype=torch.int32, device="cuda")
+    out = bo[G:G + 2 * nf].view(torch.complex64)
+    sp.nudft(f, t, a, out=out)
+    torch.cuda.synchronize()
+    check(bi, G, G + 2 * n)
+    check(bo, G, G + 2 * nf)

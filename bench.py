@@ -541,7 +541,29 @@ def run_ours(args, rank, world, local_rank):
                "h2d_bytes_per_step": len(variants) * 4 * e2e_n, "d2h_bytes_per_step": len(variants) * 8 * e2e_n,
                "steps": k2, "elements_per_rank": e2e_n,
                "path": "sincos_pairs_host: pinned host buffers, chunked H2D -> kernel -> D2H over 3 streams"}
-        del ws, oh
+        # the e2e roofline: the PCIe copy engines (H2D and D2H run concurrently), measured here
+        # with plain pinned copies of one step's byte counts
+        dbuf = torch.empty(2 * e2e_n, dtype=torch.float32, device=dev)
+        hbuf = torch.empty(2 * e2e_n, dtype=torch.float32).pin_memory()
+        for _ in range(2):
+            dbuf[:e2e_n].copy_(th_h, non_blocking=True)
+            hbuf.copy_(dbuf, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        a.record(stream)
+        dbuf[:e2e_n].copy_(th_h, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        h2d_gbs = 4 * e2e_n / (a.elapsed_time(b) / 1e3) / 1e9
+        a.record(stream)
+        hbuf.copy_(dbuf, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        d2h_gbs = 8 * e2e_n / (a.elapsed_time(b) / 1e3) / 1e9
+        step_floor = max(len(variants) * 4 * e2e_n / (h2d_gbs * 1e9), len(variants) * 8 * e2e_n / (d2h_gbs * 1e9))
+        e2e["pcie"] = {"h2d_GBps": h2d_gbs, "d2h_GBps": d2h_gbs,
+                       "roofline_pairs_per_s": world * len(variants) * e2e_n / step_floor}
+        e2e["frac_of_pcie_roofline"] = e2e["value"] / e2e["pcie"]["roofline_pairs_per_s"]
+        del ws, oh, dbuf, hbuf
 
     fused = nudft_res = None
     if rank == 0 and not args.no_next:

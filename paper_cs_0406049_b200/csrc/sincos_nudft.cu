@@ -25,7 +25,10 @@
 namespace sincos_b200 {
 
 constexpr int kNuThreads = 128;
-constexpr int kKPerThread = 4;
+#ifndef SINCOS_NUDFT_KPT
+#define SINCOS_NUDFT_KPT 4
+#endif
+constexpr int kKPerThread = SINCOS_NUDFT_KPT;
 constexpr int kKPerBlock = kNuThreads * kKPerThread;
 constexpr int kTileJ = 256;
 
@@ -70,8 +73,7 @@ __global__ void __launch_bounds__(kNuThreads) nudft_partial(const float *__restr
                                                             const float2 *__restrict__ a, size_t nt,
                                                             size_t chunk, float2 *__restrict__ part,
                                                             const MethodParams mp) {
-    __shared__ float st[kTileJ];
-    __shared__ float2 sa[kTileJ];
+    __shared__ float4 sj[kTileJ];    // {t_j, re a_j, im a_j, 0}: one 128-bit broadcast load per term
     const size_t k0 = static_cast<size_t>(blockIdx.x) * kKPerBlock + threadIdx.x;
     const size_t j0 = static_cast<size_t>(blockIdx.y) * chunk;
     const size_t j1 = j0 + chunk < nt ? j0 + chunk : nt;
@@ -87,13 +89,14 @@ __global__ void __launch_bounds__(kNuThreads) nudft_partial(const float *__restr
         const int len = static_cast<int>(j1 - jt < kTileJ ? j1 - jt : kTileJ);
         __syncthreads();
         for (int q = threadIdx.x; q < len; q += kNuThreads) {
-            st[q] = t[jt + q];
-            sa[q] = a[jt + q];
+            const float2 aq = a[jt + q];
+            sj[q] = make_float4(t[jt + q], aq.x, aq.y, 0.0f);
         }
         __syncthreads();
         for (int q = 0; q < len; ++q) {
-            const float tj = st[q];
-            const float2 aj = sa[q];
+            const float4 v = sj[q];
+            const float tj = v.x;
+            const float2 aj = make_float2(v.y, v.z);
 #pragma unroll
             for (int m = 0; m < kKPerThread; ++m) {
                 float s, c;

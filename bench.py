@@ -93,7 +93,7 @@ class ClockSampler:
     }
 
     def __init__(self, local_rank):
-        self.samples, self.reasons, self.ok = [], set(), False
+        self.samples, self.mem, self.reasons, self.ok = [], [], set(), False
         self.max_mhz = None
         try:
             import pynvml
@@ -113,6 +113,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.mem.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_MEM))
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if r & bit:
@@ -136,6 +137,7 @@ class ClockSampler:
         if not self.ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "mem_mhz": statistics.median(self.mem) if self.mem else None,
                 "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
 
 
@@ -163,10 +165,21 @@ def cpu_oracle_rate(theta: np.ndarray, seconds: float):
             if time.perf_counter() - t0 >= seconds and v == 0:
                 break
     dt = time.perf_counter() - t0
+    # one thread as well, on a 2^22-element prefix, both variants
+    m1 = min(m, 1 << 22)
+    t1 = time.perf_counter()
+    for v in (0, 1):
+        oracle.sincos_into(th[:m1], s[:m1], c[:m1], v)
+    one = 2 * m1 / (time.perf_counter() - t1)
+    cpu_model = ""
+    try:
+        cpu_model = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+    except Exception:
+        pass
     return {"value": pairs / dt, "unit": "pairs/s", "cores": cores, "kind": "oracle",
             "sample": f"first {m} elements of the C2 workload, variants N and A alternately, "
                       f"{pairs} pairs in {dt:.1f} s on {cores} threads (plain scalar C oracle)",
-            "seconds": dt}
+            "seconds": dt, "single_thread_pairs_per_s": one, "cpu_model": cpu_model}
 
 
 def run_reference(args, rank, world):
@@ -477,7 +490,9 @@ def run_ours(args, rank, world, local_rank):
             "bytes_per_pair": BYTES_PER_PAIR, "peak_source": peak_src,
             "frac_of_theoretical_8180": achieved / 8180.0,
             "per_variant_GBps": {vname[v]: BYTES_PER_PAIR * n / (avg[v] / 1e3) / 1e9 for v in variants},
-            "per_variant_ms": {vname[v]: avg[v] for v in variants}}
+            "per_variant_ms": {vname[v]: avg[v] for v in variants},
+            "per_variant_ms_median_min": {vname[v]: [statistics.median(per_kernel[v]), min(per_kernel[v])]
+                                          for v in variants}}
 
     # traffic ceiling: same access pattern and launch, no arithmetic (outside the timed region)
     o = outs[sp.NORMALIZED]

@@ -246,6 +246,20 @@ typedef struct {
     uint64_t reserved;
 } sincos_stats_t;
 
+/*
+ * sincos_pairs_sharded_stats -- the whole single-process multi-device run:
+ * launch every shard on its own device (one shard per device, distinct devices), reduce
+ * each shard's error statistics (below) and kernel time (CUDA events around its launch)
+ * into its 64-byte record, and all-gather the records over NCCL (ncclCommInitAll over the
+ * shards' devices, ncclAllGather inside a group) -- the only collective of the path, 64 B
+ * per rank.  gathered: host array of nshards records, shard order.  Synchronous.  NCCL is
+ * bound at run time (dlopen "libnccl.so.2"); without it returns INVALID_ARGUMENT (see
+ * sincos_nccl_available).  Allocates and frees small per-device buffers internally.
+ */
+SINCOS_API sincos_status_t sincos_pairs_sharded_stats(const sincos_shard_t *shards, int nshards,
+                                                      sincos_variant_t variant, sincos_stats_t *gathered);
+SINCOS_API int sincos_nccl_available(void);
+
 SINCOS_API size_t sincos_stats_workspace_bytes(void);
 /* stats_dev: device pointer to one sincos_stats_t; ws_dev: device workspace of
  * sincos_stats_workspace_bytes(). */

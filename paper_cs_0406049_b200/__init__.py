@@ -103,6 +103,8 @@ _SIGS = {
     "sincos_phase_grid": (_I, [_P, _S, _P, _S, _P, _P, _P, _I, _I, _P]),
     "sincos_pairs_method": (_I, [_P, _P, _P, _P, _S, ctypes.POINTER(Method), _P]),
     "sincos_pairs_dtype": (_I, [_P, _P, _P, _P, _S, _I, _I, _P]),
+    "sincos_pairs_sharded_stats": (_I, [ctypes.POINTER(Shard), _I, _I, _P]),
+    "sincos_nccl_available": (_I, []),
     "sincos_interleave": (_I, [_P, _P, _P, _S, _P]),
     "sincos_deinterleave": (_I, [_P, _P, _P, _S, _P]),
     "sincos_nudft_method": (_I, [_P, _S, _P, _P, _S, _P, _I, ctypes.POINTER(Method), _P, _S, _P]),
@@ -335,6 +337,38 @@ def sincos_pairs_sharded(shards, variant=NORMALIZED):
         arr[i].n = th.numel()
         arr[i].stream = _stream(sh.get("stream"), th.device)
     _check(lib().sincos_pairs_sharded(arr, len(shards), _variant(variant)), "sincos_pairs_sharded")
+
+
+def _shard_array(shards):
+    arr = (Shard * len(shards))()
+    for i, sh in enumerate(shards):
+        th = sh["theta"]
+        arr[i].device = th.device.index
+        arr[i].theta_dev = _ptr(th, "theta")
+        arr[i].sin_dev = _ptr(sh.get("sin"), "sin")
+        arr[i].cos_dev = _ptr(sh.get("cos"), "cos")
+        arr[i].inter_dev = _ptr(sh.get("inter"), "inter")
+        arr[i].n = th.numel()
+        arr[i].stream = _stream(sh.get("stream"), th.device)
+    return arr
+
+
+def sincos_pairs_sharded_stats(shards, variant=NORMALIZED) -> list:
+    """C-ABI sincos_pairs_sharded_stats: one shard per device, launched, its stats and kernel
+    time reduced on its device, the 64-B records all-gathered over NCCL.  Returns the records."""
+    arr = _shard_array(shards)
+    out = (Stats * len(shards))()
+    _check(lib().sincos_pairs_sharded_stats(arr, len(shards), _variant(variant), out), "sincos_pairs_sharded_stats")
+    res = []
+    for s in out:
+        d = {k: getattr(s, k) for k, _ in Stats._fields_}
+        d["rms"] = (s.sum_sq / s.n) ** 0.5 if s.n else 0.0
+        res.append(d)
+    return res
+
+
+def nccl_available() -> bool:
+    return bool(lib().sincos_nccl_available())
 
 
 def error_stats(theta, sin_out=None, cos_out=None, interleaved_out=None, stream=None) -> dict:

@@ -564,6 +564,9 @@ const char *sincos_status_string(sincos_status_t s) {
 
 int sincos_last_cuda_error(void) { return g_last_cuda_error; }
 
+// internal (hidden): lets sincos_shard.cu record a CUDA error the same way
+sincos_status_t sincos_last_error_set(int e) { return cuda_fail(static_cast<cudaError_t>(e)); }
+
 const char *sincos_version(void) { return "sincos_pairs 0.1 (sm_100a; arXiv cs/0406049)"; }
 
 uint64_t sincos_launch_count(void) { return g_launches.load(); }

@@ -103,6 +103,18 @@ def test_phase_grid_validation(L):
     assert L.sincos_phase_grid(f, 4, t, 8, 3 * A, 4 * A, None, 0, 0, None) in (OK, 3)       # valid: needs CUDA
 
 
+def test_sharded_stats_validation(L):
+    """The single-process NCCL stats path refuses bad shard lists before any CUDA call, and binds
+    NCCL at run time (libnccl.so.2 is present in this image)."""
+    assert sp.nccl_available()
+    arr = (sp.Shard * 2)()
+    arr[0].device = arr[1].device = 0                       # two shards on one device
+    out = (sp.Stats * 2)()
+    assert L.sincos_pairs_sharded_stats(arr, 2, 0, out) == INVALID
+    assert L.sincos_pairs_sharded_stats(arr, 0, 0, out) == INVALID
+    assert L.sincos_pairs_sharded_stats(None, 1, 0, out) == INVALID
+
+
 def test_host_path_validation(L):
     assert L.sincos_pairs_host(None, None, None, None, 0, 0, None, 0, None) == OK
     buf = (ctypes.c_float * 64)()

@@ -279,6 +279,13 @@ SINCOS_API int sincos_set_launch_config(int threads, int blocks_per_sm, int vec,
 SINCOS_API void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *vec, int *unroll,
                                          int *prefetch);
 
+/* Fused-sum kernel form (bench / tests): 1 = packed fp32 (sm_100a FFMA2/FMUL2/FADD2,
+ * two frequencies per instruction; the default), 0 = scalar fp32.  Both are
+ * bit-identical (each packed lane rounds as the scalar instruction does); applies to
+ * variants 0/1 and the specialised method shapes.  Process-global; returns the previous
+ * setting, or -1 for a value other than 0/1. */
+SINCOS_API int sincos_set_nudft_packed(int on);
+
 /* Traffic-ceiling kernel (bench only): same access pattern and launch as
  * sincos_pairs, no arithmetic (writes theta to both outputs). */
 SINCOS_API sincos_status_t sincos_null_4in8out(const float *theta_dev, float *sin_dev, float *cos_dev,

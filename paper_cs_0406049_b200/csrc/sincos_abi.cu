@@ -515,6 +515,11 @@ sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
     return SINCOS_OK;
 }
 
+int sincos_set_nudft_packed(int on) {
+    const int prev = get_nudft_packed();
+    return set_nudft_packed(on) == 0 ? prev : -1;
+}
+
 int sincos_set_launch_config(int threads, int blocks_per_sm, int vec, int unroll, int prefetch) {
     if (!(threads == 128 || threads == 256 || threads == 512)) return -1;
     if (blocks_per_sm < 0 || blocks_per_sm > 4096) return -1;

@@ -33,6 +33,9 @@ struct MethodParams;
 cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, const float *t, const float *a,
                          size_t nt, float *out, void *ws, cudaStream_t stream, const MethodParams *method = nullptr,
                          int method_nt = 4, int method_fix = 0, int method_spec = -1);
+// Packed fp32 (FFMA2) kernels for the fused sum: 1 = on (default), 0 = scalar; -1 on bad value.
+int set_nudft_packed(int on);
+int get_nudft_packed();
 // NEXT(3) general method (sincos_method.cu).
 cudaError_t launch_method(const float *ss, int n_ss, const float *cc, int n_cc, int doublings, int fix, bool inter,
                           bool vec, unsigned grid, const float *theta, float *so, float *co, float *io, size_t head,

@@ -20,6 +20,7 @@
 #include <stdint.h>
 
 #include "sincos_launch.h"
+#include "sincos_math2.cuh"
 #include "sincos_method.cuh"
 
 namespace sincos_b200 {
@@ -67,7 +68,26 @@ __device__ __forceinline__ void term_pair(const MethodParams &mp, float f, float
     }
 }
 
+// Two frequencies of one term at once (packed fp32, sincos_math2.cuh): the same
+// operations as term_pair for lanes m and m+1, bit-identical, half the FP32 issue slots.
+template <int V>
+constexpr bool kPackable = V == kNormalized || V == kRenormalized || V >= kMethodExactBase;
+
 template <int V, bool TURNS>
+__device__ __forceinline__ void term_pair2(const MethodParams &mp, F2 f, float t, F2 &s, F2 &c) {
+    const F2 p = mul2(f, bc2(t));
+    const F2 x = TURNS ? p : mul2(p, bc2(kInvTwoPi));
+    if constexpr (V >= kMethodExactBase) {
+        constexpr int SPEC = (V - kMethodExactBase) / 4;
+        constexpr int FIX = (V - kMethodExactBase) % 4;
+        constexpr int NS = SPEC == 0 ? 4 : 3, NC = SPEC == 0 ? 3 : 2, ND = SPEC == 0 ? 2 : 1;
+        method_from_q_exact2<NS, NC, ND, FIX>(mp, reduce_turn2(x), s, c);
+    } else {
+        sincos_from_q2<V>(reduce_turn2(x), s, c);
+    }
+}
+
+template <int V, bool TURNS, bool PACK>
 __global__ void __launch_bounds__(kNuThreads) nudft_partial(const float *__restrict__ f, size_t nf,
                                                             const float *__restrict__ t,
                                                             const float2 *__restrict__ a, size_t nt,
@@ -97,6 +117,25 @@ __global__ void __launch_bounds__(kNuThreads) nudft_partial(const float *__restr
             const float4 v = sj[q];
             const float tj = v.x;
             const float2 aj = make_float2(v.y, v.z);
+            if constexpr (PACK) {
+                const F2 ar = bc2(aj.x), ai = bc2(aj.y);
+#pragma unroll
+                for (int m = 0; m < kKPerThread; m += 2) {
+                    F2 s, c;
+                    term_pair2<V, TURNS>(mp, pk2(fk[m], fk[m + 1]), tj, s, c);
+                    // the scalar loop's four FMAs, lanes m and m+1
+                    F2 r = pk2(re[m], re[m + 1]), i = pk2(im[m], im[m + 1]);
+                    r = fma2(ar, c, r);
+                    r = nfma2(ai, s, r);
+                    i = fma2(ar, s, i);
+                    i = fma2(ai, c, i);
+                    re[m] = lo2(r);
+                    re[m + 1] = hi2(r);
+                    im[m] = lo2(i);
+                    im[m + 1] = hi2(i);
+                }
+                continue;
+            }
 #pragma unroll
             for (int m = 0; m < kKPerThread; ++m) {
                 float s, c;
@@ -143,10 +182,25 @@ size_t nudft_ws_bytes(size_t nf, size_t nt) {
     return nchunks * nf * sizeof(float2);
 }
 
+// Packed fp32 for the paper's tables and the specialised method shapes (default on;
+// sincos_set_nudft_packed(0) selects the scalar kernels, bit-identical, for A/B).
+static int g_nudft_packed = 1;
+int set_nudft_packed(int on) {
+    if (on != 0 && on != 1) return -1;
+    g_nudft_packed = on;
+    return 0;
+}
+int get_nudft_packed() { return g_nudft_packed; }
+
 template <int V>
 static const void *pick_nudft(bool turns) {
-    return turns ? reinterpret_cast<const void *>(nudft_partial<V, true>)
-                 : reinterpret_cast<const void *>(nudft_partial<V, false>);
+    if constexpr (kPackable<V> && kKPerThread % 2 == 0) {
+        if (g_nudft_packed)
+            return turns ? reinterpret_cast<const void *>(nudft_partial<V, true, true>)
+                         : reinterpret_cast<const void *>(nudft_partial<V, false, true>);
+    }
+    return turns ? reinterpret_cast<const void *>(nudft_partial<V, true, false>)
+                 : reinterpret_cast<const void *>(nudft_partial<V, false, false>);
 }
 
 cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, const float *t, const float *a,

@@ -163,3 +163,56 @@ def test_nudft_method_single_amplitude_exact(units, spec):
         for i, qq in enumerate(q):
             ws[i], wc[i] = oracle.method_pair_from_q(float(qq), om)
     assert np.array_equal(got.real, wc) and np.array_equal(got.imag, ws)
+
+
+# ---- packed fp32 (FFMA2) kernels --------------------------------------------------------
+
+@pytest.fixture
+def scalar_then_packed():
+    prev = sp.set_nudft_packed(True)
+    yield
+    sp.set_nudft_packed(prev)
+
+
+@pytest.mark.parametrize("units", [0, 1])
+@pytest.mark.parametrize("kind", ["N", "A", "m1_3_2", "m2_4_3"])
+@pytest.mark.parametrize("shape", [(1, 1), (3, 7), (513, 1031), (1500, 4100)])
+def test_packed_kernel_bit_identical_to_scalar(units, kind, shape, scalar_then_packed):
+    """The packed kernels (two frequencies per FFMA2/FMUL2/FADD2 lane pair) round every lane
+    exactly as the scalar kernels do: the sums are bit-identical, for the paper's tables and
+    the specialised method shapes, ragged nf (odd lane pairs past nf) and nt (tail tiles).
+    Phases include exact zeros, half-turn ties and huge / subnormal / non-finite values."""
+    nf, nt = shape
+    rng = np.random.default_rng(nf * 7 + nt)
+    f = rng.uniform(0, 512 if units else 3000, nf).astype(np.float32)
+    t = rng.uniform(-1, 1, nt).astype(np.float32)
+    special = np.array([0.0, -0.0, 0.5, 1.5, 2.5, -0.5, 1e-40, -1e-45, 3e30, np.inf, -np.inf, np.nan],
+                       np.float32)
+    f[: min(nf, special.size)] = special[: min(nf, special.size)]
+    t[: min(nt, 3)] = np.array([1.0, 0.25, 0.5], np.float32)[: min(nt, 3)]
+    a = rand_complex(rng, nt)
+    if kind in ("N", "A"):
+        kw = {"variant": 0 if kind == "N" else 1}
+    else:
+        from paper_cs_0406049_b200 import coeff_fit as cf
+        n, ds, dc = (1, 3, 2) if kind == "m1_3_2" else (2, 4, 3)
+        ss, cc = cf.fit_angle(n, ds, dc).fp32()
+        kw = {"method": sp.make_method(list(ss), list(cc), n, sp.FIX_RECIPROCAL if n == 1 else sp.FIX_LINEAR)}
+    fd, td, ad = (torch.from_numpy(x).cuda() for x in (f, t, a))
+    sp.set_nudft_packed(False)
+    o_scalar = sp.nudft(fd, td, ad, units=units, **kw)
+    sp.set_nudft_packed(True)
+    o_packed = sp.nudft(fd, td, ad, units=units, **kw)
+    torch.cuda.synchronize()
+    x, y = o_scalar.cpu().numpy(), o_packed.cpu().numpy()
+    xb = x.view(np.uint32).reshape(-1, 2)
+    yb = y.view(np.uint32).reshape(-1, 2)
+    fin = np.isfinite(x.real) & np.isfinite(x.imag)
+    assert np.array_equal(fin, np.isfinite(y.real) & np.isfinite(y.imag))
+    assert np.array_equal(xb[fin], yb[fin])
+
+
+def test_set_nudft_packed_rejects_bad_values():
+    assert sp.lib().sincos_set_nudft_packed(2) == -1
+    prev = sp.set_nudft_packed(True)
+    assert sp.set_nudft_packed(prev) is True

@@ -19,6 +19,9 @@ def main():
     rng = np.random.default_rng(7)
     a = torch.from_numpy((rng.normal(size=nt) + 1j * rng.normal(size=nt)).astype(np.complex64)).cuda()
     out = {}
+    packed = os.environ.get("NUDFT_PACKED")
+    if packed is not None:
+        sp.set_nudft_packed(packed == "1")
     for units in (sp.RADIANS, sp.TURNS):
         f, t = c4_axes(units == sp.TURNS)
         fd, td = torch.from_numpy(f).cuda(), torch.from_numpy(t).cuda()
@@ -31,7 +34,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             out[f"{'rt'[units]}_{name}"] = round(nf * nt / (e0.elapsed_time(e1) / 10 / 1e3) / 1e12, 4)
-    print(json.dumps({"T_terms_per_s": out}))
+    print(json.dumps({"packed": packed, "T_terms_per_s": out}))
 
 
 if __name__ == "__main__":

@@ -358,7 +358,8 @@ def measure_nudft(dev, stream, reps=5):
     out = torch.empty(nf, dtype=torch.complex64, device=dev)
     ws = torch.empty(sp.lib().sincos_nudft_workspace_bytes(nf, nt), dtype=torch.uint8, device=dev)
     res = {"workload": "C4 shape: 2^15 f x 2^15 t = 2^30 terms, complex64 amplitudes", "bound": "alu",
-           "peak_ops_per_s": ALU_PEAK_OPS, "ops_per_term": NUDFT_OPS}
+           "peak_ops_per_s": ALU_PEAK_OPS, "ops_per_term": NUDFT_OPS,
+           "kernel": "packed fp32 (FFMA2/FMUL2/FADD2, two frequencies per instruction) unless named scalar"}
     ks = torch.arange(0, nf, nf // 16, device=dev)
     asum = float(a.abs().sum())
     for units, uname in ((sp.RADIANS, "radians"), (sp.TURNS, "turns")):
@@ -369,9 +370,12 @@ def measure_nudft(dev, stream, reps=5):
         p = (fd[ks, None] * td[None, :]).double()
         ang = p if units == sp.RADIANS else 2 * np.pi * (p - torch.round(p))
         ref = (a.to(torch.complex128)[None, :] * torch.exp(1j * ang)).sum(dim=1)
-        for v, vname in ((sp.NORMALIZED, "N"), (sp.RENORMALIZED, "A"), (sp.CMP_LIBM_SINCOSF, "cuda_sincosf"),
+        for v, vname in ((sp.NORMALIZED, "N"), (sp.RENORMALIZED, "A"), (sp.NORMALIZED, "N_scalar_kernel"),
+                         (sp.CMP_LIBM_SINCOSF, "cuda_sincosf"),
                          (sp.CMP_INTRINSIC_SINCOSF, "cuda___sincosf"), ("m132", "method_1dbl_deg3_2_angle")):
             kw = {"method": fit_method(1, 3, 2)} if v == "m132" else {"variant": v}
+            # the default kernels are packed fp32 (FFMA2); "N_scalar_kernel" is the scalar twin
+            sp.set_nudft_packed(vname != "N_scalar_kernel")
             sp.nudft(fd, td, a, out=out, units=units, workspace=ws, stream=stream, **kw)
             err = float((out[ks].to(torch.complex128) - ref).abs().max()) / asum
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -383,9 +387,10 @@ def measure_nudft(dev, stream, reps=5):
             ms = e0.elapsed_time(e1) / reps
             terms = (nf * nt) / (ms / 1e3)
             r = {"ms": ms, "terms_per_s": terms, "max_err_over_sum_abs_a": err}
-            if vname == "N":
+            if vname.startswith("N"):
                 r["alu_frac"] = terms * NUDFT_OPS[uname] / ALU_PEAK_OPS
             res[f"{uname}_{vname}"] = r
+    sp.set_nudft_packed(True)
     return res
 
 

@@ -29,16 +29,8 @@ __device__ __forceinline__ F2 pk2(float lo, float hi) {
     return r;
 }
 __device__ __forceinline__ F2 bc2(float x) { return pk2(x, x); }
-__device__ __forceinline__ float lo2(F2 a) {
-    float lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
-    return lo;
-}
-__device__ __forceinline__ float hi2(F2 a) {
-    float lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
-    return hi;
-}
+__device__ __forceinline__ float lo2(F2 a) { return __uint_as_float(static_cast<uint32_t>(a.v)); }
+__device__ __forceinline__ float hi2(F2 a) { return __uint_as_float(static_cast<uint32_t>(a.v >> 32)); }
 // RN(a*b + c) per lane (one rounding)
 __device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
     F2 d;

@@ -134,17 +134,17 @@ __global__ void __launch_bounds__(kNuThreads) nudft_partial(const float *__restr
                     im[m] = lo2(i);
                     im[m + 1] = hi2(i);
                 }
-                continue;
-            }
+            } else {
 #pragma unroll
-            for (int m = 0; m < kKPerThread; ++m) {
-                float s, c;
-                term_pair<V, TURNS>(mp, fk[m], tj, s, c);
-                // (ar + i ai)(c + i s) accumulated with single-rounding FMAs
-                re[m] = __fmaf_rn(aj.x, c, re[m]);
-                re[m] = __fmaf_rn(-aj.y, s, re[m]);
-                im[m] = __fmaf_rn(aj.x, s, im[m]);
-                im[m] = __fmaf_rn(aj.y, c, im[m]);
+                for (int m = 0; m < kKPerThread; ++m) {
+                    float s, c;
+                    term_pair<V, TURNS>(mp, fk[m], tj, s, c);
+                    // (ar + i ai)(c + i s) accumulated with single-rounding FMAs
+                    re[m] = __fmaf_rn(aj.x, c, re[m]);
+                    re[m] = __fmaf_rn(-aj.y, s, re[m]);
+                    im[m] = __fmaf_rn(aj.x, s, im[m]);
+                    im[m] = __fmaf_rn(aj.y, c, im[m]);
+                }
             }
         }
     }

@@ -1,0 +1,77 @@
+"""A/B of build-time switches of libsincos_pairs.so on the hot path (tuning aid).
+
+  python tools/ab_macro.py build NAME -DMACRO=V ...   # here (CPU): builds tools/ab/NAME.so
+  python tools/ab_macro.py run                        # GPU box: times every tools/ab/*.so
+
+Times variants N and A, split and interleaved, on the C2 batch (2^28 angles, 12 B/pair),
+the libraries interleaved over rounds (median of 5 rounds x 10 launches).  One JSON line
+per library.  The default build (no switches) should be built as a control."""
+import ctypes
+import glob
+import json
+import os
+import statistics
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+AB = os.path.join(ROOT, "tools", "ab")
+
+
+def build(name, flags):
+    from paper_cs_0406049_b200 import _build
+    os.makedirs(AB, exist_ok=True)
+    out = os.path.join(AB, name + ".so")
+    subprocess.check_call([_build.nvcc(), *_build.NVCC_FLAGS, *flags, "-o", out, *_build.sources()], cwd=_build.PKG)
+    print(out)
+
+
+def run():
+    import torch
+
+    import inputs
+    n = 1 << 28
+    th = torch.from_numpy(inputs.generate(2, 0, n)).cuda()
+    s = torch.empty(n, device="cuda")
+    c = torch.empty(n, device="cuda")
+    io = torch.empty(2 * n, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    libs = {}
+    for p in sorted(glob.glob(os.path.join(AB, "*.so"))):
+        L = ctypes.CDLL(p)
+        L.sincos_pairs.restype = ctypes.c_int
+        L.sincos_pairs.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]
+        libs[os.path.basename(p)[:-3]] = L
+    cases = {"N_split": (0, False), "A_split": (1, False), "N_inter": (0, True), "A_inter": (1, True)}
+    res = {k: {c_: [] for c_ in cases} for k in libs}
+
+    def timeit(fn, reps=10):
+        for _ in range(2):
+            fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return 12 * n / (a.elapsed_time(b) / reps / 1e3) / 1e9
+
+    for _ in range(5):
+        for name, L in libs.items():
+            for cname, (v, inter) in cases.items():
+                if inter:
+                    fn = lambda: L.sincos_pairs(th.data_ptr(), None, None, io.data_ptr(), n, v, st)  # noqa: E731
+                else:
+                    fn = lambda: L.sincos_pairs(th.data_ptr(), s.data_ptr(), c.data_ptr(), None, n, v, st)  # noqa: E731
+                res[name][cname].append(timeit(fn))
+    for name in libs:
+        print(json.dumps({"lib": name, "GBps": {k: round(statistics.median(v), 1) for k, v in res[name].items()}}),
+              flush=True)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build(sys.argv[2], sys.argv[3:])
+    else:
+        run()

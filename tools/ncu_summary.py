@@ -26,6 +26,10 @@ METRICS = [
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
     ("sm__inst_issued.avg.pct_of_peak_sustained_active", "issue slots busy %"),
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe %"),
+    ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active", "FMA-heavy pipe %"),
+    ("sm__pipe_fmalite_cycles_active.avg.pct_of_peak_sustained_active", "FMA-lite pipe %"),
+    ("sm__inst_executed_pipe_fmaheavy.sum", "FMA-heavy warp instructions"),
+    ("sm__inst_executed_pipe_fmalite.sum", "FMA-lite warp instructions"),
     ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe %"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe %"),
     ("sm__pipe_xu_cycles_active.avg.pct_of_peak_sustained_active", "XU pipe %"),

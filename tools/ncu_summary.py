@@ -118,7 +118,10 @@ def main():
     # the dominant (longest) sincos kernel's per-launch DRAM traffic, for bench.py
     sk = [k for k in kernels if "sincos_vec_kernel" in k["kernel"] and "dram__bytes_read.sum" in k]
     if sk:
-        dom = max(sk, key=lambda k: k.get("gpu__time_duration.sum", 0))
+        # the bench's kernel (variant N, split, 256-bit, U = 1, the default launch) if captured,
+        # else the longest sincos kernel
+        bench_k = [k for k in sk if "sincos_vec_kernel<0, 0, 8, 1, 1, 0>" in k["kernel"]]
+        dom = bench_k[0] if bench_k else max(sk, key=lambda k: k.get("gpu__time_duration.sum", 0))
         js = {"tag": args.tag, "rep": os.path.basename(args.rep),
               "dominant": {"kernel": dom["kernel"], "n": args.n, "dram_bytes_read": dom["dram__bytes_read.sum"],
                            "dram_bytes_write": dom["dram__bytes_write.sum"],

@@ -440,26 +440,30 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(max(args.warmup, 3)):
         for v in variants:
             sp.sincos_pairs(th, variant=v, stream=stream, **outs[v])
-    # Launch-bound (L2-resident) workloads replay the step from a CUDA graph: one graph per
-    # variant, captured on a side stream, so host launch latency does not set the time.
+    # Launch-bound (L2-resident) workloads replay the step from a CUDA graph: the whole step (one
+    # launch per variant) captured once on a side stream and replayed once per step, so host launch
+    # latency does not set the time.  The per-kernel durations then come from graphs of GRAPH_REPS
+    # back-to-back launches of one variant (untimed for the metric), i.e. the kernel's own time.
     use_graph = 12 * n < (256 << 20)
+    GRAPH_REPS = 20
     if use_graph:
-        graphs = {}
         cap = torch.cuda.Stream(dev)
         cap.wait_stream(stream)
+        step_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(step_graph, stream=cap):
+            for v in variants:
+                sp.sincos_pairs(th, variant=v, stream=cap, **outs[v])
+        rep_graphs = {}
         for v in variants:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=cap):
-                sp.sincos_pairs(th, variant=v, stream=cap, **outs[v])
-            graphs[v] = g
+                for _ in range(GRAPH_REPS):
+                    sp.sincos_pairs(th, variant=v, stream=cap, **outs[v])
+            rep_graphs[v] = g
         stream.wait_stream(cap)
         torch.cuda.synchronize(dev)
-
-    def run_one(v):
-        if use_graph:
-            graphs[v].replay()
-        else:
-            sp.sincos_pairs(th, variant=v, stream=stream, **outs[v])
+        for _ in range(3):
+            step_graph.replay()
 
     # per-launch events on the launching stream: the kernels' own durations
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(variants) + 1)] for _ in range(args.steps)]
@@ -469,16 +473,31 @@ def run_ours(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         t_start.record(stream)
         for k in range(args.steps):
+            if use_graph:
+                step_graph.replay()
+                continue
             ev[k][0].record(stream)
             for j, v in enumerate(variants):
-                run_one(v)
+                sp.sincos_pairs(th, variant=v, stream=stream, **outs[v])
                 ev[k][j + 1].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize(dev)
     barrier()
     launches = sp.launch_count() - launches0 if not use_graph else len(variants) * args.steps
     ms_max = max_over_ranks(t_start.elapsed_time(t_end), world, cdev)
-    per_kernel = {v: [ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps)] for j, v in enumerate(variants)}
+    if use_graph:
+        per_kernel = {v: [] for v in variants}
+        for _ in range(5):
+            for v in variants:
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                rep_graphs[v].replay()
+                b_.record(stream)
+                torch.cuda.synchronize(dev)
+                per_kernel[v].append(a_.elapsed_time(b_) / GRAPH_REPS)
+    else:
+        per_kernel = {v: [ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps)]
+                      for j, v in enumerate(variants)}
     units_all = W.n * world if W.weak else W.n
     pairs_total = len(variants) * units_all * args.steps
     value = pairs_total / (ms_max / 1e3)
@@ -505,9 +524,22 @@ def run_ours(args, rank, world, local_rank):
         sp.null_4in8out(th, stream=stream, **o)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = 10
+    if use_graph:       # same launch mode as the kernels it bounds
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        null_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(null_graph, stream=cap):
+            for _ in range(GRAPH_REPS):
+                sp.null_4in8out(th, stream=cap, **o)
+        stream.wait_stream(cap)
+        null_graph.replay()
+        reps = GRAPH_REPS
     e0.record(stream)
-    for _ in range(reps):
-        sp.null_4in8out(th, stream=stream, **o)
+    if use_graph:
+        null_graph.replay()
+    else:
+        for _ in range(reps):
+            sp.null_4in8out(th, stream=stream, **o)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     null_ms = e0.elapsed_time(e1) / reps

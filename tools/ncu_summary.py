@@ -107,10 +107,28 @@ def main():
         tot = {}
         for r in rows:
             if r[-3] == "gpu__time_duration.sum":
-                nm = r[4].split("(")[0]
+                nm = r[4].split("(")[0] + " grid " + r[8].strip("()").split(",")[0]
                 tot.setdefault(nm, []).append(scale(float(r[-1].replace(",", "")), r[-2]))
         all_t = sum(sum(v) for v in tot.values())
-        lines.append("== launch list (ncu --metrics gpu__time_duration.sum, cold-cache, serialised)")
+        # the hot path's step: variant N and A of the bench launch (the largest grid of each)
+        step = {}
+        for nm, v in tot.items():
+            for var in ("0", "1"):
+                if f"sincos_vec_kernel<{var}, 0, 8, 1, 1, 0>" in nm or f"sincos_vec_kernel<{var}, 1, 8, 1, 1, 0>" in nm:
+                    g = int(nm.rsplit(" ", 1)[1])
+                    if var not in step or g > step[var][0]:
+                        step[var] = (g, nm, v)
+        if step:
+            st = sum(sum(x[2]) / len(x[2]) for x in step.values())
+            lines.append("== the hot path's step under ncu (one launch per variant, mean launch time)")
+            for var, (g, nm, v) in sorted(step.items()):
+                m = sum(v) / len(v)
+                lines.append(f"   variant {'NA'[int(var)]}: {nm:60s} launches {len(v):4d}  mean {1e6 * m:9.1f} us"
+                             f"  share of step {m / st:6.1%}  GB/s {12 * args.n / m / 1e9:8.1f}")
+            lines.append("")
+        lines.append("== launch list of the whole command (ncu --metrics gpu__time_duration.sum, cold-cache, "
+                     "serialised), by kernel and grid size; includes the untimed legs (ceiling, stats, e2e "
+                     "chunks, NEXT-row measurements)")
         for nm, v in sorted(tot.items(), key=lambda kv: -sum(kv[1])):
             lines.append(f"   {nm:70s} launches {len(v):4d}  mean {1e6 * sum(v) / len(v):9.1f} us  share {sum(v) / all_t:6.1%}")
     txt = os.path.join(ROOT, "profiles", f"ncu_{args.tag}_summary.txt")

@@ -142,7 +142,7 @@ class ClockSampler:
 
 
 # ---- the oracle as a CPU baseline ---------------------------------------------------------
-def cpu_oracle_rate(theta: np.ndarray, seconds: float):
+def cpu_oracle_rate(theta: np.ndarray, seconds: float, workload: str = "C2"):
     """Time the oracle as it stands on all host cores (chunked threads; ctypes releases the
     GIL) on a bounded prefix of the workload, both variants alternately, until `seconds`."""
     from concurrent.futures import ThreadPoolExecutor
@@ -177,9 +177,11 @@ def cpu_oracle_rate(theta: np.ndarray, seconds: float):
     except Exception:
         pass
     return {"value": pairs / dt, "unit": "pairs/s", "cores": cores, "kind": "oracle",
-            "sample": f"first {m} elements of the C2 workload, variants N and A alternately, "
+            "sample": f"first {m} elements of the {workload} workload, variants N and A alternately, "
                       f"{pairs} pairs in {dt:.1f} s on {cores} threads (plain scalar C oracle)",
-            "seconds": dt, "single_thread_pairs_per_s": one, "cpu_model": cpu_model}
+            "seconds": dt, "ns_per_pair": 1e9 * dt / pairs, "GBps": 12 * pairs / dt / 1e9,
+            "single_thread_pairs_per_s": one, "single_thread_ns_per_pair": 1e9 / one,
+            "single_thread_sample": f"first {m1} elements, both variants", "cpu_model": cpu_model}
 
 
 def run_reference(args, rank, world):
@@ -627,7 +629,7 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_oracle_rate(th_h.numpy(), args.cpu_seconds)
+        cpu = cpu_oracle_rate(th_h.numpy(), args.cpu_seconds, W.description.split(":")[0])
 
     if rank == 0:
         line = {

@@ -31,7 +31,8 @@ def run():
     import torch
 
     import inputs
-    n = 1 << 28
+    n = int(os.environ.get("AB_N", 1 << 28))
+    graph = 12 * n < (256 << 20)          # launch-bound sizes: time a graph of 20 launches
     th = torch.from_numpy(inputs.generate(2, 0, n)).cuda()
     s = torch.empty(n, device="cuda")
     c = torch.empty(n, device="cuda")
@@ -49,10 +50,24 @@ def run():
     def timeit(fn, reps=10):
         for _ in range(2):
             fn()
+        if graph:
+            reps = 20
+            cap = torch.cuda.Stream()
+            cap.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cap):
+                for _ in range(reps):
+                    fn(cap.cuda_stream)
+            torch.cuda.current_stream().wait_stream(cap)
+            g.replay()
+            torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        for _ in range(reps):
-            fn()
+        if graph:
+            g.replay()
+        else:
+            for _ in range(reps):
+                fn()
         b.record()
         torch.cuda.synchronize()
         return 12 * n / (a.elapsed_time(b) / reps / 1e3) / 1e9
@@ -61,12 +76,12 @@ def run():
         for name, L in libs.items():
             for cname, (v, inter) in cases.items():
                 if inter:
-                    fn = lambda: L.sincos_pairs(th.data_ptr(), None, None, io.data_ptr(), n, v, st)  # noqa: E731
+                    fn = lambda s_=st: L.sincos_pairs(th.data_ptr(), None, None, io.data_ptr(), n, v, s_)  # noqa: E731
                 else:
-                    fn = lambda: L.sincos_pairs(th.data_ptr(), s.data_ptr(), c.data_ptr(), None, n, v, st)  # noqa: E731
+                    fn = lambda s_=st: L.sincos_pairs(th.data_ptr(), s.data_ptr(), c.data_ptr(), None, n, v, s_)  # noqa: E731
                 res[name][cname].append(timeit(fn))
     for name in libs:
-        print(json.dumps({"lib": name, "GBps": {k: round(statistics.median(v), 1) for k, v in res[name].items()}}),
+        print(json.dumps({"lib": name, "n": n, "graph": graph, "GBps": {k: round(statistics.median(v), 1) for k, v in res[name].items()}}),
               flush=True)
 
 

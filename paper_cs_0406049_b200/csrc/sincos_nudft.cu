@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "sincos_launch.h"
 #include "sincos_math2.cuh"
 #include "sincos_method.cuh"
@@ -184,18 +186,18 @@ size_t nudft_ws_bytes(size_t nf, size_t nt) {
 
 // Packed fp32 for the paper's tables and the specialised method shapes (default on;
 // sincos_set_nudft_packed(0) selects the scalar kernels, bit-identical, for A/B).
-static int g_nudft_packed = 1;
+static std::atomic<int> g_nudft_packed{1};
 int set_nudft_packed(int on) {
     if (on != 0 && on != 1) return -1;
-    g_nudft_packed = on;
+    g_nudft_packed.store(on, std::memory_order_relaxed);
     return 0;
 }
-int get_nudft_packed() { return g_nudft_packed; }
+int get_nudft_packed() { return g_nudft_packed.load(std::memory_order_relaxed); }
 
 template <int V>
 static const void *pick_nudft(bool turns) {
     if constexpr (kPackable<V> && kKPerThread % 2 == 0) {
-        if (g_nudft_packed)
+        if (get_nudft_packed())
             return turns ? reinterpret_cast<const void *>(nudft_partial<V, true, true>)
                          : reinterpret_cast<const void *>(nudft_partial<V, false, true>);
     }

@@ -206,3 +206,25 @@ def test_product_never_touches_the_oracle():
             continue
         src = open(path, errors="ignore").read()
         assert not re.search(r"\bimport\s+oracle|from\s+oracle|sincos_oracle|liboracle", src), path
+
+
+def test_sass_packed_fused_sum_uses_ffma2():
+    """The fused sum's packed kernels (PACK = true, last template flag) run the method and the
+    complex MAC on sm_100a's two-lane fp32 instructions; their scalar twins have none."""
+    sass = _sass()
+    funcs = re.split(r"\n\s*Function : ", sass)
+    packed = scalar = 0
+    for f in funcs:
+        name = f.split("\n", 1)[0]
+        if "nudft_partial" not in name:
+            continue
+        m = re.search(r"nudft_partialILi(\d+)ELb([01])ELb([01])E", name)
+        assert m, name
+        n2 = len(re.findall(r"\bFFMA2\b", f)) + len(re.findall(r"\bFMUL2\b", f))
+        if m.group(3) == "1":
+            packed += 1
+            assert n2 >= 20 and re.search(r"\bFADD2\b", f), (name, n2)
+        else:
+            scalar += 1
+            assert n2 == 0, (name, n2)
+    assert packed >= 8 and scalar >= 8

@@ -515,6 +515,9 @@ def run_ours(args, rank, world, local_rank):
             "kernel": f"sincos_vec_kernel variant {vname[dom]}", "bytes_per_launch": BYTES_PER_PAIR * n,
             "bytes_per_pair": BYTES_PER_PAIR, "peak_source": peak_src,
             "frac_of_theoretical_8180": achieved / 8180.0,
+            # B200_PROFILING.md: 7.7 TB/s is the HGX B200 HBM3e spec figure (8 TB/s DGX); 8180 is
+            # the 3996 MHz memory clock x 2 x 8192 bits
+            "frac_of_spec_7700": achieved / 7700.0,
             "per_variant_GBps": {vname[v]: BYTES_PER_PAIR * n / (avg[v] / 1e3) / 1e9 for v in variants},
             "per_variant_ms": {vname[v]: avg[v] for v in variants},
             "per_variant_ms_median_min": {vname[v]: [statistics.median(per_kernel[v]), min(per_kernel[v])]

@@ -24,17 +24,17 @@ from paper_cs_0406049_b200.sharding import WORKLOADS  # noqa: E402
 
 
 def time_kernel(th, outs, v, reps):
+    """Median per-launch time of `reps` back-to-back launches (events between consecutive
+    launches on the stream, no host sync in between -- as bench.py times its steps)."""
     for _ in range(3):
         sp.sincos_pairs(th, variant=v, **outs)
-    ts = []
-    for _ in range(reps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+    ev[0].record()
+    for k in range(reps):
         sp.sincos_pairs(th, variant=v, **outs)
-        b.record()
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    return statistics.median(ts)
+        ev[k + 1].record()
+    torch.cuda.synchronize()
+    return statistics.median(ev[k].elapsed_time(ev[k + 1]) for k in range(reps))
 
 
 def main():

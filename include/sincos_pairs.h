@@ -93,6 +93,8 @@ SINCOS_API sincos_status_t sincos_pairs(const float *theta_dev, float *sin_dev, 
  * over three internal streams (created once per device), so the copy engines
  * run both directions while the kernel computes.  Synchronous: returns when
  * the outputs are in host memory.  Ordered after prior work on `stream`.
+ * Concurrent calls from several host threads on one device are serialised
+ * (the internal streams are shared); calls on different devices run in parallel.
  *
  *   dev_ws, ws_bytes  caller-owned device workspace of the current device
  *                     (>= sincos_host_workspace_min_bytes(); more = larger chunks).

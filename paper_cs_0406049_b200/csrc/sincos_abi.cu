@@ -165,6 +165,9 @@ struct DevStreams {
     cudaStream_t s[kSlots];
     cudaEvent_t done[kSlots];
     cudaEvent_t start;
+    // one host-path call at a time per device: the slot streams and events are shared, and an
+    // interleaved cudaEventRecord(start) from another thread would re-target this call's waits
+    std::mutex busy;
 };
 std::mutex g_dev_mu;
 DevStreams g_dev[kMaxDev];
@@ -418,6 +421,8 @@ sincos_status_t sincos_pairs_host(const float *theta_host, float *sin_host, floa
     if (e != cudaSuccess) return cuda_fail(e);
     DevStreams *ds = nullptr;
     if ((e = dev_streams(dev, &ds)) != cudaSuccess) return cuda_fail(e);
+
+    std::lock_guard<std::mutex> call_lock(ds->busy);   // reentrancy (header: thread-safe)
 
     // chunk elements per slot, a multiple of 64 so every slot buffer stays 256-B aligned
     size_t chunk = (ws_bytes / (kSlots * 12)) & ~size_t(63);

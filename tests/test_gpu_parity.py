@@ -388,3 +388,44 @@ def test_launches_are_counted():
 def test_rejects_cpu_tensors():
     with pytest.raises(ValueError):
         sp.sincos_pairs(torch.zeros(8), torch.zeros(8), torch.zeros(8))
+
+
+def test_concurrent_host_threads():
+    """Thread-safe and reentrant (header): several host threads call the device path
+    on their own streams and the host-buffer path at the same time (ctypes drops the GIL, so
+    the calls overlap); every result equals the oracle."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    n = (1 << 20) + 13
+    cases = [(seed, variant, host) for seed in (1, 2, 3) for variant in VARIANTS for host in (False, True)]
+    ths = {seed: inputs.generate(seed, 0, n) for seed in (1, 2, 3)}
+
+    def work(case):
+        seed, variant, host = case
+        th = ths[seed]
+        outs = []
+        for _ in range(3):
+            if host:
+                th_h = torch.from_numpy(th).pin_memory()
+                s_h = torch.empty(n, dtype=torch.float32).pin_memory()
+                c_h = torch.empty(n, dtype=torch.float32).pin_memory()
+                ws = torch.empty(sp.host_workspace_min_bytes(), dtype=torch.uint8, device="cuda")
+                sp.sincos_pairs_host(th_h, s_h, c_h, variant=variant, workspace=ws)
+                outs.append((s_h.numpy().copy(), c_h.numpy().copy()))
+            else:
+                st = torch.cuda.Stream()
+                with torch.cuda.stream(st):
+                    t = torch.from_numpy(th).cuda(non_blocking=False)
+                    s, c = torch.empty_like(t), torch.empty_like(t)
+                    sp.sincos_pairs(t, s, c, variant=variant, stream=st)
+                st.synchronize()
+                outs.append((s.cpu().numpy(), c.cpu().numpy()))
+        return outs
+
+    with ThreadPoolExecutor(len(cases)) as ex:
+        results = list(ex.map(work, cases))
+    want = {(seed, v): oracle_threaded(ths[seed], v) for seed in (1, 2, 3) for v in VARIANTS}
+    for (seed, variant, host), outs in zip(cases, results):
+        os_, oc = want[(seed, variant)]
+        for s, c in outs:
+            assert_parity(s, c, os_, oc, f"thread seed={seed} variant={variant} host={host}")

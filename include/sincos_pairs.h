@@ -293,6 +293,17 @@ SINCOS_API int sincos_set_nudft_packed(int on);
 SINCOS_API sincos_status_t sincos_null_4in8out(const float *theta_dev, float *sin_dev, float *cos_dev,
                                     float *inter_dev, size_t n, void *stream);
 
+/* Test hook: the packed-fp32 form of the method (sm_100a FFMA2/FMUL2/FADD2, used by the
+ * fused sum) against the scalar form, for EVERY one of the 2^32 fp32 inputs, in radians and
+ * in turns.  method == NULL: the paper's table of `variant`; else a specialised method shape
+ * (n_ss/n_cc/doublings 4/3/2 or 3/2/1, fix 0 or 1; variant ignored).  Asynchronous on
+ * `stream`: *mismatch_dev (device, 8-B aligned) is zeroed, then receives the number of
+ * differing output components (NaN equals NaN; otherwise bit patterns).  0 is expected.
+ * variant == -1 (method NULL) is the negative control: packed method 1 against scalar
+ * method 2, which must differ wherever their pairs do (proves the check can fail). */
+SINCOS_API sincos_status_t sincos_debug_packed_check(int variant, const sincos_method_t *method,
+                                                     unsigned long long *mismatch_dev, void *stream);
+
 /* Test hook: the kernel's reciprocal sequence alone, out[i] = RN(1/d[i]). */
 SINCOS_API sincos_status_t sincos_debug_reciprocal(const float *d_dev, float *out_dev, size_t n,
                                         void *stream);

@@ -94,6 +94,7 @@ _SIGS = {
     "sincos_error_stats": (_I, [_P, _P, _P, _P, _S, _P, _P, _P]),
     "sincos_set_launch_config": (_I, [_I, _I, _I, _I, _I]),
     "sincos_set_nudft_packed": (_I, [_I]),
+    "sincos_debug_packed_check": (_I, [_I, _P, _P, _P]),
     "sincos_get_launch_config": (None, [ctypes.POINTER(_I)] * 5),
     "sincos_null_4in8out": (_I, [_P, _P, _P, _P, _S, _P]),
     "sincos_debug_reciprocal": (_I, [_P, _P, _S, _P]),
@@ -428,6 +429,17 @@ def null_4in8out(theta, sin_out=None, cos_out=None, interleaved_out=None, stream
 def debug_reciprocal(d, out, stream=None):
     _check(lib().sincos_debug_reciprocal(_ptr(d, "d"), _ptr(out, "out"), d.numel(), _stream(stream, d.device)),
            "sincos_debug_reciprocal")
+
+
+def debug_packed_check(variant=NORMALIZED, method=None, stream=None) -> int:
+    """Test hook: mismatching output components of the packed-fp32 method against the scalar
+    method over all 2^32 fp32 inputs (radians and turns).  Synchronous; 0 expected."""
+    import torch
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _check(lib().sincos_debug_packed_check(-1 if variant == -1 else _variant(variant), ctypes.byref(method) if method is not None else None,
+                                           cnt.data_ptr(), _stream(stream, cnt.device)),
+           "sincos_debug_packed_check")
+    return int(cnt.item())
 
 
 def launch_count() -> int:

@@ -547,6 +547,34 @@ void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *vec, int *u
     if (unroll) *unroll = g_unroll.load();
 }
 
+sincos_status_t sincos_debug_packed_check(int variant, const sincos_method_t *method,
+                                          unsigned long long *mismatch_dev, void *stream) {
+    if (mismatch_dev == nullptr || !aligned(mismatch_dev, 8)) return SINCOS_ERR_INVALID_ARGUMENT;
+    int shape = -1, fix = 0;
+    MethodParams mp{};
+    if (method != nullptr) {
+        if (!method_ok(method)) return SINCOS_ERR_INVALID_ARGUMENT;
+        shape = method_spec(method);
+        fix = method->fix;
+        if (shape < 0 || (fix != 0 && fix != 1)) return SINCOS_ERR_INVALID_ARGUMENT;
+        mp = make_params(method->ss, method->n_ss, method->cc, method->n_cc, method->doublings);
+    } else if (variant == -1) {
+        shape = -2;                      // negative control
+    } else if (variant != SINCOS_NORMALIZED && variant != SINCOS_RENORMALIZED) {
+        return SINCOS_ERR_INVALID_ARGUMENT;
+    }
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if ((e = cudaMemsetAsync(mismatch_dev, 0, sizeof(unsigned long long), s)) != cudaSuccess) return cuda_fail(e);
+    e = launch_packcheck(variant, shape, fix, method ? &mp : nullptr, static_cast<unsigned>(sm_count(dev)) * 16,
+                         mismatch_dev, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SINCOS_OK;
+}
+
 sincos_status_t sincos_debug_reciprocal(const float *d_dev, float *out_dev, size_t n, void *stream) {
     if (n == 0) return SINCOS_OK;
     if (d_dev == nullptr || out_dev == nullptr) return SINCOS_ERR_INVALID_ARGUMENT;

@@ -33,6 +33,10 @@ struct MethodParams;
 cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, const float *t, const float *a,
                          size_t nt, float *out, void *ws, cudaStream_t stream, const MethodParams *method = nullptr,
                          int method_nt = 4, int method_fix = 0, int method_spec = -1);
+// Test hook (sincos_packcheck.cu): packed vs scalar method over all 2^32 inputs; shape -1 = the
+// paper's table of `variant`, 0 / 1 = method shapes (4,3,2) / (3,2,1) with fix 0/1.
+cudaError_t launch_packcheck(int variant, int shape, int fix, const MethodParams *m, unsigned grid,
+                             unsigned long long *mismatch_dev, cudaStream_t stream);
 // Packed fp32 (FFMA2) kernels for the fused sum: 1 = on (default), 0 = scalar; -1 on bad value.
 int set_nudft_packed(int on);
 int get_nudft_packed();

@@ -216,3 +216,26 @@ def test_set_nudft_packed_rejects_bad_values():
     assert sp.lib().sincos_set_nudft_packed(2) == -1
     prev = sp.set_nudft_packed(True)
     assert sp.set_nudft_packed(prev) is True
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_packed_method_equals_scalar_on_all_fp32_inputs(variant):
+    """Exhaustive form of the packed/scalar identity: the two-lane method (FFMA2/FMUL2/FADD2)
+    equals the scalar method bit for bit on every one of the 2^32 fp32 inputs, in radians
+    (scale by 1/2pi first) and in turns -- the phases the fused sum feeds it are a subset."""
+    assert sp.debug_packed_check(variant) == 0
+
+
+@pytest.mark.parametrize("spec", [(2, 4, 3, 0), (2, 4, 3, 1), (1, 3, 2, 0), (1, 3, 2, 1)])
+def test_packed_method_shapes_equal_scalar_on_all_fp32_inputs(spec):
+    from paper_cs_0406049_b200 import coeff_fit as cf
+    n, ds, dc, fix = spec
+    ss, cc = cf.fit_angle(n, ds, dc).fp32()
+    assert sp.debug_packed_check(method=sp.make_method(list(ss), list(cc), n, fix)) == 0
+
+
+def test_packed_check_negative_control_fails():
+    """The exhaustive check can fail: packed method 1 against scalar method 2 differs wherever
+    the two tables give different pairs (every q not tiny and not 0: roughly the patterns with
+    1e-4 < |x| < 2^23 turns, ~15% of all 2^32, x 2 units x 2 components)."""
+    assert sp.debug_packed_check(-1) > 2 ** 30

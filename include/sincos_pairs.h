@@ -281,6 +281,12 @@ SINCOS_API int sincos_set_launch_config(int threads, int blocks_per_sm, int vec,
 SINCOS_API void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *vec, int *unroll,
                                          int *prefetch);
 
+/* Unshared alignment (theta and the outputs at different offsets mod 16 B): 1 = keep the
+ * outputs' 128-bit stores and re-align theta in registers with warp shuffles (the default),
+ * 0 = one element per thread.  Identical results.  Process-global; returns the previous
+ * setting, or -1 for a value other than 0/1. */
+SINCOS_API int sincos_set_realign(int on);
+
 /* Fused-sum kernel form (bench / tests): 1 = packed fp32 (sm_100a FFMA2/FMUL2/FADD2,
  * two frequencies per instruction; the default), 0 = scalar fp32.  Both are
  * bit-identical (each packed lane rounds as the scalar instruction does); applies to

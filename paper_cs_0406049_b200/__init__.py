@@ -15,7 +15,7 @@ import os
 
 __all__ = [
     "NORMALIZED", "RENORMALIZED", "SincosError", "lib", "sincos", "sincos_pairs", "sincos_pairs_host",
-    "shard_range", "error_stats", "set_launch_config", "get_launch_config", "set_nudft_packed", "null_4in8out",
+    "shard_range", "error_stats", "set_launch_config", "get_launch_config", "set_nudft_packed", "set_realign", "null_4in8out",
     "debug_reciprocal", "launch_count", "host_workspace_min_bytes", "library_path", "sincos_pairs_sharded",
 ]
 
@@ -94,6 +94,7 @@ _SIGS = {
     "sincos_error_stats": (_I, [_P, _P, _P, _P, _S, _P, _P, _P]),
     "sincos_set_launch_config": (_I, [_I, _I, _I, _I, _I]),
     "sincos_set_nudft_packed": (_I, [_I]),
+    "sincos_set_realign": (_I, [_I]),
     "sincos_debug_packed_check": (_I, [_I, _P, _P, _P]),
     "sincos_get_launch_config": (None, [ctypes.POINTER(_I)] * 5),
     "sincos_null_4in8out": (_I, [_P, _P, _P, _P, _S, _P]),
@@ -404,6 +405,14 @@ def set_launch_config(threads=None, blocks_per_sm=None, vec=None, unroll=None, p
     if lib().sincos_set_launch_config(cfg["threads"], cfg["blocks_per_sm"], cfg["vec"], cfg["unroll"],
                                       cfg["prefetch"]) != 0:
         raise ValueError(f"unsupported launch config {cfg}")
+
+
+def set_realign(on: bool) -> bool:
+    """Unshared-alignment path: register re-alignment (True, default) or one element per thread."""
+    prev = lib().sincos_set_realign(1 if on else 0)
+    if prev < 0:
+        raise ValueError(on)
+    return bool(prev)
 
 
 def set_nudft_packed(on: bool) -> bool:

@@ -28,6 +28,7 @@ std::atomic<int> g_blocks_per_sm{0};
 std::atomic<int> g_vec{8};
 std::atomic<int> g_unroll{1};
 std::atomic<int> g_prefetch{0};
+std::atomic<int> g_shift{1};          // KB3b re-aligning path for unshared alignment (1 = on)
 
 constexpr int kMaxDev = 64;
 std::atomic<int> g_sm_count[kMaxDev];
@@ -130,7 +131,35 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
         }
     }
 
-    if (w == 0) {
+    // Re-aligning kernel (KB3b): split outputs without a shared alignment but whose sin and cos
+    // share one mod 16 B; interleaved outputs without the 256-bit path but 8-B aligned (its
+    // 256-bit store per four pairs beats the 128-bit path's half-sector stores).  Otherwise,
+    // without a shared alignment, one element per thread (KB3).
+    size_t hs = SIZE_MAX;
+    if (g_shift.load(std::memory_order_relaxed)) {
+        if (inter) {
+            // (w == 4 with the default vec 8 only: a configured vec 4 keeps its 128-bit kernel)
+            if ((w == 0 || (w == 4 && g_vec.load(std::memory_order_relaxed) == 8)) && aligned(io, 8))
+                hs = ((32 - (reinterpret_cast<uintptr_t>(io) & 31)) & 31) / 8;
+        } else if (w == 0 && ((reinterpret_cast<uintptr_t>(so) ^ reinterpret_cast<uintptr_t>(co)) & 15) == 0) {
+            hs = ((16 - (reinterpret_cast<uintptr_t>(so) & 15)) & 15) / 4;
+        }
+    }
+    if (hs != SIZE_MAX) {
+        const int k = static_cast<int>(((reinterpret_cast<uintptr_t>(theta) + 4 * hs) & 15) / 4);   // 0..3
+        size_t hb = hs >= static_cast<size_t>(k) ? hs : hs + 4;    // aligned theta base >= theta
+        if (hb > n) hb = n;
+        // k > 0: every thread's second aligned vector must lie inside theta:
+        // (hb - k) + 4 nvec + 3 <= n - 1
+        size_t nvec = (n - hb) / 4;
+        if (k > 0) nvec = n + k >= hb + 4 ? (n + k - hb - 4) / 4 : 0;
+        size_t need = (nvec + threads - 1) / threads;
+        if (need < 1) need = 1;
+        if (cfg_bps > 0 && need > static_cast<size_t>(sms) * cfg_bps) need = static_cast<size_t>(sms) * cfg_bps;
+        if (need > 0x7FFFFFFFu) need = 0x7FFFFFFFu;
+        e = launch_shift(variant, inter, k, static_cast<unsigned>(need), threads, theta, so, co, io, hb, nvec, n,
+                         stream);
+    } else if (w == 0) {
         const unsigned grid = static_cast<unsigned>(
             (n + threads - 1) / threads < static_cast<size_t>(sms) * 8 ? (n + threads - 1) / threads : sms * 8);
         e = launch_scalar(variant, inter, grid, threads, theta, so, co, io, n, stream);
@@ -518,6 +547,11 @@ sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
     if (e != cudaSuccess) return cuda_fail(e);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SINCOS_OK;
+}
+
+int sincos_set_realign(int on) {
+    if (on != 0 && on != 1) return -1;
+    return g_shift.exchange(on, std::memory_order_relaxed);
 }
 
 int sincos_set_nudft_packed(int on) {

@@ -215,6 +215,65 @@ __global__ void __launch_bounds__(512) sincos_vec_kernel(const float *theta, flo
     }
 }
 
+// KB3b: theta and the outputs do not share an alignment.  The outputs keep whole-sector
+// stores -- split: 128-bit stores to sin[] and cos[] (a warp instruction covers whole 32-B
+// sectors); interleaved: ONE 256-bit store of the four {cos, sin} pairs (two 128-bit stores
+// would each write half of every sector) -- and theta, K = 0..3 floats past a 16-B boundary
+// there, is read as ALIGNED float4 vectors and re-aligned in registers: lane l holds a =
+// theta_al[4v .. 4v+3] and takes the next vector b from lane l+1 with warp shuffles (the
+// warp's last lane, or a lane whose neighbour is past the end, loads b itself), then its four
+// angles are a[K..3] ++ b[0..K-1] -- a static register selection, K being a template
+// parameter (K = 0: no shuffle).  Every loop trip is warp-uniform (all lanes shuffle).
+// Elements [0, head) and [head + 4 nvec, n) are done one per thread; the host sizes nvec so
+// that every b load stays inside theta.  Same numerics as every other path.
+template <int V, bool INTER, int K>
+__global__ void __launch_bounds__(512) sincos_shift_kernel(const float *theta, float *so, float *co, float *io,
+                                                           size_t head, size_t nvec, size_t n) {
+    const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t tail0 = head + nvec * 4;
+    if (tid < head) emit_scalar<V, INTER>(theta, tid, so, co, io);
+    if (tid < n - tail0) emit_scalar<V, INTER>(theta, tail0 + tid, so, co, io);
+
+    const float *tal = theta + head - K;           // 16-B aligned (host guarantees head >= K)
+    const unsigned lane = threadIdx.x & 31u;
+    for (size_t w0 = tid - lane; w0 < nvec; w0 += nthr) {   // warp-uniform trips
+        const size_t v = w0 + lane;
+        const bool act = v < nvec;
+        float a[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        float x[4];
+        if constexpr (K == 0) {
+            if (act) Mem<4, true>::load(a, tal + 4 * v);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[j] = a[j];
+        } else {
+            // the lanes without a neighbour issue their own second load together with the first,
+            // so the warp waits for one memory round trip, not two
+            const bool own = act && (lane == 31u || v + 1 >= nvec);
+            float bo[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            if (act) Mem<4, true>::load(a, tal + 4 * v);
+            if (own) Mem<4, true>::load(bo, tal + 4 * v + 4);
+            float b[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = __shfl_down_sync(0xFFFFFFFFu, a[j], 1);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = own ? bo[j] : b[j];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[j] = j + K < 4 ? a[j + K] : b[j + K - 4];
+        }
+        if (!act) continue;
+        const size_t e0 = head + 4 * v;
+        if constexpr (INTER) {
+            float cs[8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) op<V>(x[j], cs[2 * j + 1], cs[2 * j]);
+            store8(io + 2 * e0, cs);
+        } else {
+            emit<V, false, 4>(x, e0, so, co, io);
+        }
+    }
+}
+
 // KB3: any alignment.
 template <int V, bool INTER>
 __global__ void __launch_bounds__(512) sincos_scalar_kernel(const float *theta, float *so, float *co, float *io,
@@ -287,6 +346,28 @@ cudaError_t launch_scalar(int variant, bool inter, unsigned grid, unsigned threa
                           float *co, float *io, size_t n, cudaStream_t stream) {
     ScalarFn fn = scalar_kernel(variant, inter);
     void *args[] = {&theta, &so, &co, &io, &n};
+    return cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(threads), args, 0, stream);
+}
+
+template <int V, bool INTER>
+static VecFn pick_shift(int k) {
+    switch (k) {
+    case 0: return sincos_shift_kernel<V, INTER, 0>;
+    case 1: return sincos_shift_kernel<V, INTER, 1>;
+    case 2: return sincos_shift_kernel<V, INTER, 2>;
+    default: return sincos_shift_kernel<V, INTER, 3>;
+    }
+}
+
+cudaError_t launch_shift(int variant, bool inter, int k, unsigned grid, unsigned threads, const float *theta,
+                         float *so, float *co, float *io, size_t head, size_t nvec, size_t n, cudaStream_t stream) {
+    VecFn fn;
+    switch (variant) {
+    case kNormalized: fn = inter ? pick_shift<kNormalized, true>(k) : pick_shift<kNormalized, false>(k); break;
+    case kRenormalized: fn = inter ? pick_shift<kRenormalized, true>(k) : pick_shift<kRenormalized, false>(k); break;
+    default: fn = inter ? pick_shift<kNull, true>(k) : pick_shift<kNull, false>(k); break;
+    }
+    void *args[] = {&theta, &so, &co, &io, &head, &nvec, &n};
     return cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(threads), args, 0, stream);
 }
 

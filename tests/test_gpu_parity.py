@@ -429,3 +429,76 @@ def test_concurrent_host_threads():
         os_, oc = want[(seed, variant)]
         for s, c in outs:
             assert_parity(s, c, os_, oc, f"thread seed={seed} variant={variant} host={host}")
+
+
+# ---- unshared alignment: register re-alignment (KB3b) and one element per thread (KB3) ----
+
+@pytest.mark.parametrize("bps", [0, 1])
+def test_realign_path(bps):
+    """theta at every offset mod 4 floats against outputs at every offset: where the outputs
+    can take 128-bit stores the re-aligning kernel runs (k = 1, 2, 3 with head peeling when the
+    aligned theta base would precede theta); lengths around the vector/tail boundaries and
+    large enough for many warps; bps = 1 forces many warp-uniform grid-stride trips."""
+    rng = np.random.default_rng(21)
+    N = 200_003
+    base = rng.uniform(-3000, 3000, N + 64).astype(np.float32)
+    ref = {v: oracle.sincos(base, v) for v in VARIANTS}
+    big_t = torch.from_numpy(base).cuda()
+    big_s = torch.empty(N + 64, dtype=torch.float32, device="cuda")
+    big_c = torch.empty(N + 64, dtype=torch.float32, device="cuda")
+    big_i = torch.empty(2 * N + 64, dtype=torch.float32, device="cuda")
+    sp.set_launch_config(blocks_per_sm=bps)
+    try:
+        for variant in VARIANTS:
+            rs, rc = ref[variant]
+            for n in list(range(0, 24)) + [127, 128, 129, 1000, 4097, N]:
+                for ot in (0, 1, 2, 3, 5):
+                    for oo in (0, 1, 2, 3, 6):
+                        if (ot - oo) % 4 == 0 and n > 24:
+                            continue          # shared alignment: the vector path, tested above
+                        t = big_t[ot:ot + n]
+                        s = big_s[oo:oo + n]
+                        c = big_c[oo + 8:oo + 8 + n] if oo + 8 + n <= N + 64 else big_c[oo:oo + n]
+                        sp.sincos_pairs(t, s, c, variant=variant)
+                        io = big_i[2 * oo:2 * oo + 2 * n]
+                        sp.sincos_pairs(t, interleaved_out=io, variant=variant)
+                        torch.cuda.synchronize()
+                        assert_parity(s.cpu().numpy(), c.cpu().numpy(), rs[ot:ot + n], rc[ot:ot + n],
+                                      f"realign n={n} off={ot},{oo} bps={bps}")
+                        iv = io.cpu().numpy()
+                        assert_parity(iv[1::2], iv[0::2], rs[ot:ot + n], rc[ot:ot + n],
+                                      f"realign inter n={n} off={ot},{oo} bps={bps}")
+    finally:
+        sp.set_launch_config()
+
+
+def test_scalar_path_unshared_outputs():
+    """The one-element-per-thread kernel: sin and cos at different offsets mod 16 B, and an
+    interleaved output only 4-B aligned (odd float offset); with re-alignment off, every
+    unshared case goes there too."""
+    rng = np.random.default_rng(22)
+    n = 70_001
+    base = rng.uniform(-100, 100, n + 16).astype(np.float32)
+    big_t = torch.from_numpy(base).cuda()
+    big_s = torch.empty(n + 16, dtype=torch.float32, device="cuda")
+    big_c = torch.empty(n + 16, dtype=torch.float32, device="cuda")
+    big_i = torch.empty(2 * n + 16, dtype=torch.float32, device="cuda")
+    for variant in VARIANTS:
+        rs, rc = oracle.sincos(base, variant)
+        for realign in (True, False):
+            prev = sp.set_realign(realign)
+            try:
+                for ot, os_, oc_, oi in ((0, 1, 2, 1), (1, 0, 3, 3), (2, 2, 2, 2), (3, 0, 0, 5)):
+                    t = big_t[ot:ot + n]
+                    s, c = big_s[os_:os_ + n], big_c[oc_:oc_ + n]
+                    io = big_i[oi:oi + 2 * n]
+                    sp.sincos_pairs(t, s, c, variant=variant)
+                    sp.sincos_pairs(t, interleaved_out=io, variant=variant)
+                    torch.cuda.synchronize()
+                    assert_parity(s.cpu().numpy(), c.cpu().numpy(), rs[ot:ot + n], rc[ot:ot + n],
+                                  f"scalar off={ot},{os_},{oc_} realign={realign}")
+                    iv = io.cpu().numpy()
+                    assert_parity(iv[1::2], iv[0::2], rs[ot:ot + n], rc[ot:ot + n],
+                                  f"scalar inter off={ot},{oi} realign={realign}")
+            finally:
+                sp.set_realign(prev)

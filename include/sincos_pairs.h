@@ -168,9 +168,12 @@ SINCOS_API sincos_status_t sincos_pairs_method(const float *theta_dev, float *si
  *                              and skips the 1/2pi scaling and its rounding.
  * Outputs as in sincos_pairs (split sin/cos of nf*nt floats each, or interleaved
  * {cos, sin}).  Only 8 B per pair are written (no theta array is read); f and t
- * must not overlap the outputs.  The fast path needs nt % 8 == 0 and 32-B aligned
- * t and outputs; any other shape/alignment runs a scalar path with identical
- * numerics.  Returns as sincos_pairs; nf*nt == 0 is a no-op.
+ * must not overlap the outputs.  Paths, identical numerics: nt % 8 == 0 with 32-B
+ * aligned t and outputs -- 256-bit vectors per row; any other nt / alignment with
+ * outputs that can take 256-bit stores (split: sin and cos at the same offset mod
+ * 32 B; interleaved: 8-B aligned) -- the flat path, 8 consecutive pairs of the
+ * row-major grid per thread; otherwise one pair per thread.  Returns as
+ * sincos_pairs; nf*nt == 0 is a no-op.
  */
 typedef enum { SINCOS_RADIANS = 0, SINCOS_TURNS = 1 } sincos_units_t;
 SINCOS_API sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_dev, size_t nt,
@@ -283,8 +286,9 @@ SINCOS_API void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *
 
 /* Unshared alignment (theta and the outputs at different offsets mod 16 B): 1 = keep the
  * outputs' 128-bit stores and re-align theta in registers with warp shuffles (the default),
- * 0 = one element per thread.  Identical results.  Process-global; returns the previous
- * setting, or -1 for a value other than 0/1. */
+ * 0 = one element per thread.  Identical results.  Also switches sincos_phase_grid's
+ * flat path for rows that are not whole 256-bit vectors.  Process-global; returns the
+ * previous setting, or -1 for a value other than 0/1. */
 SINCOS_API int sincos_set_realign(int on);
 
 /* Fused-sum kernel form (bench / tests): 1 = packed fp32 (sm_100a FFMA2/FMUL2/FADD2,

@@ -29,6 +29,7 @@ std::atomic<int> g_vec{8};
 std::atomic<int> g_unroll{1};
 std::atomic<int> g_prefetch{0};
 std::atomic<int> g_shift{1};          // KB3b re-aligning path for unshared alignment (1 = on)
+std::atomic<int> g_phase_flat{1};     // NEXT(1) flat path for rows that are not whole 256-bit vectors
 
 constexpr int kMaxDev = 64;
 std::atomic<int> g_sm_count[kMaxDev];
@@ -261,8 +262,29 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
     }
     const bool vec = nt % 8 == 0 && aligned(t_dev, 32) &&
                      (split ? aligned(sin_dev, 32) && aligned(cos_dev, 32) : aligned(inter_dev, 32));
-    cudaError_t e = launch_phase_grid(variant, inter, units == SINCOS_TURNS, vec, f_dev, nf, t_dev, nt, sin_dev,
-                                      cos_dev, inter_dev, static_cast<cudaStream_t>(stream));
+    cudaError_t e;
+    // any other shape: the flat path when the outputs can take 256-bit stores from some pair on
+    // (split: sin and cos share their alignment mod 32 B; interleaved: 8-B aligned) and the
+    // fp64 quotient estimate of a pair index is exact enough (n < 2^52); else one per thread
+    const uintptr_t so_a = reinterpret_cast<uintptr_t>(sin_dev), co_a = reinterpret_cast<uintptr_t>(cos_dev),
+                    io_a = reinterpret_cast<uintptr_t>(inter_dev);
+    const bool flat = !vec && g_phase_flat.load(std::memory_order_relaxed) && n < (size_t(1) << 52) &&
+                      (split ? ((so_a ^ co_a) & 31) == 0 : aligned(inter_dev, 8));
+    if (flat) {
+        size_t head = split ? ((32 - (so_a & 31)) & 31) / 4 : ((32 - (io_a & 31)) & 31) / 8;
+        if (head > n) head = n;
+        const size_t nvec = (n - head) / 8;
+        int dev = 0;
+        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return cuda_fail(e);
+        size_t grid = (nvec + 127) / 128;
+        if (grid < 1) grid = 1;
+        if (grid > 0x7FFFFFFFu) grid = 0x7FFFFFFFu;
+        e = launch_phase_flat(variant, inter, units == SINCOS_TURNS, f_dev, nf, t_dev, nt, sin_dev, cos_dev,
+                              inter_dev, head, nvec, static_cast<unsigned>(grid), static_cast<cudaStream_t>(stream));
+    } else {
+        e = launch_phase_grid(variant, inter, units == SINCOS_TURNS, vec, f_dev, nf, t_dev, nt, sin_dev, cos_dev,
+                              inter_dev, static_cast<cudaStream_t>(stream));
+    }
     if (e != cudaSuccess) return cuda_fail(e);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SINCOS_OK;
@@ -551,7 +573,9 @@ sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
 
 int sincos_set_realign(int on) {
     if (on != 0 && on != 1) return -1;
-    return g_shift.exchange(on, std::memory_order_relaxed);
+    const int prev = g_shift.exchange(on, std::memory_order_relaxed);
+    g_phase_flat.store(on, std::memory_order_relaxed);
+    return prev;
 }
 
 int sincos_set_nudft_packed(int on) {

@@ -27,6 +27,11 @@ cudaError_t launch_tma(int variant, bool inter, unsigned grid, const float *thet
 // NEXT(1) phase grid (sincos_phase.cu); vec = 256-bit path (nt % 8 == 0, 32-B aligned t/outputs).
 cudaError_t launch_phase_grid(int variant, bool inter, bool turns, bool vec, const float *f, size_t nf,
                               const float *t, size_t nt, float *so, float *co, float *io, cudaStream_t stream);
+// NEXT(1) flat path for any nt: pairs [head, head + 8 nvec) as 256-bit stores (outputs 32-B
+// aligned at `head`), the rest one per thread; grid-stride over `grid` blocks.
+cudaError_t launch_phase_flat(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
+                              size_t nt, float *so, float *co, float *io, size_t head, size_t nvec,
+                              unsigned grid, cudaStream_t stream);
 // NEXT(2) fused non-uniform Fourier sum (sincos_nudft.cu); variant 3/4 = comparison sincosf.
 size_t nudft_chunk(size_t nt);
 size_t nudft_ws_bytes(size_t nf, size_t nt);

@@ -92,6 +92,125 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_scalar(const float *
     }
 }
 
+// Flat path (any nt, outputs with whole-sector stores): the nf x nt grid as one row-major
+// array of n pairs; thread v owns pairs [head + 8v, head + 8v + 8) and writes them with 256-bit
+// streaming stores, like the hot path.  (i, j) of its first pair come from one fp64 quotient
+// estimate corrected to the exact integer divmod; the next seven advance j and wrap rows (any
+// nt >= 1, rows shorter than 8 included).  f and t are read through the read-only cache.
+// Pairs [0, head) and [head + 8 nvec, n) go one per thread.
+__device__ __forceinline__ void divmod_nt(size_t e, size_t nt, double inv_nt, size_t &i, size_t &j) {
+    size_t q = static_cast<size_t>(static_cast<double>(e) * inv_nt);
+    // the estimate is within a few units of e / nt for e < 2^53: correct it exactly
+    while (q * nt > e) --q;
+    while ((q + 1) * nt <= e) ++q;
+    i = q;
+    j = e - q * nt;
+}
+
+template <int V, bool INTER, bool TURNS>
+__device__ __forceinline__ void phase_one(const float *__restrict__ f, const float *__restrict__ t, size_t nt,
+                                          double inv_nt, size_t e, float *so, float *co, float *io) {
+    size_t i, j;
+    divmod_nt(e, nt, inv_nt, i, j);
+    float s, c;
+    phase_pair<V, TURNS>(__ldg(f + i), __ldg(t + j), s, c);
+    if constexpr (INTER) {
+        io[2 * e] = c;
+        io[2 * e + 1] = s;
+    } else {
+        so[e] = s;
+        co[e] = c;
+    }
+}
+
+template <int V, bool INTER, bool TURNS>
+__global__ void __launch_bounds__(kPhaseThreads) phase_grid_flat(const float *__restrict__ f,
+                                                                const float *__restrict__ t, size_t nf,
+                                                                size_t nt, float *so, float *co, float *io,
+                                                                size_t head, size_t nvec, size_t n,
+                                                                double inv_nt) {
+    const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t tail0 = head + 8 * nvec;
+    if (tid < head) phase_one<V, INTER, TURNS>(f, t, nt, inv_nt, tid, so, co, io);
+    if (tid < n - tail0) phase_one<V, INTER, TURNS>(f, t, nt, inv_nt, tail0 + tid, so, co, io);
+    for (size_t v = tid; v < nvec; v += nthr) {
+        const size_t e0 = head + 8 * v;
+        size_t i, j;
+        divmod_nt(e0, nt, inv_nt, i, j);
+        float sv[8], cv[8];
+        if (j + 8 <= nt) {
+            // the common case: the eight pairs lie in one row -- one f, eight t loads at
+            // immediate offsets from one pointer (no per-pair index arithmetic), all in flight
+            const float fi = __ldg(f + i);
+            const float *tp = t + j;
+            float tv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) tv[k] = __ldg(tp + k);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fi, tv[k], sv[k], cv[k]);
+        } else if (nt >= 8) {
+            // one row boundary inside the vector: rows i and i+1, branch-free per pair
+            const float f0 = __ldg(f + i), f1 = __ldg(f + i + 1);   // row i+1 exists: reached
+            const size_t kw = nt - j;                                // first pair of row i+1
+            float tv[8], fv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const bool next = static_cast<size_t>(k) >= kw;
+                tv[k] = __ldg(t + (next ? k - kw : j + k));
+                fv[k] = next ? f1 : f0;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fv[k], tv[k], sv[k], cv[k]);
+        } else {
+            // rows shorter than a vector: walk the pairs
+            float fi = __ldg(f + i);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                phase_pair<V, TURNS>(fi, __ldg(t + j), sv[k], cv[k]);
+                if (++j == nt && k < 7) {      // next row (only when a pair of it follows)
+                    j = 0;
+                    fi = __ldg(f + ++i);
+                }
+            }
+        }
+        if constexpr (INTER) {
+            float cs[16];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                cs[2 * k] = cv[k];
+                cs[2 * k + 1] = sv[k];
+            }
+            st8_stream(io + 2 * e0, cs);
+            st8_stream(io + 2 * e0 + 8, cs + 8);
+        } else {
+            st8_stream(so + e0, sv);
+            st8_stream(co + e0, cv);
+        }
+    }
+}
+
+template <int V, bool INTER, bool TURNS>
+static const void *pick_flat() {
+    return reinterpret_cast<const void *>(phase_grid_flat<V, INTER, TURNS>);
+}
+
+cudaError_t launch_phase_flat(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
+                              size_t nt, float *so, float *co, float *io, size_t head, size_t nvec,
+                              unsigned grid, cudaStream_t stream) {
+    const void *fn;
+    if (variant == kNormalized)
+        fn = inter ? (turns ? pick_flat<kNormalized, true, true>() : pick_flat<kNormalized, true, false>())
+                   : (turns ? pick_flat<kNormalized, false, true>() : pick_flat<kNormalized, false, false>());
+    else
+        fn = inter ? (turns ? pick_flat<kRenormalized, true, true>() : pick_flat<kRenormalized, true, false>())
+                   : (turns ? pick_flat<kRenormalized, false, true>() : pick_flat<kRenormalized, false, false>());
+    size_t n = nf * nt;
+    double inv_nt = 1.0 / static_cast<double>(nt);
+    void *args[] = {&f, &t, &nf, &nt, &so, &co, &io, &head, &nvec, &n, &inv_nt};
+    return cudaLaunchKernel(fn, dim3(grid), dim3(kPhaseThreads), args, 0, stream);
+}
+
 template <int V, bool INTER, bool TURNS>
 static const void *pick_phase(bool vec) {
     return vec ? reinterpret_cast<const void *>(phase_grid_vec<V, INTER, TURNS>)

@@ -107,3 +107,41 @@ def test_radians_equals_the_materialised_path(variant):
     sp.phase_grid(fd, td, s2, c2, units=R, variant=variant)
     torch.cuda.synchronize()
     assert torch.equal(s1, s2) and torch.equal(c1, c2)
+
+
+@pytest.mark.parametrize("units,variant", COMBOS)
+@pytest.mark.parametrize("flat", [True, False])
+def test_ragged_rows_flat_path(units, variant, flat):
+    """Rows that are not whole 256-bit vectors (nt % 8 != 0, t or outputs off 32 B) go through
+    the flat kernel (8 consecutive pairs of the row-major grid per thread, rows wrapping inside
+    a vector, nt = 1..9 included) or, with it disabled / for outputs it cannot serve, one pair
+    per thread; bit-exact either way, at several output offsets, split and interleaved."""
+    rng = np.random.default_rng(31 + units + 2 * variant)
+    prev = sp.set_realign(flat)
+    try:
+        for nf, nt in ((1, 1), (3, 1), (7, 2), (5, 3), (9, 7), (4, 9), (33, 1001), (257, 255), (64, 256)):
+            f = rng.uniform(0, 400, nf).astype(np.float32)
+            t = rng.uniform(-1, 1, nt + 1).astype(np.float32)
+            n = nf * nt
+            for toff in (0, 1):
+                tt = t[toff:toff + nt]
+                ws, wc = oracle.phase_grid(f, tt, units, variant)
+                ws, wc = ws.ravel(), wc.ravel()
+                fd = torch.from_numpy(f).cuda()
+                tbig = torch.from_numpy(t).cuda()
+                td = tbig[toff:toff + nt]
+                for oo, oc in ((0, 0), (3, 3), (5, 5), (1, 2)):
+                    big_s = torch.empty(n + 16, device="cuda")
+                    big_c = torch.empty(n + 16, device="cuda")
+                    s, c = big_s[oo:oo + n], big_c[oc:oc + n]
+                    sp.phase_grid(fd, td, s, c, units=units, variant=variant)
+                    big_i = torch.empty(2 * n + 16, device="cuda")
+                    io = big_i[oo:oo + 2 * n]
+                    sp.phase_grid(fd, td, interleaved_out=io, units=units, variant=variant)
+                    torch.cuda.synchronize()
+                    tag = f"({nf},{nt}) toff={toff} out={oo},{oc} flat={flat}"
+                    assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws, wc, "split " + tag)
+                    iv = io.cpu().numpy()
+                    assert_parity(iv[1::2], iv[0::2], ws, wc, "inter " + tag)
+    finally:
+        sp.set_realign(prev)

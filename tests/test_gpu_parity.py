@@ -502,3 +502,41 @@ def test_scalar_path_unshared_outputs():
                                   f"scalar inter off={ot},{oi} realign={realign}")
             finally:
                 sp.set_realign(prev)
+
+
+@pytest.mark.parametrize("variant,name", [(oracle.VARIANT_N, "N"), (oracle.VARIANT_A, "A")])
+@pytest.mark.parametrize("path", ["interleaved", "realign_split", "realign_interleaved", "scalar_split"])
+def test_all_fp32_bit_patterns_other_paths(golden, variant, name, path):
+    """The whole-input-space hash through the other kernels: the 256-bit interleaved kernel,
+    the re-aligning kernel (theta one float off the outputs; split and interleaved) and the
+    one-element-per-thread kernel -- each equals the oracle's committed whole-space run."""
+    import json
+    run_ = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_exhaustive.json")))
+    want = run_[name]["all_bits"]
+    chunk = 1 << 28
+    toff = 1 if path != "interleaved" else 0
+    tbuf = torch.empty(chunk + 8, dtype=torch.float32, device="cuda")
+    if path == "scalar_split":
+        prev = sp.set_realign(False)
+    try:
+        if "inter" in path:
+            io = torch.empty(2 * chunk, dtype=torch.float32, device="cuda")
+        else:
+            s = torch.empty(chunk, dtype=torch.float32, device="cuda")
+            c = torch.empty(chunk, dtype=torch.float32, device="cuda")
+        H, NN, EX = 0, 0, 0
+        for u0 in range(0, 1 << 32, chunk):
+            th = tbuf[toff:toff + chunk]
+            th.view(torch.int32).copy_(torch.arange(u0, u0 + chunk, dtype=torch.int64, device="cuda").to(torch.int32))
+            if "inter" in path:
+                sp.sincos_pairs(th, interleaved_out=io, variant=variant)
+                s, c = io[1::2], io[0::2]
+            else:
+                sp.sincos_pairs(th, s, c, variant=variant)
+            h, nn, ex = _hash_chunk(u0, s.contiguous(), c.contiguous())
+            H, NN, EX = (H + h) % (1 << 64), NN + nn, EX + ex
+    finally:
+        if path == "scalar_split":
+            sp.set_realign(prev)
+    assert "0x%016X" % H == want["hash"], path
+    assert NN == want["nan_pairs"] and EX == want["exact_0_1"]

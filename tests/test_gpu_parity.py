@@ -540,3 +540,34 @@ def test_all_fp32_bit_patterns_other_paths(golden, variant, name, path):
             sp.set_realign(prev)
     assert "0x%016X" % H == want["hash"], path
     assert NN == want["nan_pairs"] and EX == want["exact_0_1"]
+
+
+@pytest.mark.parametrize("variant,name", [(oracle.VARIANT_N, "N"), (oracle.VARIANT_A, "A")])
+@pytest.mark.parametrize("path", ["phase_vec", "phase_flat", "method_paper_table"])
+def test_all_fp32_bit_patterns_next_kernels(golden, variant, name, path):
+    """Every fp32 input through the NEXT-row kernels that evaluate the same pairs: the phase
+    grid with f = [1] (p = RN(1 * t) = t exactly, radians; 256-bit row kernel, and the flat
+    kernel with t one float off) and the general-method kernel with the paper's own table --
+    hash, NaN and exact-(0, 1) counts equal the oracle's whole-space run."""
+    import json
+    run_ = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_exhaustive.json")))
+    want = run_[name]["all_bits"]
+    chunk = 1 << 28
+    toff = 1 if path == "phase_flat" else 0
+    tbuf = torch.empty(chunk + 8, dtype=torch.float32, device="cuda")
+    s = torch.empty(chunk, dtype=torch.float32, device="cuda")
+    c = torch.empty(chunk, dtype=torch.float32, device="cuda")
+    one = torch.ones(1, dtype=torch.float32, device="cuda")
+    m = sp.make_method(*sp.PAPER_METHODS[variant])
+    H, NN, EX = 0, 0, 0
+    for u0 in range(0, 1 << 32, chunk):
+        th = tbuf[toff:toff + chunk]
+        th.view(torch.int32).copy_(torch.arange(u0, u0 + chunk, dtype=torch.int64, device="cuda").to(torch.int32))
+        if path.startswith("phase"):
+            sp.phase_grid(one, th, s, c, units=sp.RADIANS, variant=variant)
+        else:
+            sp.sincos_pairs_method(th, m, s, c)
+        h, nn, ex = _hash_chunk(u0, s, c)
+        H, NN, EX = (H + h) % (1 << 64), NN + nn, EX + ex
+    assert "0x%016X" % H == want["hash"], path
+    assert NN == want["nan_pairs"] and EX == want["exact_0_1"]

@@ -108,3 +108,29 @@ def test_adapter_matches_interleaved_kernel_output():
     io2 = sp.sincos(t, variant=1, interleaved=True).reshape(-1)
     torch.cuda.synchronize()
     assert torch.equal(io.view(torch.int32), io2.view(torch.int32))
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("dtype", ["float16", "bfloat16"])
+def test_all_fp32_inputs_16bit_equal_library_rounding_of_fp32_path(variant, dtype):
+    """Every one of the 2^32 fp32 inputs: the 16-bit kernel's bits equal torch's RN cast of the
+    fp32 kernel's pair (whose whole-space hash equals the oracle's, test_gpu_parity), NaN
+    matching NaN; split and interleaved 16-bit layouts."""
+    dt = getattr(torch, dtype)
+    chunk = 1 << 28
+    s32 = torch.empty(chunk, dtype=torch.float32, device="cuda")
+    c32 = torch.empty(chunk, dtype=torch.float32, device="cuda")
+    s16 = torch.empty(chunk, dtype=dt, device="cuda")
+    c16 = torch.empty(chunk, dtype=dt, device="cuda")
+    i16 = torch.empty(2 * chunk, dtype=dt, device="cuda")
+    bad = 0
+    for u0 in range(0, 1 << 32, chunk):
+        th = torch.arange(u0, u0 + chunk, dtype=torch.int64, device="cuda").to(torch.int32).view(torch.float32)
+        sp.sincos_pairs(th, s32, c32, variant=variant)
+        sp.sincos_pairs_dtype(th, s16, c16, variant=variant)
+        sp.sincos_pairs_dtype(th, interleaved_out=i16, variant=variant)
+        for got, ref in ((s16, s32), (c16, c32), (i16[1::2], s32), (i16[0::2], c32)):
+            want = ref.to(dt)
+            same = (got.view(torch.int16) == want.view(torch.int16)) | (torch.isnan(got) & torch.isnan(want))
+            bad += int((~same).sum().item())
+    assert bad == 0

@@ -97,3 +97,23 @@ def test_phase_grid_and_nudft(shape):
     torch.cuda.synchronize()
     check(bi, G, G + 2 * n)
     check(bo, G, G + 2 * nf)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (3, 7), (9, 13), (33, 1001), (16, 256)])
+@pytest.mark.parametrize("off", [0, 1, 3, 6])
+def test_phase_grid_split_offsets(shape, off):
+    """Split phase-grid outputs at offsets (the flat kernel's head/body/tail and the row kernel),
+    interleaved at odd and even float offsets (flat kernel / one pair per thread)."""
+    nf, nt = shape
+    f = torch.rand(nf, device="cuda") * 100
+    t = torch.rand(nt, device="cuda")
+    n = nf * nt
+    bs = torch.full((2 * G + n + 8,), SENT, dtype=torch.int32, device="cuda")
+    bc = bs.clone()
+    sp.phase_grid(f, t, bs[G + off:G + off + n].view(torch.float32), bc[G + off:G + off + n].view(torch.float32))
+    bi = torch.full((2 * G + 2 * n + 8,), SENT, dtype=torch.int32, device="cuda")
+    sp.phase_grid(f, t, interleaved_out=bi[G + off:G + off + 2 * n].view(torch.float32), units=sp.TURNS)
+    torch.cuda.synchronize()
+    check(bs, G + off, G + off + n)
+    check(bc, G + off, G + off + n)
+    check(bi, G + off, G + off + 2 * n)

@@ -15,6 +15,7 @@
 #include "../../include/sincos_pairs.h"
 #include "sincos_launch.h"
 #include "sincos_method.cuh"
+#include "sincos_realign.cuh"
 
 using namespace sincos_b200;
 
@@ -311,22 +312,26 @@ sincos_status_t sincos_pairs_dtype(const float *theta_dev, void *sin_dev, void *
     } else if (overlaps(theta_dev, 4 * n, inter_dev, 4 * n)) {
         return SINCOS_ERR_OVERLAP;
     }
-    const uintptr_t t = reinterpret_cast<uintptr_t>(theta_dev);
-    const size_t h = ((32 - (t & 31)) & 31) / 4;
-    const bool vec = inter ? aligned(static_cast<const char *>(inter_dev) + 4 * h, 32)
-                           : aligned(static_cast<const char *>(sin_dev) + 2 * h, 16) &&
-                                 aligned(static_cast<const char *>(cos_dev) + 2 * h, 16);
+    // vector body: the outputs' alignment fixes the first vector element (split: 128-bit stores,
+    // sin and cos at one offset mod 16 B; interleaved: one 256-bit store per 8 pairs), theta is
+    // re-aligned in registers when it sits off that alignment (sincos_realign.cuh)
+    const uintptr_t so_a = reinterpret_cast<uintptr_t>(sin_dev), co_a = reinterpret_cast<uintptr_t>(cos_dev),
+                    io_a = reinterpret_cast<uintptr_t>(inter_dev);
+    bool vec = inter || ((so_a ^ co_a) & 15) == 0;
+    const size_t h0 = inter ? ((32 - (io_a & 31)) & 31) / 4 : ((16 - (so_a & 15)) & 15) / 2;
+    int k = 0;
     size_t head = 0, nvec = 0;
     if (vec) {
-        head = h < n ? h : n;
-        nvec = (n - head) / 8;
+        realign_plan(theta_dev, n, h0, &k, &head, &nvec);
+        if (k != 0 && !g_shift.load(std::memory_order_relaxed)) vec = false;
     }
+    if (!vec) head = nvec = 0, k = 0;
     // without the vector path every element is a "tail" element: one per thread
     const size_t work = vec ? (nvec > 8 ? nvec : 8) : n;
     size_t grid = (work + 127) / 128;
     if (grid > 0x7FFFFFFFu) return SINCOS_ERR_INVALID_ARGUMENT;
     cudaError_t e = launch_pairs16(variant, out_dtype, inter, static_cast<unsigned>(grid), theta_dev, sin_dev,
-                                   cos_dev, inter_dev, head, nvec, n, static_cast<cudaStream_t>(stream));
+                                   cos_dev, inter_dev, head, nvec, n, k, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SINCOS_OK;
@@ -372,20 +377,26 @@ sincos_status_t sincos_pairs_method(const float *theta_dev, float *sin_dev, floa
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e);
     const bool inter = inter_dev != nullptr;
-    // 32-B vector body when theta and the outputs share their alignment after a scalar head
-    const uintptr_t t = reinterpret_cast<uintptr_t>(theta_dev);
-    const size_t h = ((32 - (t & 31)) & 31) / 4;
-    bool vec = inter ? aligned(reinterpret_cast<const char *>(inter_dev) + 8 * h, 32)
-                     : aligned(reinterpret_cast<const char *>(sin_dev) + 4 * h, 32) &&
-                           aligned(reinterpret_cast<const char *>(cos_dev) + 4 * h, 32);
-    size_t head = vec ? (h < n ? h : n) : 0;
-    size_t nvec = vec ? (n - head) / 8 : 0;
+    // 256-bit vector body where the outputs take 256-bit stores (split: sin and cos at one
+    // offset mod 32 B; interleaved: 8-B aligned), theta re-aligned in registers when it sits
+    // off that alignment (sincos_realign.cuh)
+    const uintptr_t so_a = reinterpret_cast<uintptr_t>(sin_dev), co_a = reinterpret_cast<uintptr_t>(cos_dev),
+                    io_a = reinterpret_cast<uintptr_t>(inter_dev);
+    bool vec = inter ? aligned(inter_dev, 8) : ((so_a ^ co_a) & 31) == 0;
+    const size_t h0 = inter ? ((32 - (io_a & 31)) & 31) / 8 : ((32 - (so_a & 31)) & 31) / 4;
+    int k = 0;
+    size_t head = 0, nvec = 0;
+    if (vec) {
+        realign_plan(theta_dev, n, h0, &k, &head, &nvec);
+        if (k != 0 && !g_shift.load(std::memory_order_relaxed)) vec = false;
+    }
+    if (!vec) head = nvec = 0, k = 0;
     size_t work = vec ? (nvec > 0 ? nvec : 1) : n;
     size_t grid = (work + 127) / 128;
     if (!vec && grid > static_cast<size_t>(sm_count(dev)) * 16) grid = static_cast<size_t>(sm_count(dev)) * 16;
     if (grid > 0x7FFFFFFFu) grid = 0x7FFFFFFFu;
     e = launch_method(m->ss, m->n_ss, m->cc, m->n_cc, m->doublings, m->fix, inter, vec, static_cast<unsigned>(grid),
-                      theta_dev, sin_dev, cos_dev, inter_dev, head, nvec, n, static_cast<cudaStream_t>(stream));
+                      theta_dev, sin_dev, cos_dev, inter_dev, head, nvec, n, k, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SINCOS_OK;

@@ -12,6 +12,7 @@
 
 #include "sincos_launch.h"
 #include "sincos_math.cuh"
+#include "sincos_realign.cuh"
 
 namespace sincos_b200 {
 
@@ -44,21 +45,26 @@ __device__ __forceinline__ void emit16_scalar(const float *theta, size_t e, uint
     }
 }
 
-// Full grid, one 256-bit theta load per thread; outputs: split 2 x 128-bit, interleaved 256-bit.
+// Full grid, eight angles per thread (one aligned 256-bit load, re-aligned in registers when
+// theta sits k floats off the outputs' vector alignment, sincos_realign.cuh); outputs: split
+// 2 x 128-bit, interleaved 256-bit.  Warp-uniform trips (the re-alignment shuffles).
 template <int V, int DT, bool INTER>
 __global__ void __launch_bounds__(128) sincos16_kernel(const float *theta, uint16_t *so, uint16_t *co, uint16_t *io,
-                                                       size_t head, size_t nvec, size_t n) {
+                                                       size_t head, size_t nvec, size_t n, int k) {
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const size_t tail0 = head + 8 * nvec;
     if (tid < head) emit16_scalar<V, DT, INTER>(theta, tid, so, co, io);
     if (tid < n - tail0) emit16_scalar<V, DT, INTER>(theta, tail0 + tid, so, co, io);
-    for (size_t v = tid; v < nvec; v += nthr) {
-        const size_t e0 = head + 8 * v;
+    const unsigned lane = threadIdx.x & 31u;
+    const float *tal = theta + head - k;
+    for (size_t w0 = tid - lane; w0 < nvec; w0 += nthr) {
+        const size_t v = w0 + lane;
+        const bool act = v < nvec;
         float x[8];
-        asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]), "=f"(x[6]), "=f"(x[7])
-                     : "l"(theta + e0));
+        load8_realigned(tal, v, nvec, lane, k, act, x);
+        if (!act) continue;
+        const size_t e0 = head + 8 * v;
         uint16_t s16[8], c16[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -89,14 +95,14 @@ static const void *pick16i(bool inter) {
 }
 
 cudaError_t launch_pairs16(int variant, int dtype, bool inter, unsigned grid, const float *theta, void *so, void *co,
-                           void *io, size_t head, size_t nvec, size_t n, cudaStream_t stream) {
+                           void *io, size_t head, size_t nvec, size_t n, int k, cudaStream_t stream) {
     const void *fn;
     if (variant == kNormalized)
         fn = dtype == 1 ? pick16i<kNormalized, 1>(inter) : pick16i<kNormalized, 2>(inter);
     else
         fn = dtype == 1 ? pick16i<kRenormalized, 1>(inter) : pick16i<kRenormalized, 2>(inter);
     uint16_t *s = static_cast<uint16_t *>(so), *c = static_cast<uint16_t *>(co), *i = static_cast<uint16_t *>(io);
-    void *args[] = {&theta, &s, &c, &i, &head, &nvec, &n};
+    void *args[] = {&theta, &s, &c, &i, &head, &nvec, &n, &k};
     return cudaLaunchKernel(fn, dim3(grid), dim3(128), args, 0, stream);
 }
 

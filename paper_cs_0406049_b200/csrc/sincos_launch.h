@@ -49,12 +49,13 @@ cudaError_t launch_packcheck(int variant, int shape, int fix, const MethodParams
 int set_nudft_packed(int on);
 int get_nudft_packed();
 // NEXT(3) general method (sincos_method.cu).
+// k = theta's float offset past the 32-B boundary at element head - k (0 = aligned).
 cudaError_t launch_method(const float *ss, int n_ss, const float *cc, int n_cc, int doublings, int fix, bool inter,
                           bool vec, unsigned grid, const float *theta, float *so, float *co, float *io, size_t head,
-                          size_t nvec, size_t n, cudaStream_t stream);
+                          size_t nvec, size_t n, int k, cudaStream_t stream);
 // NEXT(4) 16-bit outputs (dtype 1 = fp16, 2 = bf16) and fp32 layout adapters (sincos_dtype.cu).
 cudaError_t launch_pairs16(int variant, int dtype, bool inter, unsigned grid, const float *theta, void *so, void *co,
-                           void *io, size_t head, size_t nvec, size_t n, cudaStream_t stream);
+                           void *io, size_t head, size_t nvec, size_t n, int k, cudaStream_t stream);
 cudaError_t launch_interleave(bool to_inter, unsigned grid, const float *s, const float *c, float *io, size_t n,
                               cudaStream_t stream);
 const void *vec_kernel_ptr(int variant, bool inter, int w, int unroll, bool nc, bool pf);

@@ -13,6 +13,7 @@
 
 #include "sincos_launch.h"
 #include "sincos_method.cuh"
+#include "sincos_realign.cuh"
 
 namespace sincos_b200 {
 
@@ -36,12 +37,14 @@ __device__ __forceinline__ void st8m(float *p, const float *r) {
                  : "memory");
 }
 
-// Full grid, one 256-bit vector per thread over [head, head + 8 nvec); scalar head/tail.
-// vec == false: every element scalar (pointers without a shared 32-B alignment).
+// Full grid, eight angles per thread over [head, head + 8 nvec) (one aligned 256-bit load,
+// re-aligned in registers when theta sits k floats off the outputs' alignment,
+// sincos_realign.cuh); scalar head/tail; warp-uniform trips.
+// vec == false: every element scalar (outputs that cannot take 256-bit stores).
 template <int NT, int FIX, bool INTER>
 __global__ void __launch_bounds__(128) method_kernel(const MethodParams m, const float *theta, float *so,
                                                      float *co, float *io, size_t head, size_t nvec, size_t n,
-                                                     bool vec) {
+                                                     bool vec, int k) {
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (!vec) {
@@ -51,12 +54,15 @@ __global__ void __launch_bounds__(128) method_kernel(const MethodParams m, const
     const size_t tail0 = head + 8 * nvec;
     if (tid < head) method_scalar<NT, FIX, INTER>(m, theta, tid, so, co, io);
     if (tid < n - tail0) method_scalar<NT, FIX, INTER>(m, theta, tail0 + tid, so, co, io);
-    for (size_t v = tid; v < nvec; v += nthr) {
-        const size_t e0 = head + 8 * v;
+    const unsigned lane = threadIdx.x & 31u;
+    const float *tal = theta + head - k;
+    for (size_t w0 = tid - lane; w0 < nvec; w0 += nthr) {
+        const size_t v = w0 + lane;
+        const bool act = v < nvec;
         float x[8];
-        asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]), "=f"(x[6]), "=f"(x[7])
-                     : "l"(theta + e0));
+        load8_realigned(tal, v, nvec, lane, k, act, x);
+        if (!act) continue;
+        const size_t e0 = head + 8 * v;
         if constexpr (INTER) {
             float cs[16];
 #pragma unroll
@@ -83,7 +89,7 @@ static const void *pick_m(bool inter) {
 // 4-term Horner, otherwise the 8-term one.
 cudaError_t launch_method(const float *ss, int n_ss, const float *cc, int n_cc, int doublings, int fix, bool inter,
                           bool vec, unsigned grid, const float *theta, float *so, float *co, float *io, size_t head,
-                          size_t nvec, size_t n, cudaStream_t stream) {
+                          size_t nvec, size_t n, int k, cudaStream_t stream) {
     MethodParams m = make_params(ss, n_ss, cc, n_cc, doublings);
     const bool small = n_ss <= 4 && n_cc <= 4;
     const void *fn;
@@ -91,7 +97,7 @@ cudaError_t launch_method(const float *ss, int n_ss, const float *cc, int n_cc, 
         fn = fix == 0 ? pick_m<4, 0>(inter) : fix == 1 ? pick_m<4, 1>(inter) : pick_m<4, 3>(inter);
     else
         fn = fix == 0 ? pick_m<8, 0>(inter) : fix == 1 ? pick_m<8, 1>(inter) : pick_m<8, 3>(inter);
-    void *args[] = {&m, &theta, &so, &co, &io, &head, &nvec, &n, &vec};
+    void *args[] = {&m, &theta, &so, &co, &io, &head, &nvec, &n, &vec, &k};
     return cudaLaunchKernel(fn, dim3(grid), dim3(128), args, 0, stream);
 }
 

@@ -1,0 +1,77 @@
+// sincos_realign.cuh -- eight consecutive angles from any 4-B offset, with aligned 256-bit
+// loads: the re-alignment of KB3b (sincos_kernels.cu) for the kernels whose outputs fix the
+// vector alignment (16-bit outputs, general methods).
+//
+// The caller's vector v covers angles theta[head + 8v .. head + 8v + 7]; tal = theta + head - K
+// is 32-B aligned, K = 0..7 the angles' float offset past that boundary (warp-uniform, a
+// runtime value).  Lane l loads a = tal[8v .. 8v+7]; the next aligned vector b comes from
+// lane l+1 by warp shuffles, or from its own load for the warp's last lane and for a lane
+// whose neighbour is past the end (issued together with the first load: one round trip).
+// x = a[K..7] ++ b[0..K-1], selected by a uniform switch over K (register moves only).
+// Must be called by all 32 lanes (act = false for lanes past the end); the host sizes nvec
+// so that tal[8 nvec + 7] lies inside theta when K > 0.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sincos_b200 {
+
+__device__ __forceinline__ void ld8_stream(float (&r)[8], const float *p) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+                 : "l"(p));
+}
+
+template <int K>
+__device__ __forceinline__ void select8(const float (&a)[8], const float (&b)[8], float (&x)[8]) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = j + K < 8 ? a[j + K] : b[j + K - 8];
+}
+
+__device__ __forceinline__ void load8_realigned(const float *tal, size_t v, size_t nvec, unsigned lane, int k,
+                                                bool act, float (&x)[8]) {
+    float a[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+    if (k == 0) {                                  // uniform: the aligned case, no shuffle
+        if (act) ld8_stream(a, tal + 8 * v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = a[j];
+        return;
+    }
+    const bool own = act && (lane == 31u || v + 1 >= nvec);
+    float bo[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+    if (act) ld8_stream(a, tal + 8 * v);
+    if (own) ld8_stream(bo, tal + 8 * v + 8);
+    float b[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b[j] = __shfl_down_sync(0xFFFFFFFFu, a[j], 1);   // every lane shuffles
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b[j] = own ? bo[j] : b[j];
+    switch (k) {
+    case 1: select8<1>(a, b, x); break;
+    case 2: select8<2>(a, b, x); break;
+    case 3: select8<3>(a, b, x); break;
+    case 4: select8<4>(a, b, x); break;
+    case 5: select8<5>(a, b, x); break;
+    case 6: select8<6>(a, b, x); break;
+    default: select8<7>(a, b, x); break;
+    }
+}
+
+// Host side: the aligned-angle offset K and the first vector element, for outputs whose vector
+// alignment holds at element head0 and repeats every 8 elements (so K is the same at head0 + 8):
+// head >= K keeps tal inside theta; nvec such that every second aligned load stays inside
+// theta (K > 0).
+inline void realign_plan(const float *theta, size_t n, size_t head0, int *k, size_t *head, size_t *nvec) {
+    const int kk = static_cast<int>(((reinterpret_cast<uintptr_t>(theta) + 4 * head0) & 31) / 4);
+    size_t h = head0;
+    if (h < static_cast<size_t>(kk)) h += 8;
+    if (h > n) h = n;
+    size_t nv = (n - h) / 8;
+    if (kk > 0) nv = n + kk >= h + 8 ? (n + kk - h - 8) / 8 : 0;   // (h - K) + 8 nvec + 7 <= n - 1
+    *k = kk;
+    *head = h;
+    *nvec = nv;
+}
+
+}  // namespace sincos_b200

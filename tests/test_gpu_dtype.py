@@ -134,3 +134,40 @@ def test_all_fp32_inputs_16bit_equal_library_rounding_of_fp32_path(variant, dtyp
             same = (got.view(torch.int16) == want.view(torch.int16)) | (torch.isnan(got) & torch.isnan(want))
             bad += int((~same).sum().item())
     assert bad == 0
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("realign", [True, False])
+def test_16bit_every_theta_offset(dtype, realign):
+    """theta at every float offset 0..7 against outputs at several offsets (split with sin and
+    cos sharing an offset, interleaved): the re-aligning vector body (every K = 0..7), or with
+    re-alignment off the one-per-thread path; lengths around the vector boundaries and large."""
+    rng = np.random.default_rng(5)
+    N = 100_003
+    base = rng.uniform(-300, 300, N + 16).astype(np.float32)
+    prev = sp.set_realign(realign)
+    try:
+        for variant in (0, 1):
+            ws, wc = oracle.sincos(base, variant)
+            bt = torch.from_numpy(base).cuda()
+            bs = torch.empty(N + 64, dtype=dtype, device="cuda")
+            bc = torch.empty(N + 64, dtype=dtype, device="cuda")
+            bi = torch.empty(2 * N + 64, dtype=dtype, device="cuda")
+            for n in list(range(0, 20)) + [63, 64, 65, 1001, N]:
+                for ot in range(8):
+                    for oo in (0, 1, 6):
+                        s, c = bs[oo:oo + n], bc[oo + 8:oo + 8 + n]
+                        sp.sincos_pairs_dtype(bt[ot:ot + n], s, c, variant=variant)
+                        io = bi[2 * oo:2 * oo + 2 * n]
+                        sp.sincos_pairs_dtype(bt[ot:ot + n], interleaved_out=io, variant=variant)
+                        torch.cuda.synchronize()
+                        tag = (n, ot, oo, variant, realign)
+                        gs = s.view(torch.int16).cpu().numpy().view(np.uint16)
+                        gc = c.view(torch.int16).cpu().numpy().view(np.uint16)
+                        assert same16(gs, rn16(ws[ot:ot + n], dtype), dtype).all(), tag
+                        assert same16(gc, rn16(wc[ot:ot + n], dtype), dtype).all(), tag
+                        gi = io.view(torch.int16).cpu().numpy().view(np.uint16)
+                        assert same16(gi[1::2], rn16(ws[ot:ot + n], dtype), dtype).all(), tag
+                        assert same16(gi[0::2], rn16(wc[ot:ot + n], dtype), dtype).all(), tag
+    finally:
+        sp.set_realign(prev)

@@ -102,3 +102,37 @@ def test_method_validation():
             sp.sincos_pairs_method(t, bad, s, c)
     with pytest.raises(sp.SincosError):
         sp.sincos_pairs_method(t, sp.make_method([1.0], [], 2, 0), t, c)     # in-place not supported
+
+
+@pytest.mark.parametrize("realign", [True, False])
+def test_method_every_theta_offset(realign):
+    """The general-method kernel with theta at every float offset 0..7 against split outputs
+    (sin and cos at one offset) and interleaved outputs at 8-B and 4-B offsets: the re-aligning
+    vector body for every K, or one element per thread; bit-exact vs the oracle's method."""
+    rng = np.random.default_rng(4)
+    N = 100_003
+    base = rng.uniform(-300, 300, N + 16).astype(np.float32)
+    f = cf.fit_angle(1, 3, 2)
+    ss, cc = f.fp32()
+    m = sp.make_method(list(ss), list(cc), 1, sp.FIX_RECIPROCAL)
+    ws, wc = oracle.method_sincos(base, omethod(list(ss), list(cc), 1, sp.FIX_RECIPROCAL))
+    bt = torch.from_numpy(base).cuda()
+    bs = torch.empty(N + 64, device="cuda")
+    bc = torch.empty(N + 64, device="cuda")
+    bi = torch.empty(2 * N + 64, device="cuda")
+    prev = sp.set_realign(realign)
+    try:
+        for n in list(range(0, 20)) + [63, 64, 65, 1001, N]:
+            for ot in range(8):
+                for oo in (0, 1, 6):
+                    s, c = bs[oo:oo + n], bc[oo + 8:oo + 8 + n]
+                    sp.sincos_pairs_method(bt[ot:ot + n], m, s, c)
+                    io = bi[oo:oo + 2 * n]                    # oo odd: only 4-B aligned pairs
+                    sp.sincos_pairs_method(bt[ot:ot + n], m, interleaved_out=io)
+                    torch.cuda.synchronize()
+                    tag = f"n={n} ot={ot} oo={oo} realign={realign}"
+                    assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws[ot:ot + n], wc[ot:ot + n], tag)
+                    iv = io.cpu().numpy()
+                    assert_parity(iv[1::2], iv[0::2], ws[ot:ot + n], wc[ot:ot + n], "inter " + tag)
+    finally:
+        sp.set_realign(prev)

@@ -27,3 +27,28 @@ for realign in (True, False):
     b.record(); torch.cuda.synchronize()
     res[f"{name} realign={int(realign)}"] = round(12 * n / (a.elapsed_time(b) / 10 / 1e3) / 1e9, 1)
 print(json.dumps(res))
+
+
+def more():
+    """16-bit outputs (8 B/pair) and the general-method kernel (12 B/pair) with theta one float
+    off the outputs, re-alignment on / off."""
+    out = {}
+    m = sp.make_method(*sp.PAPER_METHODS[0])
+    s16 = torch.empty(n, dtype=torch.float16, device='cuda'); c16 = torch.empty(n, dtype=torch.float16, device='cuda')
+    for realign in (True, False):
+        sp.set_realign(realign)
+        for to in (0, 1):
+            th = base[to:to + n]
+            for name, fn, bpp in (("fp16 split", lambda: sp.sincos_pairs_dtype(th, s16, c16), 8),
+                                  ("method N table split", lambda: sp.sincos_pairs_method(th, m, s[:n], c[:n]), 12)):
+                for _ in range(3): fn()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(10): fn()
+                b.record(); torch.cuda.synchronize()
+                out[f"{name} theta+{to} realign={int(realign)}"] = round(bpp * n / (a.elapsed_time(b) / 10 / 1e3) / 1e9, 1)
+    sp.set_realign(True)
+    print(json.dumps(out))
+
+
+more()

@@ -45,10 +45,11 @@ __device__ __forceinline__ void emit16_scalar(const float *theta, size_t e, uint
     }
 }
 
-// Full grid, eight angles per thread (one aligned 256-bit load, re-aligned in registers when
-// theta sits k floats off the outputs' vector alignment, sincos_realign.cuh); outputs: split
-// 2 x 128-bit, interleaved 256-bit.  Warp-uniform trips (the re-alignment shuffles).
-template <int V, int DT, bool INTER>
+// Full grid, eight angles per thread; outputs: split 2 x 128-bit, interleaved 256-bit.
+// RE = false: theta shares the outputs' vector alignment (one aligned 256-bit load per
+// thread, 32 registers: full occupancy).  RE = true: theta sits k = 1..7 floats off it and is
+// re-aligned in registers (sincos_realign.cuh), with warp-uniform trips for the shuffles.
+template <int V, int DT, bool INTER, bool RE>
 __global__ void __launch_bounds__(128) sincos16_kernel(const float *theta, uint16_t *so, uint16_t *co, uint16_t *io,
                                                        size_t head, size_t nvec, size_t n, int k) {
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
@@ -58,12 +59,16 @@ __global__ void __launch_bounds__(128) sincos16_kernel(const float *theta, uint1
     if (tid < n - tail0) emit16_scalar<V, DT, INTER>(theta, tail0 + tid, so, co, io);
     const unsigned lane = threadIdx.x & 31u;
     const float *tal = theta + head - k;
-    for (size_t w0 = tid - lane; w0 < nvec; w0 += nthr) {
-        const size_t v = w0 + lane;
-        const bool act = v < nvec;
+    for (size_t w0 = RE ? tid - lane : tid; w0 < nvec; w0 += nthr) {
+        const size_t v = RE ? w0 + lane : w0;
         float x[8];
-        load8_realigned(tal, v, nvec, lane, k, act, x);
-        if (!act) continue;
+        if constexpr (RE) {
+            const bool act = v < nvec;
+            load8_realigned(tal, v, nvec, lane, k, act, x);
+            if (!act) continue;
+        } else {
+            ld8_stream(x, theta + head + 8 * v);
+        }
         const size_t e0 = head + 8 * v;
         uint16_t s16[8], c16[8];
 #pragma unroll
@@ -88,19 +93,24 @@ __global__ void __launch_bounds__(128) sincos16_kernel(const float *theta, uint1
     }
 }
 
+template <int V, int DT, bool RE>
+static const void *pick16r(bool inter) {
+    return inter ? reinterpret_cast<const void *>(sincos16_kernel<V, DT, true, RE>)
+                 : reinterpret_cast<const void *>(sincos16_kernel<V, DT, false, RE>);
+}
 template <int V, int DT>
-static const void *pick16i(bool inter) {
-    return inter ? reinterpret_cast<const void *>(sincos16_kernel<V, DT, true>)
-                 : reinterpret_cast<const void *>(sincos16_kernel<V, DT, false>);
+static const void *pick16i(bool inter, bool re) {
+    return re ? pick16r<V, DT, true>(inter) : pick16r<V, DT, false>(inter);
 }
 
 cudaError_t launch_pairs16(int variant, int dtype, bool inter, unsigned grid, const float *theta, void *so, void *co,
                            void *io, size_t head, size_t nvec, size_t n, int k, cudaStream_t stream) {
     const void *fn;
+    const bool re = k != 0;
     if (variant == kNormalized)
-        fn = dtype == 1 ? pick16i<kNormalized, 1>(inter) : pick16i<kNormalized, 2>(inter);
+        fn = dtype == 1 ? pick16i<kNormalized, 1>(inter, re) : pick16i<kNormalized, 2>(inter, re);
     else
-        fn = dtype == 1 ? pick16i<kRenormalized, 1>(inter) : pick16i<kRenormalized, 2>(inter);
+        fn = dtype == 1 ? pick16i<kRenormalized, 1>(inter, re) : pick16i<kRenormalized, 2>(inter, re);
     uint16_t *s = static_cast<uint16_t *>(so), *c = static_cast<uint16_t *>(co), *i = static_cast<uint16_t *>(io);
     void *args[] = {&theta, &s, &c, &i, &head, &nvec, &n, &k};
     return cudaLaunchKernel(fn, dim3(grid), dim3(128), args, 0, stream);

@@ -8,6 +8,8 @@
 // lane l+1 by warp shuffles, or from its own load for the warp's last lane and for a lane
 // whose neighbour is past the end (issued together with the first load: one round trip).
 // x = a[K..7] ++ b[0..K-1], selected by a uniform switch over K (register moves only).
+// K = 1..7: the callers run a separate kernel instance for K = 0 (a plain aligned load, and
+// fewer registers -- full occupancy -- than this path needs).
 // Must be called by all 32 lanes (act = false for lanes past the end); the host sizes nvec
 // so that tal[8 nvec + 7] lies inside theta when K > 0.
 #pragma once
@@ -32,12 +34,6 @@ __device__ __forceinline__ void select8(const float (&a)[8], const float (&b)[8]
 __device__ __forceinline__ void load8_realigned(const float *tal, size_t v, size_t nvec, unsigned lane, int k,
                                                 bool act, float (&x)[8]) {
     float a[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
-    if (k == 0) {                                  // uniform: the aligned case, no shuffle
-        if (act) ld8_stream(a, tal + 8 * v);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = a[j];
-        return;
-    }
     const bool own = act && (lane == 31u || v + 1 >= nvec);
     float bo[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
     if (act) ld8_stream(a, tal + 8 * v);

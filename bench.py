@@ -450,11 +450,16 @@ def run_ours(args, rank, world, local_rank):
     GRAPH_REPS = 20
     if use_graph:
         cap = torch.cuda.Stream(dev)
+        side = torch.cuda.Stream(dev)
         cap.wait_stream(stream)
         step_graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(step_graph, stream=cap):
-            for v in variants:
-                sp.sincos_pairs(th, variant=v, stream=cap, **outs[v])
+            # the two variants are independent (same theta, separate outputs): two graph branches,
+            # so the latency-bound small launches overlap instead of running back to back
+            side.wait_stream(cap)
+            sp.sincos_pairs(th, variant=variants[0], stream=cap, **outs[variants[0]])
+            sp.sincos_pairs(th, variant=variants[1], stream=side, **outs[variants[1]])
+            cap.wait_stream(side)
         rep_graphs = {}
         for v in variants:
             g = torch.cuda.CUDAGraph()

@@ -123,12 +123,19 @@ __device__ __forceinline__ void phase_one(const float *__restrict__ f, const flo
     }
 }
 
+template <int R>
+__device__ __forceinline__ void select_t(const float (&w)[12], float (&tv)[8]) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tv[k] = w[R + k];
+}
+
 template <int V, bool INTER, bool TURNS>
 __global__ void __launch_bounds__(kPhaseThreads) phase_grid_flat(const float *__restrict__ f,
                                                                 const float *__restrict__ t, size_t nf,
                                                                 size_t nt, float *so, float *co, float *io,
                                                                 size_t head, size_t nvec, size_t n,
                                                                 double inv_nt) {
+    const bool t_al16 = (reinterpret_cast<uintptr_t>(t) & 15) == 0;
     const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t tail0 = head + 8 * nvec;
@@ -140,13 +147,27 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_flat(const float *__
         divmod_nt(e0, nt, inv_nt, i, j);
         float sv[8], cv[8];
         if (j + 8 <= nt) {
-            // the common case: the eight pairs lie in one row -- one f, eight t loads at
-            // immediate offsets from one pointer (no per-pair index arithmetic), all in flight
+            // the common case: the eight pairs lie in one row -- one f and t[j .. j+7]: with t
+            // 16-B aligned, three aligned 128-bit loads from t[j - r] (r = j mod 4, uniform along
+            // a row) and a register selection; else eight loads at immediate offsets
             const float fi = __ldg(f + i);
-            const float *tp = t + j;
             float tv[8];
+            const size_t r = j & 3;
+            if (t_al16 && j - r + 12 <= nt) {
+                const float4 *tq = reinterpret_cast<const float4 *>(t + (j - r));
+                const float4 q0 = __ldg(tq), q1 = __ldg(tq + 1), q2 = __ldg(tq + 2);
+                const float w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+                switch (r) {
+                case 0: select_t<0>(w, tv); break;
+                case 1: select_t<1>(w, tv); break;
+                case 2: select_t<2>(w, tv); break;
+                default: select_t<3>(w, tv); break;
+                }
+            } else {
+                const float *tp = t + j;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) tv[k] = __ldg(tp + k);
+                for (int k = 0; k < 8; ++k) tv[k] = __ldg(tp + k);
+            }
 #pragma unroll
             for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fi, tv[k], sv[k], cv[k]);
         } else if (nt >= 8) {

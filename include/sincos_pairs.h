@@ -190,7 +190,8 @@ SINCOS_API sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, cons
  *   ws_dev   device workspace of >= sincos_nudft_workspace_bytes(nf, nt) bytes
  *            (8-B aligned), not overlapping anything else
  * Arithmetic: complex products and per-chunk sums in fp32 with FMA (chunks of
- * sincos_nudft_chunk(nt) consecutive terms, summed in order), the chunk partials
+ * sincos_nudft_chunk(nt) consecutive terms -- 256 for nt < 4096, else 1024, longer
+ * when needed so that at most 65535 chunks remain -- summed in order), the chunk partials
  * added in fp64 in chunk order, rounded once to fp32: deterministic.  Error bound
  * against the exact sum of the same pairs:
  *   |out[k] - F_k| <= (chunk + 2) * 2^-24 * sum_j |a_j| + 2^-24 |F_k|.

@@ -172,9 +172,14 @@ __global__ void __launch_bounds__(256) nudft_reduce(const float2 *__restrict__ p
 
 size_t nudft_chunk(size_t nt) {
     // terms per thread per chunk: enough chunks to fill the GPU, long enough to amortise
-    // the partial sums; a multiple of the shared-memory tile
+    // the partial sums; a multiple of the shared-memory tile; at most 65535 chunks (grid.y)
     size_t chunk = 1024;
     if (nt < 4 * chunk) chunk = kTileJ;
+    const size_t max_chunks = 65535;
+    if ((nt + chunk - 1) / chunk > max_chunks) {
+        chunk = (nt + max_chunks - 1) / max_chunks;
+        chunk = (chunk + kTileJ - 1) / kTileJ * kTileJ;
+    }
     return chunk;
 }
 

@@ -229,3 +229,15 @@ def test_sass_packed_fused_sum_uses_ffma2():
             scalar += 1
             assert n2 == 0, (name, n2)
     assert packed >= 8 and scalar >= 8
+
+
+def test_nudft_chunk_rule():
+    """The fused sum's chunk length (it enters the error bound): 256 for short sums, 1024
+    normally, and long enough that the chunk count fits the grid's y extent (65535)."""
+    L = sp.lib()
+    assert L.sincos_nudft_chunk(1000) == 256 and L.sincos_nudft_chunk(1 << 15) == 1024
+    for nt in (1 << 26, 65535 * 1024, 65535 * 1024 + 1, 1 << 27, 10 ** 9, 1 << 36):
+        ch = L.sincos_nudft_chunk(nt)
+        assert ch % 256 == 0 and ch >= 1024 and (nt + ch - 1) // ch <= 65535, (nt, ch)
+        need = -(-nt // 65535)                       # fewest terms per chunk that fit
+        assert ch == max(1024, -(-need // 256) * 256), (nt, ch)

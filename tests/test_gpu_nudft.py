@@ -239,3 +239,21 @@ def test_packed_check_negative_control_fails():
     the two tables give different pairs (every q not tiny and not 0: roughly the patterns with
     1e-4 < |x| < 2^23 turns, ~15% of all 2^32, x 2 units x 2 components)."""
     assert sp.debug_packed_check(-1) > 2 ** 30
+
+
+def test_very_long_sum_chunking():
+    """nt beyond 65535 chunks of 1024 terms (the grid's y extent): the chunk grows; a single
+    unit amplitude far down the sum still returns exactly that term's pair."""
+    nt = (1 << 26) + (1 << 25) + 77            # 100.7 M terms -> chunk 1536
+    assert sp.nudft_chunk(nt) > 1024
+    f = torch.tensor([0.0, 1.0, 3.25, 77.5], device="cuda")
+    t = torch.rand(nt, device="cuda")
+    a = torch.zeros(nt, dtype=torch.complex64, device="cuda")
+    j0 = nt - 5
+    a[j0] = 1
+    out = sp.nudft(f, t, a, units=sp.TURNS).cpu().numpy()
+    p = (f.cpu().numpy() * t[j0].cpu().numpy()).astype(np.float32)        # RN(f t0)
+    q = (p.astype(np.float64) - np.rint(p.astype(np.float64))).astype(np.float32)
+    want = np.array([oracle.pair_from_q(float(x), 0) for x in q])
+    assert np.array_equal(out.real.astype(np.float32), want[:, 1].astype(np.float32))
+    assert np.array_equal(out.imag.astype(np.float32), want[:, 0].astype(np.float32))

@@ -189,10 +189,12 @@ SINCOS_API sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, cons
  *   out_dev  nf complex64 results, interleaved {re, im} (8-B aligned)
  *   ws_dev   device workspace of >= sincos_nudft_workspace_bytes(nf, nt) bytes
  *            (8-B aligned), not overlapping anything else
- * Arithmetic: complex products and per-chunk sums in fp32 with FMA (chunks of
- * sincos_nudft_chunk(nt) consecutive terms -- 256 for nt < 4096, else 1024, longer
- * when needed so that at most 65535 chunks remain -- summed in order), the chunk partials
- * added in fp64 in chunk order, rounded once to fp32: deterministic.  Error bound
+ * Arithmetic: complex products and sums in fp32 with FMA over runs ("chunks") of
+ * sincos_nudft_chunk(nt) consecutive terms (256 for nt < 4096, else 1024), summed in
+ * order; each run's sum is added into fp64, the terms split into segments for
+ * parallelism (a fixed rule, the same on every device) whose fp64 partials are added in
+ * segment order; one final rounding to fp32: deterministic.  Workspace: 16 B per
+ * frequency per segment (a few MB at 2^15 x 2^15).  Error bound
  * against the exact sum of the same pairs:
  *   |out[k] - F_k| <= (chunk + 2) * 2^-24 * sum_j |a_j| + 2^-24 |F_k|.
  * Two launches (partials, reduction).  nf == 0 is a no-op; nt == 0 zeroes out.

@@ -10,12 +10,14 @@
 // (~23 FP32-pipe ops + FRND, N) + 4 FFMA (complex multiply-accumulate).
 //
 // Layout: block (x, y) owns kKPerBlock frequencies (kKPerThread per thread, strided by
-// the block size so the partial stores coalesce) and chunk y of kChunk consecutive
-// terms j.  The chunk's (t_j, a_j) are staged through shared memory in tiles and read
-// by all threads as broadcasts.  Each thread accumulates its kKPerThread complex sums
-// over the chunk in fp32 (kChunk terms, sequential), writes the partial to the
-// workspace, and a second kernel adds the partials of all chunks in fp64 in chunk
-// order (deterministic) and rounds to complex64.
+// the block size so the partial stores coalesce) and segment y of consecutive terms j
+// (nudft_segment: about 8192 blocks in all, a fixed count, so the arithmetic does not
+// depend on the device).  The segment's (t_j, a_j) are staged through shared memory in
+// tiles and read by all threads as broadcasts.  Each thread sums its kKPerThread complex
+// sums in fp32 over runs of nudft_chunk(nt) consecutive terms (sequential FMAs), adds each
+// run into fp64 accumulators, writes the segment's fp64 partial to the workspace, and a
+// second kernel adds the segments' partials in fp64 in order (deterministic) and rounds to
+// complex64.  The error bound needs only the fp32 run length, whatever the segment length.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -90,15 +92,18 @@ __device__ __forceinline__ void term_pair2(const MethodParams &mp, F2 f, float t
 }
 
 template <int V, bool TURNS, bool PACK>
-__global__ void __launch_bounds__(kNuThreads) nudft_partial(const float *__restrict__ f, size_t nf,
+__global__ void __launch_bounds__(kNuThreads, 9) nudft_partial(const float *__restrict__ f, size_t nf,
                                                             const float *__restrict__ t,
                                                             const float2 *__restrict__ a, size_t nt,
-                                                            size_t chunk, float2 *__restrict__ part,
+                                                            size_t seg, size_t chunk, double2 *__restrict__ part,
                                                             const MethodParams mp) {
     __shared__ float4 sj[kTileJ];    // {t_j, re a_j, im a_j, 0}: one 128-bit broadcast load per term
+    // the thread's fp64 accumulators live in shared memory (touched once per chunk), keeping
+    // the registers -- and so the occupancy -- of the fp32 inner loop
+    __shared__ double2 acc[kKPerThread][kNuThreads];
     const size_t k0 = static_cast<size_t>(blockIdx.x) * kKPerBlock + threadIdx.x;
-    const size_t j0 = static_cast<size_t>(blockIdx.y) * chunk;
-    const size_t j1 = j0 + chunk < nt ? j0 + chunk : nt;
+    const size_t j0 = static_cast<size_t>(blockIdx.y) * seg;
+    const size_t j1 = j0 + seg < nt ? j0 + seg : nt;
     float fk[kKPerThread], re[kKPerThread], im[kKPerThread];
 #pragma unroll
     for (int m = 0; m < kKPerThread; ++m) {
@@ -106,8 +111,21 @@ __global__ void __launch_bounds__(kNuThreads) nudft_partial(const float *__restr
         fk[m] = k < nf ? f[k] : 0.0f;
         re[m] = 0.0f;
         im[m] = 0.0f;
+        acc[m][threadIdx.x] = make_double2(0.0, 0.0);
     }
     for (size_t jt = j0; jt < j1; jt += kTileJ) {
+        // every `chunk` terms (a multiple of the tile) the fp32 sums move into fp64
+        if (jt != j0 && (jt - j0) % chunk == 0) {
+#pragma unroll
+            for (int m = 0; m < kKPerThread; ++m) {
+                double2 d = acc[m][threadIdx.x];
+                d.x += re[m];
+                d.y += im[m];
+                acc[m][threadIdx.x] = d;
+                re[m] = 0.0f;
+                im[m] = 0.0f;
+            }
+        }
         const int len = static_cast<int>(j1 - jt < kTileJ ? j1 - jt : kTileJ);
         __syncthreads();
         for (int q = threadIdx.x; q < len; q += kNuThreads) {
@@ -153,40 +171,49 @@ __global__ void __launch_bounds__(kNuThreads) nudft_partial(const float *__restr
 #pragma unroll
     for (int m = 0; m < kKPerThread; ++m) {
         const size_t k = k0 + m * kNuThreads;
-        if (k < nf) part[static_cast<size_t>(blockIdx.y) * nf + k] = make_float2(re[m], im[m]);
+        const double2 d = acc[m][threadIdx.x];
+        if (k < nf) part[static_cast<size_t>(blockIdx.y) * nf + k] = make_double2(d.x + re[m], d.y + im[m]);
     }
 }
 
-__global__ void __launch_bounds__(256) nudft_reduce(const float2 *__restrict__ part, size_t nf, size_t nchunks,
+__global__ void __launch_bounds__(256) nudft_reduce(const double2 *__restrict__ part, size_t nf, size_t nseg,
                                                     float2 *__restrict__ out) {
     const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k >= nf) return;
     double re = 0.0, im = 0.0;
-    for (size_t c = 0; c < nchunks; ++c) {
-        const float2 p = part[c * nf + k];
+    for (size_t c = 0; c < nseg; ++c) {
+        const double2 p = part[c * nf + k];
         re += p.x;
         im += p.y;
     }
     out[k] = make_float2(__double2float_rn(re), __double2float_rn(im));
 }
 
-size_t nudft_chunk(size_t nt) {
-    // terms per thread per chunk: enough chunks to fill the GPU, long enough to amortise
-    // the partial sums; a multiple of the shared-memory tile; at most 65535 chunks (grid.y)
-    size_t chunk = 1024;
-    if (nt < 4 * chunk) chunk = kTileJ;
-    const size_t max_chunks = 65535;
-    if ((nt + chunk - 1) / chunk > max_chunks) {
-        chunk = (nt + max_chunks - 1) / max_chunks;
-        chunk = (chunk + kTileJ - 1) / kTileJ * kTileJ;
-    }
-    return chunk;
+// The fp32 summation length: terms summed in fp32, in order, before they move into fp64 (the
+// error bound's "chunk").  256 for short sums, else 1024.
+size_t nudft_chunk(size_t nt) { return nt < 4096 ? static_cast<size_t>(kTileJ) : 1024; }
+
+// Terms per block row (grid.y = segments): a multiple of the chunk, short enough that the grid
+// has about kNudftTargetBlocks blocks (a fixed count, so the arithmetic is the same on every
+// device), and at most 65535 segments.
+constexpr size_t kNudftTargetBlocks = 8192;
+size_t nudft_segment(size_t nf, size_t nt) {
+    const size_t chunk = nudft_chunk(nt);
+    size_t gx = (nf + kKPerBlock - 1) / kKPerBlock;
+    if (gx < 1) gx = 1;                                                // nf == 0: any (unused) value
+    size_t want = (kNudftTargetBlocks + gx - 1) / gx;                 // segments wanted
+    if (want < 1) want = 1;
+    size_t seg = (nt + want - 1) / want;
+    const size_t min_seg = (nt + 65534) / 65535;
+    if (seg < min_seg) seg = min_seg;
+    seg = (seg + chunk - 1) / chunk * chunk;
+    return seg > 0 ? seg : chunk;
 }
 
 size_t nudft_ws_bytes(size_t nf, size_t nt) {
-    const size_t chunk = nudft_chunk(nt);
-    const size_t nchunks = (nt + chunk - 1) / chunk;
-    return nchunks * nf * sizeof(float2);
+    const size_t seg = nudft_segment(nf, nt);
+    const size_t nseg = (nt + seg - 1) / seg;
+    return nseg * nf * sizeof(double2);
 }
 
 // Packed fp32 for the paper's tables and the specialised method shapes (default on;
@@ -214,7 +241,8 @@ cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, con
                          size_t nt, float *out, void *ws, cudaStream_t stream, const MethodParams *method,
                          int method_nt, int method_fix, int method_spec) {
     size_t chunk = nudft_chunk(nt);
-    const size_t nchunks = (nt + chunk - 1) / chunk;
+    size_t seg = nudft_segment(nf, nt);
+    const size_t nchunks = (nt + seg - 1) / seg;                       // segments (grid.y)
     const size_t gx = (nf + kKPerBlock - 1) / kKPerBlock;
     if (gx > 0x7FFFFFFFu || nchunks > 65535) return cudaErrorInvalidValue;
     const void *fn;
@@ -240,8 +268,8 @@ cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, con
     }
     MethodParams mp = method ? *method : MethodParams{};
     const float2 *a2 = reinterpret_cast<const float2 *>(a);
-    float2 *part = static_cast<float2 *>(ws);
-    void *args[] = {&f, &nf, &t, &a2, &nt, &chunk, &part, &mp};
+    double2 *part = static_cast<double2 *>(ws);
+    void *args[] = {&f, &nf, &t, &a2, &nt, &seg, &chunk, &part, &mp};
     cudaError_t e = cudaLaunchKernel(fn, dim3(static_cast<unsigned>(gx), static_cast<unsigned>(nchunks)),
                                      dim3(kNuThreads), args, 0, stream);
     if (e != cudaSuccess) return e;

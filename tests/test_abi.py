@@ -232,12 +232,18 @@ def test_sass_packed_fused_sum_uses_ffma2():
 
 
 def test_nudft_chunk_rule():
-    """The fused sum's chunk length (it enters the error bound): 256 for short sums, 1024
-    normally, and long enough that the chunk count fits the grid's y extent (65535)."""
+    """The fused sum's fp32 run length (it enters the error bound): 256 for short sums, else
+    1024, whatever nt (longer sums use more segments, not longer fp32 runs)."""
     L = sp.lib()
-    assert L.sincos_nudft_chunk(1000) == 256 and L.sincos_nudft_chunk(1 << 15) == 1024
-    for nt in (1 << 26, 65535 * 1024, 65535 * 1024 + 1, 1 << 27, 10 ** 9, 1 << 36):
-        ch = L.sincos_nudft_chunk(nt)
-        assert ch % 256 == 0 and ch >= 1024 and (nt + ch - 1) // ch <= 65535, (nt, ch)
-        need = -(-nt // 65535)                       # fewest terms per chunk that fit
-        assert ch == max(1024, -(-need // 256) * 256), (nt, ch)
+    assert L.sincos_nudft_chunk(1000) == 256 and L.sincos_nudft_chunk(4095) == 256
+    for nt in (4096, 1 << 15, 1 << 26, 65535 * 1024 + 1, 10 ** 9, 1 << 36):
+        assert L.sincos_nudft_chunk(nt) == 1024
+
+
+def test_nudft_workspace_sizes_host_only():
+    """Pure host functions: no crash or division by zero on degenerate shapes; 16 B per
+    frequency per segment, at most 65535 segments."""
+    L = sp.lib()
+    for nf, nt in ((0, 0), (0, 5), (5, 0), (1, 1), (1 << 15, 1 << 15), (10, 10 ** 9), (10 ** 6, 100)):
+        ws = L.sincos_nudft_workspace_bytes(nf, nt)
+        assert ws % 16 == 0 and ws <= 16 * max(nf, 1) * 65535

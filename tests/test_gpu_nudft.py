@@ -242,10 +242,11 @@ def test_packed_check_negative_control_fails():
 
 
 def test_very_long_sum_chunking():
-    """nt beyond 65535 chunks of 1024 terms (the grid's y extent): the chunk grows; a single
-    unit amplitude far down the sum still returns exactly that term's pair."""
-    nt = (1 << 26) + (1 << 25) + 77            # 100.7 M terms -> chunk 1536
-    assert sp.nudft_chunk(nt) > 1024
+    """nt beyond 65535 x 1024 terms (the grid's y extent at one fp32 run per segment): segments
+    hold several runs; a single unit amplitude far down the sum still returns exactly that
+    term's pair (every partial sum is exact)."""
+    nt = (1 << 26) + (1 << 25) + 77            # 100.7 M terms
+    assert sp.nudft_chunk(nt) == 1024
     f = torch.tensor([0.0, 1.0, 3.25, 77.5], device="cuda")
     t = torch.rand(nt, device="cuda")
     a = torch.zeros(nt, dtype=torch.complex64, device="cuda")

@@ -15,7 +15,7 @@ import os
 
 __all__ = [
     "NORMALIZED", "RENORMALIZED", "SincosError", "lib", "sincos", "sincos_pairs", "sincos_pairs_host",
-    "shard_range", "error_stats", "set_launch_config", "get_launch_config", "set_nudft_packed", "set_realign", "null_4in8out",
+    "shard_range", "error_stats", "set_launch_config", "get_launch_config", "set_nudft_packed", "set_realign", "sincos_turns", "null_4in8out",
     "debug_reciprocal", "launch_count", "host_workspace_min_bytes", "library_path", "sincos_pairs_sharded",
 ]
 
@@ -218,6 +218,23 @@ def phase_grid(f, t, sin_out=None, cos_out=None, interleaved_out=None, units=RAD
                                  _ptr(cos_out, "cos_out"), _ptr(interleaved_out, "interleaved_out"), int(units),
                                  _variant(variant), _stream(stream, f.device))
     _check(st, "sincos_phase_grid")
+
+
+def sincos_turns(x, variant="normalized", interleaved=False, out=None, stream=None):
+    """Pairs of angles given in TURNS (x = theta / 2 pi): the method from the reduction on
+    (P:53-54), without the 1/2 pi scaling and its rounding.  Served by the C-ABI
+    sincos_phase_grid with f = [1] (p = RN(1 * x) = x exactly): one row of nt = n pairs.
+    Returns (sin 2 pi x, cos 2 pi x) or, if interleaved, a (n, 2) tensor of {cos, sin} rows."""
+    import torch
+    one = torch.ones(1, dtype=torch.float32, device=x.device)
+    xf = x.reshape(-1)
+    if interleaved:
+        o = out if out is not None else torch.empty(x.shape + (2,), dtype=torch.float32, device=x.device)
+        phase_grid(one, xf, interleaved_out=o.reshape(-1), units=TURNS, variant=variant, stream=stream)
+        return o
+    s, c = out if out is not None else (torch.empty_like(x), torch.empty_like(x))
+    phase_grid(one, xf, s.reshape(-1), c.reshape(-1), units=TURNS, variant=variant, stream=stream)
+    return s, c
 
 
 def sincos_pairs_method(theta, method: Method, sin_out=None, cos_out=None, interleaved_out=None, stream=None):

@@ -145,3 +145,23 @@ def test_ragged_rows_flat_path(units, variant, flat):
                     assert_parity(iv[1::2], iv[0::2], ws, wc, "inter " + tag)
     finally:
         sp.set_realign(prev)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("inter", [False, True])
+@pytest.mark.parametrize("config", [1, 3, 5])
+def test_sincos_turns(variant, inter, config):
+    """sincos_turns(x): the method on angles given in turns, from the reduction on -- the
+    oracle's phase pairs with f = 1 in turns; BASELINE generators (read as turns), the C3 edge
+    set included, a ragged length (flat kernel) and a multiple of 8 (row kernel)."""
+    for n in ((1 << 18) + 3, 1 << 18):
+        x = inputs.generate(config, 7, n)
+        xd = torch.from_numpy(x).cuda()
+        ws, wc = oracle.phase_points(np.ones_like(x), x, T, variant)
+        if inter:
+            o = sp.sincos_turns(xd, variant=variant, interleaved=True).cpu().numpy()
+            gs, gc = o[:, 1], o[:, 0]
+        else:
+            s, c = sp.sincos_turns(xd, variant=variant)
+            gs, gc = s.cpu().numpy(), c.cpu().numpy()
+        assert_parity(gs, gc, ws, wc, f"turns config={config} n={n}")

@@ -113,9 +113,12 @@ __global__ void __launch_bounds__(kNuThreads, 9) nudft_partial(const float *__re
         im[m] = 0.0f;
         acc[m][threadIdx.x] = make_double2(0.0, 0.0);
     }
+    const unsigned tiles_per_chunk = static_cast<unsigned>(chunk / kTileJ);
+    unsigned tiles = 0;
     for (size_t jt = j0; jt < j1; jt += kTileJ) {
         // every `chunk` terms (a multiple of the tile) the fp32 sums move into fp64
-        if (jt != j0 && (jt - j0) % chunk == 0) {
+        if (tiles++ == tiles_per_chunk) {
+            tiles = 1;
 #pragma unroll
             for (int m = 0; m < kKPerThread; ++m) {
                 double2 d = acc[m][threadIdx.x];

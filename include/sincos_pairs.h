@@ -77,9 +77,14 @@ typedef enum {
  *                    P:262; reading G13).  Exactly one form must be given.
  *   n                element count; 0 is a no-op (pointers may then be NULL).
  *
- * Any 4-B aligned pointers are accepted.  When theta and the outputs share
- * their alignment the body runs 256-bit vector loads/stores; otherwise a
- * scalar path with identical numerics.  theta_dev == sin_dev or
+ * Any 4-B aligned pointers are accepted; every path has identical numerics.
+ * When theta and the outputs share their alignment the body runs 256-bit
+ * vector loads/stores (128-bit if they share only 16 B); otherwise, if the
+ * outputs can still take whole-sector stores (split: sin and cos at one offset
+ * mod 16 B; interleaved: 8-B aligned), theta is read as aligned vectors and
+ * re-aligned in registers (warp shuffles; sincos_set_realign); otherwise one
+ * element per thread.  A scalar head and tail cover the ragged ends.
+ * theta_dev == sin_dev or
  * theta_dev == cos_dev (exact in-place) is allowed.  Validation happens
  * before any CUDA call; the return value reports validation and the launch
  * status only (the kernel itself cannot fail short of invalid addresses).
@@ -111,8 +116,10 @@ SINCOS_API size_t sincos_host_workspace_min_bytes(void);
  * method's fp32 result to out_dtype -- IEEE binary16 or bfloat16 (2 B per value; 8 B per
  * pair of traffic instead of 12) -- or fp32 (= sincos_pairs).  Outputs are 2-B aligned
  * uint16 arrays (split) or n {cos, sin} 16-bit pairs (interleaved); theta must not overlap
- * them.  Vector path when theta is 32-B and the outputs 16-B (split) / 32-B (interleaved)
- * aligned after the same scalar head, otherwise one element per thread; identical values.
+ * them.  Vector path (8 pairs per thread; 128-bit split / 256-bit interleaved stores) when
+ * sin and cos share their offset mod 16 B (interleaved: always), theta read as one aligned
+ * 256-bit vector or re-aligned in registers when it sits off the outputs' alignment
+ * (sincos_set_realign); otherwise one element per thread; identical values.
  *
  * sincos_interleave / sincos_deinterleave: fp32 split (sin[], cos[]) <-> interleaved
  * ({cos, sin} float2) copies; no overlap allowed.
@@ -138,8 +145,10 @@ SINCOS_API sincos_status_t sincos_deinterleave(const float *inter_dev, float *si
  * for penultimate magnitudes^2 in [0.5, 2), i.e. any usable fit), 3 = none.
  * The paper's two methods are {its coefficients, n_ss 4, n_cc 3, doublings 2, fix 0/1}
  * and give bit-identical results to sincos_pairs.  Same buffers, alignment and error
- * conventions as sincos_pairs (in-place not supported).  `method` is a host pointer,
- * read before return.
+ * conventions as sincos_pairs (in-place not supported); vector path (256-bit stores) when
+ * the outputs allow it (split: sin and cos at one offset mod 32 B; interleaved: 8-B
+ * aligned), theta re-aligned in registers when needed, else one element per thread.
+ * `method` is a host pointer, read before return.
  */
 typedef struct {
     float ss[8];

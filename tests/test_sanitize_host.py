@@ -1,0 +1,27 @@
+"""The host C code -- the oracle (oracle/*.c) and the input generators (inputs/gen.c) -- under
+AddressSanitizer and UndefinedBehaviorSanitizer (SURVEY 4 sanitizer row; CPU only).
+tests/c/oracle_sanitize.c calls every entry point on exactly-sized buffers, degenerate shapes
+and special values; any sanitizer report aborts it (-fno-sanitize-recover=all)."""
+import glob
+import os
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.skipif(shutil.which("gcc") is None, reason="needs gcc")
+def test_oracle_and_generators_clean_under_asan_ubsan(tmp_path):
+    exe = str(tmp_path / "oracle_sanitize")
+    srcs = [os.path.join(ROOT, "tests", "c", "oracle_sanitize.c")] + sorted(
+        glob.glob(os.path.join(ROOT, "oracle", "*.c"))) + [os.path.join(ROOT, "inputs", "gen.c")]
+    cmd = ["gcc", "-std=c99", "-D_GNU_SOURCE", "-O1", "-g", "-fno-omit-frame-pointer", "-ffp-contract=off",
+           "-fsanitize=address,undefined", "-fno-sanitize-recover=all", "-fopenmp", "-o", exe, *srcs, "-lm"]
+    subprocess.check_call(cmd)
+    env = dict(os.environ, ASAN_OPTIONS="detect_leaks=1:abort_on_error=1", UBSAN_OPTIONS="print_stacktrace=1",
+               OMP_NUM_THREADS="2")
+    r = subprocess.run([exe], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "oracle_sanitize: ok" in r.stdout

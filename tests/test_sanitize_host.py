@@ -25,3 +25,26 @@ def test_oracle_and_generators_clean_under_asan_ubsan(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, env=env, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "oracle_sanitize: ok" in r.stdout
+
+
+@pytest.mark.skipif(shutil.which("gcc") is None or shutil.which("nvcc") is None and
+                    not os.path.exists("/usr/local/cuda/bin/nvcc"), reason="needs gcc and nvcc")
+def test_library_host_logic_clean_under_asan_ubsan(tmp_path):
+    """The library's host code (argument validation before any CUDA call, the sharder's
+    range arithmetic up to n = 2^64 - 1, workspace sizing, tuning knobs) built with
+    -fsanitize=address,undefined and driven without a GPU (tests/c/abi_sanitize.py)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_cs_0406049_b200 import _build
+    lib = str(tmp_path / "libsincos_san.so")
+    flags = list(_build.NVCC_FLAGS)
+    i = flags.index("-Xcompiler")
+    flags[i + 1] += ",-fsanitize=address,-fsanitize=undefined,-fno-omit-frame-pointer"
+    subprocess.check_call([_build.nvcc(), *flags, "-Xlinker", "-lasan", "-Xlinker", "-lubsan", "-o", lib,
+                           *_build.sources()], cwd=_build.PKG)
+    pre = " ".join(subprocess.check_output(["gcc", f"-print-file-name={x}"], text=True).strip()
+                   for x in ("libasan.so", "libubsan.so"))
+    env = dict(os.environ, LD_PRELOAD=pre, ASAN_OPTIONS="detect_leaks=0", UBSAN_OPTIONS="halt_on_error=1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "c", "abi_sanitize.py"), lib],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0 and "san_abi ok" in r.stdout, r.stdout + r.stderr[-3000:]

@@ -15,7 +15,7 @@ import os
 
 __all__ = [
     "NORMALIZED", "RENORMALIZED", "SincosError", "lib", "sincos", "sincos_pairs", "sincos_pairs_host",
-    "shard_range", "error_stats", "set_launch_config", "get_launch_config", "set_nudft_packed", "set_realign", "sincos_turns", "null_4in8out",
+    "shard_range", "error_stats", "set_launch_config", "get_launch_config", "set_nudft_packed", "set_realign", "sincos_turns", "cis", "null_4in8out",
     "debug_reciprocal", "launch_count", "host_workspace_min_bytes", "library_path", "sincos_pairs_sharded",
 ]
 
@@ -218,6 +218,14 @@ def phase_grid(f, t, sin_out=None, cos_out=None, interleaved_out=None, units=RAD
                                  _ptr(cos_out, "cos_out"), _ptr(interleaved_out, "interleaved_out"), int(units),
                                  _variant(variant), _stream(stream, f.device))
     _check(st, "sincos_phase_grid")
+
+
+def cis(theta, variant="normalized", stream=None):
+    """e^{i theta} as a complex64 tensor of theta's shape: the interleaved {cos, sin} output of
+    the hot path viewed as complex (reading G13: struct phase {c, s} = re, im)."""
+    import torch
+    o = sincos(theta, variant=variant, interleaved=True, stream=stream)
+    return torch.view_as_complex(o)
 
 
 def sincos_turns(x, variant="normalized", interleaved=False, out=None, stream=None):

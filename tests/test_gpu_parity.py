@@ -571,3 +571,14 @@ def test_all_fp32_bit_patterns_next_kernels(golden, variant, name, path):
         H, NN, EX = (H + h) % (1 << 64), NN + nn, EX + ex
     assert "0x%016X" % H == want["hash"], path
     assert NN == want["nan_pairs"] and EX == want["exact_0_1"]
+
+
+def test_cis_complex_view():
+    """cis(theta) = e^{i theta} as complex64: real part the method's cos, imaginary its sin."""
+    th = inputs.generate(1, 0, 3000).reshape(3, 1000)
+    t = torch.from_numpy(th).cuda()
+    z = sp.cis(t)
+    assert z.dtype == torch.complex64 and z.shape == t.shape
+    ws, wc = oracle.sincos(th.ravel(), 0)
+    zz = z.cpu().numpy().ravel()
+    assert_parity(zz.imag.copy(), zz.real.copy(), ws, wc, "cis")

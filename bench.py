@@ -313,6 +313,32 @@ def measure_methods(dev, stream, th, outs, peak, reps=10):
     return res
 
 
+def measure_cuda_functions(dev, stream, th, outs, peak, reps=10):
+    """Context (SURVEY 8(d) optional rows): the hot path's kernel shape with CUDA's sincosf and
+    __sincosf instead of the paper's method, same 12 B/pair traffic on the C2 batch -- an
+    HBM-bound kernel sits at the same roofline whatever the per-element math."""
+    import torch
+
+    import paper_cs_0406049_b200 as sp
+    n = th.numel()
+    res = {"workload": "C2 batch, split outputs", "bytes_per_pair": BYTES_PER_PAIR, "peak": peak,
+           "note": "not the paper's method; context only"}
+    s, c = outs
+    for which, name in ((3, "cuda_sincosf"), (4, "cuda___sincosf")):
+        for _ in range(2):
+            sp.compare_cuda(th, s, c, which=which, stream=stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            sp.compare_cuda(th, s, c, which=which, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = a.elapsed_time(b) / reps
+        gbs = BYTES_PER_PAIR * n / (ms / 1e3) / 1e9
+        res[name] = {"ms": ms, "GBps": gbs, "frac": gbs / peak}
+    return res
+
+
 def measure_dtypes(dev, stream, th, peak, reps=10):
     """NEXT(4) side measurement: sincos_pairs_dtype with 16-bit split outputs on the C2 batch
     (8 algorithmic bytes per pair: 4 in, 2 x 2 out)."""
@@ -571,6 +597,8 @@ def run_ours(args, rank, world, local_rank):
         o = outs[sp.NORMALIZED]
         methods_res = measure_methods(dev, stream, th, (o["sin_out"], o["cos_out"]), peak)
         methods_res["dtypes"] = measure_dtypes(dev, stream, th, peak)
+        methods_res["context_cuda_functions"] = measure_cuda_functions(dev, stream, th,
+                                                                       (o["sin_out"], o["cos_out"]), peak)
 
     # end to end through the C ABI with host buffers, copies inside the timed region
     e2e = None

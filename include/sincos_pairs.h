@@ -315,6 +315,13 @@ SINCOS_API int sincos_set_nudft_packed(int on);
 SINCOS_API sincos_status_t sincos_null_4in8out(const float *theta_dev, float *sin_dev, float *cos_dev,
                                     float *inter_dev, size_t n, void *stream);
 
+/* Context kernels (bench only, not the paper's method): the same 4-in / 8-out streaming
+ * kernel with CUDA's own functions -- which = 3: libm sincosf (accurate; Payne-Hanek slow
+ * path for large |theta|), 4: the __sincosf intrinsic.  Buffers 32-B aligned (else
+ * INVALID_ARGUMENT), no in-place; otherwise as sincos_pairs. */
+SINCOS_API sincos_status_t sincos_compare_cuda(const float *theta_dev, float *sin_dev, float *cos_dev,
+                                               float *inter_dev, size_t n, int which, void *stream);
+
 /* Test hook: the packed-fp32 form of the method (sm_100a FFMA2/FMUL2/FADD2, used by the
  * fused sum) against the scalar form, for EVERY one of the 2^32 fp32 inputs, in radians and
  * in turns.  method == NULL: the paper's table of `variant`; else a specialised method shape

@@ -98,6 +98,7 @@ _SIGS = {
     "sincos_debug_packed_check": (_I, [_I, _P, _P, _P]),
     "sincos_get_launch_config": (None, [ctypes.POINTER(_I)] * 5),
     "sincos_null_4in8out": (_I, [_P, _P, _P, _P, _S, _P]),
+    "sincos_compare_cuda": (_I, [_P, _P, _P, _P, _S, _I, _P]),
     "sincos_debug_reciprocal": (_I, [_P, _P, _S, _P]),
     "sincos_status_string": (ctypes.c_char_p, [_I]),
     "sincos_last_cuda_error": (_I, []),
@@ -452,6 +453,13 @@ def get_launch_config() -> dict:
     v = [ctypes.c_int() for _ in range(5)]
     lib().sincos_get_launch_config(*[ctypes.byref(x) for x in v])
     return dict(zip(("threads", "blocks_per_sm", "vec", "unroll", "prefetch"), (x.value for x in v)))
+
+
+def compare_cuda(theta, sin_out=None, cos_out=None, interleaved_out=None, which=3, stream=None):
+    """Context (bench): the hot path's kernel shape with CUDA sincosf (which=3) or __sincosf (4)."""
+    _check(lib().sincos_compare_cuda(_ptr(theta, "theta"), _ptr(sin_out, "sin_out"), _ptr(cos_out, "cos_out"),
+                                     _ptr(interleaved_out, "interleaved_out"), theta.numel(), int(which),
+                                     _stream(stream, theta.device)), "sincos_compare_cuda")
 
 
 def null_4in8out(theta, sin_out=None, cos_out=None, interleaved_out=None, stream=None):

@@ -233,6 +233,26 @@ sincos_status_t sincos_pairs(const float *theta_dev, float *sin_dev, float *cos_
     return launch(theta_dev, sin_dev, cos_dev, inter_dev, n, variant, static_cast<cudaStream_t>(stream));
 }
 
+sincos_status_t sincos_compare_cuda(const float *theta_dev, float *sin_dev, float *cos_dev, float *inter_dev,
+                                    size_t n, int which, void *stream) {
+    if (which != 3 && which != 4) return SINCOS_ERR_INVALID_ARGUMENT;
+    sincos_status_t st = validate(theta_dev, sin_dev, cos_dev, inter_dev, n, SINCOS_NORMALIZED, false);
+    if (st != SINCOS_OK || n == 0) return st;
+    const bool inter = inter_dev != nullptr;
+    if (!aligned(theta_dev, 32) || (inter ? !aligned(inter_dev, 32) : !aligned(sin_dev, 32) || !aligned(cos_dev, 32)))
+        return SINCOS_ERR_INVALID_ARGUMENT;
+    if (theta_dev == sin_dev || theta_dev == cos_dev) return SINCOS_ERR_OVERLAP;
+    const size_t nvec = n / 8;
+    size_t grid = (nvec + 127) / 128;
+    if (grid < 1) grid = 1;
+    if (grid > 0x7FFFFFFFu) grid = 0x7FFFFFFFu;
+    cudaError_t e = launch_compare(which, inter, static_cast<unsigned>(grid), 128, theta_dev, sin_dev, cos_dev,
+                                   inter_dev, nvec, n, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SINCOS_OK;
+}
+
 sincos_status_t sincos_null_4in8out(const float *theta_dev, float *sin_dev, float *cos_dev, float *inter_dev,
                                     size_t n, void *stream) {
     sincos_status_t st = validate(theta_dev, sin_dev, cos_dev, inter_dev, n, 2, true);

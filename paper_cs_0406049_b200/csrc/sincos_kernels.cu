@@ -29,12 +29,20 @@
 namespace sincos_b200 {
 
 constexpr int kNull = 2;  // KB4: the traffic-ceiling "variant"
+// Context only (bench): CUDA's own functions with the same traffic -- libm sincosf (accurate,
+// Payne-Hanek slow path for large arguments) and the __sincosf intrinsic.
+constexpr int kCmpSincosf = 3;
+constexpr int kCmpIntrinsic = 4;
 
 template <int V>
 __device__ __forceinline__ void op(float t, float &s, float &c) {
     if constexpr (V == kNull) {
         s = t;
         c = t;
+    } else if constexpr (V == kCmpSincosf) {
+        sincosf(t, &s, &c);
+    } else if constexpr (V == kCmpIntrinsic) {
+        __sincosf(t, &s, &c);
     } else {
         sincos_pair<V>(t, s, c);
     }
@@ -374,6 +382,21 @@ cudaError_t launch_shift(int variant, bool inter, int k, unsigned grid, unsigned
 cudaError_t launch_rcp(unsigned grid, unsigned threads, const float *d, float *out, size_t n, cudaStream_t stream) {
     void *args[] = {&d, &out, &n};
     return cudaLaunchKernel(reinterpret_cast<const void *>(rcp_kernel), dim3(grid), dim3(threads), args, 0, stream);
+}
+
+// Context kernels (kCmpSincosf / kCmpIntrinsic): the default launch shape only (256-bit, U = 1).
+cudaError_t launch_compare(int which, bool inter, unsigned grid, unsigned threads, const float *theta, float *so,
+                           float *co, float *io, size_t nvec, size_t n, cudaStream_t stream) {
+    VecFn fn;
+    if (which == kCmpSincosf)
+        fn = inter ? sincos_vec_kernel<kCmpSincosf, true, 8, 1, true, false>
+                   : sincos_vec_kernel<kCmpSincosf, false, 8, 1, true, false>;
+    else
+        fn = inter ? sincos_vec_kernel<kCmpIntrinsic, true, 8, 1, true, false>
+                   : sincos_vec_kernel<kCmpIntrinsic, false, 8, 1, true, false>;
+    size_t head = 0;
+    void *args[] = {&theta, &so, &co, &io, &head, &nvec, &n};
+    return cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(threads), args, 0, stream);
 }
 
 const void *vec_kernel_ptr(int variant, bool inter, int w, int unroll, bool nc, bool pf) {

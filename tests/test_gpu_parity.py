@@ -582,3 +582,28 @@ def test_cis_complex_view():
     ws, wc = oracle.sincos(th.ravel(), 0)
     zz = z.cpu().numpy().ravel()
     assert_parity(zz.imag.copy(), zz.real.copy(), ws, wc, "cis")
+
+
+@pytest.mark.parametrize("which", [3, 4])
+@pytest.mark.parametrize("inter", [False, True])
+def test_compare_cuda_context_kernels(which, inter):
+    """The bench's context kernels (CUDA sincosf / __sincosf in the hot path's kernel shape) run
+    and compute sin/cos (loose check against torch's fp64), ragged tail included; misaligned
+    buffers are refused."""
+    n = (1 << 16) + 5
+    t = torch.rand(n, device="cuda", dtype=torch.float32) * 20 - 10
+    if inter:
+        o = torch.empty(2 * n, device="cuda")
+        sp.compare_cuda(t, interleaved_out=o, which=which)
+        s, c = o[1::2], o[0::2]
+    else:
+        s, c = torch.empty_like(t), torch.empty_like(t)
+        sp.compare_cuda(t, s, c, which=which)
+    torch.cuda.synchronize()
+    td = t.double()
+    tol = 1e-6 if which == 3 else 1e-5
+    assert torch.max(torch.abs(s.double() - torch.sin(td))) < tol
+    assert torch.max(torch.abs(c.double() - torch.cos(td))) < tol
+    with pytest.raises(sp.SincosError):
+        sp.compare_cuda(t[1:], s[1:], c[1:], which=which) if not inter else \
+            sp.compare_cuda(t[1:], interleaved_out=o[2:], which=which)

@@ -607,3 +607,37 @@ def test_compare_cuda_context_kernels(which, inter):
     with pytest.raises(sp.SincosError):
         sp.compare_cuda(t[1:], s[1:], c[1:], which=which) if not inter else \
             sp.compare_cuda(t[1:], interleaved_out=o[2:], which=which)
+
+
+@pytest.mark.parametrize("inter", [False, True])
+def test_c5_full_size_realigned(inter):
+    """2^32 angles with theta one float off the outputs: the re-aligning kernel over 64-bit
+    element indices (every warp's shuffles and the last lanes' own loads past 2^31 and up to
+    2^32 - 1); sampled elements vs the oracle, the last element included."""
+    n = inputs.size(5)
+    tb = torch.empty(n + 8, dtype=torch.float32, device="cuda")
+    chunk = 1 << 28
+    for off in range(0, n, chunk):
+        m = min(chunk, n - off)
+        tb[1 + off:1 + off + m].copy_(torch.from_numpy(inputs.generate(5, off, m)))
+    th = tb[1:1 + n]
+    if inter:
+        io = torch.empty(2 * n, dtype=torch.float32, device="cuda")
+        sp.sincos_pairs(th, interleaved_out=io, variant=1)
+    else:
+        s = torch.empty(n, dtype=torch.float32, device="cuda")
+        c = torch.empty(n, dtype=torch.float32, device="cuda")
+        sp.sincos_pairs(th, s, c, variant=1)
+    torch.cuda.synchronize()
+    idx = sampled_indices(n, seed=55)
+    it = torch.from_numpy(idx).cuda()
+    want_th = inputs.generate_at(5, idx.astype(np.uint64))
+    os_, oc = oracle.sincos(want_th, 1)
+    if inter:
+        gs, gc = io[2 * it + 1].cpu().numpy(), io[2 * it].cpu().numpy()
+    else:
+        gs, gc = s[it].cpu().numpy(), c[it].cpu().numpy()
+    assert_parity(gs, gc, os_, oc, f"C5 realigned inter={inter}")
+    assert int(idx.max()) == n - 1
+    del tb, th
+    torch.cuda.empty_cache()

@@ -554,6 +554,32 @@ def run_ours(args, rank, world, local_rank):
             "per_variant_ms_median_min": {vname[v]: [statistics.median(per_kernel[v]), min(per_kernel[v])]
                                           for v in variants}}
 
+    # energy (outside the timed region): steps back to back for >= 2 s, the board's energy
+    # counter (NVML, mJ) read before and after -> joules per step, pairs per joule, mean power
+    energy = None
+    if clk.ok and rank == 0:
+        try:
+            nv, h = clk.nv, clk.h
+            steps_e = max(1, int(2.0 / max(ms_max / args.steps / 1e3, 1e-6)))
+            torch.cuda.synchronize(dev)
+            e_a, t_a = nv.nvmlDeviceGetTotalEnergyConsumption(h), time.perf_counter()
+            for _ in range(steps_e):
+                if use_graph:
+                    step_graph.replay()
+                else:
+                    for v in variants:
+                        sp.sincos_pairs(th, variant=v, stream=stream, **outs[v])
+            torch.cuda.synchronize(dev)
+            e_b, t_b = nv.nvmlDeviceGetTotalEnergyConsumption(h), time.perf_counter()
+            joules = (e_b - e_a) / 1e3
+            pairs_e = len(variants) * n * steps_e
+            energy = {"steps": steps_e, "seconds": t_b - t_a, "joules": joules,
+                      "mean_power_w": joules / (t_b - t_a), "pairs_per_joule": pairs_e / joules,
+                      "joules_per_step": joules / steps_e,
+                      "how": "NVML total energy counter around back-to-back steps (this GPU, one rank)"}
+        except Exception as e:  # counter not supported: no energy figure
+            energy = {"error": repr(e)}
+
     # traffic ceiling: same access pattern and launch, no arithmetic (outside the timed region)
     o = outs[sp.NORMALIZED]
     for _ in range(3):
@@ -683,6 +709,7 @@ def run_ours(args, rank, world, local_rank):
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.result(),
+            "energy": energy,
             "max_error": summary["max_err"],
             "rms_error": summary["rms_err"],
             "error_reference": "fp64 sin/cos on the device (P:137-138 metric); large-|theta| reduction error "

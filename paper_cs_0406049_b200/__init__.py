@@ -174,6 +174,26 @@ def _stream(stream, device) -> int:
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
+def _on_tensor_device(fn):
+    """Run a device entry point with the CUDA device of its tensors current (the C ABI works on
+    the current device's buffers and stream); tensors on two different devices are refused."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(*args, **kwargs):
+        import torch
+        devs = {a.device for a in list(args) + list(kwargs.values())
+                if isinstance(a, torch.Tensor) and a.is_cuda}
+        if len(devs) > 1:
+            raise ValueError(f"{fn.__name__}: tensors on different devices {sorted(map(str, devs))}")
+        if not devs:
+            return fn(*args, **kwargs)
+        with torch.cuda.device(next(iter(devs))):
+            return fn(*args, **kwargs)
+    return wrapped
+
+
+@_on_tensor_device
 def sincos_pairs(theta, sin_out=None, cos_out=None, interleaved_out=None, variant=NORMALIZED, stream=None):
     """C-ABI sincos_pairs on CUDA tensors (asynchronous on `stream`, default: current stream).
 
@@ -204,6 +224,7 @@ def sincos(theta, variant="normalized", interleaved=False, out=None, stream=None
     return s, c
 
 
+@_on_tensor_device
 def phase_grid(f, t, sin_out=None, cos_out=None, interleaved_out=None, units=RADIANS, variant=NORMALIZED,
                stream=None):
     """NEXT(1) C-ABI sincos_phase_grid: pairs of p_ij = RN(f[i] * t[j]) (radians, or turns with
@@ -246,6 +267,7 @@ def sincos_turns(x, variant="normalized", interleaved=False, out=None, stream=No
     return s, c
 
 
+@_on_tensor_device
 def sincos_pairs_method(theta, method: Method, sin_out=None, cos_out=None, interleaved_out=None, stream=None):
     """NEXT(3) C-ABI sincos_pairs_method: the method with the given series / doublings / fix."""
     n = theta.numel()
@@ -263,6 +285,7 @@ def _ptr_any(t, name: str):
     return t.data_ptr()
 
 
+@_on_tensor_device
 def sincos_pairs_dtype(theta, sin_out=None, cos_out=None, interleaved_out=None, variant=NORMALIZED, stream=None):
     """NEXT(4) C-ABI sincos_pairs_dtype: outputs in the dtype of the given tensors (float32,
     float16 or bfloat16); 16-bit values are the method's fp32 pair rounded to nearest even."""
@@ -278,6 +301,7 @@ def sincos_pairs_dtype(theta, sin_out=None, cos_out=None, interleaved_out=None, 
     _check(st, "sincos_pairs_dtype")
 
 
+@_on_tensor_device
 def interleave(sin_in, cos_in, interleaved_out, stream=None):
     """NEXT(4): split fp32 (sin[], cos[]) -> interleaved {cos, sin}."""
     st = lib().sincos_interleave(_ptr(sin_in, "sin"), _ptr(cos_in, "cos"), _ptr(interleaved_out, "inter"),
@@ -285,6 +309,7 @@ def interleave(sin_in, cos_in, interleaved_out, stream=None):
     _check(st, "sincos_interleave")
 
 
+@_on_tensor_device
 def deinterleave(interleaved_in, sin_out, cos_out, stream=None):
     """NEXT(4): interleaved {cos, sin} fp32 -> split (sin[], cos[])."""
     st = lib().sincos_deinterleave(_ptr(interleaved_in, "inter"), _ptr(sin_out, "sin"), _ptr(cos_out, "cos"),
@@ -296,6 +321,7 @@ def nudft_chunk(nt: int) -> int:
     return int(lib().sincos_nudft_chunk(nt))
 
 
+@_on_tensor_device
 def nudft(f, t, a, out=None, units=RADIANS, variant=NORMALIZED, workspace=None, stream=None, method=None):
     """NEXT(2) C-ABI sincos_nudft: out[k] = sum_j a[j] e^{i RN(f[k] t[j])} (complex64 a, out;
     float32 f, t; CUDA tensors).  With `method` (a Method), sincos_nudft_method: the pairs of
@@ -400,6 +426,7 @@ def nccl_available() -> bool:
     return bool(lib().sincos_nccl_available())
 
 
+@_on_tensor_device
 def error_stats(theta, sin_out=None, cos_out=None, interleaved_out=None, stream=None) -> dict:
     """KB5 fp64 error statistics of outputs on the device (P:135-139 metrics)."""
     import torch
@@ -455,6 +482,7 @@ def get_launch_config() -> dict:
     return dict(zip(("threads", "blocks_per_sm", "vec", "unroll", "prefetch"), (x.value for x in v)))
 
 
+@_on_tensor_device
 def compare_cuda(theta, sin_out=None, cos_out=None, interleaved_out=None, which=3, stream=None):
     """Context (bench): the hot path's kernel shape with CUDA sincosf (which=3) or __sincosf (4)."""
     _check(lib().sincos_compare_cuda(_ptr(theta, "theta"), _ptr(sin_out, "sin_out"), _ptr(cos_out, "cos_out"),
@@ -462,12 +490,14 @@ def compare_cuda(theta, sin_out=None, cos_out=None, interleaved_out=None, which=
                                      _stream(stream, theta.device)), "sincos_compare_cuda")
 
 
+@_on_tensor_device
 def null_4in8out(theta, sin_out=None, cos_out=None, interleaved_out=None, stream=None):
     _check(lib().sincos_null_4in8out(_ptr(theta, "theta"), _ptr(sin_out, "sin_out"), _ptr(cos_out, "cos_out"),
                                      _ptr(interleaved_out, "interleaved_out"), theta.numel(),
                                      _stream(stream, theta.device)), "sincos_null_4in8out")
 
 
+@_on_tensor_device
 def debug_reciprocal(d, out, stream=None):
     _check(lib().sincos_debug_reciprocal(_ptr(d, "d"), _ptr(out, "out"), d.numel(), _stream(stream, d.device)),
            "sincos_debug_reciprocal")

@@ -641,3 +641,25 @@ def test_c5_full_size_realigned(inter):
     assert int(idx.max()) == n - 1
     del tb, th
     torch.cuda.empty_cache()
+
+
+def test_binding_refuses_mixed_devices_and_follows_tensor_device():
+    """The binding runs each call on its tensors' device (made current for the call) and refuses
+    tensors on two devices; on a 1-GPU box the mixed case is CPU + CUDA (refused as before) and
+    the current device is left unchanged."""
+    t = torch.rand(100, device="cuda")
+    s, c = torch.empty_like(t), torch.empty_like(t)
+    cur = torch.cuda.current_device()
+    sp.sincos_pairs(t, s, c)
+    assert torch.cuda.current_device() == cur
+    with pytest.raises(ValueError):
+        sp.sincos_pairs(t, torch.empty(100), c)
+    if torch.cuda.device_count() > 1:
+        t1 = torch.rand(100, device="cuda:1")
+        with pytest.raises(ValueError):
+            sp.sincos_pairs(t1, s, c)
+        s1, c1 = torch.empty_like(t1), torch.empty_like(t1)
+        sp.sincos_pairs(t1, s1, c1)                    # runs on device 1 though 0 is current
+        torch.cuda.synchronize(1)
+        ws, wc = oracle.sincos(t1.cpu().numpy(), 0)
+        assert_parity(s1.cpu().numpy(), c1.cpu().numpy(), ws, wc, "device 1")

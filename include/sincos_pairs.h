@@ -197,7 +197,7 @@ SINCOS_API sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, cons
  *   a_dev    nt complex64 amplitudes, interleaved {re, im} (8-B aligned)
  *   out_dev  nf complex64 results, interleaved {re, im} (8-B aligned)
  *   ws_dev   device workspace of >= sincos_nudft_workspace_bytes(nf, nt) bytes
- *            (8-B aligned), not overlapping anything else
+ *            (16-B aligned), not overlapping anything else
  * Arithmetic: complex products and sums in fp32 with FMA over runs ("chunks") of
  * sincos_nudft_chunk(nt) consecutive terms (256 for nt < 4096, else 1024), summed in
  * order; each run's sum is added into fp64, the terms split into segments for

@@ -456,7 +456,7 @@ sincos_status_t nudft_impl(const float *f_dev, size_t nf, const float *t_dev, co
         return e == cudaSuccess ? SINCOS_OK : cuda_fail(e);
     }
     if (t_dev == nullptr || a_dev == nullptr || ws_dev == nullptr || !aligned(t_dev, 4) || !aligned(a_dev, 8) ||
-        !aligned(ws_dev, 8))
+        !aligned(ws_dev, 16))                            // fp64 {re, im} partials: 16-B accesses
         return SINCOS_ERR_INVALID_ARGUMENT;
     const size_t need = nudft_ws_bytes(nf, nt);
     if (ws_bytes < need) return SINCOS_ERR_INVALID_ARGUMENT;

@@ -258,3 +258,17 @@ def test_very_long_sum_chunking():
     want = np.array([oracle.pair_from_q(float(x), 0) for x in q])
     assert np.array_equal(out.real.astype(np.float32), want[:, 1].astype(np.float32))
     assert np.array_equal(out.imag.astype(np.float32), want[:, 0].astype(np.float32))
+
+
+def test_workspace_alignment_and_size_checked():
+    """The fp64 partials need a 16-B aligned workspace of sincos_nudft_workspace_bytes(nf, nt):
+    an 8-B offset or one byte short is INVALID_ARGUMENT, not a fault."""
+    f = torch.rand(100, device="cuda")
+    t = torch.rand(5000, device="cuda")
+    a = torch.randn(5000, dtype=torch.complex64, device="cuda")
+    need = sp.lib().sincos_nudft_workspace_bytes(100, 5000)
+    ws = torch.empty(need + 64, dtype=torch.uint8, device="cuda")
+    sp.nudft(f, t, a, workspace=ws[16:16 + need])                 # 16-B aligned: fine
+    for bad in (ws[8:8 + need], ws[:need - 1]):
+        with pytest.raises(sp.SincosError):
+            sp.nudft(f, t, a, workspace=bad)

@@ -278,8 +278,9 @@ SINCOS_API sincos_status_t sincos_pairs_sharded_stats(const sincos_shard_t *shar
 SINCOS_API int sincos_nccl_available(void);
 
 SINCOS_API size_t sincos_stats_workspace_bytes(void);
-/* stats_dev: device pointer to one sincos_stats_t; ws_dev: device workspace of
- * sincos_stats_workspace_bytes(). */
+/* stats_dev: device pointer to one sincos_stats_t (8-B aligned); ws_dev: device workspace
+ * of sincos_stats_workspace_bytes() (8-B aligned), not shared by concurrent calls.
+ * Outputs as in sincos_pairs (split or interleaved, 4-B aligned).  Asynchronous. */
 SINCOS_API sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
                                    const float *cos_dev, const float *inter_dev, size_t n,
                                    sincos_stats_t *stats_dev, void *ws_dev, void *stream);

@@ -595,6 +595,11 @@ sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
     const bool inter = sin_dev == nullptr && cos_dev == nullptr && inter_dev != nullptr;
     if (stats_dev == nullptr || ws_dev == nullptr || (n > 0 && (theta_dev == nullptr || !(split || inter))))
         return SINCOS_ERR_INVALID_ARGUMENT;
+    // fp64 / 64-bit fields in the record and the workspace; fp32 arrays
+    if (!aligned(stats_dev, 8) || !aligned(ws_dev, 8) ||
+        (n > 0 && (!aligned(theta_dev, 4) || (split && (!aligned(sin_dev, 4) || !aligned(cos_dev, 4))) ||
+                   (inter && !aligned(inter_dev, 4)))))
+        return SINCOS_ERR_INVALID_ARGUMENT;
     cudaError_t e = launch_stats(theta_dev, sin_dev, cos_dev, inter_dev, n, stats_dev, ws_dev,
                                  static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e);

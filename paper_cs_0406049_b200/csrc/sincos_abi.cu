@@ -671,7 +671,8 @@ sincos_status_t sincos_debug_packed_check(int variant, const sincos_method_t *me
 
 sincos_status_t sincos_debug_reciprocal(const float *d_dev, float *out_dev, size_t n, void *stream) {
     if (n == 0) return SINCOS_OK;
-    if (d_dev == nullptr || out_dev == nullptr) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (d_dev == nullptr || out_dev == nullptr || !aligned(d_dev, 4) || !aligned(out_dev, 4))
+        return SINCOS_ERR_INVALID_ARGUMENT;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e);

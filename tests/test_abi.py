@@ -247,3 +247,32 @@ def test_nudft_workspace_sizes_host_only():
     for nf, nt in ((0, 0), (0, 5), (5, 0), (1, 1), (1 << 15, 1 << 15), (10, 10 ** 9), (10 ** 6, 100)):
         ws = L.sincos_nudft_workspace_bytes(nf, nt)
         assert ws % 16 == 0 and ws <= 16 * max(nf, 1) * 65535
+
+
+def test_alignment_checks_of_the_other_entry_points(L):
+    """Every entry point refuses pointers its kernels could not access aligned -- before any
+    CUDA call (fake addresses are never dereferenced)."""
+    P, S, I = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+    L.sincos_error_stats.argtypes = [P, P, P, P, S, P, P, P]
+    L.sincos_error_stats.restype = I
+    assert L.sincos_error_stats(A, 2 * A, 3 * A, None, 16, 4 * A + 4, 5 * A, None) == INVALID   # record 4-B
+    assert L.sincos_error_stats(A, 2 * A, 3 * A, None, 16, 4 * A, 5 * A + 4, None) == INVALID   # workspace
+    assert L.sincos_error_stats(A + 2, 2 * A, 3 * A, None, 16, 4 * A, 5 * A, None) == INVALID   # theta 2-B
+    L.sincos_nudft.argtypes = [P, S, P, P, S, P, I, I, P, S, P]
+    L.sincos_nudft.restype = I
+    ws = L.sincos_nudft_workspace_bytes(100, 5000)
+    assert L.sincos_nudft(A, 100, 2 * A, 3 * A, 5000, 4 * A, 0, 0, 5 * A + 8, ws, None) == INVALID  # ws 8-B
+    assert L.sincos_nudft(A, 100, 2 * A, 3 * A, 5000, 4 * A, 0, 0, 5 * A, ws - 1, None) == INVALID  # ws short
+    assert L.sincos_nudft(A, 100, 2 * A, 3 * A + 4, 5000, 4 * A, 0, 0, 5 * A, ws, None) == INVALID  # a 4-B
+    assert L.sincos_nudft(A, 100, 2 * A, 3 * A, 5000, 4 * A + 4, 0, 0, 5 * A, ws, None) == INVALID  # out 4-B
+    L.sincos_debug_reciprocal.argtypes = [P, P, S, P]
+    L.sincos_debug_reciprocal.restype = I
+    assert L.sincos_debug_reciprocal(A + 1, 2 * A, 8, None) == INVALID
+    L.sincos_compare_cuda.argtypes = [P, P, P, P, S, I, P]
+    L.sincos_compare_cuda.restype = I
+    assert L.sincos_compare_cuda(A + 4, 2 * A, 3 * A, None, 64, 3, None) == INVALID          # needs 32-B
+    assert L.sincos_compare_cuda(A, 2 * A, 3 * A, None, 64, 5, None) == INVALID              # which
+    L.sincos_debug_packed_check.argtypes = [I, P, P, P]
+    L.sincos_debug_packed_check.restype = I
+    assert L.sincos_debug_packed_check(0, None, A + 4, None) == INVALID
+    assert L.sincos_debug_packed_check(7, None, A, None) == INVALID

@@ -14,9 +14,18 @@ import ctypes
 import os
 
 __all__ = [
-    "NORMALIZED", "RENORMALIZED", "SincosError", "lib", "sincos", "sincos_pairs", "sincos_pairs_host",
-    "shard_range", "error_stats", "set_launch_config", "get_launch_config", "set_nudft_packed", "set_realign", "sincos_turns", "cis", "null_4in8out",
-    "debug_reciprocal", "launch_count", "host_workspace_min_bytes", "library_path", "sincos_pairs_sharded",
+    # the hot path
+    "NORMALIZED", "RENORMALIZED", "SincosError", "lib", "library_path", "sincos", "cis", "sincos_pairs",
+    "sincos_pairs_host", "host_workspace_min_bytes",
+    # multi-GPU / statistics (8(e))
+    "shard_range", "sincos_pairs_sharded", "sincos_pairs_sharded_stats", "nccl_available", "error_stats",
+    # NEXT rows (8(f))
+    "RADIANS", "TURNS", "phase_grid", "sincos_turns", "nudft", "nudft_chunk", "Method", "make_method",
+    "PAPER_METHODS", "FIX_LINEAR", "FIX_RECIPROCAL", "FIX_NONE", "sincos_pairs_method", "sincos_pairs_dtype",
+    "interleave", "deinterleave",
+    # tuning, context and test hooks
+    "set_launch_config", "get_launch_config", "set_realign", "set_nudft_packed", "null_4in8out",
+    "compare_cuda", "debug_reciprocal", "debug_packed_check", "launch_count",
 ]
 
 NORMALIZED = 0      # method 1, P:124-150 (Fig. 1 FASTER_SINCOS)

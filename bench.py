@@ -578,6 +578,7 @@ def run_ours(args, rank, world, local_rank):
             pairs_e = len(variants) * n * steps_e
             energy = {"steps": steps_e, "seconds": t_b - t_a, "joules": joules,
                       "mean_power_w": joules / (t_b - t_a), "pairs_per_joule": pairs_e / joules,
+                      "sustained_pairs_per_s": pairs_e / (t_b - t_a),
                       "joules_per_step": joules / steps_e,
                       "how": "NVML total energy counter around back-to-back steps (this GPU, one rank)"}
         except Exception as e:  # counter not supported: no energy figure

@@ -82,8 +82,10 @@ typedef enum {
  * vector loads/stores (128-bit if they share only 16 B); otherwise, if the
  * outputs can still take whole-sector stores (split: sin and cos at one offset
  * mod 16 B; interleaved: 8-B aligned), theta is read as aligned vectors and
- * re-aligned in registers (warp shuffles; sincos_set_realign); otherwise one
- * element per thread.  A scalar head and tail cover the ragged ends.
+ * re-aligned in registers (warp shuffles; sincos_set_realign); otherwise the
+ * outputs are re-aligned instead (theta's 256-bit frame, whole 32-B output blocks
+ * from neighbouring lanes).  With re-alignment off: one element per thread.  A
+ * scalar head and tail cover the ragged ends.
  * theta_dev == sin_dev or
  * theta_dev == cos_dev (exact in-place) is allowed.  Validation happens
  * before any CUDA call; the return value reports validation and the launch

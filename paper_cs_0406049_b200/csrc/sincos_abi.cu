@@ -161,6 +161,25 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
         if (need > 0x7FFFFFFFu) need = 0x7FFFFFFFu;
         e = launch_shift(variant, inter, k, static_cast<unsigned>(need), threads, theta, so, co, io, hb, nvec, n,
                          stream);
+    } else if (w == 0 && g_shift.load(std::memory_order_relaxed)) {
+        // KB3c: theta's frame, outputs re-aligned (sin and cos apart mod 16 B; pairs only 4-B aligned)
+        const uintptr_t ta = reinterpret_cast<uintptr_t>(theta);
+        size_t hb = ((32 - (ta & 31)) & 31) / 4;
+        if (hb > n) hb = n;
+        const size_t nvec = (n - hb) / 8;
+        int ks, kc = 0;
+        if (inter) {
+            ks = static_cast<int>(((reinterpret_cast<uintptr_t>(io) + 8 * hb) & 31) / 4);
+        } else {
+            ks = static_cast<int>(((reinterpret_cast<uintptr_t>(so) + 4 * hb) & 31) / 4);
+            kc = static_cast<int>(((reinterpret_cast<uintptr_t>(co) + 4 * hb) & 31) / 4);
+        }
+        size_t need = (nvec + threads - 1) / threads;
+        if (need < 1) need = 1;
+        if (cfg_bps > 0 && need > static_cast<size_t>(sms) * cfg_bps) need = static_cast<size_t>(sms) * cfg_bps;
+        if (need > 0x7FFFFFFFu) need = 0x7FFFFFFFu;
+        e = launch_outshift(variant, inter, ks, kc, static_cast<unsigned>(need), threads, theta, so, co, io, hb, nvec,
+                            n, stream);
     } else if (w == 0) {
         const unsigned grid = static_cast<unsigned>(
             (n + threads - 1) / threads < static_cast<size_t>(sms) * 8 ? (n + threads - 1) / threads : sms * 8);

@@ -117,3 +117,25 @@ def test_phase_grid_split_offsets(shape, off):
     check(bs, G + off, G + off + n)
     check(bc, G + off, G + off + n)
     check(bi, G + off, G + off + 2 * n)
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("offs", [(0, 1, 2), (1, 0, 3), (3, 2, 0), (2, 1, 1)])
+def test_pairs_outputs_apart(n, offs):
+    """sin and cos at different offsets mod 16 B, interleaved pairs only 4-B aligned (the
+    output-realigning kernel: lane 0 / last-lane scalar edges, whole blocks in between)."""
+    ot, os_, oc = offs
+    tb = torch.from_numpy(inputs.generate(2, 0, n + 4)).cuda()
+    th = tb[ot:ot + n]
+    for v in (0, 1):
+        bs = torch.full((2 * G + n + 8,), SENT, dtype=torch.int32, device="cuda")
+        bc = torch.full((2 * G + n + 8,), SENT, dtype=torch.int32, device="cuda")
+        sp.sincos_pairs(th, bs[G + os_:G + os_ + n].view(torch.float32), bc[G + oc:G + oc + n].view(torch.float32),
+                        variant=v)
+        bi = torch.full((2 * G + 2 * n + 8,), SENT, dtype=torch.int32, device="cuda")
+        oi = 2 * os_ + 1                                  # odd: pairs 4-B aligned only
+        sp.sincos_pairs(th, interleaved_out=bi[G + oi:G + oi + 2 * n].view(torch.float32), variant=v)
+        torch.cuda.synchronize()
+        check(bs, G + os_, G + os_ + n)
+        check(bc, G + oc, G + oc + n)
+        check(bi, G + oi, G + oi + 2 * n)

@@ -505,7 +505,8 @@ def test_scalar_path_unshared_outputs():
 
 
 @pytest.mark.parametrize("variant,name", [(oracle.VARIANT_N, "N"), (oracle.VARIANT_A, "A")])
-@pytest.mark.parametrize("path", ["interleaved", "realign_split", "realign_interleaved", "scalar_split"])
+@pytest.mark.parametrize("path", ["interleaved", "realign_split", "realign_interleaved", "scalar_split",
+                                  "outshift_split", "outshift_interleaved"])
 def test_all_fp32_bit_patterns_other_paths(golden, variant, name, path):
     """The whole-input-space hash through the other kernels: the 256-bit interleaved kernel,
     the re-aligning kernel (theta one float off the outputs; split and interleaved) and the
@@ -514,13 +515,18 @@ def test_all_fp32_bit_patterns_other_paths(golden, variant, name, path):
     run_ = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_exhaustive.json")))
     want = run_[name]["all_bits"]
     chunk = 1 << 28
-    toff = 1 if path != "interleaved" else 0
+    toff = 1 if path in ("realign_split", "realign_interleaved", "scalar_split") else 0
     tbuf = torch.empty(chunk + 8, dtype=torch.float32, device="cuda")
     if path == "scalar_split":
         prev = sp.set_realign(False)
     try:
         if "inter" in path:
-            io = torch.empty(2 * chunk, dtype=torch.float32, device="cuda")
+            ibuf = torch.empty(2 * chunk + 8, dtype=torch.float32, device="cuda")
+            io = ibuf[1:1 + 2 * chunk] if path == "outshift_interleaved" else ibuf[:2 * chunk]   # 4-B pairs
+        elif path == "outshift_split":
+            sbuf = torch.empty(chunk + 8, dtype=torch.float32, device="cuda")
+            cbuf = torch.empty(chunk + 8, dtype=torch.float32, device="cuda")
+            s, c = sbuf[1:1 + chunk], cbuf[2:2 + chunk]      # sin and cos apart mod 16 B
         else:
             s = torch.empty(chunk, dtype=torch.float32, device="cuda")
             c = torch.empty(chunk, dtype=torch.float32, device="cuda")

@@ -9,8 +9,9 @@ s = torch.empty(n + 8, device='cuda'); c = torch.empty(n + 8, device='cuda')
 res = {}
 for realign in (True, False):
   sp.set_realign(realign)
-  for name, (to, so) in {'aligned': (0, 0), 'theta+1': (1, 0), 'out+1': (0, 1), 'all+1': (1, 1), 'theta+4': (4, 0)}.items():
-    th, ss, cc = base[to:to + n], s[so:so + n], c[so:so + n]
+  for name, (to, so, co) in {'aligned': (0, 0, 0), 'theta+1': (1, 0, 0), 'out+1': (0, 1, 1), 'all+1': (1, 1, 1),
+                             'theta+4': (4, 0, 0), 'sin+1 cos+2': (0, 1, 2), 'theta+3 sin+1 cos+0': (3, 1, 0)}.items():
+    th, ss, cc = base[to:to + n], s[so:so + n], c[co:co + n]
     for _ in range(3): sp.sincos_pairs(th, ss, cc)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()

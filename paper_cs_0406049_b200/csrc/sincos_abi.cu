@@ -85,7 +85,22 @@ sincos_status_t validate(const float *theta, const float *so, const float *co, c
     return SINCOS_OK;
 }
 
+// Blocks for `units` work items of `per_block` per block: the full grid (one trip each), capped at
+// SMs x blocks_per_sm when that is configured (grid-stride), and at grid.x's limit.
+unsigned grid_for(size_t units, size_t per_block, int sms, int cfg_bps) {
+    size_t need = (units + per_block - 1) / per_block;
+    if (need < 1) need = 1;
+    if (cfg_bps > 0 && need > static_cast<size_t>(sms) * cfg_bps) need = static_cast<size_t>(sms) * cfg_bps;
+    if (need > 0x7FFFFFFFu) need = 0x7FFFFFFFu;   // the kernels grid-stride past it
+    return static_cast<unsigned>(need);
+}
+
 // Launch on already-validated arguments, n > 0.  pf_mode: -1 = the configured mode.
+// Path, first that applies (identical numerics on every path):
+//   TMA pipeline (pf_mode 2, experimental) ->
+//   KB1/KB2 vector kernel (theta and outputs share a 32-B / 16-B alignment after a head) ->
+//   KB3b  theta re-aligned (split sin/cos share an offset mod 16 B; interleaved 8-B aligned) ->
+//   KB3c  outputs re-aligned (everything else) -> KB3 one element per thread (re-alignment off).
 sincos_status_t launch(const float *theta, float *so, float *co, float *io, size_t n, int variant,
                        cudaStream_t stream, int pf_mode = -1) {
     int dev = 0;
@@ -133,10 +148,9 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
         }
     }
 
-    // Re-aligning kernel (KB3b): split outputs without a shared alignment but whose sin and cos
-    // share one mod 16 B; interleaved outputs without the 256-bit path but 8-B aligned (its
-    // 256-bit store per four pairs beats the 128-bit path's half-sector stores).  Otherwise,
-    // without a shared alignment, one element per thread (KB3).
+    // KB3b: split outputs without a shared alignment but whose sin and cos share one mod 16 B;
+    // interleaved outputs without the 256-bit path but 8-B aligned (its 256-bit store per four
+    // pairs beats the 128-bit path's half-sector stores).
     size_t hs = SIZE_MAX;
     if (g_shift.load(std::memory_order_relaxed)) {
         if (inter) {
@@ -155,12 +169,8 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
         // (hb - k) + 4 nvec + 3 <= n - 1
         size_t nvec = (n - hb) / 4;
         if (k > 0) nvec = n + k >= hb + 4 ? (n + k - hb - 4) / 4 : 0;
-        size_t need = (nvec + threads - 1) / threads;
-        if (need < 1) need = 1;
-        if (cfg_bps > 0 && need > static_cast<size_t>(sms) * cfg_bps) need = static_cast<size_t>(sms) * cfg_bps;
-        if (need > 0x7FFFFFFFu) need = 0x7FFFFFFFu;
-        e = launch_shift(variant, inter, k, static_cast<unsigned>(need), threads, theta, so, co, io, hb, nvec, n,
-                         stream);
+        e = launch_shift(variant, inter, k, grid_for(nvec, threads, sms, cfg_bps), threads, theta, so, co, io, hb,
+                         nvec, n, stream);
     } else if (w == 0 && g_shift.load(std::memory_order_relaxed)) {
         // KB3c: theta's frame, outputs re-aligned (sin and cos apart mod 16 B; pairs only 4-B aligned)
         const uintptr_t ta = reinterpret_cast<uintptr_t>(theta);
@@ -174,12 +184,8 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
             ks = static_cast<int>(((reinterpret_cast<uintptr_t>(so) + 4 * hb) & 31) / 4);
             kc = static_cast<int>(((reinterpret_cast<uintptr_t>(co) + 4 * hb) & 31) / 4);
         }
-        size_t need = (nvec + threads - 1) / threads;
-        if (need < 1) need = 1;
-        if (cfg_bps > 0 && need > static_cast<size_t>(sms) * cfg_bps) need = static_cast<size_t>(sms) * cfg_bps;
-        if (need > 0x7FFFFFFFu) need = 0x7FFFFFFFu;
-        e = launch_outshift(variant, inter, ks, kc, static_cast<unsigned>(need), threads, theta, so, co, io, hb, nvec,
-                            n, stream);
+        e = launch_outshift(variant, inter, ks, kc, grid_for(nvec, threads, sms, cfg_bps), threads, theta, so, co,
+                            io, hb, nvec, n, stream);
     } else if (w == 0) {
         const unsigned grid = static_cast<unsigned>(
             (n + threads - 1) / threads < static_cast<size_t>(sms) * 8 ? (n + threads - 1) / threads : sms * 8);
@@ -190,15 +196,7 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
         // Default (blocks_per_sm == 0): the full grid, one trip of `unroll` vectors per thread --
         // measured fastest on B200.  blocks_per_sm > 0: a grid-stride grid of
         // SMs x blocks_per_sm blocks.
-        const size_t per_block = static_cast<size_t>(threads) * unroll;
-        size_t need = (nvec + per_block - 1) / per_block;
-        if (need < 1) need = 1;
-        if (cfg_bps > 0) {
-            const size_t cap = static_cast<size_t>(sms) * cfg_bps;
-            if (need > cap) need = cap;
-        }
-        if (need > 0x7FFFFFFFu) need = 0x7FFFFFFFu;  // grid.x limit; the kernel grid-strides past it
-        const unsigned grid = static_cast<unsigned>(need);
+        const unsigned grid = grid_for(nvec, static_cast<size_t>(threads) * unroll, sms, cfg_bps);
         e = launch_vec(variant, inter, w, unroll, nc, pf, grid, threads, theta, so, co, io, head, nvec, n, stream);
     }
     if (e != cudaSuccess) return cuda_fail(e);

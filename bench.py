@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--same-device", action="store_true",
                     help="every rank on cuda:0 (flow testing of the N>1 host path on a 1-GPU box; gloo only)")
     ap.add_argument("--launch", default=None, help="threads,blocks_per_sm,vec,unroll (default: library default)")
+    ap.add_argument("--pdl", type=int, default=None, choices=[0, 1],
+                    help="programmatic dependent launch of the hot kernel (default: the library's)")
     return ap.parse_args()
 
 
@@ -433,6 +435,8 @@ def run_ours(args, rank, world, local_rank):
     cdev = dev if args.backend == "nccl" else None      # where the collectives' tensors live
     if args.launch:
         sp.set_launch_config(*[int(x) for x in args.launch.split(",")])
+    if args.pdl is not None:
+        sp.set_pdl(bool(args.pdl))
     W = WORKLOADS[args.workload]
     if args.n and args.workload == "c2":
         W = type(W)(**{**W.__dict__, "n": args.n})

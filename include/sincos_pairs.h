@@ -306,6 +306,13 @@ SINCOS_API void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *
  * previous setting, or -1 for a value other than 0/1. */
 SINCOS_API int sincos_set_realign(int on);
 
+/* Programmatic dependent launch of the hot kernel (bench / tests): 1 = on (the default) --
+ * back-to-back launches on a stream overlap their launch latency and block scheduling, the
+ * kernel waiting (griddepcontrol.wait) for the previous kernel's completion before it touches
+ * memory, so stream order is unchanged; 0 = plain launches.  Process-global; returns the
+ * previous setting, or -1 for a value other than 0/1. */
+SINCOS_API int sincos_set_pdl(int on);
+
 /* Fused-sum kernel form (bench / tests): 1 = packed fp32 (sm_100a FFMA2/FMUL2/FADD2,
  * two frequencies per instruction; the default), 0 = scalar fp32.  Both are
  * bit-identical (each packed lane rounds as the scalar instruction does); applies to

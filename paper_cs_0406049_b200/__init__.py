@@ -24,7 +24,7 @@ __all__ = [
     "PAPER_METHODS", "FIX_LINEAR", "FIX_RECIPROCAL", "FIX_NONE", "sincos_pairs_method", "sincos_pairs_dtype",
     "interleave", "deinterleave",
     # tuning, context and test hooks
-    "set_launch_config", "get_launch_config", "set_realign", "set_nudft_packed", "null_4in8out",
+    "set_launch_config", "get_launch_config", "set_realign", "set_pdl", "set_nudft_packed", "null_4in8out",
     "compare_cuda", "debug_reciprocal", "debug_packed_check", "launch_count",
 ]
 
@@ -104,6 +104,7 @@ _SIGS = {
     "sincos_set_launch_config": (_I, [_I, _I, _I, _I, _I]),
     "sincos_set_nudft_packed": (_I, [_I]),
     "sincos_set_realign": (_I, [_I]),
+    "sincos_set_pdl": (_I, [_I]),
     "sincos_debug_packed_check": (_I, [_I, _P, _P, _P]),
     "sincos_get_launch_config": (None, [ctypes.POINTER(_I)] * 5),
     "sincos_null_4in8out": (_I, [_P, _P, _P, _P, _S, _P]),
@@ -472,6 +473,14 @@ def set_launch_config(threads=None, blocks_per_sm=None, vec=None, unroll=None, p
 def set_realign(on: bool) -> bool:
     """Unshared-alignment path: register re-alignment (True, default) or one element per thread."""
     prev = lib().sincos_set_realign(1 if on else 0)
+    if prev < 0:
+        raise ValueError(on)
+    return bool(prev)
+
+
+def set_pdl(on: bool) -> bool:
+    """Programmatic dependent launch of the hot kernel (True, default) or plain launches."""
+    prev = lib().sincos_set_pdl(1 if on else 0)
     if prev < 0:
         raise ValueError(on)
     return bool(prev)

@@ -624,6 +624,8 @@ sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
     return SINCOS_OK;
 }
 
+int sincos_set_pdl(int on) { return set_pdl(on); }
+
 int sincos_set_realign(int on) {
     if (on != 0 && on != 1) return -1;
     const int prev = g_shift.exchange(on, std::memory_order_relaxed);

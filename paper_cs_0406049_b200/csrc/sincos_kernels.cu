@@ -169,9 +169,20 @@ __device__ __forceinline__ void emit_scalar(const float *theta, size_t e, float 
 
 // KB1/KB2.  Elements [0, head) and [head + nvec*W, n) scalar; the body is nvec
 // vectors of W elements starting at element `head` (aligned by the host).
+// Programmatic dependent launch (sm_90+): let the next kernel on the stream be scheduled as soon
+// as every block of this one has started, and wait -- before touching global memory -- until
+// the previous kernel has completed and its writes are visible.  Stream order is unchanged
+// (nothing is read or written before the wait); only launch latency and block scheduling of
+// back-to-back launches overlap.  Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 template <int V, bool INTER, int W, int U, bool NC, bool PF>
 __global__ void __launch_bounds__(512) sincos_vec_kernel(const float *theta, float *so, float *co, float *io,
                                                          size_t head, size_t nvec, size_t n) {
+    pdl_enter();
     const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t tail0 = head + nvec * W;
@@ -452,12 +463,34 @@ ScalarFn scalar_kernel(int variant, bool inter) {
     }
 }
 
+static int g_pdl = 1;   // programmatic dependent launch of the vector kernel (see pdl_enter)
+int set_pdl(int on) {
+    if (on != 0 && on != 1) return -1;
+    const int prev = g_pdl;
+    g_pdl = on;
+    return prev;
+}
+
 cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, bool pf, unsigned grid,
                        unsigned threads, const float *theta, float *so, float *co, float *io, size_t head,
                        size_t nvec, size_t n, cudaStream_t stream) {
     VecFn fn = vec_kernel(variant, inter, w, unroll, nc, pf);
     void *args[] = {&theta, &so, &co, &io, &head, &nvec, &n};
-    return cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(threads), args, 0, stream);
+    // inside a CUDA graph capture the plain launch is kept: graph replay already removes the
+    // launch latency, and the programmatic edges measured slower for small graphed kernels
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (!g_pdl || cudaStreamIsCapturing(stream, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+        return cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(threads), args, 0, stream);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(fn), args);
 }
 
 cudaError_t launch_scalar(int variant, bool inter, unsigned grid, unsigned threads, const float *theta, float *so,

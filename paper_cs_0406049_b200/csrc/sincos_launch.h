@@ -25,6 +25,8 @@ cudaError_t launch_shift(int variant, bool inter, int k, unsigned grid, unsigned
 cudaError_t launch_outshift(int variant, bool inter, int ks, int kc, unsigned grid, unsigned threads,
                             const float *theta, float *so, float *co, float *io, size_t head, size_t nvec, size_t n,
                             cudaStream_t stream);
+// Programmatic dependent launch of the vector kernel: 1 = on (default), 0 = plain launches.
+int set_pdl(int on);
 cudaError_t launch_scalar(int variant, bool inter, unsigned grid, unsigned threads, const float *theta, float *so,
                           float *co, float *io, size_t n, cudaStream_t stream);
 cudaError_t launch_rcp(unsigned grid, unsigned threads, const float *d, float *out, size_t n, cudaStream_t stream);

@@ -669,3 +669,30 @@ def test_binding_refuses_mixed_devices_and_follows_tensor_device():
         torch.cuda.synchronize(1)
         ws, wc = oracle.sincos(t1.cpu().numpy(), 0)
         assert_parity(s1.cpu().numpy(), c1.cpu().numpy(), ws, wc, "device 1")
+
+
+@pytest.mark.parametrize("pdl", [True, False])
+def test_dependent_launch_chain_keeps_stream_order(pdl):
+    """Programmatic dependent launch must not let a kernel read its predecessor's output early:
+    a chain of 12 back-to-back launches, each reading the previous one's sin output (in place
+    every other step), no host sync in between, equals the oracle applied 12 times."""
+    prev = sp.set_pdl(pdl)
+    try:
+        n = (1 << 22) + 3
+        th = inputs.generate(1, 0, n)
+        cur = torch.from_numpy(th).cuda()
+        c = torch.empty_like(cur)
+        want = th
+        for k in range(12):
+            v = k % 2
+            if k % 2 == 0:
+                nxt = torch.empty_like(cur)
+                sp.sincos_pairs(cur, nxt, c, variant=v)
+                cur = nxt
+            else:
+                sp.sincos_pairs(cur, cur, c, variant=v)         # in place: sin over theta
+            want, wc = oracle.sincos(want, v)
+        torch.cuda.synchronize()
+        assert_parity(cur.cpu().numpy(), c.cpu().numpy(), want, wc, f"chain pdl={pdl}")
+    finally:
+        sp.set_pdl(prev)

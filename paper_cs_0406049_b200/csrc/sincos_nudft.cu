@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(kNuThreads, 9) nudft_partial(const float *__re
     // the thread's fp64 accumulators live in shared memory (touched once per chunk), keeping
     // the registers -- and so the occupancy -- of the fp32 inner loop
     __shared__ double2 acc[kKPerThread][kNuThreads];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // let nudft_reduce be scheduled
     const size_t k0 = static_cast<size_t>(blockIdx.x) * kKPerBlock + threadIdx.x;
     const size_t j0 = static_cast<size_t>(blockIdx.y) * seg;
     const size_t j1 = j0 + seg < nt ? j0 + seg : nt;
@@ -181,6 +182,9 @@ __global__ void __launch_bounds__(kNuThreads, 9) nudft_partial(const float *__re
 
 __global__ void __launch_bounds__(256) nudft_reduce(const double2 *__restrict__ part, size_t nf, size_t nseg,
                                                     float2 *__restrict__ out) {
+    // launched as a programmatic dependent of nudft_partial: scheduled while the partial sums
+    // drain, it waits here for their completion (and visibility) before reading them
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k >= nf) return;
     double re = 0.0, im = 0.0;
@@ -279,8 +283,16 @@ cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, con
     float2 *o = reinterpret_cast<float2 *>(out);
     size_t nch = nchunks;
     void *rargs[] = {&part, &nf, &nch, &o};
-    return cudaLaunchKernel(reinterpret_cast<const void *>(nudft_reduce),
-                            dim3(static_cast<unsigned>((nf + 255) / 256)), dim3(256), rargs, 0, stream);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>((nf + 255) / 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(nudft_reduce), rargs);
 }
 
 }  // namespace sincos_b200

@@ -178,12 +178,46 @@ def cpu_oracle_rate(theta: np.ndarray, seconds: float, workload: str = "C2"):
         cpu_model = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
     except Exception:
         pass
+    libm = libm_sincosf_rate(th, s, c, cores, min(seconds, 3.0))
     return {"value": pairs / dt, "unit": "pairs/s", "cores": cores, "kind": "oracle",
             "sample": f"first {m} elements of the {workload} workload, variants N and A alternately, "
                       f"{pairs} pairs in {dt:.1f} s on {cores} threads (plain scalar C oracle)",
             "seconds": dt, "ns_per_pair": 1e9 * dt / pairs, "GBps": 12 * pairs / dt / 1e9,
             "single_thread_pairs_per_s": one, "single_thread_ns_per_pair": 1e9 / one,
-            "single_thread_sample": f"first {m1} elements, both variants", "cpu_model": cpu_model}
+            "single_thread_sample": f"first {m1} elements, both variants", "cpu_model": cpu_model,
+            "context_glibc_sincosf": libm}
+
+
+def libm_sincosf_rate(th, s, c, cores, seconds):
+    """Context only (SURVEY 8(d) optional row): glibc sincosf over the same sample on all host
+    cores (tools/libm_baseline.c, compiled here with gcc); None if no compiler."""
+    import ctypes
+    import subprocess
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
+    try:
+        so = os.path.join(tempfile.gettempdir(), f"libm_baseline_{os.getpid()}.so")
+        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-o", so,
+                               os.path.join(ROOT, "tools", "libm_baseline.c"), "-lm"])
+        L = ctypes.CDLL(so)
+        L.libm_sincosf_array.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
+    except Exception as e:
+        return {"error": repr(e)}
+    chunk = 1 << 18
+    m = th.size
+    spans = [(i, min(i + chunk, m)) for i in range(0, m, chunk)]
+    pairs, t0 = 0, time.perf_counter()
+    with ThreadPoolExecutor(cores) as ex:
+        while time.perf_counter() - t0 < seconds:
+            list(ex.map(lambda ab: L.libm_sincosf_array(th[ab[0]:ab[1]].ctypes.data, s[ab[0]:ab[1]].ctypes.data,
+                                                        c[ab[0]:ab[1]].ctypes.data, ab[1] - ab[0]), spans))
+            pairs += m
+    dt = time.perf_counter() - t0
+    try:
+        os.remove(so)
+    except OSError:
+        pass
+    return {"value": pairs / dt, "unit": "pairs/s", "cores": cores, "what": "glibc sincosf, not the method"}
 
 
 def run_reference(args, rank, world):

@@ -174,15 +174,21 @@ __device__ __forceinline__ void emit_scalar(const float *theta, size_t e, float 
 // the previous kernel has completed and its writes are visible.  Stream order is unchanged
 // (nothing is read or written before the wait); only launch latency and block scheduling of
 // back-to-back launches overlap.  Without the launch attribute both are no-ops.
+// Only the 256-bit (W = 8) instances carry it: in the 128-bit instances, with twice the blocks,
+// the per-block PREEXIT / ACQBULK cost 15% even on plain launches (measured); launch_vec uses
+// the PDL attribute only for W = 8 (a kernel launched with it must wait before any access).
+template <int W>
 __device__ __forceinline__ void pdl_enter() {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr (W == 8) {
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
 }
 
 template <int V, bool INTER, int W, int U, bool NC, bool PF>
 __global__ void __launch_bounds__(512) sincos_vec_kernel(const float *theta, float *so, float *co, float *io,
                                                          size_t head, size_t nvec, size_t n) {
-    pdl_enter();
+    pdl_enter<W>();
     const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t tail0 = head + nvec * W;
@@ -321,9 +327,10 @@ __device__ __forceinline__ void store_realigned(float *x, size_t f0, const float
         }
         return;
     }
+    // only the predecessor's last k <= 7 values are ever used: shuffle those 7
     float prev[W];
 #pragma unroll
-    for (int j = 0; j < W; ++j) prev[j] = __shfl_up_sync(0xFFFFFFFFu, val[j], 1);
+    for (int j = 0; j < W; ++j) prev[j] = j >= W - 7 ? __shfl_up_sync(0xFFFFFFFFu, val[j], 1) : 0.0f;
     if (!act) return;
     if (lane > 0) {
         float blk[W];
@@ -479,7 +486,7 @@ cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, bool
     // inside a CUDA graph capture the plain launch is kept: graph replay already removes the
     // launch latency, and the programmatic edges measured slower for small graphed kernels
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (!g_pdl || cudaStreamIsCapturing(stream, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+    if (!g_pdl || w != 8 || cudaStreamIsCapturing(stream, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
         return cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(threads), args, 0, stream);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);

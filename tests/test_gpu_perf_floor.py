@@ -1,0 +1,88 @@
+"""Performance floors (``pytest -m gpu``): each kernel path at ~88% of what DESIGN.md records on
+one B200, so a regression of >= 12% in any path fails a test rather than going unnoticed (the
+programmatic-dependent-launch change once cost the 128-bit path 15%; only a probe caught it).
+HBM-bound paths do not depend on the SM clock, so power capping does not trip them."""
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_cs_0406049_b200 as sp  # noqa: E402
+
+N = 1 << 27
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    sp.set_launch_config()
+    yield
+
+
+def gbps(fn, nbytes, reps=10):
+    for _ in range(3):
+        fn()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return nbytes / (a.elapsed_time(b) / reps / 1e3) / 1e9
+
+
+@pytest.fixture(scope="module")
+def bufs():
+    base = torch.rand(N + 16, device="cuda") * 2e4 - 1e4
+    sb, cb = torch.empty(N + 16, device="cuda"), torch.empty(N + 16, device="cuda")
+    ib = torch.empty(2 * N + 16, device="cuda")
+    yield base, sb, cb, ib
+    del base, sb, cb, ib
+    torch.cuda.empty_cache()
+
+
+# (theta offset, sin offset, cos offset, interleaved?, floor GB/s, recorded GB/s)
+CASES = {
+    "aligned split (256-bit)": (0, 0, 0, False, 6000, 6870),
+    "aligned interleaved": (0, 0, 0, True, 6000, 6890),
+    "shared 16 B (128-bit)": (4, 0, 0, False, 6000, 6890),
+    "theta realigned (KB3b)": (1, 0, 0, False, 5800, 6660),
+    "theta realigned interleaved": (1, 0, 0, True, 5800, 6770),
+    "outputs realigned (KB3c)": (0, 1, 2, False, 4500, 5200),
+    "pairs 4-B only (KB3c)": (0, 1, 1, "odd", 4500, 5400),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_hot_path_floor(bufs, name):
+    base, sb, cb, ib = bufs
+    ot, os_, oc, inter, floor, _ = CASES[name]
+    th = base[ot:ot + N]
+    if inter:
+        o = ib[1:1 + 2 * N] if inter == "odd" else ib[:2 * N]
+        fn = lambda: sp.sincos_pairs(th, interleaved_out=o)  # noqa: E731
+    else:
+        s, c = sb[os_:os_ + N], cb[oc:oc + N]
+        fn = lambda: sp.sincos_pairs(th, s, c)  # noqa: E731
+    got = gbps(fn, 12 * N)
+    assert got >= floor, f"{name}: {got:.0f} GB/s < floor {floor}"
+
+
+def test_phase_grid_floor():
+    f = torch.rand(1 << 13, device="cuda") * 512
+    t = torch.rand(1 << 14, device="cuda")
+    o = torch.empty(2 * (1 << 27), device="cuda")
+    got = gbps(lambda: sp.phase_grid(f, t, interleaved_out=o, units=sp.TURNS), 8 * (1 << 27))
+    assert got >= 6500, got                        # recorded 7.5-7.6 TB/s (write-only ceiling)
+
+
+def test_fused_sum_floor():
+    nf = nt = 1 << 15                              # the C4 shape the number is recorded on
+    f = torch.rand(nf, device="cuda") * 512
+    t = torch.rand(nt, device="cuda")
+    a = torch.randn(nt, dtype=torch.complex64, device="cuda")
+    out = torch.empty(nf, dtype=torch.complex64, device="cuda")
+    ws = torch.empty(sp.lib().sincos_nudft_workspace_bytes(nf, nt), dtype=torch.uint8, device="cuda")
+    terms_per_s = gbps(lambda: sp.nudft(f, t, a, out=out, units=sp.TURNS, workspace=ws), nf * nt) * 1e9
+    assert terms_per_s >= 1.15e12, terms_per_s     # recorded 1.31 T terms/s

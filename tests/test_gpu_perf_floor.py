@@ -85,4 +85,4 @@ def test_fused_sum_floor():
     out = torch.empty(nf, dtype=torch.complex64, device="cuda")
     ws = torch.empty(sp.lib().sincos_nudft_workspace_bytes(nf, nt), dtype=torch.uint8, device="cuda")
     terms_per_s = gbps(lambda: sp.nudft(f, t, a, out=out, units=sp.TURNS, workspace=ws), nf * nt) * 1e9
-    assert terms_per_s >= 1.15e12, terms_per_s     # recorded 1.31 T terms/s
+    assert terms_per_s >= 1.0e12, terms_per_s      # recorded 1.31 T terms/s (ALU-bound: margin for the SM clock)

@@ -86,3 +86,15 @@ def test_fused_sum_floor():
     ws = torch.empty(sp.lib().sincos_nudft_workspace_bytes(nf, nt), dtype=torch.uint8, device="cuda")
     terms_per_s = gbps(lambda: sp.nudft(f, t, a, out=out, units=sp.TURNS, workspace=ws), nf * nt) * 1e9
     assert terms_per_s >= 1.0e12, terms_per_s      # recorded 1.31 T terms/s (ALU-bound: margin for the SM clock)
+
+
+def test_16bit_and_method_floors(bufs):
+    base, sb, cb, ib = bufs
+    th = base[:N]
+    s16 = torch.empty(N, dtype=torch.float16, device="cuda")
+    c16 = torch.empty(N, dtype=torch.float16, device="cuda")
+    got = gbps(lambda: sp.sincos_pairs_dtype(th, s16, c16), 8 * N)
+    assert got >= 6000, f"fp16 {got:.0f}"           # recorded 6.83-6.86 TB/s
+    m = sp.make_method(*sp.PAPER_METHODS[0])
+    got = gbps(lambda: sp.sincos_pairs_method(th, m, sb[:N], cb[:N]), 12 * N)
+    assert got >= 6000, f"method {got:.0f}"         # recorded 6.83-6.89 TB/s

@@ -189,16 +189,27 @@ def _on_tensor_device(fn):
     the current device's buffers and stream); tensors on two different devices are refused."""
     import functools
 
+    import torch
+    Tensor = torch.Tensor
+
     @functools.wraps(fn)
     def wrapped(*args, **kwargs):
-        import torch
-        devs = {a.device for a in list(args) + list(kwargs.values())
-                if isinstance(a, torch.Tensor) and a.is_cuda}
-        if len(devs) > 1:
-            raise ValueError(f"{fn.__name__}: tensors on different devices {sorted(map(str, devs))}")
-        if not devs:
-            return fn(*args, **kwargs)
-        with torch.cuda.device(next(iter(devs))):
+        dev = None
+        for a in args:
+            if isinstance(a, Tensor) and a.is_cuda:
+                if dev is None:
+                    dev = a.get_device()
+                elif a.get_device() != dev:
+                    raise ValueError(f"{fn.__name__}: tensors on different devices")
+        for a in kwargs.values():
+            if isinstance(a, Tensor) and a.is_cuda:
+                if dev is None:
+                    dev = a.get_device()
+                elif a.get_device() != dev:
+                    raise ValueError(f"{fn.__name__}: tensors on different devices")
+        if dev is None or dev == torch.cuda.current_device():
+            return fn(*args, **kwargs)              # the common case: no device switch
+        with torch.cuda.device(dev):
             return fn(*args, **kwargs)
     return wrapped
 

@@ -112,6 +112,25 @@ SINCOS_API sincos_status_t sincos_pairs_host(const float *theta_host, float *sin
 SINCOS_API size_t sincos_host_workspace_min_bytes(void);
 
 /*
+ * sincos_pairs_batched -- many independent arrays in ONE kernel launch (serving many small
+ * requests: below ~10^5 elements a launch per array is dominated by launch latency).
+ * items: host array of `count` descriptors, each with the buffers and conventions of
+ * sincos_pairs (split or interleaved, any 4-B alignment, exact in-place allowed); items must
+ * not overlap one another.  The host validates every item (returning before any CUDA call on
+ * the first invalid one) and launches one grid per 480 items, the item table travelling in
+ * the kernel's parameter block (no workspace, no copy, asynchronous on `stream`; `items` may be
+ * reused as soon as the call returns): each block finds its item and 1024-element chunk by
+ * binary search.  Numerics identical to sincos_pairs.
+ */
+typedef struct {
+    const float *theta_dev;
+    float *sin_dev, *cos_dev, *inter_dev;
+    uint64_t n;
+} sincos_item_t;
+SINCOS_API sincos_status_t sincos_pairs_batched(const sincos_item_t *items, int count, sincos_variant_t variant,
+                                                void *stream);
+
+/*
  * NEXT(4): other output dtypes and layout adapters.
  *
  * sincos_pairs_dtype: the hot path with the pair rounded once (to nearest even) from the

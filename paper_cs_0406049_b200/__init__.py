@@ -16,7 +16,7 @@ import os
 __all__ = [
     # the hot path
     "NORMALIZED", "RENORMALIZED", "SincosError", "lib", "library_path", "sincos", "cis", "sincos_pairs",
-    "sincos_pairs_host", "host_workspace_min_bytes",
+    "sincos_pairs_host", "host_workspace_min_bytes", "Item", "sincos_pairs_batched", "sincos_batched",
     # multi-GPU / statistics (8(e))
     "shard_range", "sincos_pairs_sharded", "sincos_pairs_sharded_stats", "nccl_available", "error_stats",
     # NEXT rows (8(f))
@@ -105,6 +105,7 @@ _SIGS = {
     "sincos_set_nudft_packed": (_I, [_I]),
     "sincos_set_realign": (_I, [_I]),
     "sincos_set_pdl": (_I, [_I]),
+    "sincos_pairs_batched": (_I, [ctypes.c_void_p, _I, _I, _P]),
     "sincos_debug_packed_check": (_I, [_I, _P, _P, _P]),
     "sincos_get_launch_config": (None, [ctypes.POINTER(_I)] * 5),
     "sincos_null_4in8out": (_I, [_P, _P, _P, _P, _S, _P]),
@@ -261,6 +262,52 @@ def phase_grid(f, t, sin_out=None, cos_out=None, interleaved_out=None, units=RAD
                                  _ptr(cos_out, "cos_out"), _ptr(interleaved_out, "interleaved_out"), int(units),
                                  _variant(variant), _stream(stream, f.device))
     _check(st, "sincos_phase_grid")
+
+
+class Item(ctypes.Structure):
+    """sincos_item_t: one array of a batched call."""
+    _fields_ = [("theta", ctypes.c_void_p), ("sin", ctypes.c_void_p), ("cos", ctypes.c_void_p),
+                ("inter", ctypes.c_void_p), ("n", ctypes.c_uint64)]
+
+
+@_on_tensor_device
+def sincos_pairs_batched(thetas, sin_outs=None, cos_outs=None, interleaved_outs=None, variant=NORMALIZED,
+                         stream=None):
+    """C-ABI sincos_pairs_batched: many arrays in one launch (per 480 arrays).  thetas: list of
+    CUDA float32 tensors; outputs: lists of the same length (split) or interleaved_outs."""
+    k = len(thetas)
+    arr = (Item * max(k, 1))()
+    for i, th in enumerate(thetas):
+        n = th.numel()
+        if interleaved_outs is not None:
+            io = interleaved_outs[i]
+            if io.numel() != 2 * n:
+                raise ValueError("interleaved_out must hold 2*n floats")
+            arr[i] = Item(_ptr(th, "theta"), None, None, _ptr(io, "interleaved_out"), n)
+        else:
+            so, co = sin_outs[i], cos_outs[i]
+            if so.numel() != n or co.numel() != n:
+                raise ValueError("outputs must hold n floats")
+            arr[i] = Item(_ptr(th, "theta"), _ptr(so, "sin_out"), _ptr(co, "cos_out"), None, n)
+    dev = thetas[0].device if k else None
+    st = lib().sincos_pairs_batched(ctypes.addressof(arr), k, _variant(variant), _stream(stream, dev) if k else None)
+    _check(st, "sincos_pairs_batched")
+
+
+def sincos_batched(thetas, variant="normalized", interleaved=False, stream=None):
+    """Allocate outputs and run many arrays in one launch; returns a list of (sin, cos) or of
+    (n, 2) {cos, sin} tensors."""
+    import torch
+    if interleaved:
+        outs = [torch.empty(t.shape + (2,), dtype=torch.float32, device=t.device) for t in thetas]
+        sincos_pairs_batched([t.reshape(-1) for t in thetas], interleaved_outs=[o.reshape(-1) for o in outs],
+                             variant=variant, stream=stream)
+        return outs
+    ss = [torch.empty_like(t) for t in thetas]
+    cs = [torch.empty_like(t) for t in thetas]
+    sincos_pairs_batched([t.reshape(-1) for t in thetas], [x.reshape(-1) for x in ss], [x.reshape(-1) for x in cs],
+                         variant=variant, stream=stream)
+    return list(zip(ss, cs))
 
 
 def cis(theta, variant="normalized", stream=None):

@@ -9,6 +9,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <vector>
 #include <stdint.h>
 #include <string.h>
 
@@ -621,6 +622,56 @@ sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
                                  static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e);
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SINCOS_OK;
+}
+
+sincos_status_t sincos_pairs_batched(const sincos_item_t *items, int count, sincos_variant_t variant,
+                                     void *stream) {
+    if (count < 0 || (count > 0 && items == nullptr)) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (variant != SINCOS_NORMALIZED && variant != SINCOS_RENORMALIZED) return SINCOS_ERR_INVALID_ARGUMENT;
+    for (int i = 0; i < count; ++i) {           // every item valid before anything is launched
+        const sincos_item_t &it = items[i];
+        sincos_status_t st = validate(it.theta_dev, it.sin_dev, it.cos_dev, it.inter_dev, it.n, variant, false);
+        if (st != SINCOS_OK) return st;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    static thread_local BatchParams p;          // ~29 KB: not on the stack
+    for (int first = 0; first < count; first += kBatchMax) {
+        const int m = count - first < kBatchMax ? count - first : kBatchMax;
+        p.count = m;
+        p.pad = 0;
+        p.prefix[0] = 0;
+        for (int i = 0; i < m; ++i) {
+            const sincos_item_t &it = items[first + i];
+            BatchItem &b = p.items[i];
+            b.theta = it.theta_dev;
+            b.so = it.sin_dev;
+            b.co = it.cos_dev;
+            b.io = it.inter_dev;
+            b.n = it.n;
+            // 256-bit body when theta and the outputs share a 32-B alignment after the same head
+            // (exact in-place items take the plain-load one-per-thread form)
+            const uintptr_t t = reinterpret_cast<uintptr_t>(it.theta_dev);
+            const uint64_t h = ((32 - (t & 31)) & 31) / 4;
+            bool vec = it.n > 0 && it.theta_dev != it.sin_dev && it.theta_dev != it.cos_dev;
+            if (vec) {
+                if (it.inter_dev)
+                    vec = aligned(reinterpret_cast<const char *>(it.inter_dev) + 8 * h, 32);
+                else
+                    vec = aligned(reinterpret_cast<const char *>(it.sin_dev) + 4 * h, 32) &&
+                          aligned(reinterpret_cast<const char *>(it.cos_dev) + 4 * h, 32);
+            }
+            b.head = vec ? (h < it.n ? h : it.n) : 0;
+            b.vec = vec ? 1u : 0u;
+            b.pad = 0;
+            p.prefix[i + 1] = p.prefix[i] + batched_chunks(it.n, b.head, vec);
+        }
+        if (p.prefix[m] > 0x7FFFFFFFull) return SINCOS_ERR_INVALID_ARGUMENT;
+        if (p.prefix[m] == 0) continue;
+        cudaError_t e = launch_batched(variant, p, s);   // parameters are copied at launch
+        if (e != cudaSuccess) return cuda_fail(e);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
     return SINCOS_OK;
 }
 

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <stdint.h>
 #include <stddef.h>
 
 #include "../../include/sincos_pairs.h"
@@ -25,6 +26,23 @@ cudaError_t launch_shift(int variant, bool inter, int k, unsigned grid, unsigned
 cudaError_t launch_outshift(int variant, bool inter, int ks, int kc, unsigned grid, unsigned threads,
                             const float *theta, float *so, float *co, float *io, size_t head, size_t nvec, size_t n,
                             cudaStream_t stream);
+// Many arrays in one launch (sincos_batched.cu): one record per item in device memory.
+struct BatchItem {
+    const float *theta;
+    float *so, *co, *io;
+    uint64_t n, head;      // head: elements before the 32-B aligned vector body (vec == 1)
+    uint32_t vec, pad;     // 1: 256-bit body from `head`; 0: one element per thread
+};
+constexpr int kBatchMax = 480;   // items per launch: the table fits the 32 KB parameter block
+struct BatchParams {
+    int count;
+    int pad;
+    uint64_t prefix[kBatchMax + 1];   // cumulative 1024-element chunks (blocks)
+    BatchItem items[kBatchMax];
+};
+static_assert(sizeof(BatchParams) <= 32764, "kernel parameter block limit");
+uint64_t batched_chunks(uint64_t n, uint64_t head, bool vec);
+cudaError_t launch_batched(int variant, const BatchParams &p, cudaStream_t stream);
 // Programmatic dependent launch of the vector kernel: 1 = on (default), 0 = plain launches.
 int set_pdl(int on);
 cudaError_t launch_scalar(int variant, bool inter, unsigned grid, unsigned threads, const float *theta, float *so,

@@ -276,3 +276,19 @@ def test_alignment_checks_of_the_other_entry_points(L):
     L.sincos_debug_packed_check.restype = I
     assert L.sincos_debug_packed_check(0, None, A + 4, None) == INVALID
     assert L.sincos_debug_packed_check(7, None, A, None) == INVALID
+
+
+def test_batched_validation_before_cuda(L):
+    """sincos_pairs_batched validates every item before launching anything (fake addresses)."""
+    Item = sp.Item
+    assert L.sincos_pairs_batched(None, 0, 0, None) == OK                 # empty batch
+    assert L.sincos_pairs_batched(None, -1, 0, None) == INVALID
+    good = Item(A, 2 * A, 3 * A, None, 64)
+    bad_forms = Item(A, 2 * A, None, None, 64)                            # half a split form
+    bad_align = Item(A + 2, 2 * A, 3 * A, None, 64)
+    overlap = Item(A, 2 * A, 2 * A + 8, None, 64)
+    for bad, want in ((bad_forms, INVALID), (bad_align, INVALID), (overlap, OVERLAP)):
+        arr = (Item * 3)(good, good, bad)
+        assert L.sincos_pairs_batched(ctypes.addressof(arr), 3, 0, None) == want
+    arr = (Item * 1)(good)
+    assert L.sincos_pairs_batched(ctypes.addressof(arr), 1, 9, None) == INVALID  # variant

@@ -34,8 +34,8 @@ __device__ __forceinline__ void batch_one(const BatchItem &it, uint64_t e) {
     }
 }
 
-template <int V>
-__global__ void __launch_bounds__(kBatchThreads) sincos_batched_kernel(const __grid_constant__ BatchParams p) {
+template <int V, int CAP>
+__global__ void __launch_bounds__(kBatchThreads) sincos_batched_kernel(const __grid_constant__ BatchParamsT<CAP> p) {
     const uint64_t b = blockIdx.x;
     int lo = 0, hi = p.count;                 // the item i with prefix[i] <= b < prefix[i + 1]
     while (hi - lo > 1) {
@@ -93,12 +93,29 @@ __global__ void __launch_bounds__(kBatchThreads) sincos_batched_kernel(const __g
     }
 }
 
+template <int CAP>
+static cudaError_t launch_cap(int variant, const BatchParams &p, uint64_t blocks, cudaStream_t stream) {
+    BatchParamsT<CAP> q;                      // the first `count` records, in a smaller block
+    q.count = p.count;
+    q.pad = 0;
+    for (int i = 0; i <= p.count; ++i) q.prefix[i] = p.prefix[i];
+    for (int i = 0; i < p.count; ++i) q.items[i] = p.items[i];
+    const void *fn = variant == kNormalized
+                         ? reinterpret_cast<const void *>(sincos_batched_kernel<kNormalized, CAP>)
+                         : reinterpret_cast<const void *>(sincos_batched_kernel<kRenormalized, CAP>);
+    void *args[] = {&q};
+    return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(blocks)), dim3(kBatchThreads), args, 0, stream);
+}
+
 cudaError_t launch_batched(int variant, const BatchParams &p, cudaStream_t stream) {
     const uint64_t blocks = p.prefix[p.count];
     if (blocks == 0) return cudaSuccess;
     if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidValue;
-    const void *fn = variant == kNormalized ? reinterpret_cast<const void *>(sincos_batched_kernel<kNormalized>)
-                                            : reinterpret_cast<const void *>(sincos_batched_kernel<kRenormalized>);
+    if (p.count <= 16) return launch_cap<16>(variant, p, blocks, stream);
+    if (p.count <= 96) return launch_cap<96>(variant, p, blocks, stream);
+    const void *fn = variant == kNormalized
+                         ? reinterpret_cast<const void *>(sincos_batched_kernel<kNormalized, kBatchMax>)
+                         : reinterpret_cast<const void *>(sincos_batched_kernel<kRenormalized, kBatchMax>);
     void *args[] = {const_cast<BatchParams *>(&p)};
     return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(blocks)), dim3(kBatchThreads), args, 0, stream);
 }

@@ -34,12 +34,16 @@ struct BatchItem {
     uint32_t vec, pad;     // 1: 256-bit body from `head`; 0: one element per thread
 };
 constexpr int kBatchMax = 480;   // items per launch: the table fits the 32 KB parameter block
-struct BatchParams {
+// The table travels in the kernel's parameter block; the launch copies the whole struct, so it
+// comes in three capacities (the smallest that holds the batch is launched).
+template <int CAP>
+struct BatchParamsT {
     int count;
     int pad;
-    uint64_t prefix[kBatchMax + 1];   // cumulative 1024-element chunks (blocks)
-    BatchItem items[kBatchMax];
+    uint64_t prefix[CAP + 1];   // cumulative 1024-element chunks (blocks)
+    BatchItem items[CAP];
 };
+using BatchParams = BatchParamsT<kBatchMax>;
 static_assert(sizeof(BatchParams) <= 32764, "kernel parameter block limit");
 uint64_t batched_chunks(uint64_t n, uint64_t head, bool vec);
 cudaError_t launch_batched(int variant, const BatchParams &p, cudaStream_t stream);

@@ -30,7 +30,7 @@ def timed(fn, reps=20):
 def main():
     L = sp.lib()
     out = {}
-    for count, n in ((1000, 256), (1000, 4096), (100, 65536), (2000, 1000)):
+    for count, n in ((1000, 256), (1000, 4096), (100, 65536), (2000, 1000), (10, 4096), (60, 4096)):
         base = torch.rand(count * n, device="cuda") * 200 - 100
         s = torch.empty_like(base)
         c = torch.empty_like(base)

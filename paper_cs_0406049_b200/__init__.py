@@ -16,7 +16,7 @@ import os
 __all__ = [
     # the hot path
     "NORMALIZED", "RENORMALIZED", "SincosError", "lib", "library_path", "sincos", "cis", "sincos_pairs",
-    "sincos_pairs_host", "host_workspace_min_bytes", "Item", "sincos_pairs_batched", "sincos_batched",
+    "sincos_pairs_host", "host_workspace_min_bytes", "Item", "BatchTable", "sincos_pairs_batched", "sincos_batched",
     # multi-GPU / statistics (8(e))
     "shard_range", "sincos_pairs_sharded", "sincos_pairs_sharded_stats", "nccl_available", "error_stats",
     # NEXT rows (8(f))
@@ -270,28 +270,61 @@ class Item(ctypes.Structure):
                 ("inter", ctypes.c_void_p), ("n", ctypes.c_uint64)]
 
 
-@_on_tensor_device
+class BatchTable:
+    """A validated, reusable item table for sincos_pairs_batched (the sincos_item_t layout as one
+    uint64 array): build it once for a fixed set of buffers, then run() costs one C call --
+    the per-item Python work (~1 us each) is paid once, not per call.  Keeps the tensors alive."""
+
+    def __init__(self, thetas, sin_outs=None, cos_outs=None, interleaved_outs=None):
+        self.tab = _batch_table(thetas, sin_outs, cos_outs, interleaved_outs)
+        self.tensors = (list(thetas), sin_outs, cos_outs, interleaved_outs)
+        self.count = len(thetas)
+
+    def run(self, variant=NORMALIZED, stream=None):
+        import torch
+        if self.count:
+            st = lib().sincos_pairs_batched(self.tab.ctypes.data, self.count, _variant(variant),
+                                            _stream(stream, torch.device("cuda", torch.cuda.current_device())))
+            _check(st, "sincos_pairs_batched")
+
+
+def _batch_table(thetas, sin_outs, cos_outs, interleaved_outs):
+    import numpy as np
+    import torch
+    k = len(thetas)
+    tab = np.zeros((k, 5), dtype=np.uint64)
+    if k == 0:
+        return tab
+    dev = torch.cuda.current_device()
+
+    def ok(t, name):
+        if t.dtype != torch.float32 or not t.is_cuda or t.get_device() != dev or not t.is_contiguous():
+            raise ValueError(f"{name}: every tensor must be a contiguous float32 CUDA tensor on the current device")
+        return t.data_ptr()
+
+    tab[:, 0] = [ok(t, "theta") for t in thetas]
+    n = np.array([t.numel() for t in thetas], dtype=np.uint64)
+    tab[:, 4] = n
+    if interleaved_outs is not None:
+        if len(interleaved_outs) != k or any(o.numel() != 2 * int(m) for o, m in zip(interleaved_outs, n)):
+            raise ValueError("interleaved_outs must hold 2*n floats each")
+        tab[:, 3] = [ok(o, "interleaved_out") for o in interleaved_outs]
+    else:
+        if len(sin_outs) != k or len(cos_outs) != k or any(
+                so.numel() != int(m) or co.numel() != int(m) for so, co, m in zip(sin_outs, cos_outs, n)):
+            raise ValueError("outputs must hold n floats each")
+        tab[:, 1] = [ok(o, "sin_out") for o in sin_outs]
+        tab[:, 2] = [ok(o, "cos_out") for o in cos_outs]
+    return tab
+
+
 def sincos_pairs_batched(thetas, sin_outs=None, cos_outs=None, interleaved_outs=None, variant=NORMALIZED,
                          stream=None):
     """C-ABI sincos_pairs_batched: many arrays in one launch (per 480 arrays).  thetas: list of
-    CUDA float32 tensors; outputs: lists of the same length (split) or interleaved_outs."""
-    k = len(thetas)
-    arr = (Item * max(k, 1))()
-    for i, th in enumerate(thetas):
-        n = th.numel()
-        if interleaved_outs is not None:
-            io = interleaved_outs[i]
-            if io.numel() != 2 * n:
-                raise ValueError("interleaved_out must hold 2*n floats")
-            arr[i] = Item(_ptr(th, "theta"), None, None, _ptr(io, "interleaved_out"), n)
-        else:
-            so, co = sin_outs[i], cos_outs[i]
-            if so.numel() != n or co.numel() != n:
-                raise ValueError("outputs must hold n floats")
-            arr[i] = Item(_ptr(th, "theta"), _ptr(so, "sin_out"), _ptr(co, "cos_out"), None, n)
-    dev = thetas[0].device if k else None
-    st = lib().sincos_pairs_batched(ctypes.addressof(arr), k, _variant(variant), _stream(stream, dev) if k else None)
-    _check(st, "sincos_pairs_batched")
+    CUDA float32 contiguous tensors on the current device; outputs: lists of the same length
+    (split) or interleaved_outs.  The item table is built as one uint64 array (the
+    sincos_item_t layout: 4 pointers + n), so marshalling costs ~1 us per item."""
+    BatchTable(thetas, sin_outs, cos_outs, interleaved_outs).run(variant, stream)
 
 
 def sincos_batched(thetas, variant="normalized", interleaved=False, stream=None):

@@ -98,3 +98,16 @@ def test_16bit_and_method_floors(bufs):
     m = sp.make_method(*sp.PAPER_METHODS[0])
     got = gbps(lambda: sp.sincos_pairs_method(th, m, sb[:N], cb[:N]), 12 * N)
     assert got >= 6000, f"method {got:.0f}"         # recorded 6.83-6.89 TB/s
+
+
+def test_batched_floor():
+    """1000 arrays of 4096 angles in one batched call (recorded 24 us = 169 G pairs/s)."""
+    count, n = 1000, 4096
+    base = torch.rand(count * n, device="cuda")
+    s, c = torch.empty_like(base), torch.empty_like(base)
+    ts = [base[i * n:(i + 1) * n] for i in range(count)]
+    ss = [s[i * n:(i + 1) * n] for i in range(count)]
+    cs = [c[i * n:(i + 1) * n] for i in range(count)]
+    table = sp.BatchTable(ts, ss, cs)                 # per-item marshalling paid once
+    pairs_per_s = gbps(table.run, count * n, reps=200) * 1e9   # host-bound: ~26 us per call
+    assert pairs_per_s >= 8e10, pairs_per_s

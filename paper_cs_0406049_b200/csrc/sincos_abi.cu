@@ -385,9 +385,9 @@ static sincos_status_t interleave_impl(bool to_inter, const float *s, const floa
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e);
-    size_t grid = (n + 255) / 256;
-    const size_t cap = static_cast<size_t>(sm_count(dev)) * 32;
-    if (grid > cap) grid = cap;
+    size_t grid = (n / 4 + 255) / 256;                // a vector of 4 per thread, one trip
+    if (grid < 1) grid = 1;
+    if (grid > 0x7FFFFFFFu) grid = 0x7FFFFFFFu;
     e = launch_interleave(to_inter, static_cast<unsigned>(grid), s, c, io, n, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e);
     g_launches.fetch_add(1, std::memory_order_relaxed);

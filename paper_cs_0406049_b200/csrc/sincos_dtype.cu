@@ -116,18 +116,41 @@ cudaError_t launch_pairs16(int variant, int dtype, bool inter, unsigned grid, co
     return cudaLaunchKernel(fn, dim3(grid), dim3(128), args, 0, stream);
 }
 
-// ---- adapters: split <-> interleaved (fp32), one element per thread per trip ----------------
+// ---- adapters: split <-> interleaved (fp32) ---------------------------------------------------
+// Vector body when sin, cos and the pairs are 16-B aligned: a thread moves 4 elements -- two
+// 128-bit loads and two 128-bit stores (whole sectors per warp instruction); any other alignment
+// and the ragged tail one element per thread.  Grid-stride.
 __global__ void __launch_bounds__(256) interleave_kernel(const float *__restrict__ s, const float *__restrict__ c,
                                                          float2 *__restrict__ io, size_t n) {
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
-    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += nthr)
-        io[e] = make_float2(__ldcs(c + e), __ldcs(s + e));
+    const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(c) |
+                       reinterpret_cast<uintptr_t>(io)) & 15) == 0;
+    const size_t nv = vec ? n / 4 : 0;
+    for (size_t v = tid; v < nv; v += nthr) {
+        const float4 sv = __ldcs(reinterpret_cast<const float4 *>(s) + v);
+        const float4 cv = __ldcs(reinterpret_cast<const float4 *>(c) + v);
+        float4 *o = reinterpret_cast<float4 *>(io + 4 * v);
+        __stcs(o, make_float4(cv.x, sv.x, cv.y, sv.y));
+        __stcs(o + 1, make_float4(cv.z, sv.z, cv.w, sv.w));
+    }
+    for (size_t e = 4 * nv + tid; e < n; e += nthr) io[e] = make_float2(__ldcs(c + e), __ldcs(s + e));
 }
 
 __global__ void __launch_bounds__(256) deinterleave_kernel(const float2 *__restrict__ io, float *__restrict__ s,
                                                            float *__restrict__ c, size_t n) {
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
-    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += nthr) {
+    const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(c) |
+                       reinterpret_cast<uintptr_t>(io)) & 15) == 0;
+    const size_t nv = vec ? n / 4 : 0;
+    for (size_t v = tid; v < nv; v += nthr) {
+        const float4 *p = reinterpret_cast<const float4 *>(io + 4 * v);
+        const float4 a = __ldcs(p), b = __ldcs(p + 1);
+        __stcs(reinterpret_cast<float4 *>(c) + v, make_float4(a.x, a.z, b.x, b.z));
+        __stcs(reinterpret_cast<float4 *>(s) + v, make_float4(a.y, a.w, b.y, b.w));
+    }
+    for (size_t e = 4 * nv + tid; e < n; e += nthr) {
         const float2 v = __ldcs(io + e);
         __stcs(c + e, v.x);
         __stcs(s + e, v.y);

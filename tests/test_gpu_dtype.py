@@ -171,3 +171,23 @@ def test_16bit_every_theta_offset(dtype, realign):
                         assert same16(gi[0::2], rn16(wc[ot:ot + n], dtype), dtype).all(), tag
     finally:
         sp.set_realign(prev)
+
+
+@pytest.mark.parametrize("n", [1, 5, 1003, (1 << 20) + 7])
+@pytest.mark.parametrize("offs", [(0, 0, 0), (1, 1, 2), (3, 0, 1), (0, 2, 0)])
+def test_adapters_any_alignment(n, offs):
+    """split <-> interleaved at 4-B offsets (the one-element path) and aligned (the 4-wide
+    vector body with a ragged tail): exact round trip, outputs equal the inputs' layout."""
+    os_, oc, oi = offs
+    sb = torch.randn(n + 8, device="cuda")
+    cb = torch.randn(n + 8, device="cuda")
+    s, c = sb[os_:os_ + n], cb[oc:oc + n]
+    ib = torch.empty(2 * n + 8, device="cuda")
+    io = ib[2 * oi:2 * oi + 2 * n]
+    sp.interleave(s, c, io)
+    s2b, c2b = torch.empty(n + 8, device="cuda"), torch.empty(n + 8, device="cuda")
+    s2, c2 = s2b[oc:oc + n], c2b[os_:os_ + n]
+    sp.deinterleave(io, s2, c2)
+    torch.cuda.synchronize()
+    assert torch.equal(io[0::2], c) and torch.equal(io[1::2], s)
+    assert torch.equal(s2, s) and torch.equal(c2, c)

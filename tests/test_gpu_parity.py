@@ -696,3 +696,19 @@ def test_dependent_launch_chain_keeps_stream_order(pdl):
         assert_parity(cur.cpu().numpy(), c.cpu().numpy(), want, wc, f"chain pdl={pdl}")
     finally:
         sp.set_pdl(prev)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("coff", [1, 2, 3, 5])
+def test_in_place_with_cos_off_alignment(variant, coff):
+    """theta == sin_out (exact in place) with cos at another offset: the output-realigning
+    kernel reads theta through the read-only path while writing sin over it, one owner thread
+    per element -- still the oracle's pairs."""
+    th = inputs.generate(2, 0, (1 << 20) + 11)
+    os_, oc = oracle.sincos(th, variant)
+    t = torch.from_numpy(th).cuda()
+    cb = torch.empty(t.numel() + 8, device="cuda")
+    c = cb[coff:coff + t.numel()]
+    sp.sincos_pairs(t, t, c, variant=variant)
+    torch.cuda.synchronize()
+    assert_parity(t.cpu().numpy(), c.cpu().numpy(), os_, oc, f"in place, cos +{coff}")

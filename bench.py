@@ -71,16 +71,21 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(n):
-    """dram read+write bytes per launch of the dominant kernel from the committed ncu capture."""
+def ncu_traffic(n, interleaved=False):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu captures
+    (the full-set capture of the bench kernel, else the per-config DRAM capture for this n and
+    layout: profiles/ncu_summary.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     try:
         d = json.load(open(p))
         k = d.get("dominant", {})
-        if int(k.get("n", -1)) == n:
+        if int(k.get("n", -1)) == n and not interleaved:
             return float(k["dram_bytes_read"]) + float(k["dram_bytes_write"])
+        for c in d.get("by_config", {}).values():
+            if int(c["n"]) == n and bool(c["interleaved"]) == bool(interleaved):
+                return float(c["dram_bytes_read"]) + float(c["dram_bytes_write"])
     except Exception:
         pass
     return None
@@ -583,7 +588,7 @@ def run_ours(args, rank, world, local_rank):
     achieved = BYTES_PER_PAIR * n / (avg[dom] / 1e3) / 1e9
     vname = {0: "N", 1: "A"}
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": ncu_traffic(n) if args.workload == "c2" else None,
+            "traffic": ncu_traffic(n, W.interleaved) if world == 1 else None,
             "kernel": f"sincos_vec_kernel variant {vname[dom]}", "bytes_per_launch": BYTES_PER_PAIR * n,
             "bytes_per_pair": BYTES_PER_PAIR, "peak_source": peak_src,
             "frac_of_theoretical_8180": achieved / 8180.0,

@@ -317,9 +317,11 @@ __device__ __forceinline__ void shift_block(const float (&prev)[W], const float 
 
 // Store the W values `val` (W = 8 or 16) of floats [f0, f0 + W) of stream x, whose aligned
 // 8-float (32-B) blocks start k floats (0..7) before f0.  All 32 lanes call it (shuffles).
-template <int W>
-__device__ __forceinline__ void store_realigned(float *x, size_t f0, const float (&val)[W], int k, unsigned lane,
+// KC >= 0: k known at compile time (== KC); KC < 0: k at run time (a switch over register moves).
+template <int W, int KC>
+__device__ __forceinline__ void store_realigned(float *x, size_t f0, const float (&val)[W], int k_rt, unsigned lane,
                                                 bool act, bool last) {
+    const int k = KC >= 0 ? KC : k_rt;
     if (k == 0) {
         if (act) {
 #pragma unroll
@@ -327,21 +329,26 @@ __device__ __forceinline__ void store_realigned(float *x, size_t f0, const float
         }
         return;
     }
-    // only the predecessor's last k <= 7 values are ever used: shuffle those 7
+    // only the predecessor's last k <= 7 values are ever used: shuffle those (7, or K)
+    constexpr int NS = KC > 0 ? KC : 7;
     float prev[W];
 #pragma unroll
-    for (int j = 0; j < W; ++j) prev[j] = j >= W - 7 ? __shfl_up_sync(0xFFFFFFFFu, val[j], 1) : 0.0f;
+    for (int j = 0; j < W; ++j) prev[j] = j >= W - NS ? __shfl_up_sync(0xFFFFFFFFu, val[j], 1) : 0.0f;
     if (!act) return;
     if (lane > 0) {
         float blk[W];
-        switch (k) {
-        case 1: shift_block<1, W>(prev, val, blk); break;
-        case 2: shift_block<2, W>(prev, val, blk); break;
-        case 3: shift_block<3, W>(prev, val, blk); break;
-        case 4: shift_block<4, W>(prev, val, blk); break;
-        case 5: shift_block<5, W>(prev, val, blk); break;
-        case 6: shift_block<6, W>(prev, val, blk); break;
-        default: shift_block<7, W>(prev, val, blk); break;
+        if constexpr (KC > 0) {
+            shift_block<(KC > 0 ? KC : 1), W>(prev, val, blk);
+        } else {
+            switch (k) {
+            case 1: shift_block<1, W>(prev, val, blk); break;
+            case 2: shift_block<2, W>(prev, val, blk); break;
+            case 3: shift_block<3, W>(prev, val, blk); break;
+            case 4: shift_block<4, W>(prev, val, blk); break;
+            case 5: shift_block<5, W>(prev, val, blk); break;
+            case 6: shift_block<6, W>(prev, val, blk); break;
+            default: shift_block<7, W>(prev, val, blk); break;
+            }
         }
 #pragma unroll
         for (int h = 0; h < W; h += 8) store8(x + f0 - k + h, blk + h);
@@ -357,7 +364,9 @@ __device__ __forceinline__ void store_realigned(float *x, size_t f0, const float
     }
 }
 
-template <int V, bool INTER>
+// KI: the interleaved stream's offset at compile time (1, 3, 5, 7: pairs only 4-B aligned) or
+// -1 (run time; split outputs)
+template <int V, bool INTER, int KI>
 __global__ void __launch_bounds__(512) sincos_outshift_kernel(const float *theta, float *so, float *co, float *io,
                                                               size_t head, size_t nvec, size_t n, int ks, int kc) {
     const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -377,35 +386,35 @@ __global__ void __launch_bounds__(512) sincos_outshift_kernel(const float *theta
             float cs[16];
 #pragma unroll
             for (int j = 0; j < 8; ++j) op<V>(x[j], cs[2 * j + 1], cs[2 * j]);
-            store_realigned<16>(io, 2 * e0, cs, ks, lane, act, last);
+            store_realigned<16, KI>(io, 2 * e0, cs, ks, lane, act, last);
         } else {
             float sv[8], cv[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) op<V>(x[j], sv[j], cv[j]);
-            store_realigned<8>(so, e0, sv, ks, lane, act, last);
-            store_realigned<8>(co, e0, cv, kc, lane, act, last);
+            store_realigned<8, -1>(so, e0, sv, ks, lane, act, last);
+            store_realigned<8, -1>(co, e0, cv, kc, lane, act, last);
         }
+    }
+}
+
+template <int V>
+static const void *pick_outshift(bool inter, int ks) {
+    if (!inter) return reinterpret_cast<const void *>(sincos_outshift_kernel<V, false, -1>);
+    switch (ks) {
+    case 1: return reinterpret_cast<const void *>(sincos_outshift_kernel<V, true, 1>);
+    case 3: return reinterpret_cast<const void *>(sincos_outshift_kernel<V, true, 3>);
+    case 5: return reinterpret_cast<const void *>(sincos_outshift_kernel<V, true, 5>);
+    case 7: return reinterpret_cast<const void *>(sincos_outshift_kernel<V, true, 7>);
+    default: return reinterpret_cast<const void *>(sincos_outshift_kernel<V, true, -1>);
     }
 }
 
 cudaError_t launch_outshift(int variant, bool inter, int ks, int kc, unsigned grid, unsigned threads,
                             const float *theta, float *so, float *co, float *io, size_t head, size_t nvec, size_t n,
                             cudaStream_t stream) {
-    const void *fn;
-    switch (variant) {
-    case kNormalized:
-        fn = inter ? reinterpret_cast<const void *>(sincos_outshift_kernel<kNormalized, true>)
-                   : reinterpret_cast<const void *>(sincos_outshift_kernel<kNormalized, false>);
-        break;
-    case kRenormalized:
-        fn = inter ? reinterpret_cast<const void *>(sincos_outshift_kernel<kRenormalized, true>)
-                   : reinterpret_cast<const void *>(sincos_outshift_kernel<kRenormalized, false>);
-        break;
-    default:
-        fn = inter ? reinterpret_cast<const void *>(sincos_outshift_kernel<kNull, true>)
-                   : reinterpret_cast<const void *>(sincos_outshift_kernel<kNull, false>);
-        break;
-    }
+    const void *fn = variant == kNormalized     ? pick_outshift<kNormalized>(inter, ks)
+                     : variant == kRenormalized ? pick_outshift<kRenormalized>(inter, ks)
+                                                : pick_outshift<kNull>(inter, ks);
     void *args[] = {&theta, &so, &co, &io, &head, &nvec, &n, &ks, &kc};
     return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, 0, stream);
 }

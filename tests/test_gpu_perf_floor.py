@@ -50,7 +50,7 @@ CASES = {
     "theta realigned (KB3b)": (1, 0, 0, False, 5800, 6660),
     "theta realigned interleaved": (1, 0, 0, True, 5800, 6770),
     "outputs realigned (KB3c)": (0, 1, 2, False, 4500, 5200),
-    "pairs 4-B only (KB3c)": (0, 1, 1, "odd", 4500, 5400),
+    "pairs 4-B only (KB3c)": (0, 1, 1, "odd", 5500, 6370),
 }
 
 

@@ -47,16 +47,34 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra_flags=(), out: str | None = None,
+          link_flags=()) -> str:
+    """Compile every csrc/*.cu to an object in parallel (one nvcc per file), then link the shared
+    library (cudart static).  extra_flags: e.g. -D switches for A/B builds; out: another path;
+    link_flags: extra flags for the link step (e.g. sanitizer runtimes)."""
+    out = out or LIB
+    if out == LIB and not force and not _stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *sources()]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd, cwd=PKG)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
+    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-cudart", "static")]
+    with tempfile.TemporaryDirectory() as tmp:
+        objs = []
+
+        def one(src):
+            obj = os.path.join(tmp, os.path.basename(src) + ".o")
+            cmd = [nvcc(), *compile_flags, *extra_flags, "-c", "-o", obj, src]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            subprocess.check_call(cmd, cwd=PKG)
+            return obj
+
+        with ThreadPoolExecutor(max(1, min(len(sources()), os.cpu_count() or 1))) as ex:
+            objs = list(ex.map(one, sources()))
+        subprocess.check_call([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+                               "-Xcompiler", "-fPIC", *link_flags, "-o", out + ".tmp", *objs], cwd=PKG)
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

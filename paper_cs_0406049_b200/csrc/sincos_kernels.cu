@@ -23,149 +23,9 @@
 #include <stdint.h>
 
 #include "sincos_launch.h"
-#include "sincos_math.cuh"
-#include "sincos_math2.cuh"
+#include "sincos_stream.cuh"
 
 namespace sincos_b200 {
-
-constexpr int kNull = 2;  // KB4: the traffic-ceiling "variant"
-// Context only (bench): CUDA's own functions with the same traffic -- libm sincosf (accurate,
-// Payne-Hanek slow path for large arguments) and the __sincosf intrinsic.
-constexpr int kCmpSincosf = 3;
-constexpr int kCmpIntrinsic = 4;
-
-template <int V>
-__device__ __forceinline__ void op(float t, float &s, float &c) {
-    if constexpr (V == kNull) {
-        s = t;
-        c = t;
-    } else if constexpr (V == kCmpSincosf) {
-        sincosf(t, &s, &c);
-    } else if constexpr (V == kCmpIntrinsic) {
-        __sincosf(t, &s, &c);
-    } else {
-        sincos_pair<V>(t, s, c);
-    }
-}
-
-// ---- streaming memory access ----------------------------------------------
-// Cache-policy qualifiers of the 256-bit accesses (overridable at build time for the
-// policy experiment in tools/hint_experiment.py; the defaults were measured best).
-#ifndef SINCOS_LD8_Q
-#define SINCOS_LD8_Q ".L1::no_allocate.L2::evict_first"
-#endif
-#ifndef SINCOS_ST8_Q
-#define SINCOS_ST8_Q ".L1::no_allocate.L2::evict_first"
-#endif
-template <int W, bool NC> struct Mem;
-
-template <> struct Mem<8, true> {
-    static __device__ __forceinline__ void load(float (&r)[8], const float *p) {
-        asm volatile("ld.global.nc" SINCOS_LD8_Q ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
-                     : "l"(p));
-    }
-};
-template <> struct Mem<8, false> {
-    static __device__ __forceinline__ void load(float (&r)[8], const float *p) {
-        asm volatile("ld.global" SINCOS_LD8_Q ".v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
-                     : "l"(p));
-    }
-};
-template <> struct Mem<4, true> {
-    static __device__ __forceinline__ void load(float (&r)[4], const float *p) {
-        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                     : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
-                     : "l"(p));
-    }
-};
-template <> struct Mem<4, false> {
-    static __device__ __forceinline__ void load(float (&r)[4], const float *p) {
-        asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                     : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
-                     : "l"(p));
-    }
-};
-
-__device__ __forceinline__ void store8(float *p, const float *r) {
-    asm volatile("st.global" SINCOS_ST8_Q ".v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
-                 :: "l"(p), "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7])
-                 : "memory");
-}
-__device__ __forceinline__ void store4(float *p, const float *r) {
-    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
-                 :: "l"(p), "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3])
-                 : "memory");
-}
-template <int W>
-__device__ __forceinline__ void storeW(float *p, const float *r) {
-    if constexpr (W == 8) store8(p, r); else store4(p, r);
-}
-
-// Packed-fp32 form of the vector body (sincos_math2.cuh; bit-identical).  Build-time
-// switch for measurement only: the path is HBM-bound, so halving FP32 issue slots does
-// not move it.
-#ifndef SINCOS_PACKED_HOT
-#define SINCOS_PACKED_HOT 0
-#endif
-
-// Compute and store one vector of W elements whose first element is `e0`.
-template <int V, bool INTER, int W>
-__device__ __forceinline__ void emit(const float (&x)[W], size_t e0, float *so, float *co, float *io) {
-    if constexpr (SINCOS_PACKED_HOT && V != kNull) {
-        float s[W], c[W];
-#pragma unroll
-        for (int k = 0; k < W; k += 2) {
-            F2 s2, c2;
-            sincos_from_q2<V>(reduce_turn2(mul2(pk2(x[k], x[k + 1]), bc2(kInvTwoPi))), s2, c2);
-            s[k] = lo2(s2);
-            s[k + 1] = hi2(s2);
-            c[k] = lo2(c2);
-            c[k + 1] = hi2(c2);
-        }
-        if constexpr (INTER) {
-            float cs[2 * W];
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-                cs[2 * k] = c[k];
-                cs[2 * k + 1] = s[k];
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) storeW<W>(io + 2 * e0 + h * W, cs + h * W);
-        } else {
-            storeW<W>(so + e0, s);
-            storeW<W>(co + e0, c);
-        }
-        return;
-    }
-    if constexpr (INTER) {
-        float cs[2 * W];
-#pragma unroll
-        for (int k = 0; k < W; ++k) op<V>(x[k], cs[2 * k + 1], cs[2 * k]);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) storeW<W>(io + 2 * e0 + h * W, cs + h * W);
-    } else {
-        float s[W], c[W];
-#pragma unroll
-        for (int k = 0; k < W; ++k) op<V>(x[k], s[k], c[k]);
-        storeW<W>(so + e0, s);
-        storeW<W>(co + e0, c);
-    }
-}
-
-template <int V, bool INTER>
-__device__ __forceinline__ void emit_scalar(const float *theta, size_t e, float *so, float *co, float *io) {
-    float s, c;
-    op<V>(theta[e], s, c);
-    if constexpr (INTER) {
-        io[2 * e] = c;
-        io[2 * e + 1] = s;
-    } else {
-        so[e] = s;
-        co[e] = c;
-    }
-}
 
 // KB1/KB2.  Elements [0, head) and [head + nvec*W, n) scalar; the body is nvec
 // vectors of W elements starting at element `head` (aligned by the host).
@@ -297,126 +157,6 @@ __global__ void __launch_bounds__(512) sincos_shift_kernel(const float *theta, f
             emit<V, false, 4>(x, e0, so, co, io);
         }
     }
-}
-
-// KB3c: the outputs are what does not share theta's alignment (split: sin and cos at
-// different offsets mod 16 B; interleaved: only 4-B aligned pairs).  The frame is theta's:
-// thread v loads the aligned 256-bit theta[head + 8v ..] and computes its eight pairs; each
-// output stream X sits K_X floats past a 32-B boundary at that frame and is written as
-// whole aligned vectors anyway -- the block of X that thread v stores holds the last K_X values
-// of thread v-1 (one warp shuffle up) and its own first values.  A warp's lane 0 has no
-// predecessor in the warp and stores its own part one float at a time; the warp's last
-// active lane stores the K_X values that spill into the next warp's frame the same way, so
-// every element is written exactly once.  K_X is warp-uniform at run time (a switch over
-// register moves).  Head [0, head) and tail one element per thread.  Same numerics.
-template <int K, int W>
-__device__ __forceinline__ void shift_block(const float (&prev)[W], const float (&val)[W], float (&blk)[W]) {
-#pragma unroll
-    for (int j = 0; j < W; ++j) blk[j] = j < K ? prev[W - K + j] : val[j - K];
-}
-
-// Store the W values `val` (W = 8 or 16) of floats [f0, f0 + W) of stream x, whose aligned
-// 8-float (32-B) blocks start k floats (0..7) before f0.  All 32 lanes call it (shuffles).
-// KC >= 0: k known at compile time (== KC); KC < 0: k at run time (a switch over register moves).
-template <int W, int KC>
-__device__ __forceinline__ void store_realigned(float *x, size_t f0, const float (&val)[W], int k_rt, unsigned lane,
-                                                bool act, bool last) {
-    const int k = KC >= 0 ? KC : k_rt;
-    if (k == 0) {
-        if (act) {
-#pragma unroll
-            for (int h = 0; h < W; h += 8) store8(x + f0 + h, val + h);
-        }
-        return;
-    }
-    // only the predecessor's last k <= 7 values are ever used: shuffle those (7, or K)
-    constexpr int NS = KC > 0 ? KC : 7;
-    float prev[W];
-#pragma unroll
-    for (int j = 0; j < W; ++j) prev[j] = j >= W - NS ? __shfl_up_sync(0xFFFFFFFFu, val[j], 1) : 0.0f;
-    if (!act) return;
-    if (lane > 0) {
-        float blk[W];
-        if constexpr (KC > 0) {
-            shift_block<(KC > 0 ? KC : 1), W>(prev, val, blk);
-        } else {
-            switch (k) {
-            case 1: shift_block<1, W>(prev, val, blk); break;
-            case 2: shift_block<2, W>(prev, val, blk); break;
-            case 3: shift_block<3, W>(prev, val, blk); break;
-            case 4: shift_block<4, W>(prev, val, blk); break;
-            case 5: shift_block<5, W>(prev, val, blk); break;
-            case 6: shift_block<6, W>(prev, val, blk); break;
-            default: shift_block<7, W>(prev, val, blk); break;
-            }
-        }
-#pragma unroll
-        for (int h = 0; h < W; h += 8) store8(x + f0 - k + h, blk + h);
-    } else {
-#pragma unroll
-        for (int j = 0; j < W; ++j)
-            if (j < W - k) x[f0 + j] = val[j];
-    }
-    if (last) {
-#pragma unroll
-        for (int j = 0; j < W; ++j)
-            if (j >= W - k) x[f0 + j] = val[j];
-    }
-}
-
-// KI: the interleaved stream's offset at compile time (1, 3, 5, 7: pairs only 4-B aligned) or
-// -1 (run time; split outputs)
-template <int V, bool INTER, int KI>
-__global__ void __launch_bounds__(512) sincos_outshift_kernel(const float *theta, float *so, float *co, float *io,
-                                                              size_t head, size_t nvec, size_t n, int ks, int kc) {
-    const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
-    const size_t tail0 = head + nvec * 8;
-    if (tid < head) emit_scalar<V, INTER>(theta, tid, so, co, io);
-    if (tid < n - tail0) emit_scalar<V, INTER>(theta, tail0 + tid, so, co, io);
-    const unsigned lane = threadIdx.x & 31u;
-    for (size_t w0 = tid - lane; w0 < nvec; w0 += nthr) {   // warp-uniform trips
-        const size_t v = w0 + lane;
-        const bool act = v < nvec;
-        const bool last = act && (lane == 31u || v + 1 >= nvec);
-        float x[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
-        if (act) Mem<8, true>::load(x, theta + head + 8 * v);
-        const size_t e0 = head + 8 * v;
-        if constexpr (INTER) {
-            float cs[16];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) op<V>(x[j], cs[2 * j + 1], cs[2 * j]);
-            store_realigned<16, KI>(io, 2 * e0, cs, ks, lane, act, last);
-        } else {
-            float sv[8], cv[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) op<V>(x[j], sv[j], cv[j]);
-            store_realigned<8, -1>(so, e0, sv, ks, lane, act, last);
-            store_realigned<8, -1>(co, e0, cv, kc, lane, act, last);
-        }
-    }
-}
-
-template <int V>
-static const void *pick_outshift(bool inter, int ks) {
-    if (!inter) return reinterpret_cast<const void *>(sincos_outshift_kernel<V, false, -1>);
-    switch (ks) {
-    case 1: return reinterpret_cast<const void *>(sincos_outshift_kernel<V, true, 1>);
-    case 3: return reinterpret_cast<const void *>(sincos_outshift_kernel<V, true, 3>);
-    case 5: return reinterpret_cast<const void *>(sincos_outshift_kernel<V, true, 5>);
-    case 7: return reinterpret_cast<const void *>(sincos_outshift_kernel<V, true, 7>);
-    default: return reinterpret_cast<const void *>(sincos_outshift_kernel<V, true, -1>);
-    }
-}
-
-cudaError_t launch_outshift(int variant, bool inter, int ks, int kc, unsigned grid, unsigned threads,
-                            const float *theta, float *so, float *co, float *io, size_t head, size_t nvec, size_t n,
-                            cudaStream_t stream) {
-    const void *fn = variant == kNormalized     ? pick_outshift<kNormalized>(inter, ks)
-                     : variant == kRenormalized ? pick_outshift<kRenormalized>(inter, ks)
-                                                : pick_outshift<kNull>(inter, ks);
-    void *args[] = {&theta, &so, &co, &io, &head, &nvec, &n, &ks, &kc};
-    return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, 0, stream);
 }
 
 // KB3: any alignment.

@@ -49,7 +49,7 @@ CASES = {
     "shared 16 B (128-bit)": (4, 0, 0, False, 6000, 6890),
     "theta realigned (KB3b)": (1, 0, 0, False, 5800, 6660),
     "theta realigned interleaved": (1, 0, 0, True, 5800, 6770),
-    "outputs realigned (KB3c)": (0, 1, 2, False, 4500, 5200),
+    "outputs realigned (KB3c)": (0, 1, 2, False, 5500, 6230),
     "pairs 4-B only (KB3c)": (0, 1, 1, "odd", 5500, 6370),
 }
 

@@ -37,11 +37,8 @@ def test_library_host_logic_clean_under_asan_ubsan(tmp_path):
     sys.path.insert(0, ROOT)
     from paper_cs_0406049_b200 import _build
     lib = str(tmp_path / "libsincos_san.so")
-    flags = list(_build.NVCC_FLAGS)
-    i = flags.index("-Xcompiler")
-    flags[i + 1] += ",-fsanitize=address,-fsanitize=undefined,-fno-omit-frame-pointer"
-    subprocess.check_call([_build.nvcc(), *flags, "-Xlinker", "-lasan", "-Xlinker", "-lubsan", "-o", lib,
-                           *_build.sources()], cwd=_build.PKG)
+    _build.build(extra_flags=["-Xcompiler", "-fsanitize=address,-fsanitize=undefined,-fno-omit-frame-pointer"],
+                 out=lib, link_flags=["-Xlinker", "-lasan", "-Xlinker", "-lubsan"])
     pre = " ".join(subprocess.check_output(["gcc", f"-print-file-name={x}"], text=True).strip()
                    for x in ("libasan.so", "libubsan.so"))
     env = dict(os.environ, LD_PRELOAD=pre, ASAN_OPTIONS="detect_leaks=0", UBSAN_OPTIONS="halt_on_error=1")

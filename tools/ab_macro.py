@@ -23,7 +23,7 @@ def build(name, flags):
     from paper_cs_0406049_b200 import _build
     os.makedirs(AB, exist_ok=True)
     out = os.path.join(AB, name + ".so")
-    subprocess.check_call([_build.nvcc(), *_build.NVCC_FLAGS, *flags, "-o", out, *_build.sources()], cwd=_build.PKG)
+    _build.build(extra_flags=flags, out=out)
     print(out)
 
 

@@ -320,9 +320,9 @@ SINCOS_API void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *
 
 /* Unshared alignment (theta and the outputs at different offsets mod 16 B): 1 = keep the
  * outputs' 128-bit stores and re-align theta in registers with warp shuffles (the default),
- * 0 = one element per thread.  Identical results.  Also switches sincos_phase_grid's
- * flat path for rows that are not whole 256-bit vectors.  Process-global; returns the
- * previous setting, or -1 for a value other than 0/1. */
+ * 0 = one element per thread, 2 = re-alignment in its 128-bit form only (A/B).  Identical
+ * results.  Also switches sincos_phase_grid's flat path for rows that are not whole 256-bit
+ * vectors.  Process-global; returns the previous setting, or -1 for a value other than 0/1/2. */
 SINCOS_API int sincos_set_realign(int on);
 
 /* Programmatic dependent launch of the hot kernel (bench / tests): 1 = on (the default) --

@@ -561,12 +561,14 @@ def set_launch_config(threads=None, blocks_per_sm=None, vec=None, unroll=None, p
         raise ValueError(f"unsupported launch config {cfg}")
 
 
-def set_realign(on: bool) -> bool:
-    """Unshared-alignment path: register re-alignment (True, default) or one element per thread."""
-    prev = lib().sincos_set_realign(1 if on else 0)
+def set_realign(on) -> int:
+    """Unshared-alignment path: register re-alignment (True / 1, default), one element per thread
+    (False / 0), or re-alignment in its 128-bit form only (2, A/B).  Returns the previous value."""
+    v = 2 if on == 2 else (1 if on else 0)
+    prev = lib().sincos_set_realign(v)
     if prev < 0:
         raise ValueError(on)
-    return bool(prev)
+    return prev
 
 
 def set_pdl(on: bool) -> bool:

@@ -31,7 +31,8 @@ std::atomic<int> g_vec{8};
 std::atomic<int> g_unroll{1};
 std::atomic<int> g_prefetch{0};
 std::atomic<int> g_shift{1};          // KB3b re-aligning path for unshared alignment (1 = on)
-std::atomic<int> g_phase_flat{1};     // NEXT(1) flat path for rows that are not whole 256-bit vectors
+std::atomic<int> g_phase_flat{1};
+std::atomic<int> g_shift8{1};         // KB3b in its 256-bit form where the outputs allow it     // NEXT(1) flat path for rows that are not whole 256-bit vectors
 
 constexpr int kMaxDev = 64;
 std::atomic<int> g_sm_count[kMaxDev];
@@ -160,6 +161,25 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
                 hs = ((32 - (reinterpret_cast<uintptr_t>(io) & 31)) & 31) / 8;
         } else if (w == 0 && ((reinterpret_cast<uintptr_t>(so) ^ reinterpret_cast<uintptr_t>(co)) & 15) == 0) {
             hs = ((16 - (reinterpret_cast<uintptr_t>(so) & 15)) & 15) / 4;
+        }
+    }
+    // 256-bit form when the outputs take 256-bit stores at a common element (split: sin and cos
+    // share their offset mod 32 B; interleaved: always, being 8-B aligned here)
+    if (hs != SIZE_MAX && g_shift8.load(std::memory_order_relaxed) &&
+        (inter || ((reinterpret_cast<uintptr_t>(so) ^ reinterpret_cast<uintptr_t>(co)) & 31) == 0)) {
+        const size_t h0 = inter ? ((32 - (reinterpret_cast<uintptr_t>(io) & 31)) & 31) / 8
+                                : ((32 - (reinterpret_cast<uintptr_t>(so) & 31)) & 31) / 4;
+        const int k = static_cast<int>(((reinterpret_cast<uintptr_t>(theta) + 4 * h0) & 31) / 4);   // 0..7
+        if (k != 0) {
+            size_t hb = h0 >= static_cast<size_t>(k) ? h0 : h0 + 8;
+            if (hb > n) hb = n;
+            // the second aligned vector of every thread inside theta: (hb - k) + 8 nvec + 7 <= n - 1
+            const size_t nvec = n + k >= hb + 8 ? (n + k - hb - 8) / 8 : 0;
+            e = launch_shift8(variant, inter, k, grid_for(nvec, threads, sms, cfg_bps), threads, theta, so, co, io,
+                              hb, nvec, n, stream);
+            if (e != cudaSuccess) return cuda_fail(e);
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            return SINCOS_OK;
         }
     }
     if (hs != SIZE_MAX) {
@@ -678,9 +698,12 @@ sincos_status_t sincos_pairs_batched(const sincos_item_t *items, int count, sinc
 int sincos_set_pdl(int on) { return set_pdl(on); }
 
 int sincos_set_realign(int on) {
-    if (on != 0 && on != 1) return -1;
-    const int prev = g_shift.exchange(on, std::memory_order_relaxed);
-    g_phase_flat.store(on, std::memory_order_relaxed);
+    if (on != 0 && on != 1 && on != 2) return -1;
+    const int prev = g_shift.load(std::memory_order_relaxed) == 0 ? 0
+                     : g_shift8.load(std::memory_order_relaxed) ? 1 : 2;
+    g_shift.store(on != 0, std::memory_order_relaxed);
+    g_shift8.store(on == 1, std::memory_order_relaxed);
+    g_phase_flat.store(on != 0, std::memory_order_relaxed);
     return prev;
 }
 

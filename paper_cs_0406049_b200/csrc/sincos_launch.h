@@ -21,6 +21,10 @@ cudaError_t launch_compare(int which, bool inter, unsigned grid, unsigned thread
 // KB3b: outputs 16-B aligned from element `head`, theta K = k floats past a 16-B boundary there.
 cudaError_t launch_shift(int variant, bool inter, int k, unsigned grid, unsigned threads, const float *theta,
                          float *so, float *co, float *io, size_t head, size_t nvec, size_t n, cudaStream_t stream);
+// KB3b, 256-bit form (sincos_outshift.cu): outputs 32-B aligned from `head`, theta k = 1..7 floats
+// past a 32-B boundary there.
+cudaError_t launch_shift8(int variant, bool inter, int k, unsigned grid, unsigned threads, const float *theta,
+                          float *so, float *co, float *io, size_t head, size_t nvec, size_t n, cudaStream_t stream);
 // KB3c: theta 32-B aligned from element `head`; outputs re-aligned (ks / kc: sin / cos float
 // offsets past a 32-B boundary there; interleaved: ks = the pairs' float offset past 32 B).
 cudaError_t launch_outshift(int variant, bool inter, int ks, int kc, unsigned grid, unsigned threads,

@@ -142,4 +142,67 @@ cudaError_t launch_outshift(int variant, bool inter, int ks, int kc, unsigned gr
     return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, 0, stream);
 }
 
+// KB3b, 256-bit form: theta K = 1..7 floats past a 32-B boundary where the outputs take
+// 256-bit stores (split: sin and cos at one offset mod 32 B; interleaved: 8-B aligned pairs).
+// Lane l loads a = tal[8v .. 8v+7] (aligned 256-bit); b = the next vector from lane l+1 (only
+// its first K values, K shuffles), or the lane's own load when it has no right-hand neighbour
+// (issued with the first: one round trip).  K is a template parameter: the selection is
+// register renaming.  Head and tail one element per thread.
+template <int V, bool INTER, int K>
+__global__ void __launch_bounds__(512) sincos_shift8_kernel(const float *theta, float *so, float *co, float *io,
+                                                            size_t head, size_t nvec, size_t n) {
+    const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t tail0 = head + nvec * 8;
+    if (tid < head) emit_scalar<V, INTER>(theta, tid, so, co, io);
+    if (tid < n - tail0) emit_scalar<V, INTER>(theta, tail0 + tid, so, co, io);
+    const float *tal = theta + head - K;           // 32-B aligned (host guarantees head >= K)
+    const unsigned lane = threadIdx.x & 31u;
+    for (size_t w0 = tid - lane; w0 < nvec; w0 += nthr) {   // warp-uniform trips
+        const size_t v = w0 + lane;
+        const bool act = v < nvec;
+        const bool own = act && (lane == 31u || v + 1 >= nvec);
+        float a[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+        float bo[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+        if (act) Mem<8, true>::load(a, tal + 8 * v);
+        if (own) Mem<8, true>::load(bo, tal + 8 * v + 8);
+        float x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j + K < 8) {
+                x[j] = a[j + K];
+            } else {
+                const float b = __shfl_down_sync(0xFFFFFFFFu, a[j + K - 8], 1);
+                x[j] = own ? bo[j + K - 8] : b;
+            }
+        }
+        if (act) emit<V, INTER, 8>(x, head + 8 * v, so, co, io);
+    }
+}
+
+template <int V, bool INTER>
+static const void *pick_shift8(int k) {
+    switch (k) {
+    case 1: return reinterpret_cast<const void *>(sincos_shift8_kernel<V, INTER, 1>);
+    case 2: return reinterpret_cast<const void *>(sincos_shift8_kernel<V, INTER, 2>);
+    case 3: return reinterpret_cast<const void *>(sincos_shift8_kernel<V, INTER, 3>);
+    case 4: return reinterpret_cast<const void *>(sincos_shift8_kernel<V, INTER, 4>);
+    case 5: return reinterpret_cast<const void *>(sincos_shift8_kernel<V, INTER, 5>);
+    case 6: return reinterpret_cast<const void *>(sincos_shift8_kernel<V, INTER, 6>);
+    default: return reinterpret_cast<const void *>(sincos_shift8_kernel<V, INTER, 7>);
+    }
+}
+
+cudaError_t launch_shift8(int variant, bool inter, int k, unsigned grid, unsigned threads, const float *theta,
+                          float *so, float *co, float *io, size_t head, size_t nvec, size_t n, cudaStream_t stream) {
+    const void *fn;
+    switch (variant) {
+    case kNormalized: fn = inter ? pick_shift8<kNormalized, true>(k) : pick_shift8<kNormalized, false>(k); break;
+    case kRenormalized: fn = inter ? pick_shift8<kRenormalized, true>(k) : pick_shift8<kRenormalized, false>(k); break;
+    default: fn = inter ? pick_shift8<kNull, true>(k) : pick_shift8<kNull, false>(k); break;
+    }
+    void *args[] = {&theta, &so, &co, &io, &head, &nvec, &n};
+    return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, 0, stream);
+}
+
 }  // namespace sincos_b200

@@ -433,8 +433,9 @@ def test_concurrent_host_threads():
 
 # ---- unshared alignment: register re-alignment (KB3b) and one element per thread (KB3) ----
 
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("bps", [0, 1])
-def test_realign_path(bps):
+def test_realign_path(bps, mode):
     """theta at every offset mod 4 floats against outputs at every offset: where the outputs
     can take 128-bit stores the re-aligning kernel runs (k = 1, 2, 3 with head peeling when the
     aligned theta base would precede theta); lengths around the vector/tail boundaries and
@@ -448,6 +449,7 @@ def test_realign_path(bps):
     big_c = torch.empty(N + 64, dtype=torch.float32, device="cuda")
     big_i = torch.empty(2 * N + 64, dtype=torch.float32, device="cuda")
     sp.set_launch_config(blocks_per_sm=bps)
+    prev = sp.set_realign(mode)              # 1: 256-bit form where possible; 2: 128-bit form only
     try:
         for variant in VARIANTS:
             rs, rc = ref[variant]
@@ -470,6 +472,7 @@ def test_realign_path(bps):
                                       f"realign inter n={n} off={ot},{oo} bps={bps}")
     finally:
         sp.set_launch_config()
+        sp.set_realign(prev)
 
 
 def test_scalar_path_unshared_outputs():

@@ -47,8 +47,8 @@ CASES = {
     "aligned split (256-bit)": (0, 0, 0, False, 6000, 6870),
     "aligned interleaved": (0, 0, 0, True, 6000, 6890),
     "shared 16 B (128-bit)": (4, 0, 0, False, 6000, 6890),
-    "theta realigned (KB3b)": (1, 0, 0, False, 5800, 6660),
-    "theta realigned interleaved": (1, 0, 0, True, 5800, 6770),
+    "theta realigned (KB3b)": (1, 0, 0, False, 6000, 6810),
+    "theta realigned interleaved": (1, 0, 0, True, 6000, 6890),
     "outputs realigned (KB3c)": (0, 1, 2, False, 5500, 6230),
     "pairs 4-B only (KB3c)": (0, 1, 1, "odd", 5500, 6370),
 }

@@ -7,7 +7,7 @@ n = 1 << 28
 base = torch.rand(n + 8, device='cuda') * 2e4 - 1e4
 s = torch.empty(n + 8, device='cuda'); c = torch.empty(n + 8, device='cuda')
 res = {}
-for realign in (True, False):
+for realign in (1, 2, 0):
   sp.set_realign(realign)
   for name, (to, so, co) in {'aligned': (0, 0, 0), 'theta+1': (1, 0, 0), 'out+1': (0, 1, 1), 'all+1': (1, 1, 1),
                              'theta+4': (4, 0, 0), 'sin+1 cos+2': (0, 1, 2), 'theta+3 sin+1 cos+0': (3, 1, 0)}.items():

@@ -46,10 +46,10 @@ __device__ __forceinline__ void emit16_scalar(const float *theta, size_t e, uint
 }
 
 // Full grid, eight angles per thread; outputs: split 2 x 128-bit, interleaved 256-bit.
-// RE = false: theta shares the outputs' vector alignment (one aligned 256-bit load per
-// thread, 32 registers: full occupancy).  RE = true: theta sits k = 1..7 floats off it and is
+// K = 0: theta shares the outputs' vector alignment (one aligned 256-bit load per thread, 32
+// registers: full occupancy).  K = 1..7 (a template parameter): theta sits K floats off it and is
 // re-aligned in registers (sincos_realign.cuh), with warp-uniform trips for the shuffles.
-template <int V, int DT, bool INTER, bool RE>
+template <int V, int DT, bool INTER, int K>
 __global__ void __launch_bounds__(128) sincos16_kernel(const float *theta, uint16_t *so, uint16_t *co, uint16_t *io,
                                                        size_t head, size_t nvec, size_t n, int k) {
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
@@ -59,12 +59,13 @@ __global__ void __launch_bounds__(128) sincos16_kernel(const float *theta, uint1
     if (tid < n - tail0) emit16_scalar<V, DT, INTER>(theta, tail0 + tid, so, co, io);
     const unsigned lane = threadIdx.x & 31u;
     const float *tal = theta + head - k;
+    constexpr bool RE = K > 0;
     for (size_t w0 = RE ? tid - lane : tid; w0 < nvec; w0 += nthr) {
         const size_t v = RE ? w0 + lane : w0;
         float x[8];
         if constexpr (RE) {
             const bool act = v < nvec;
-            load8_realigned(tal, v, nvec, lane, k, act, x);
+            load8_realigned_k<(K > 0 ? K : 1)>(tal, v, nvec, lane, act, x);
             if (!act) continue;
         } else {
             ld8_stream(x, theta + head + 8 * v);
@@ -93,24 +94,32 @@ __global__ void __launch_bounds__(128) sincos16_kernel(const float *theta, uint1
     }
 }
 
-template <int V, int DT, bool RE>
+template <int V, int DT, int K>
 static const void *pick16r(bool inter) {
-    return inter ? reinterpret_cast<const void *>(sincos16_kernel<V, DT, true, RE>)
-                 : reinterpret_cast<const void *>(sincos16_kernel<V, DT, false, RE>);
+    return inter ? reinterpret_cast<const void *>(sincos16_kernel<V, DT, true, K>)
+                 : reinterpret_cast<const void *>(sincos16_kernel<V, DT, false, K>);
 }
 template <int V, int DT>
-static const void *pick16i(bool inter, bool re) {
-    return re ? pick16r<V, DT, true>(inter) : pick16r<V, DT, false>(inter);
+static const void *pick16i(bool inter, int k) {
+    switch (k) {
+    case 0: return pick16r<V, DT, 0>(inter);
+    case 1: return pick16r<V, DT, 1>(inter);
+    case 2: return pick16r<V, DT, 2>(inter);
+    case 3: return pick16r<V, DT, 3>(inter);
+    case 4: return pick16r<V, DT, 4>(inter);
+    case 5: return pick16r<V, DT, 5>(inter);
+    case 6: return pick16r<V, DT, 6>(inter);
+    default: return pick16r<V, DT, 7>(inter);
+    }
 }
 
 cudaError_t launch_pairs16(int variant, int dtype, bool inter, unsigned grid, const float *theta, void *so, void *co,
                            void *io, size_t head, size_t nvec, size_t n, int k, cudaStream_t stream) {
     const void *fn;
-    const bool re = k != 0;
     if (variant == kNormalized)
-        fn = dtype == 1 ? pick16i<kNormalized, 1>(inter, re) : pick16i<kNormalized, 2>(inter, re);
+        fn = dtype == 1 ? pick16i<kNormalized, 1>(inter, k) : pick16i<kNormalized, 2>(inter, k);
     else
-        fn = dtype == 1 ? pick16i<kRenormalized, 1>(inter, re) : pick16i<kRenormalized, 2>(inter, re);
+        fn = dtype == 1 ? pick16i<kRenormalized, 1>(inter, k) : pick16i<kRenormalized, 2>(inter, k);
     uint16_t *s = static_cast<uint16_t *>(so), *c = static_cast<uint16_t *>(co), *i = static_cast<uint16_t *>(io);
     void *args[] = {&theta, &s, &c, &i, &head, &nvec, &n, &k};
     return cudaLaunchKernel(fn, dim3(grid), dim3(128), args, 0, stream);

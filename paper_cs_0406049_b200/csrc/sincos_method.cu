@@ -38,11 +38,11 @@ __device__ __forceinline__ void st8m(float *p, const float *r) {
 }
 
 // Full grid, eight angles per thread over [head, head + 8 nvec); scalar head/tail.
-// RE = false: theta shares the outputs' 32-B alignment (one aligned 256-bit load per thread).
-// RE = true: theta sits k = 1..7 floats off it and is re-aligned in registers
+// K = 0: theta shares the outputs' 32-B alignment (one aligned 256-bit load per thread).
+// K = 1..7 (a template parameter): theta sits K floats off it and is re-aligned in registers
 // (sincos_realign.cuh), with warp-uniform trips for the shuffles.
 // vec == false: every element scalar (outputs that cannot take 256-bit stores).
-template <int NT, int FIX, bool INTER, bool RE>
+template <int NT, int FIX, bool INTER, int K>
 __global__ void __launch_bounds__(128) method_kernel(const MethodParams m, const float *theta, float *so,
                                                      float *co, float *io, size_t head, size_t nvec, size_t n,
                                                      bool vec, int k) {
@@ -57,12 +57,13 @@ __global__ void __launch_bounds__(128) method_kernel(const MethodParams m, const
     if (tid < n - tail0) method_scalar<NT, FIX, INTER>(m, theta, tail0 + tid, so, co, io);
     const unsigned lane = threadIdx.x & 31u;
     const float *tal = theta + head - k;
+    constexpr bool RE = K > 0;
     for (size_t w0 = RE ? tid - lane : tid; w0 < nvec; w0 += nthr) {
         const size_t v = RE ? w0 + lane : w0;
         float x[8];
         if constexpr (RE) {
             const bool act = v < nvec;
-            load8_realigned(tal, v, nvec, lane, k, act, x);
+            load8_realigned_k<(K > 0 ? K : 1)>(tal, v, nvec, lane, act, x);
             if (!act) continue;
         } else {
             ld8_stream(x, theta + head + 8 * v);
@@ -84,14 +85,23 @@ __global__ void __launch_bounds__(128) method_kernel(const MethodParams m, const
     }
 }
 
-template <int NT, int FIX, bool RE>
+template <int NT, int FIX, int K>
 static const void *pick_mr(bool inter) {
-    return inter ? reinterpret_cast<const void *>(method_kernel<NT, FIX, true, RE>)
-                 : reinterpret_cast<const void *>(method_kernel<NT, FIX, false, RE>);
+    return inter ? reinterpret_cast<const void *>(method_kernel<NT, FIX, true, K>)
+                 : reinterpret_cast<const void *>(method_kernel<NT, FIX, false, K>);
 }
 template <int NT, int FIX>
-static const void *pick_m(bool inter, bool re) {
-    return re ? pick_mr<NT, FIX, true>(inter) : pick_mr<NT, FIX, false>(inter);
+static const void *pick_m(bool inter, int k) {
+    switch (k) {
+    case 0: return pick_mr<NT, FIX, 0>(inter);
+    case 1: return pick_mr<NT, FIX, 1>(inter);
+    case 2: return pick_mr<NT, FIX, 2>(inter);
+    case 3: return pick_mr<NT, FIX, 3>(inter);
+    case 4: return pick_mr<NT, FIX, 4>(inter);
+    case 5: return pick_mr<NT, FIX, 5>(inter);
+    case 6: return pick_mr<NT, FIX, 6>(inter);
+    default: return pick_mr<NT, FIX, 7>(inter);
+    }
 }
 
 // fix: 0 linear (penultimate), 1 reciprocal (penultimate), 3 none.  Terms <= 4 use the
@@ -102,11 +112,11 @@ cudaError_t launch_method(const float *ss, int n_ss, const float *cc, int n_cc, 
     MethodParams m = make_params(ss, n_ss, cc, n_cc, doublings);
     const bool small = n_ss <= 4 && n_cc <= 4;
     const void *fn;
-    const bool re = vec && k != 0;
+    const int kk = vec ? k : 0;
     if (small)
-        fn = fix == 0 ? pick_m<4, 0>(inter, re) : fix == 1 ? pick_m<4, 1>(inter, re) : pick_m<4, 3>(inter, re);
+        fn = fix == 0 ? pick_m<4, 0>(inter, kk) : fix == 1 ? pick_m<4, 1>(inter, kk) : pick_m<4, 3>(inter, kk);
     else
-        fn = fix == 0 ? pick_m<8, 0>(inter, re) : fix == 1 ? pick_m<8, 1>(inter, re) : pick_m<8, 3>(inter, re);
+        fn = fix == 0 ? pick_m<8, 0>(inter, kk) : fix == 1 ? pick_m<8, 1>(inter, kk) : pick_m<8, 3>(inter, kk);
     void *args[] = {&m, &theta, &so, &co, &io, &head, &nvec, &n, &vec, &k};
     return cudaLaunchKernel(fn, dim3(grid), dim3(128), args, 0, stream);
 }

@@ -3,13 +3,11 @@
 // vector alignment (16-bit outputs, general methods).
 //
 // The caller's vector v covers angles theta[head + 8v .. head + 8v + 7]; tal = theta + head - K
-// is 32-B aligned, K = 0..7 the angles' float offset past that boundary (warp-uniform, a
-// runtime value).  Lane l loads a = tal[8v .. 8v+7]; the next aligned vector b comes from
+// is 32-B aligned, K = 1..7 the angles' float offset past that boundary (the callers run an
+// aligned-load instance for K = 0).  Lane l loads a = tal[8v .. 8v+7]; the next aligned vector b comes from
 // lane l+1 by warp shuffles, or from its own load for the warp's last lane and for a lane
 // whose neighbour is past the end (issued together with the first load: one round trip).
-// x = a[K..7] ++ b[0..K-1], selected by a uniform switch over K (register moves only).
-// K = 1..7: the callers run a separate kernel instance for K = 0 (a plain aligned load, and
-// fewer registers -- full occupancy -- than this path needs).
+// x = a[K..7] ++ b[0..K-1].
 // Must be called by all 32 lanes (act = false for lanes past the end); the host sizes nvec
 // so that tal[8 nvec + 7] lies inside theta when K > 0.
 #pragma once
@@ -25,32 +23,25 @@ __device__ __forceinline__ void ld8_stream(float (&r)[8], const float *p) {
                  : "l"(p));
 }
 
+// K (1..7) is a compile-time parameter: only the K values taken from the next lane are shuffled
+// and the selection is register renaming (a run-time K with a switch over register moves was
+// measured 15-20% slower).
 template <int K>
-__device__ __forceinline__ void select8(const float (&a)[8], const float (&b)[8], float (&x)[8]) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = j + K < 8 ? a[j + K] : b[j + K - 8];
-}
-
-__device__ __forceinline__ void load8_realigned(const float *tal, size_t v, size_t nvec, unsigned lane, int k,
-                                                bool act, float (&x)[8]) {
-    float a[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+__device__ __forceinline__ void load8_realigned_k(const float *tal, size_t v, size_t nvec, unsigned lane, bool act,
+                                                  float (&x)[8]) {
     const bool own = act && (lane == 31u || v + 1 >= nvec);
+    float a[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
     float bo[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
     if (act) ld8_stream(a, tal + 8 * v);
     if (own) ld8_stream(bo, tal + 8 * v + 8);
-    float b[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) b[j] = __shfl_down_sync(0xFFFFFFFFu, a[j], 1);   // every lane shuffles
-#pragma unroll
-    for (int j = 0; j < 8; ++j) b[j] = own ? bo[j] : b[j];
-    switch (k) {
-    case 1: select8<1>(a, b, x); break;
-    case 2: select8<2>(a, b, x); break;
-    case 3: select8<3>(a, b, x); break;
-    case 4: select8<4>(a, b, x); break;
-    case 5: select8<5>(a, b, x); break;
-    case 6: select8<6>(a, b, x); break;
-    default: select8<7>(a, b, x); break;
+    for (int j = 0; j < 8; ++j) {
+        if (j + K < 8) {
+            x[j] = a[j + K];
+        } else {
+            const float b = __shfl_down_sync(0xFFFFFFFFu, a[j + K - 8], 1);
+            x[j] = own ? bo[j + K - 8] : b;
+        }
     }
 }
 

@@ -98,6 +98,11 @@ def test_16bit_and_method_floors(bufs):
     m = sp.make_method(*sp.PAPER_METHODS[0])
     got = gbps(lambda: sp.sincos_pairs_method(th, m, sb[:N], cb[:N]), 12 * N)
     assert got >= 6000, f"method {got:.0f}"         # recorded 6.83-6.89 TB/s
+    tb = base[1:1 + N]                                # theta one float off: the re-aligning instances
+    got = gbps(lambda: sp.sincos_pairs_dtype(tb, s16, c16), 8 * N)
+    assert got >= 5600, f"fp16 realigned {got:.0f}"  # recorded 6.47 TB/s
+    got = gbps(lambda: sp.sincos_pairs_method(tb, m, sb[:N], cb[:N]), 12 * N)
+    assert got >= 6000, f"method realigned {got:.0f}"  # recorded 6.82 TB/s
 
 
 def test_batched_floor():

@@ -39,7 +39,7 @@ def one_case(rng):
     th = draw_theta(rng, n)
     variant = int(rng.integers(0, 2))
     inter = bool(rng.integers(0, 2))
-    entry = ["pairs", "dtype32", "method", "phase", "batched"][int(rng.integers(0, 5))]
+    entry = ["pairs", "dtype32", "method", "phase", "batched", "fp16", "bf16"][int(rng.integers(0, 7))]
     ot, os_, oc = (int(x) for x in rng.integers(0, 8, 3))
     if rng.random() < 0.5:
         oc = os_
@@ -50,18 +50,21 @@ def one_case(rng):
     tbuf = torch.empty(n + 16, dtype=torch.float32, device="cuda")
     tbuf[ot:ot + n].copy_(torch.from_numpy(th))
     t = tbuf[ot:ot + n]
+    dt = {"fp16": torch.float16, "bf16": torch.bfloat16}.get(entry, torch.float32)
     if inter:
-        io = torch.empty(2 * n + 16, dtype=torch.float32, device="cuda")[os_:os_ + 2 * n]
+        io = torch.empty(2 * n + 16, dtype=dt, device="cuda")[2 * os_ if dt != torch.float32 else os_:][:2 * n]
         outs = {"interleaved_out": io}
     else:
-        outs = {"sin_out": torch.empty(n + 16, device="cuda")[os_:os_ + n],
-                "cos_out": torch.empty(n + 16, device="cuda")[oc:oc + n]}
+        outs = {"sin_out": torch.empty(n + 16, dtype=dt, device="cuda")[os_:os_ + n],
+                "cos_out": torch.empty(n + 16, dtype=dt, device="cuda")[oc:oc + n]}
     if entry == "pairs":
         sp.sincos_pairs(t, variant=variant, **outs)
     elif entry == "dtype32":
         sp.sincos_pairs_dtype(t, variant=variant, **outs)
     elif entry == "method":
         sp.sincos_pairs_method(t, sp.make_method(*sp.PAPER_METHODS[variant]), **outs)
+    elif entry in ("fp16", "bf16"):
+        sp.sincos_pairs_dtype(t, variant=variant, **outs)
     elif entry == "phase":
         sp.phase_grid(torch.ones(1, device="cuda"), t, units=sp.RADIANS, variant=variant, **outs)
     else:
@@ -72,11 +75,14 @@ def one_case(rng):
             sp.sincos_pairs_batched([t], [outs["sin_out"]], [outs["cos_out"]], variant=variant)
     torch.cuda.synchronize()
     if inter:
-        v = outs["interleaved_out"].cpu().numpy()
+        v = outs["interleaved_out"].float().cpu().numpy()
         gs, gc = v[1::2], v[0::2]
     else:
-        gs, gc = outs["sin_out"].cpu().numpy(), outs["cos_out"].cpu().numpy()
+        gs, gc = outs["sin_out"].float().cpu().numpy(), outs["cos_out"].float().cpu().numpy()
     ws, wc = oracle.sincos(th, variant)
+    if dt != torch.float32:               # the library's RN cast of the oracle's fp32 pair
+        ws = torch.from_numpy(ws).to(dt).float().numpy()
+        wc = torch.from_numpy(wc).to(dt).float().numpy()
     ok = bool(same_values(gs, ws).all() and same_values(gc, wc).all())
     return ok, n, entry
 

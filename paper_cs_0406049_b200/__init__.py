@@ -563,8 +563,10 @@ def set_launch_config(threads=None, blocks_per_sm=None, vec=None, unroll=None, p
 
 def set_realign(on) -> int:
     """Unshared-alignment path: register re-alignment (True / 1, default), one element per thread
-    (False / 0), or re-alignment in its 128-bit form only (2, A/B).  Returns the previous value."""
-    v = 2 if on == 2 else (1 if on else 0)
+    (False / 0), re-alignment in its 128-bit form only (2, A/B), or 1 with the phase grid's
+    ragged rows through its flat kernel instead of the row kernel (3, A/B).  Returns the
+    previous value."""
+    v = on if on in (2, 3) else (1 if on else 0)
     prev = lib().sincos_set_realign(v)
     if prev < 0:
         raise ValueError(on)

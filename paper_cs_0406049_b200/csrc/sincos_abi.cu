@@ -32,6 +32,7 @@ std::atomic<int> g_unroll{1};
 std::atomic<int> g_prefetch{0};
 std::atomic<int> g_shift{1};          // KB3b re-aligning path for unshared alignment (1 = on)
 std::atomic<int> g_phase_flat{1};
+std::atomic<int> g_phase_rows{1};   // 0 (sincos_set_realign(3), A/B): ragged phase rows via the flat kernel
 std::atomic<int> g_shift8{1};         // KB3b in its 256-bit form where the outputs allow it     // NEXT(1) flat path for rows that are not whole 256-bit vectors
 
 constexpr int kMaxDev = 64;
@@ -322,14 +323,21 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
     const bool vec = nt % 8 == 0 && aligned(t_dev, 32) &&
                      (split ? aligned(sin_dev, 32) && aligned(cos_dev, 32) : aligned(inter_dev, 32));
     cudaError_t e;
-    // any other shape: the flat path when the outputs can take 256-bit stores from some pair on
-    // (split: sin and cos share their alignment mod 32 B; interleaved: 8-B aligned) and the
-    // fp64 quotient estimate of a pair index is exact enough (n < 2^52); else one per thread
+    // any other shape: when the outputs can take 256-bit stores from some pair on (split: sin
+    // and cos share their alignment mod 32 B; interleaved: 8-B aligned), the row path for
+    // nt >= kPhaseRowsMinNt, else the flat path (its fp64 quotient estimate of a pair index needs
+    // n < 2^52); else one per thread
     const uintptr_t so_a = reinterpret_cast<uintptr_t>(sin_dev), co_a = reinterpret_cast<uintptr_t>(cos_dev),
                     io_a = reinterpret_cast<uintptr_t>(inter_dev);
     const bool flat = !vec && g_phase_flat.load(std::memory_order_relaxed) && n < (size_t(1) << 52) &&
                       (split ? ((so_a ^ co_a) & 31) == 0 : aligned(inter_dev, 8));
-    if (flat) {
+    if (flat && nt >= kPhaseRowsMinNt && g_phase_rows.load(std::memory_order_relaxed)) {
+        const unsigned h0 = static_cast<unsigned>(split ? ((32 - (so_a & 31)) & 31) / 4 : ((32 - (io_a & 31)) & 31) / 8);
+        int dev = 0;
+        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return cuda_fail(e);
+        e = launch_phase_rows(variant, inter, units == SINCOS_TURNS, f_dev, nf, t_dev, nt, sin_dev, cos_dev,
+                              inter_dev, h0, sm_count(dev), static_cast<cudaStream_t>(stream));
+    } else if (flat) {
         size_t head = split ? ((32 - (so_a & 31)) & 31) / 4 : ((32 - (io_a & 31)) & 31) / 8;
         if (head > n) head = n;
         const size_t nvec = (n - head) / 8;
@@ -698,12 +706,15 @@ sincos_status_t sincos_pairs_batched(const sincos_item_t *items, int count, sinc
 int sincos_set_pdl(int on) { return set_pdl(on); }
 
 int sincos_set_realign(int on) {
-    if (on != 0 && on != 1 && on != 2) return -1;
-    const int prev = g_shift.load(std::memory_order_relaxed) == 0 ? 0
-                     : g_shift8.load(std::memory_order_relaxed) ? 1 : 2;
+    if (on < 0 || on > 3) return -1;
+    const int prev = g_shift.load(std::memory_order_relaxed) == 0        ? 0
+                     : !g_phase_rows.load(std::memory_order_relaxed)     ? 3
+                     : g_shift8.load(std::memory_order_relaxed)          ? 1
+                                                                         : 2;
     g_shift.store(on != 0, std::memory_order_relaxed);
-    g_shift8.store(on == 1, std::memory_order_relaxed);
+    g_shift8.store(on == 1 || on == 3, std::memory_order_relaxed);
     g_phase_flat.store(on != 0, std::memory_order_relaxed);
+    g_phase_rows.store(on != 3, std::memory_order_relaxed);
     return prev;
 }
 

@@ -68,6 +68,19 @@ cudaError_t launch_phase_grid(int variant, bool inter, bool turns, bool vec, con
 cudaError_t launch_phase_flat(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
                               size_t nt, float *so, float *co, float *io, size_t head, size_t nvec,
                               unsigned grid, cudaStream_t stream);
+// NEXT(1) row path for nt % 8 != 0 or unaligned t (nt >= kPhaseRowsMinNt): h0 = the first
+// pair at which the outputs are 32-B aligned (0..7); t any 4-B alignment.
+#ifndef SINCOS_PHASE_ROWS_MIN_NT
+#define SINCOS_PHASE_ROWS_MIN_NT 128
+#endif
+constexpr size_t kPhaseRowsMinNt = SINCOS_PHASE_ROWS_MIN_NT;   // shorter rows: the flat path (measured faster below ~128)
+#ifndef SINCOS_PHASE_ROWS_PER_BLOCK
+#define SINCOS_PHASE_ROWS_PER_BLOCK 8
+#endif
+constexpr size_t kPhaseRowsPerBlock = SINCOS_PHASE_ROWS_PER_BLOCK;   // target rows per row slot
+cudaError_t launch_phase_rows(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
+                              size_t nt, float *so, float *co, float *io, unsigned h0, int sms,
+                              cudaStream_t stream);
 // NEXT(2) fused non-uniform Fourier sum (sincos_nudft.cu); variant 3/4 = comparison sincosf.
 size_t nudft_chunk(size_t nt);
 size_t nudft_ws_bytes(size_t nf, size_t nt);

@@ -16,6 +16,7 @@
 
 #include "sincos_launch.h"
 #include "sincos_math.cuh"
+#include "sincos_realign.cuh"
 
 namespace sincos_b200 {
 
@@ -209,6 +210,155 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_flat(const float *__
             st8_stream(co + e0, cv);
         }
     }
+}
+
+// Row path (nt % 8 != 0 or t not 32-B aligned; nt >= kPhaseRowsMinNt): the vector kernel's
+// structure -- a thread keeps eight t-values in registers and writes them for several rows --
+// with the rows' changing alignment taken care of by the row stride.  Output row i's first
+// 32-B aligned pair is j = a_i = (h0 - i nt) mod 8 (h0: the first aligned pair of the output
+// array), which depends on i mod 8 only; a row slot (lx threads) takes rows q, q + S, ... with
+// the slot count S a multiple of 8, so every row of a slot starts its vectors at the same
+// column `head` and reads the same t windows t[head + 8v .. head + 8v + 7].  Those are loaded
+// once per slot from aligned 256-bit vectors re-aligned by warp shuffles (load8_realigned_k,
+// compile-time offset K = the window's float offset past a 32-B boundary, warp-uniform: one
+// switch over the load only, so that the slots of different row classes share one copy of the
+// row loop in the instruction cache).  Pairs before head and after the last vector (<= 14
+// each) go one per lane in the slot's first warp of block column 0.  f comes 32 rows at a
+// time, one per lane, broadcast by shuffles.
+template <int K>
+__device__ __forceinline__ void rows_window(const float *__restrict__ t, size_t head, size_t v, size_t nvec,
+                                            unsigned lane, bool act, float (&tv)[8]) {
+    if constexpr (K == 0) {
+        if (act) ld8_keep(tv, t + head + 8 * v);
+    } else {
+        load8_realigned_k<K, true>(t + head - K, v, nvec, lane, act, tv);
+    }
+}
+
+template <int V, bool INTER, bool TURNS>
+__global__ void __launch_bounds__(kPhaseThreads) phase_grid_rows(const float *__restrict__ f,
+                                                                const float *__restrict__ t, size_t nf,
+                                                                size_t nt, float *so, float *co, float *io,
+                                                                unsigned h0, unsigned lx) {
+    // the block's 128 threads: 128 / lx row slots of lx threads (lx = 32, 64, 128: short rows
+    // keep every warp busy); slot q = blockIdx.y * (128 / lx) + ty takes rows q, q + S, q + 2S
+    // ... with S = gridDim.y * (128 / lx) a multiple of 8: one row class per slot
+    const unsigned ty = threadIdx.x / lx, tx = threadIdx.x % lx;
+    const size_t by = kPhaseThreads / lx;
+    const size_t q = static_cast<size_t>(blockIdx.y) * by + ty;
+    const size_t gy = static_cast<size_t>(gridDim.y) * by;
+    // the slot's row class: a = first aligned column of its rows, then the realign plan of t
+    // from column a (as realign_plan): head >= K keeps the aligned loads inside t
+    const unsigned ri = static_cast<unsigned>((q & 7u) * (nt & 7u)) & 7u;            // i nt mod 8
+    const size_t a = (h0 + 8u - ri) & 7u;
+    const int K = static_cast<int>(((reinterpret_cast<uintptr_t>(t) + 4 * a) & 31) / 4);
+    const size_t head = a < static_cast<size_t>(K) ? a + 8 : a;
+    const size_t nvec = K > 0 ? (nt + K - head - 8) / 8 : (nt - head) / 8;   // nt >= kPhaseRowsMinNt >= 64: no underflow
+    const unsigned lane = threadIdx.x & 31u;
+    const size_t v = static_cast<size_t>(blockIdx.x) * lx + tx;
+    const bool edge = blockIdx.x == 0 && tx < 32;                          // the row ends' warp
+    if (v - lane >= nvec && !edge) return;                                 // whole warp idle
+    const bool act = v < nvec;
+    // rows i = q + r gy, 32 at a time: lane l loads f of the chunk's row l (issued first, with
+    // the row-end t and the t windows, so the three latencies overlap), the row loop takes it
+    // by a shuffle one row ahead
+    size_t i0 = q;
+    float fl = i0 + lane * gy < nf ? __ldg(f + i0 + lane * gy) : 0.0f;
+    // row-end pair of this lane: lanes 0..15 the head columns, 16..31 the tail columns
+    const size_t je = lane < 16 ? lane : head + 8 * nvec + (lane - 16);
+    const bool has_e = edge && (lane < 16 ? je < head : je < nt);
+    const float te = has_e ? __ldg(t + je) : 0.0f;
+    float tv[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+    switch (K) {
+    case 0: rows_window<0>(t, head, v, nvec, lane, act, tv); break;
+    case 1: rows_window<1>(t, head, v, nvec, lane, act, tv); break;
+    case 2: rows_window<2>(t, head, v, nvec, lane, act, tv); break;
+    case 3: rows_window<3>(t, head, v, nvec, lane, act, tv); break;
+    case 4: rows_window<4>(t, head, v, nvec, lane, act, tv); break;
+    case 5: rows_window<5>(t, head, v, nvec, lane, act, tv); break;
+    case 6: rows_window<6>(t, head, v, nvec, lane, act, tv); break;
+    default: rows_window<7>(t, head, v, nvec, lane, act, tv); break;
+    }
+    for (; i0 < nf; i0 += 32 * gy) {
+        if (i0 != q) {
+            const size_t il = i0 + lane * gy;
+            fl = il < nf ? __ldg(f + il) : 0.0f;
+        }
+        const size_t rows = (nf - i0 + gy - 1) / gy;                       // rows of this block left
+        const int nr = rows < 32 ? static_cast<int>(rows) : 32;
+        float fi = __shfl_sync(0xFFFFFFFFu, fl, 0);
+        for (int r = 0; r < nr; ++r) {
+            const float fn = __shfl_sync(0xFFFFFFFFu, fl, (r + 1) & 31);
+            const size_t r0 = (i0 + r * gy) * nt;
+            if (has_e) {
+                float s, c;
+                phase_pair<V, TURNS>(fi, te, s, c);
+                if constexpr (INTER) {
+                    io[2 * (r0 + je)] = c;
+                    io[2 * (r0 + je) + 1] = s;
+                } else {
+                    so[r0 + je] = s;
+                    co[r0 + je] = c;
+                }
+            }
+            if (act) {
+                const size_t e0 = r0 + head + 8 * v;
+                if constexpr (INTER) {
+                    float cs[16];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fi, tv[k], cs[2 * k + 1], cs[2 * k]);
+                    st8_stream(io + 2 * e0, cs);
+                    st8_stream(io + 2 * e0 + 8, cs + 8);
+                } else {
+                    float sv[8], cv[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fi, tv[k], sv[k], cv[k]);
+                    st8_stream(so + e0, sv);
+                    st8_stream(co + e0, cv);
+                }
+            }
+            fi = fn;
+        }
+    }
+}
+
+template <int V, bool INTER, bool TURNS>
+static const void *pick_rows() {
+    return reinterpret_cast<const void *>(phase_grid_rows<V, INTER, TURNS>);
+}
+
+cudaError_t launch_phase_rows(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
+                              size_t nt, float *so, float *co, float *io, unsigned h0, int sms,
+                              cudaStream_t stream) {
+    static_assert(kPhaseRowsMinNt >= 64, "row path: every row class needs whole vectors");
+    if (nt < kPhaseRowsMinNt || h0 > 7) return cudaErrorInvalidValue;
+    const void *fn;
+    if (variant == kNormalized)
+        fn = inter ? (turns ? pick_rows<kNormalized, true, true>() : pick_rows<kNormalized, true, false>())
+                   : (turns ? pick_rows<kNormalized, false, true>() : pick_rows<kNormalized, false, false>());
+    else
+        fn = inter ? (turns ? pick_rows<kRenormalized, true, true>() : pick_rows<kRenormalized, true, false>())
+                   : (turns ? pick_rows<kRenormalized, false, true>() : pick_rows<kRenormalized, false, false>());
+    // lx threads per row slot (a warp for rows of <= 32 vectors), 128 / lx slots per block;
+    // S = row slots in all: a multiple of 8 (one row class per slot), kPhaseRowsPerBlock rows
+    // per slot (the set-up -- t windows, row ends -- amortised over a few rows; 1-2 rows per
+    // slot and 16-32 measured slower: tools/ab_phase.py), but >= 8 blocks per SM in all
+    const size_t nv8 = nt / 8;                                            // >= nvec of every class
+    const unsigned lx = nv8 <= 32 ? 32u : nv8 <= 64 ? 64u : 128u;
+    const size_t by = kPhaseThreads / lx;
+    const size_t gx = (nv8 + lx - 1) / lx;
+    const size_t fill = (static_cast<size_t>(sms > 0 ? sms : 148) * 8 + gx - 1) / gx * by;
+    size_t slots = (nf + kPhaseRowsPerBlock - 1) / kPhaseRowsPerBlock;
+    if (slots < fill) slots = fill;
+    slots = (slots + 7) / 8 * 8;
+    const size_t rows8 = (nf + 7) / 8 * 8;
+    if (slots > rows8) slots = rows8;
+    if (slots > 65528 * by) slots = 65528 * by;
+    const size_t gy = (slots + by - 1) / by;                               // slots is a multiple of by (<= 4)
+    if (gx == 0 || gx > 0x7FFFFFFFu) return cudaErrorInvalidValue;
+    void *args[] = {&f, &t, &nf, &nt, &so, &co, &io, &h0, const_cast<unsigned *>(&lx)};
+    return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)), dim3(kPhaseThreads),
+                            args, 0, stream);
 }
 
 template <int V, bool INTER, bool TURNS>

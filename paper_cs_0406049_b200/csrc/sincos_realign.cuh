@@ -23,17 +23,29 @@ __device__ __forceinline__ void ld8_stream(float (&r)[8], const float *p) {
                  : "l"(p));
 }
 
+// the same load kept in the caches (operands re-read by many blocks, e.g. the phase grid's t)
+__device__ __forceinline__ void ld8_keep(float (&r)[8], const float *p) {
+    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+                 : "l"(p));
+}
+
 // K (1..7) is a compile-time parameter: only the K values taken from the next lane are shuffled
 // and the selection is register renaming (a run-time K with a switch over register moves was
-// measured 15-20% slower).
-template <int K>
+// measured 15-20% slower).  KEEP: cache-resident loads (ld8_keep) instead of streaming ones.
+template <int K, bool KEEP = false>
 __device__ __forceinline__ void load8_realigned_k(const float *tal, size_t v, size_t nvec, unsigned lane, bool act,
                                                   float (&x)[8]) {
     const bool own = act && (lane == 31u || v + 1 >= nvec);
     float a[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
     float bo[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
-    if (act) ld8_stream(a, tal + 8 * v);
-    if (own) ld8_stream(bo, tal + 8 * v + 8);
+    if constexpr (KEEP) {
+        if (act) ld8_keep(a, tal + 8 * v);
+        if (own) ld8_keep(bo, tal + 8 * v + 8);
+    } else {
+        if (act) ld8_stream(a, tal + 8 * v);
+        if (own) ld8_stream(bo, tal + 8 * v + 8);
+    }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         if (j + K < 8) {

@@ -110,16 +110,19 @@ def test_radians_equals_the_materialised_path(variant):
 
 
 @pytest.mark.parametrize("units,variant", COMBOS)
-@pytest.mark.parametrize("flat", [True, False])
-def test_ragged_rows_flat_path(units, variant, flat):
+@pytest.mark.parametrize("mode", [1, 3, 0])
+def test_ragged_rows_flat_path(units, variant, mode):
     """Rows that are not whole 256-bit vectors (nt % 8 != 0, t or outputs off 32 B) go through
-    the flat kernel (8 consecutive pairs of the row-major grid per thread, rows wrapping inside
-    a vector, nt = 1..9 included) or, with it disabled / for outputs it cannot serve, one pair
-    per thread; bit-exact either way, at several output offsets, split and interleaved."""
+    the row kernel (nt >= 128: t windows re-aligned per row class), the flat kernel (8
+    consecutive pairs of the row-major grid per thread, rows wrapping inside a vector, nt = 1..9
+    included; for every nt with set_realign(3)) or, with both disabled / for outputs they
+    cannot serve, one pair per thread; bit-exact either way, at several output offsets, split
+    and interleaved."""
     rng = np.random.default_rng(31 + units + 2 * variant)
-    prev = sp.set_realign(flat)
+    prev = sp.set_realign(mode)
     try:
-        for nf, nt in ((1, 1), (3, 1), (7, 2), (5, 3), (9, 7), (4, 9), (33, 1001), (257, 255), (64, 256)):
+        for nf, nt in ((1, 1), (3, 1), (7, 2), (5, 3), (9, 7), (4, 9), (33, 1001), (257, 255), (64, 256), (5, 127),
+                       (6, 129), (2, 5000)):
             f = rng.uniform(0, 400, nf).astype(np.float32)
             t = rng.uniform(-1, 1, nt + 1).astype(np.float32)
             n = nf * nt
@@ -139,12 +142,77 @@ def test_ragged_rows_flat_path(units, variant, flat):
                     io = big_i[oo:oo + 2 * n]
                     sp.phase_grid(fd, td, interleaved_out=io, units=units, variant=variant)
                     torch.cuda.synchronize()
-                    tag = f"({nf},{nt}) toff={toff} out={oo},{oc} flat={flat}"
+                    tag = f"({nf},{nt}) toff={toff} out={oo},{oc} mode={mode}"
                     assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws, wc, "split " + tag)
                     iv = io.cpu().numpy()
                     assert_parity(iv[1::2], iv[0::2], ws, wc, "inter " + tag)
     finally:
         sp.set_realign(prev)
+
+
+@pytest.mark.parametrize("units,variant", COMBOS)
+@pytest.mark.parametrize("nt", [128, 129, 130, 131, 132, 133, 134, 135, 300, 1001])
+def test_row_path_every_alignment(units, variant, nt):
+    """The row kernel at every t offset (its re-alignment K = 0..7) x every output offset
+    (the rows' first aligned column, per row class) x nt mod 8, with nf = 19 rows (every row
+    class, more rows than classes), split and interleaved: bit-exact vs the oracle."""
+    rng = np.random.default_rng(nt * 7 + units + 2 * variant)
+    nf = 19
+    n = nf * nt
+    f = rng.uniform(0, 400, nf).astype(np.float32)
+    t = rng.uniform(-1, 1, nt + 8).astype(np.float32)
+    fd, tbig = torch.from_numpy(f).cuda(), torch.from_numpy(t).cuda()
+    big_s = torch.empty(n + 16, device="cuda")
+    big_c = torch.empty(n + 16, device="cuda")
+    big_i = torch.empty(2 * n + 16, device="cuda")
+    for toff in range(8):
+        ws, wc = oracle.phase_grid(f, t[toff:toff + nt], units, variant)
+        ws, wc = ws.ravel(), wc.ravel()
+        td = tbig[toff:toff + nt]
+        for oo in range(8):
+            s, c = big_s[oo:oo + n], big_c[oo:oo + n]
+            sp.phase_grid(fd, td, s, c, units=units, variant=variant)
+            io = big_i[2 * (oo % 4):2 * (oo % 4) + 2 * n]
+            sp.phase_grid(fd, td, interleaved_out=io, units=units, variant=variant)
+            tag = f"({nf},{nt}) toff={toff} out={oo}"
+            assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws, wc, "split " + tag)
+            iv = io.cpu().numpy()
+            assert_parity(iv[1::2], iv[0::2], ws, wc, "inter " + tag)
+
+
+@pytest.mark.parametrize("inter", [False, True])
+@pytest.mark.parametrize("shape", [(70001, 131), (2_240_032, 521)])
+def test_row_path_many_rows(inter, shape):
+    """Many rows: (70001, 131) -- 4 row slots per block, past the 65528-block grid height's
+    rows; (2 240 032, 521) -- slot count capped, > 32 rows per slot (f re-loaded per 32-row
+    chunk), 1.17e9 pairs.  Row i depends on f_i and t only, so sampled rows (the first and
+    last, rows around the slot-count multiples, random rows) are compared with the oracle's
+    grid of those f values: bit-exact."""
+    nf, nt = shape
+    rng = np.random.default_rng(77 + nt)
+    f = rng.uniform(0, 400, nf).astype(np.float32)
+    tb = rng.uniform(-1, 1, nt + 1).astype(np.float32)
+    t = tb[1:]                                            # t off 32 B: re-aligned windows
+    fd = torch.from_numpy(f).cuda()
+    td = torch.from_numpy(tb).cuda()[1:]
+    n = nf * nt
+    rows = np.unique(np.concatenate([[0, 1, 2, nf - 2, nf - 1], rng.integers(0, nf, 3000),
+                                     *[np.arange(k - 9, k + 9) for k in (65528, 262112, 524224, 2 * 262112)
+                                       if k + 9 < nf]]))
+    ws, wc = oracle.phase_grid(f[rows], t, R, 1)
+    ri = torch.from_numpy(rows).cuda()
+    if inter:
+        o = torch.empty(2 * n, device="cuda")
+        sp.phase_grid(fd, td, interleaved_out=o, units=R, variant=1)
+        o = o.view(nf, nt, 2)[ri].cpu().numpy()
+        gs, gc = o[..., 1], o[..., 0]
+        del o
+    else:
+        s, c = torch.empty(n, device="cuda"), torch.empty(n, device="cuda")
+        sp.phase_grid(fd, td, s, c, units=R, variant=1)
+        gs, gc = s.view(nf, nt)[ri].cpu().numpy(), c.view(nf, nt)[ri].cpu().numpy()
+        del s, c
+    assert_parity(gs.ravel(), gc.ravel(), ws.ravel(), wc.ravel(), f"({nf},{nt}) inter={inter}")
 
 
 @pytest.mark.parametrize("variant", [0, 1])

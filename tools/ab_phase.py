@@ -1,0 +1,77 @@
+"""A/B of build-time switches of libsincos_pairs.so on sincos_phase_grid (tuning aid).
+
+  python tools/ab_phase.py build NAME -DMACRO=V ...   # here (CPU): builds tools/ab_phase/NAME.so
+  python tools/ab_phase.py run                        # GPU box: times every tools/ab_phase/*.so
+
+Cases: ragged row lengths (and t offsets) at ~2^30 pairs per launch, split and interleaved,
+turns, variant N; GB/s of the 8 B written per pair, median of 5 rounds x 5 launches, the
+libraries interleaved over rounds.  One JSON line per library."""
+import ctypes
+import glob
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+AB = os.path.join(ROOT, "tools", "ab_phase")
+CASES = [(32767, 0), (32772, 0), (1001, 0), (1001, 3), (4000, 5), (255, 0), (300, 0), (500, 1), (131, 0),
+         (65, 0), (100, 1), (200, 2)]
+
+
+def build(name, flags):
+    from paper_cs_0406049_b200 import _build
+    os.makedirs(AB, exist_ok=True)
+    out = os.path.join(AB, name + ".so")
+    _build.build(extra_flags=flags, out=out)
+    print(out)
+
+
+def run():
+    import torch
+    libs = {}
+    for p in sorted(glob.glob(os.path.join(AB, "*.so"))):
+        L = ctypes.CDLL(p)
+        L.sincos_phase_grid.restype = ctypes.c_int
+        L.sincos_phase_grid.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                        ctypes.c_int, ctypes.c_void_p]
+        libs[os.path.basename(p)[:-3]] = L
+    st = torch.cuda.current_stream().cuda_stream
+    s = torch.empty(1 << 30, device="cuda")
+    c = torch.empty(1 << 30, device="cuda")
+    io = torch.empty(1 << 31, device="cuda")
+    res = {k: {} for k in libs}
+    for nt, toff in CASES:
+        nf = (1 << 30) // nt
+        f = torch.rand(nf, device="cuda") * 512
+        t = torch.rand(nt + 8, device="cuda")[toff:toff + nt]
+        for inter in (False, True):
+            key = f"nt={nt} toff={toff} {'inter' if inter else 'split'}"
+            outs = (0, 0, io.data_ptr()) if inter else (s.data_ptr(), c.data_ptr(), 0)
+            samples = {k: [] for k in libs}
+            for _ in range(5):
+                for name, L in libs.items():
+                    def go():
+                        r = L.sincos_phase_grid(f.data_ptr(), nf, t.data_ptr(), nt, *outs, 1, 0, st)
+                        assert r == 0, r
+                    go()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    for _ in range(5):
+                        go()
+                    b.record()
+                    torch.cuda.synchronize()
+                    samples[name].append(a.elapsed_time(b) / 5)
+            for name in libs:
+                res[name][key] = round(8 * nf * nt / (statistics.median(samples[name]) / 1e3) / 1e9, 1)
+    for name in libs:
+        print(json.dumps({"lib": name, "GBps": res[name]}))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build(sys.argv[2], sys.argv[3:])
+    else:
+        run()

@@ -1,5 +1,7 @@
 """GB/s (8 B written per pair) of sincos_phase_grid for row lengths nt with and without the
-256-bit path (nt % 8 == 0 and 32-B aligned t/outputs), split and interleaved (GPU box).
+256-bit row path (nt % 8 == 0 and 32-B aligned t/outputs), split and interleaved (GPU box);
+ragged rows through the row kernel (set_realign(1)) and the flat kernel (set_realign(3)).
+~2^30 pairs per launch.
   python tools/phase_ragged_probe.py"""
 import json
 import os
@@ -13,14 +15,21 @@ import torch  # noqa: E402
 import paper_cs_0406049_b200 as sp  # noqa: E402
 
 
+MIN_NT = int(os.environ.get("ROWS_MIN_NT", "256"))   # the library's kPhaseRowsMinNt (A/B builds)
+
+
 def main():
     res = {}
-    nf = 1 << 15
-    for nt in (1 << 15, (1 << 15) - 1, (1 << 15) + 4, 1000, 1001):
+    for nt, toff in ((1 << 15, 0), ((1 << 15) - 1, 0), ((1 << 15) + 4, 0), (1000, 0), (1001, 0), (1001, 3),
+                     (65, 0), (100, 1), (131, 0), (200, 2), (255, 0), (300, 0), (500, 1), (4000, 5)):
+        nf = (1 << 30) // nt
         f = torch.rand(nf, device="cuda") * 512
-        t = torch.rand(nt, device="cuda")
+        t = torch.rand(nt + 8, device="cuda")[toff:toff + nt]
         n = nf * nt
-        for inter in (False, True):
+        for inter, mode in ((False, 1), (True, 1), (False, 3), (True, 3)):
+            if mode == 3 and nt % 8 == 0 and toff == 0:
+                continue
+            sp.set_realign(mode)
             if inter:
                 outs = {"interleaved_out": torch.empty(2 * n, device="cuda")}
             else:
@@ -34,8 +43,10 @@ def main():
             b.record()
             torch.cuda.synchronize()
             ms = a.elapsed_time(b) / 5
-            res[f"nt={nt} {'inter' if inter else 'split'}"] = round(8 * n / (ms / 1e3) / 1e9, 1)
+            kern = "vec" if nt % 8 == 0 and toff == 0 else ("rows" if mode == 1 and nt >= MIN_NT else "flat")
+            res[f"nt={nt} toff={toff} {'inter' if inter else 'split'} {kern}"] = round(8 * n / (ms / 1e3) / 1e9, 1)
             del outs
+    sp.set_realign(1)
     print(json.dumps(res))
 
 

@@ -16,6 +16,7 @@
 
 #include "sincos_launch.h"
 #include "sincos_math.cuh"
+#include "sincos_math2.cuh"
 #include "sincos_realign.cuh"
 
 namespace sincos_b200 {
@@ -29,6 +30,35 @@ __device__ __forceinline__ void phase_pair(float f, float t, float &s, float &c)
         sincos_pair_turns<V>(p, s, c);
     else
         sincos_pair<V>(p, s, c);
+}
+
+// Eight pairs of one row: p_k = RN(f t_k).  SINCOS_PACKED_PHASE (default): two at a time in
+// packed fp32 (FMUL2/FFMA2, sincos_math2.cuh; each lane rounds as the scalar instruction) --
+// identical values, half the FP32 instructions issued.  The write-only grid runs into the
+// board's power cap within ~0.1 s; packed: 1.18-1.21 J per 2^30-pair launch vs 1.33-1.43 J
+// and 6.57 vs 6.35-6.39 TB/s sustained, the same 7.55-7.58 TB/s burst (tools/ab_phase.py
+// sustain, profiles/ab_phase_rows_r01.jsonl).
+#ifndef SINCOS_PACKED_PHASE
+#define SINCOS_PACKED_PHASE 1
+#endif
+template <int V, bool TURNS>
+__device__ __forceinline__ void phase8(float fi, const float (&tv)[8], float (&sv)[8], float (&cv)[8]) {
+    if constexpr (SINCOS_PACKED_PHASE) {
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+            F2 x = mul2(bc2(fi), pk2(tv[k], tv[k + 1]));
+            if constexpr (!TURNS) x = mul2(x, bc2(kInvTwoPi));
+            F2 s2, c2;
+            sincos_from_q2<V>(reduce_turn2(x), s2, c2);
+            sv[k] = lo2(s2);
+            sv[k + 1] = hi2(s2);
+            cv[k] = lo2(c2);
+            cv[k + 1] = hi2(c2);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fi, tv[k], sv[k], cv[k]);
+    }
 }
 
 __device__ __forceinline__ void st8_stream(float *p, const float *r) {
@@ -55,16 +85,18 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_vec(const float *__r
     for (size_t i = blockIdx.y; i < nf; i += gridDim.y) {
         const float fi = __ldg(f + i);
         const size_t e0 = i * nt + 8 * v;
+        float sv[8], cv[8];
+        phase8<V, TURNS>(fi, tt, sv, cv);
         if constexpr (INTER) {
             float cs[16];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fi, tt[k], cs[2 * k + 1], cs[2 * k]);
+            for (int k = 0; k < 8; ++k) {
+                cs[2 * k] = cv[k];
+                cs[2 * k + 1] = sv[k];
+            }
             st8_stream(io + 2 * e0, cs);
             st8_stream(io + 2 * e0 + 8, cs + 8);
         } else {
-            float sv[8], cv[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fi, tt[k], sv[k], cv[k]);
             st8_stream(so + e0, sv);
             st8_stream(co + e0, cv);
         }
@@ -303,16 +335,18 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_rows(const float *__
             }
             if (act) {
                 const size_t e0 = r0 + head + 8 * v;
+                float sv[8], cv[8];
+                phase8<V, TURNS>(fi, tv, sv, cv);
                 if constexpr (INTER) {
                     float cs[16];
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fi, tv[k], cs[2 * k + 1], cs[2 * k]);
+                    for (int k = 0; k < 8; ++k) {
+                        cs[2 * k] = cv[k];
+                        cs[2 * k + 1] = sv[k];
+                    }
                     st8_stream(io + 2 * e0, cs);
                     st8_stream(io + 2 * e0 + 8, cs + 8);
                 } else {
-                    float sv[8], cv[8];
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fi, tv[k], sv[k], cv[k]);
                     st8_stream(so + e0, sv);
                     st8_stream(co + e0, cv);
                 }

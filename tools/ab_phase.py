@@ -2,6 +2,7 @@
 
   python tools/ab_phase.py build NAME -DMACRO=V ...   # here (CPU): builds tools/ab_phase/NAME.so
   python tools/ab_phase.py run                        # GPU box: times every tools/ab_phase/*.so
+  python tools/ab_phase.py sustain                    # GPU box: 0.5-1 s of load per library from idle
 
 Cases: ragged row lengths (and t offsets) at ~2^30 pairs per launch, split and interleaved,
 turns, variant N; GB/s of the 8 B written per pair, median of 5 rounds x 5 launches, the
@@ -72,8 +73,61 @@ def run():
         print(json.dumps({"lib": name, "GBps": res[name]}))
 
 
+def sustain():
+    """Per library, twice (alternating), after 3 s idle: 100 groups of 5 launches of the aligned
+    C4 shape (2^15 x 2^15, split, turns, variant N): GB/s of the first 5 groups and of the last
+    20, the SM clock at the end, and board energy per launch (NVML total-energy counter)."""
+    import time
+
+    import pynvml
+    import torch
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    libs = {}
+    for p in sorted(glob.glob(os.path.join(AB, "*.so"))):
+        L = ctypes.CDLL(p)
+        L.sincos_phase_grid.restype = ctypes.c_int
+        L.sincos_phase_grid.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                        ctypes.c_int, ctypes.c_void_p]
+        libs[os.path.basename(p)[:-3]] = L
+    st = torch.cuda.current_stream().cuda_stream
+    nf = nt = 1 << 15
+    f = torch.rand(nf, device="cuda") * 512
+    t = torch.rand(nt, device="cuda")
+    s = torch.empty(nf * nt, device="cuda")
+    c = torch.empty(nf * nt, device="cuda")
+    nbytes = 8 * nf * nt
+    out = {k: [] for k in libs}
+    for rep in range(2):
+        for name, L in libs.items():
+            L.sincos_phase_grid(f.data_ptr(), nf, t.data_ptr(), nt, s.data_ptr(), c.data_ptr(), 0, 1, 0, st)
+            torch.cuda.synchronize()
+            time.sleep(3)
+            e0 = pynvml.nvmlDeviceGetTotalEnergyConsumption(h)
+            gbs = []
+            for _ in range(100):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(5):
+                    L.sincos_phase_grid(f.data_ptr(), nf, t.data_ptr(), nt, s.data_ptr(), c.data_ptr(), 0, 1, 0, st)
+                b.record()
+                torch.cuda.synchronize()
+                gbs.append(nbytes / (a.elapsed_time(b) / 5 / 1e3) / 1e9)
+            mj = pynvml.nvmlDeviceGetTotalEnergyConsumption(h) - e0
+            out[name].append({"first5_gbs": round(statistics.mean(gbs[:5]), 1),
+                              "last20_gbs": round(statistics.mean(gbs[-20:]), 1),
+                              "sm_mhz_end": pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                              "reasons_end": hex(pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)),
+                              "mJ_per_launch": round(mj / 500, 2)})
+    for name in libs:
+        print(json.dumps({"lib": name, "sustain": out[name]}))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "build":
         build(sys.argv[2], sys.argv[3:])
+    elif sys.argv[1] == "sustain":
+        sustain()
     else:
         run()

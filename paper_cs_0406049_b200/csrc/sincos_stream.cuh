@@ -97,7 +97,7 @@ __device__ __forceinline__ void storeW(float *p, const float *r) {
 // Compute and store one vector of W elements whose first element is `e0`.
 template <int V, bool INTER, int W>
 __device__ __forceinline__ void emit(const float (&x)[W], size_t e0, float *so, float *co, float *io) {
-    if constexpr (SINCOS_PACKED_HOT && V != kNull) {
+    if constexpr (SINCOS_PACKED_HOT && (V == kNormalized || V == kRenormalized)) {
         float s[W], c[W];
 #pragma unroll
         for (int k = 0; k < W; k += 2) {

@@ -2,6 +2,7 @@
 
   python tools/ab_macro.py build NAME -DMACRO=V ...   # here (CPU): builds tools/ab/NAME.so
   python tools/ab_macro.py run                        # GPU box: times every tools/ab/*.so
+  python tools/ab_macro.py energy                     # GPU box: 2 s of C2 launches per library, J/launch
 
 Times variants N and A, split and interleaved, on the C2 batch (2^28 angles, 12 B/pair),
 the libraries interleaved over rounds (median of 5 rounds x 10 launches).  One JSON line
@@ -85,8 +86,67 @@ def run():
               flush=True)
 
 
+def energy():
+    """Per library and variant (N, A; split), twice alternating, after 3 s idle: 2 s of C2
+    launches back to back -- board energy per launch (NVML total-energy counter), mean launch
+    time over the last half, SM clock and throttle reasons at the end."""
+    import time
+
+    import pynvml
+    import torch
+
+    import inputs
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    n = 1 << 28
+    th = torch.from_numpy(inputs.generate(2, 0, n)).cuda()
+    s = torch.empty(n, device="cuda")
+    c = torch.empty(n, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    libs = {}
+    for p in sorted(glob.glob(os.path.join(AB, "*.so"))):
+        L = ctypes.CDLL(p)
+        L.sincos_pairs.restype = ctypes.c_int
+        L.sincos_pairs.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]
+        libs[os.path.basename(p)[:-3]] = L
+    out = {k: [] for k in libs}
+    for _ in range(2):
+        for v in (0, 1):
+            for name, L in libs.items():
+                go = lambda: L.sincos_pairs(th.data_ptr(), s.data_ptr(), c.data_ptr(), None, n, v, st)  # noqa: E731
+                go()
+                torch.cuda.synchronize()
+                time.sleep(3)
+                e0 = pynvml.nvmlDeviceGetTotalEnergyConsumption(h)
+                t0 = time.time()
+                k = 0
+                evs = []
+                while time.time() - t0 < 2.0:
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    for _ in range(20):
+                        go()
+                    b.record()
+                    evs.append((a, b))
+                    k += 20
+                    if len(evs) > 8:
+                        evs[-9][1].synchronize()
+                torch.cuda.synchronize()
+                mj = pynvml.nvmlDeviceGetTotalEnergyConsumption(h) - e0
+                half = evs[len(evs) // 2:]
+                ms = statistics.mean(a.elapsed_time(b) / 20 for a, b in half)
+                out[name].append({"variant": v, "launches": k, "mJ_per_launch": round(mj / k, 2),
+                                  "ms_last_half": round(ms, 4),
+                                  "sm_mhz_end": pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                  "reasons_end": hex(pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h))})
+    for name in libs:
+        print(json.dumps({"lib": name, "energy": out[name]}), flush=True)
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "build":
         build(sys.argv[2], sys.argv[3:])
+    elif sys.argv[1] == "energy":
+        energy()
     else:
         run()

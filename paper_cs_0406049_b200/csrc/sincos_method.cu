@@ -69,16 +69,18 @@ __global__ void __launch_bounds__(128) method_kernel(const MethodParams m, const
             ld8_stream(x, theta + head + 8 * v);
         }
         const size_t e0 = head + 8 * v;
+        float sv[8], cv[8];
+        method_pair8<NT, FIX>(m, x, sv, cv);
         if constexpr (INTER) {
             float cs[16];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) method_pair<NT, FIX>(m, x[k], cs[2 * k + 1], cs[2 * k]);
+            for (int k = 0; k < 8; ++k) {
+                cs[2 * k] = cv[k];
+                cs[2 * k + 1] = sv[k];
+            }
             st8m(io + 2 * e0, cs);
             st8m(io + 2 * e0 + 8, cs + 8);
         } else {
-            float sv[8], cv[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) method_pair<NT, FIX>(m, x[k], sv[k], cv[k]);
             st8m(so + e0, sv);
             st8m(co + e0, cv);
         }

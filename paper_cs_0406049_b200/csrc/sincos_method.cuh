@@ -84,6 +84,49 @@ __device__ __forceinline__ void method_pair(const MethodParams &m, float theta, 
     method_from_q<NT, FIX>(m, reduce_turn(__fmul_rn(theta, kInvTwoPi)), s_out, c_out);
 }
 
+// Eight pairs at once, stage by stage: the run-time doubling loop runs once over all eight
+// (per element it would serialise the eight independent chains behind eight loops).  The
+// same operations on each element as method_pair: bit-identical.
+template <int NT, int FIX>
+__device__ __forceinline__ void method_pair8(const MethodParams &m, const float (&theta)[8], float (&s_out)[8],
+                                             float (&c_out)[8]) {
+    // s_out / c_out hold the running pair from the series on (no separate arrays live)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const float q1 = reduce_turn(__fmul_rn(theta[k], kInvTwoPi));
+        const float q2 = __fmul_rn(q1, q1);
+        float ps = m.ss[NT - 1];
+#pragma unroll
+        for (int i = NT - 2; i >= 0; --i) ps = __fmaf_rn(q2, ps, m.ss[i]);
+        float pc = m.cc[NT - 1];
+#pragma unroll
+        for (int i = NT - 2; i >= 0; --i) pc = __fmaf_rn(q2, pc, m.cc[i]);
+        s_out[k] = __fmul_rn(q1, ps);
+        c_out[k] = __fmaf_rn(q2, pc, 1.0f);
+    }
+    if (m.doublings > 0) {
+        for (int i = 0; i < m.doublings - 1; ++i) {          // warp-uniform bound
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float s = s_out[k], c = c_out[k];
+                c_out[k] = __fmaf_rn(-s, s, __fmul_rn(c, c));
+                s_out[k] = __fmul_rn(2.0f, __fmul_rn(s, c));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float s = s_out[k], c = c_out[k];          // the penultimate pair
+            const float cc2 = __fmul_rn(c, c);
+            float f = 1.0f;
+            if constexpr (FIX == 0) f = __fmaf_rn(-s, s, __fmaf_rn(-c, c, 2.0f));
+            if constexpr (FIX == 1) f = rcp_rn(__fmaf_rn(s, s, cc2));
+            c_out[k] = __fmul_rn(__fmaf_rn(-s, s, cc2), f);
+            s_out[k] = __fmul_rn(__fmul_rn(2.0f, __fmul_rn(s, c)), f);
+        }
+    }
+    // (no doublings: the series pair times f = 1, i.e. unchanged -- as method_from_q)
+}
+
 inline MethodParams make_params(const float *ss, int n_ss, const float *cc, int n_cc, int doublings) {
     MethodParams m;
     for (int i = 0; i < 8; ++i) {

@@ -3,6 +3,7 @@
   python tools/ab_macro.py build NAME -DMACRO=V ...   # here (CPU): builds tools/ab/NAME.so
   python tools/ab_macro.py run                        # GPU box: times every tools/ab/*.so
   python tools/ab_macro.py energy                     # GPU box: 2 s of C2 launches per library, J/launch
+  python tools/ab_macro.py method                     # GPU box: sincos_pairs_method (paper tables) per library
 
 Times variants N and A, split and interleaved, on the C2 batch (2^28 angles, 12 B/pair),
 the libraries interleaved over rounds (median of 5 rounds x 10 launches).  One JSON line
@@ -143,9 +144,57 @@ def energy():
         print(json.dumps({"lib": name, "energy": out[name]}), flush=True)
 
 
+def method():
+    """sincos_pairs_method with the paper's two tables (and a 3-doubling shape) on the C2 batch,
+    split and interleaved, theta aligned and 1 float off: GB/s (12 B/pair), median of 5 rounds
+    x 10 launches, libraries interleaved."""
+    import torch
+
+    import inputs
+    import paper_cs_0406049_b200 as sp
+    n = 1 << 28
+    base = torch.from_numpy(inputs.generate(2, 0, n + 8)).cuda()
+    s = torch.empty(n, device="cuda")
+    c = torch.empty(n, device="cuda")
+    io = torch.empty(2 * n, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    methods = {"paperN": sp.make_method(*sp.PAPER_METHODS[0]), "paperA": sp.make_method(*sp.PAPER_METHODS[1]),
+               "deg3_3dbl": sp.make_method([1.5707963, -0.6459636, 0.0796820], [-1.2336978, 0.2536086], 3,
+                                           sp.FIX_LINEAR)}
+    libs = {}
+    for p in sorted(glob.glob(os.path.join(AB, "*.so"))):
+        L = ctypes.CDLL(p)
+        L.sincos_pairs_method.restype = ctypes.c_int
+        L.sincos_pairs_method.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]
+        libs[os.path.basename(p)[:-3]] = L
+    res = {k: {} for k in libs}
+    for _ in range(5):
+        for name, L in libs.items():
+            for mname, m in methods.items():
+                for inter in (False, True):
+                    for off in (0, 1):
+                        th = base[off:off + n]
+                        outs = (None, None, io.data_ptr()) if inter else (s.data_ptr(), c.data_ptr(), None)
+                        go = lambda: L.sincos_pairs_method(th.data_ptr(), *outs, n, ctypes.byref(m), st)  # noqa: E731
+                        assert go() == 0
+                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        a.record()
+                        for _ in range(10):
+                            go()
+                        b.record()
+                        torch.cuda.synchronize()
+                        key = f"{mname} {'inter' if inter else 'split'} off={off}"
+                        res[name].setdefault(key, []).append(12 * n / (a.elapsed_time(b) / 10 / 1e3) / 1e9)
+    for name in libs:
+        print(json.dumps({"lib": name, "method_GBps": {k: round(statistics.median(v), 1) for k, v in res[name].items()}}),
+              flush=True)
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "build":
         build(sys.argv[2], sys.argv[3:])
+    elif sys.argv[1] == "method":
+        method()
     elif sys.argv[1] == "energy":
         energy()
     else:

@@ -84,37 +84,36 @@ __device__ __forceinline__ void method_pair(const MethodParams &m, float theta, 
     method_from_q<NT, FIX>(m, reduce_turn(__fmul_rn(theta, kInvTwoPi)), s_out, c_out);
 }
 
-// Eight pairs at once, stage by stage: the run-time doubling loop runs once over all eight
-// (per element it would serialise the eight independent chains behind eight loops).  The
-// same operations on each element as method_pair: bit-identical.
-template <int NT, int FIX>
-__device__ __forceinline__ void method_pair8(const MethodParams &m, const float (&theta)[8], float (&s_out)[8],
-                                             float (&c_out)[8]) {
+// N pairs at once from their reduced turns, stage by stage: the run-time doubling loop runs
+// once over all N (per pair it would serialise the N independent chains behind N loops).  The
+// same operations on each element as method_from_q: bit-identical.
+template <int NT, int FIX, int N>
+__device__ __forceinline__ void method_from_q_n(const MethodParams &m, const float (&q1)[N], float (&s_out)[N],
+                                                float (&c_out)[N]) {
     // s_out / c_out hold the running pair from the series on (no separate arrays live)
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const float q1 = reduce_turn(__fmul_rn(theta[k], kInvTwoPi));
-        const float q2 = __fmul_rn(q1, q1);
+    for (int k = 0; k < N; ++k) {
+        const float q2 = __fmul_rn(q1[k], q1[k]);
         float ps = m.ss[NT - 1];
 #pragma unroll
         for (int i = NT - 2; i >= 0; --i) ps = __fmaf_rn(q2, ps, m.ss[i]);
         float pc = m.cc[NT - 1];
 #pragma unroll
         for (int i = NT - 2; i >= 0; --i) pc = __fmaf_rn(q2, pc, m.cc[i]);
-        s_out[k] = __fmul_rn(q1, ps);
+        s_out[k] = __fmul_rn(q1[k], ps);
         c_out[k] = __fmaf_rn(q2, pc, 1.0f);
     }
     if (m.doublings > 0) {
         for (int i = 0; i < m.doublings - 1; ++i) {          // warp-uniform bound
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < N; ++k) {
                 const float s = s_out[k], c = c_out[k];
                 c_out[k] = __fmaf_rn(-s, s, __fmul_rn(c, c));
                 s_out[k] = __fmul_rn(2.0f, __fmul_rn(s, c));
             }
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < N; ++k) {
             const float s = s_out[k], c = c_out[k];          // the penultimate pair
             const float cc2 = __fmul_rn(c, c);
             float f = 1.0f;
@@ -125,6 +124,16 @@ __device__ __forceinline__ void method_pair8(const MethodParams &m, const float 
         }
     }
     // (no doublings: the series pair times f = 1, i.e. unchanged -- as method_from_q)
+}
+
+// Eight pairs of angles in radians (the streaming kernel's vector).
+template <int NT, int FIX>
+__device__ __forceinline__ void method_pair8(const MethodParams &m, const float (&theta)[8], float (&s_out)[8],
+                                             float (&c_out)[8]) {
+    float q[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) q[k] = reduce_turn(__fmul_rn(theta[k], kInvTwoPi));
+    method_from_q_n<NT, FIX, 8>(m, q, s_out, c_out);
 }
 
 inline MethodParams make_params(const float *ss, int n_ss, const float *cc, int n_cc, int doublings) {

@@ -158,6 +158,24 @@ __global__ void __launch_bounds__(kNuThreads, 9) nudft_partial(const float *__re
                     im[m] = lo2(i);
                     im[m + 1] = hi2(i);
                 }
+            } else if constexpr (V >= kMethodBase && V < kMethodExactBase) {
+                // general methods: all the thread's frequencies stage by stage (method_from_q_n)
+                constexpr int NT = (V - kMethodBase) >= 4 ? 8 : 4;
+                constexpr int FIX = (V - kMethodBase) % 4;
+                float q[kKPerThread], sv[kKPerThread], cv[kKPerThread];
+#pragma unroll
+                for (int m = 0; m < kKPerThread; ++m) {
+                    const float p = __fmul_rn(fk[m], tj);
+                    q[m] = reduce_turn(TURNS ? p : __fmul_rn(p, kInvTwoPi));
+                }
+                method_from_q_n<NT, FIX, kKPerThread>(mp, q, sv, cv);
+#pragma unroll
+                for (int m = 0; m < kKPerThread; ++m) {
+                    re[m] = __fmaf_rn(aj.x, cv[m], re[m]);
+                    re[m] = __fmaf_rn(-aj.y, sv[m], re[m]);
+                    im[m] = __fmaf_rn(aj.x, sv[m], im[m]);
+                    im[m] = __fmaf_rn(aj.y, cv[m], im[m]);
+                }
             } else {
 #pragma unroll
                 for (int m = 0; m < kKPerThread; ++m) {

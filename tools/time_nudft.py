@@ -25,7 +25,9 @@ def main():
     for units in (sp.RADIANS, sp.TURNS):
         f, t = c4_axes(units == sp.TURNS)
         fd, td = torch.from_numpy(f).cuda(), torch.from_numpy(t).cuda()
-        for name, kw in (("N", {"variant": 0}), ("A", {"variant": 1}), ("m132", {"method": fit_method(1, 3, 2)})):
+        for name, kw in (("N", {"variant": 0}), ("A", {"variant": 1}), ("m132", {"method": fit_method(1, 3, 2)}),
+                         ("m332_general", {"method": fit_method(3, 3, 2)}),
+                         ("m254_general", {"method": fit_method(2, 5, 4)})):
             sp.nudft(fd, td, a, units=units, **kw)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()

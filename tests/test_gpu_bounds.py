@@ -99,14 +99,16 @@ def test_phase_grid_and_nudft(shape):
     check(bo, G, G + 2 * nf)
 
 
-@pytest.mark.parametrize("shape", [(1, 1), (3, 7), (9, 13), (33, 1001), (16, 256)])
+@pytest.mark.parametrize("shape", [(1, 1), (3, 7), (9, 13), (33, 1001), (16, 256), (9, 131), (21, 300), (3, 4000)])
 @pytest.mark.parametrize("off", [0, 1, 3, 6])
 def test_phase_grid_split_offsets(shape, off):
-    """Split phase-grid outputs at offsets (the flat kernel's head/body/tail and the row kernel),
-    interleaved at odd and even float offsets (flat kernel / one pair per thread)."""
+    """Split phase-grid outputs at offsets (the flat kernel's head/body/tail, the ragged-row
+    kernel's row ends and re-aligned t windows -- t at a float offset too -- and the aligned row
+    kernel), interleaved at odd and even float offsets (flat / row kernel, one pair per thread)."""
     nf, nt = shape
     f = torch.rand(nf, device="cuda") * 100
-    t = torch.rand(nt, device="cuda")
+    toff = off % 5
+    t = torch.rand(nt + 8, device="cuda")[toff:toff + nt]
     n = nf * nt
     bs = torch.full((2 * G + n + 8,), SENT, dtype=torch.int32, device="cuda")
     bc = bs.clone()

@@ -48,10 +48,21 @@ def test_fuzz_pairs(block):
         r = rng.random()
         n = int(rng.integers(0, 40)) if r < 0.3 else int(rng.integers(40, 5000)) if r < 0.8 \
             else int(rng.integers(5000, 300_000))
-        th = draw_theta(rng, n)
         variant = int(rng.integers(0, 2))
         inter = bool(rng.integers(0, 2))
-        entry = ["pairs", "dtype32", "method", "phase"][int(rng.integers(0, 4))]
+        entry = ["pairs", "dtype32", "method", "phase", "phase2d"][int(rng.integers(0, 5))]
+        if entry == "phase2d":                           # an nf x nt grid: theta_ij = RN(f_i t_j)
+            nf2 = int(rng.integers(1, 24))
+            nt2 = max(1, n // nf2)
+            f2 = rng.uniform(-50, 50, nf2).astype(np.float32)
+            t2 = draw_theta(rng, nt2 + 8)
+            toff2 = int(rng.integers(0, 8))
+            t2 = t2[toff2:toff2 + nt2]
+            n = nf2 * nt2
+            with np.errstate(over="ignore", invalid="ignore"):   # inf / NaN products are inputs too
+                th = (f2[:, None] * t2[None, :]).astype(np.float32).ravel()   # IEEE fp32 products
+        else:
+            th = draw_theta(rng, n)
         ot, os_, oc = (int(x) for x in rng.integers(0, 8, 3))
         if rng.random() < 0.5:
             oc = os_                                     # sin and cos at one offset (common)
@@ -75,9 +86,14 @@ def test_fuzz_pairs(block):
             sp.sincos_pairs_dtype(t, variant=variant, **outs)
         elif entry == "method":
             sp.sincos_pairs_method(t, sp.make_method(*sp.PAPER_METHODS[variant]), **outs)
-        else:
+        elif entry == "phase":
             one = torch.ones(1, dtype=torch.float32, device="cuda")
             sp.phase_grid(one, t, units=sp.RADIANS, variant=variant, **outs)
+        else:
+            tb2 = torch.empty(nt2 + 8, dtype=torch.float32, device="cuda")
+            tb2[toff2:toff2 + nt2].copy_(torch.from_numpy(t2))
+            sp.phase_grid(torch.from_numpy(f2).cuda(), tb2[toff2:toff2 + nt2], units=sp.RADIANS, variant=variant,
+                          **outs)
         torch.cuda.synchronize()
         if inter:
             v = outs["interleaved_out"].cpu().numpy()

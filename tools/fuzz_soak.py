@@ -36,10 +36,20 @@ def one_case(rng):
     r = rng.random()
     n = int(rng.integers(0, 40)) if r < 0.3 else int(rng.integers(40, 5000)) if r < 0.8 \
         else int(rng.integers(5000, 300_000))
-    th = draw_theta(rng, n)
     variant = int(rng.integers(0, 2))
     inter = bool(rng.integers(0, 2))
-    entry = ["pairs", "dtype32", "method", "phase", "batched", "fp16", "bf16"][int(rng.integers(0, 7))]
+    entry = ["pairs", "dtype32", "method", "phase", "batched", "fp16", "bf16", "phase2d"][int(rng.integers(0, 8))]
+    if entry == "phase2d":                # an nf x nt grid: theta_ij = RN(f_i t_j), the fp32 products
+        nf2 = int(rng.integers(1, 24))
+        nt2 = max(1, n // nf2)
+        f2 = rng.uniform(-50, 50, nf2).astype(np.float32)
+        toff2 = int(rng.integers(0, 8))
+        t2 = draw_theta(rng, nt2 + 8)[toff2:toff2 + nt2]
+        n = nf2 * nt2
+        with np.errstate(over="ignore", invalid="ignore"):   # inf / NaN products are inputs too
+            th = (f2[:, None] * t2[None, :]).astype(np.float32).ravel()
+    else:
+        th = draw_theta(rng, n)
     ot, os_, oc = (int(x) for x in rng.integers(0, 8, 3))
     if rng.random() < 0.5:
         oc = os_
@@ -67,6 +77,10 @@ def one_case(rng):
         sp.sincos_pairs_dtype(t, variant=variant, **outs)
     elif entry == "phase":
         sp.phase_grid(torch.ones(1, device="cuda"), t, units=sp.RADIANS, variant=variant, **outs)
+    elif entry == "phase2d":
+        tb2 = torch.empty(nt2 + 8, device="cuda")
+        tb2[toff2:toff2 + nt2].copy_(torch.from_numpy(t2))
+        sp.phase_grid(torch.from_numpy(f2).cuda(), tb2[toff2:toff2 + nt2], units=sp.RADIANS, variant=variant, **outs)
     else:
         if inter:
             sp.sincos_pairs_batched([t, t[: n // 2]], interleaved_outs=[io, torch.empty(2 * (n // 2), device="cuda")],

@@ -128,4 +128,43 @@ __device__ __forceinline__ void method_from_q_exact2(const MethodParams &m, F2 q
     s_out = mul2(s, f);
 }
 
+// method_from_q_n<NT, FIX, 2 N2> on N2 lane pairs (run-time doubling count, zero-padded
+// Horner): the same operations, stage by stage, lane by lane.
+template <int NT, int FIX, int N2>
+__device__ __forceinline__ void method_from_q_n2(const MethodParams &m, const F2 (&q1)[N2], F2 (&s_out)[N2],
+                                                 F2 (&c_out)[N2]) {
+#pragma unroll
+    for (int k = 0; k < N2; ++k) {
+        const F2 q2 = mul2(q1[k], q1[k]);
+        F2 ps = bc2(m.ss[NT - 1]);
+#pragma unroll
+        for (int i = NT - 2; i >= 0; --i) ps = fma2(q2, ps, bc2(m.ss[i]));
+        F2 pc = bc2(m.cc[NT - 1]);
+#pragma unroll
+        for (int i = NT - 2; i >= 0; --i) pc = fma2(q2, pc, bc2(m.cc[i]));
+        s_out[k] = mul2(q1[k], ps);
+        c_out[k] = fma2(q2, pc, bc2(1.0f));
+    }
+    if (m.doublings > 0) {
+        for (int i = 0; i < m.doublings - 1; ++i) {          // warp-uniform bound
+#pragma unroll
+            for (int k = 0; k < N2; ++k) {
+                const F2 s = s_out[k], c = c_out[k];
+                c_out[k] = nfma2(s, s, mul2(c, c));
+                s_out[k] = mul2(bc2(2.0f), mul2(s, c));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < N2; ++k) {
+            const F2 s = s_out[k], c = c_out[k];             // the penultimate pair
+            const F2 cc2 = mul2(c, c);
+            F2 f = bc2(1.0f);
+            if constexpr (FIX == 0) f = nfma2(s, s, nfma2(c, c, bc2(2.0f)));
+            if constexpr (FIX == 1) f = rcp_rn2(fma2(s, s, cc2));
+            c_out[k] = mul2(nfma2(s, s, cc2), f);
+            s_out[k] = mul2(mul2(bc2(2.0f), mul2(s, c)), f);
+        }
+    }
+}
+
 }  // namespace sincos_b200

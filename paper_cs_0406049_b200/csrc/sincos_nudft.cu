@@ -75,7 +75,7 @@ __device__ __forceinline__ void term_pair(const MethodParams &mp, float f, float
 // Two frequencies of one term at once (packed fp32, sincos_math2.cuh): the same
 // operations as term_pair for lanes m and m+1, bit-identical, half the FP32 issue slots.
 template <int V>
-constexpr bool kPackable = V == kNormalized || V == kRenormalized || V >= kMethodExactBase;
+constexpr bool kPackable = V == kNormalized || V == kRenormalized || V >= kMethodBase;
 
 template <int V, bool TURNS>
 __device__ __forceinline__ void term_pair2(const MethodParams &mp, F2 f, float t, F2 &s, F2 &c) {
@@ -141,7 +141,32 @@ __global__ void __launch_bounds__(kNuThreads, 9) nudft_partial(const float *__re
             const float4 v = sj[q];
             const float tj = v.x;
             const float2 aj = make_float2(v.y, v.z);
-            if constexpr (PACK) {
+            if constexpr (PACK && V >= kMethodBase && V < kMethodExactBase) {
+                // general methods, packed: all the thread's frequencies stage by stage
+                constexpr int NT = (V - kMethodBase) >= 4 ? 8 : 4;
+                constexpr int FIX = (V - kMethodBase) % 4;
+                constexpr int N2 = kKPerThread / 2;
+                F2 q[N2], sv[N2], cv[N2];
+#pragma unroll
+                for (int m = 0; m < N2; ++m) {
+                    const F2 p = mul2(pk2(fk[2 * m], fk[2 * m + 1]), bc2(tj));
+                    q[m] = reduce_turn2(TURNS ? p : mul2(p, bc2(kInvTwoPi)));
+                }
+                method_from_q_n2<NT, FIX, N2>(mp, q, sv, cv);
+                const F2 ar = bc2(aj.x), ai = bc2(aj.y);
+#pragma unroll
+                for (int m = 0; m < N2; ++m) {
+                    F2 r = pk2(re[2 * m], re[2 * m + 1]), i = pk2(im[2 * m], im[2 * m + 1]);
+                    r = fma2(ar, cv[m], r);
+                    r = nfma2(ai, sv[m], r);
+                    i = fma2(ar, sv[m], i);
+                    i = fma2(ai, cv[m], i);
+                    re[2 * m] = lo2(r);
+                    re[2 * m + 1] = hi2(r);
+                    im[2 * m] = lo2(i);
+                    im[2 * m + 1] = hi2(i);
+                }
+            } else if constexpr (PACK) {
                 const F2 ar = bc2(aj.x), ai = bc2(aj.y);
 #pragma unroll
                 for (int m = 0; m < kKPerThread; m += 2) {

@@ -175,12 +175,13 @@ def scalar_then_packed():
 
 
 @pytest.mark.parametrize("units", [0, 1])
-@pytest.mark.parametrize("kind", ["N", "A", "m1_3_2", "m2_4_3"])
+@pytest.mark.parametrize("kind", ["N", "A", "m1_3_2", "m2_4_3", "g3_3_2", "g2_5_4", "g1_4_4"])
 @pytest.mark.parametrize("shape", [(1, 1), (3, 7), (513, 1031), (1500, 4100)])
 def test_packed_kernel_bit_identical_to_scalar(units, kind, shape, scalar_then_packed):
     """The packed kernels (two frequencies per FFMA2/FMUL2/FADD2 lane pair) round every lane
-    exactly as the scalar kernels do: the sums are bit-identical, for the paper's tables and
-    the specialised method shapes, ragged nf (odd lane pairs past nf) and nt (tail tiles).
+    exactly as the scalar kernels do: the sums are bit-identical, for the paper's tables, the
+    specialised method shapes and general shapes, ragged nf (odd lane pairs past nf) and nt
+    (tail tiles).
     Phases include exact zeros, half-turn ties and huge / subnormal / non-finite values."""
     nf, nt = shape
     rng = np.random.default_rng(nf * 7 + nt)
@@ -195,9 +196,13 @@ def test_packed_kernel_bit_identical_to_scalar(units, kind, shape, scalar_then_p
         kw = {"variant": 0 if kind == "N" else 1}
     else:
         from paper_cs_0406049_b200 import coeff_fit as cf
-        n, ds, dc = (1, 3, 2) if kind == "m1_3_2" else (2, 4, 3)
+        n, ds, dc = (int(x) for x in kind[1:].split("_"))
         ss, cc = cf.fit_angle(n, ds, dc).fp32()
-        kw = {"method": sp.make_method(list(ss), list(cc), n, sp.FIX_RECIPROCAL if n == 1 else sp.FIX_LINEAR)}
+        # m*: the compile-time shapes; g*: general shapes (run-time doubling loop, zero-padded
+        # Horner of 4 or 8 terms), fix reciprocal / linear / none
+        fix = {"m1_3_2": sp.FIX_RECIPROCAL, "m2_4_3": sp.FIX_LINEAR, "g3_3_2": sp.FIX_RECIPROCAL,
+               "g2_5_4": sp.FIX_LINEAR, "g1_4_4": sp.FIX_NONE}[kind]
+        kw = {"method": sp.make_method(list(ss), list(cc), n, fix)}
     fd, td, ad = (torch.from_numpy(x).cuda() for x in (f, t, a))
     sp.set_nudft_packed(False)
     o_scalar = sp.nudft(fd, td, ad, units=units, **kw)

@@ -339,7 +339,7 @@ SINCOS_API int sincos_set_pdl(int on);
 /* Fused-sum kernel form (bench / tests): 1 = packed fp32 (sm_100a FFMA2/FMUL2/FADD2,
  * two frequencies per instruction; the default), 0 = scalar fp32.  Both are
  * bit-identical (each packed lane rounds as the scalar instruction does); applies to
- * variants 0/1 and the specialised method shapes.  Process-global; returns the previous
+ * variants 0/1 and every method (specialised and general shapes).  Process-global; returns the previous
  * setting, or -1 for a value other than 0/1. */
 SINCOS_API int sincos_set_nudft_packed(int on);
 

@@ -201,11 +201,12 @@ SINCOS_API sincos_status_t sincos_pairs_method(const float *theta_dev, float *si
  * must not overlap the outputs.  Paths, identical numerics: nt % 8 == 0 with 32-B
  * aligned t and outputs -- 256-bit vectors per row; any other nt / alignment with
  * outputs that can take 256-bit stores (split: sin and cos at the same offset mod
- * 32 B; interleaved: 8-B aligned) -- for nt >= 128 the row path (each thread keeps
+ * 32 B; interleaved: 8-B aligned) -- for nt >= 1024 the row path (each thread keeps
  * eight t-values, re-aligned by warp shuffles to the rows' output alignment, and
- * writes them for the rows of one alignment class), for shorter rows the flat path
- * (8 consecutive pairs of the row-major grid per thread); otherwise one pair per
- * thread.  Returns as sincos_pairs; nf*nt == 0 is a no-op.
+ * writes them for the rows of one alignment class), for 8 <= nt < 1024 the short-row
+ * path (8 consecutive pairs of the row-major grid per thread, t from shared memory),
+ * for nt < 8 the flat path; otherwise one pair per thread.  Returns as sincos_pairs;
+ * nf*nt == 0 is a no-op.
  */
 typedef enum { SINCOS_RADIANS = 0, SINCOS_TURNS = 1 } sincos_units_t;
 SINCOS_API sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_dev, size_t nt,
@@ -323,7 +324,8 @@ SINCOS_API void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *
 /* Unshared alignment (theta and the outputs at different offsets mod 16 B): 1 = keep the
  * outputs' 128-bit stores and re-align theta in registers with warp shuffles (the default),
  * 0 = one element per thread, 2 = re-alignment in its 128-bit form only (A/B), 3 = as 1 but
- * sincos_phase_grid's ragged rows through the flat path instead of the row path (A/B).
+ * sincos_phase_grid's ragged rows through the flat path instead of the row / short-row
+ * paths (A/B).
  * Identical results.  0 also turns off sincos_phase_grid's row and flat paths for rows that
  * are not whole 256-bit vectors.  Process-global; returns the previous setting, or -1 for a
  * value other than 0..3. */

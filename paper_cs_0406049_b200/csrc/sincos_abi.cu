@@ -346,8 +346,14 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
         size_t grid = (nvec + 127) / 128;
         if (grid < 1) grid = 1;
         if (grid > 0x7FFFFFFFu) grid = 0x7FFFFFFFu;
+        const bool short_rows = g_phase_rows.load(std::memory_order_relaxed) != 0 && nt >= 8 && nt < kPhaseRowsMinNt;
+        // the short-row kernel stages t in shared memory once per block: a grid of a few
+        // blocks per SM, grid-striding, amortises that
+        const size_t cap = static_cast<size_t>(sm_count(dev)) * kPhaseShortBlocksPerSm;
+        if (short_rows && grid > cap) grid = cap;
         e = launch_phase_flat(variant, inter, units == SINCOS_TURNS, f_dev, nf, t_dev, nt, sin_dev, cos_dev,
-                              inter_dev, head, nvec, static_cast<unsigned>(grid), static_cast<cudaStream_t>(stream));
+                              inter_dev, head, nvec, static_cast<unsigned>(grid), short_rows,
+                              static_cast<cudaStream_t>(stream));
     } else {
         e = launch_phase_grid(variant, inter, units == SINCOS_TURNS, vec, f_dev, nf, t_dev, nt, sin_dev, cos_dev,
                               inter_dev, static_cast<cudaStream_t>(stream));

@@ -64,20 +64,25 @@ cudaError_t launch_tma(int variant, bool inter, unsigned grid, const float *thet
 cudaError_t launch_phase_grid(int variant, bool inter, bool turns, bool vec, const float *f, size_t nf,
                               const float *t, size_t nt, float *so, float *co, float *io, cudaStream_t stream);
 // NEXT(1) flat path for any nt: pairs [head, head + 8 nvec) as 256-bit stores (outputs 32-B
-// aligned at `head`), the rest one per thread; grid-stride over `grid` blocks.
+// aligned at `head`), the rest one per thread; grid-stride over `grid` blocks.  short_rows:
+// for 8 <= nt < kPhaseRowsMinNt the one-path kernel with t in shared memory.
 cudaError_t launch_phase_flat(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
                               size_t nt, float *so, float *co, float *io, size_t head, size_t nvec,
-                              unsigned grid, cudaStream_t stream);
+                              unsigned grid, bool short_rows, cudaStream_t stream);
 // NEXT(1) row path for nt % 8 != 0 or unaligned t (nt >= kPhaseRowsMinNt): h0 = the first
 // pair at which the outputs are 32-B aligned (0..7); t any 4-B alignment.
 #ifndef SINCOS_PHASE_ROWS_MIN_NT
-#define SINCOS_PHASE_ROWS_MIN_NT 128
+#define SINCOS_PHASE_ROWS_MIN_NT 1024
 #endif
-constexpr size_t kPhaseRowsMinNt = SINCOS_PHASE_ROWS_MIN_NT;   // shorter rows: the flat path (measured faster below ~128)
+constexpr size_t kPhaseRowsMinNt = SINCOS_PHASE_ROWS_MIN_NT;   // shorter rows: the short-row kernel (t in shared memory; measured faster below ~1000)
 #ifndef SINCOS_PHASE_ROWS_PER_BLOCK
 #define SINCOS_PHASE_ROWS_PER_BLOCK 8
 #endif
 constexpr size_t kPhaseRowsPerBlock = SINCOS_PHASE_ROWS_PER_BLOCK;   // target rows per row slot
+#ifndef SINCOS_PHASE_SHORT_BPS
+#define SINCOS_PHASE_SHORT_BPS 256
+#endif
+constexpr size_t kPhaseShortBlocksPerSm = SINCOS_PHASE_SHORT_BPS;     // short-row kernel grid, per SM
 cudaError_t launch_phase_rows(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
                               size_t nt, float *so, float *co, float *io, unsigned h0, int sms,
                               cudaStream_t stream);

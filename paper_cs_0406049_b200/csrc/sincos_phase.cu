@@ -42,6 +42,26 @@ __device__ __forceinline__ void phase_pair(float f, float t, float &s, float &c)
 #define SINCOS_PACKED_PHASE 1
 #endif
 template <int V, bool TURNS>
+__device__ __forceinline__ void phase8f(const float (&fv)[8], const float (&tv)[8], float (&sv)[8], float (&cv)[8]) {
+    if constexpr (SINCOS_PACKED_PHASE) {
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+            F2 x = mul2(pk2(fv[k], fv[k + 1]), pk2(tv[k], tv[k + 1]));
+            if constexpr (!TURNS) x = mul2(x, bc2(kInvTwoPi));
+            F2 s2, c2;
+            sincos_from_q2<V>(reduce_turn2(x), s2, c2);
+            sv[k] = lo2(s2);
+            sv[k + 1] = hi2(s2);
+            cv[k] = lo2(c2);
+            cv[k + 1] = hi2(c2);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fv[k], tv[k], sv[k], cv[k]);
+    }
+}
+
+template <int V, bool TURNS>
 __device__ __forceinline__ void phase8(float fi, const float (&tv)[8], float (&sv)[8], float (&cv)[8]) {
     if constexpr (SINCOS_PACKED_PHASE) {
 #pragma unroll
@@ -395,6 +415,74 @@ cudaError_t launch_phase_rows(int variant, bool inter, bool turns, const float *
                             args, 0, stream);
 }
 
+// Short rows (8 <= nt < kPhaseRowsMinNt = 1024): the flat kernel's mapping (8 consecutive pairs of the
+// row-major grid per thread, (i, j) of the first by the corrected fp64 quotient) with one code
+// path for every vector -- a warp spans several short rows, and the flat kernel's separate
+// in-row / row-boundary forms ran both in most warps (17 of 32 lanes active per instruction).
+// t comes from shared memory: four copies ts[r][m] = t[(m + r) mod nt], so that the window
+// t[(j .. j+7) mod nt] (wrapping into the next row's first t-values) is ts[j & 3][(j & ~3) ..]:
+// two aligned 128-bit loads and no selection; each pair takes f_i or f_{i+1} by a select.
+// 16.6 KB of shared memory per block; a grid of 256 blocks per SM, grid-striding (fewer blocks
+// with longer strides measured slower, the full grid too: tools/ab_phase.py).  Below 1024 it
+// beats the row kernel, whose slots are partly idle and which pays per-row ends.
+constexpr int kShortNtMax = static_cast<int>(kPhaseRowsMinNt);
+constexpr int kShortStride = kShortNtMax + 16;                              // floats per copy (16-B rows)
+
+template <int V, bool INTER, bool TURNS>
+__global__ void __launch_bounds__(kPhaseThreads) phase_grid_short(const float *__restrict__ f,
+                                                                 const float *__restrict__ t, size_t nf,
+                                                                 size_t nt, float *so, float *co, float *io,
+                                                                 size_t head, size_t nvec, size_t n,
+                                                                 double inv_nt) {
+    __shared__ __align__(16) float ts[4][kShortStride];
+    const unsigned ntu = static_cast<unsigned>(nt);
+    for (unsigned q = threadIdx.x; q < 4u * (ntu + 8u); q += blockDim.x) {
+        const unsigned r = q / (ntu + 8u), m = q % (ntu + 8u);
+        ts[r][m] = __ldg(t + (m + r) % ntu);
+    }
+    __syncthreads();
+    const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t tail0 = head + 8 * nvec;
+    if (tid < head) phase_one<V, INTER, TURNS>(f, t, nt, inv_nt, tid, so, co, io);
+    if (tid < n - tail0) phase_one<V, INTER, TURNS>(f, t, nt, inv_nt, tail0 + tid, so, co, io);
+    for (size_t v = tid; v < nvec; v += nthr) {
+        const size_t e0 = head + 8 * v;
+        size_t i, j;
+        divmod_nt(e0, nt, inv_nt, i, j);
+        const unsigned ju = static_cast<unsigned>(j), r = ju & 3u;
+        const float4 *w = reinterpret_cast<const float4 *>(&ts[r][ju - r]);
+        const float4 w0 = w[0], w1 = w[1];
+        const float tv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        const unsigned kw = ntu - ju;                                     // first pair of row i+1
+        const float f0 = __ldg(f + i);
+        const float f1 = kw < 8u ? __ldg(f + i + 1) : f0;                 // row i+1 exists when reached
+        float fv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) fv[k] = static_cast<unsigned>(k) >= kw ? f1 : f0;
+        float sv[8], cv[8];
+        phase8f<V, TURNS>(fv, tv, sv, cv);
+        if constexpr (INTER) {
+            float cs[16];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                cs[2 * k] = cv[k];
+                cs[2 * k + 1] = sv[k];
+            }
+            st8_stream(io + 2 * e0, cs);
+            st8_stream(io + 2 * e0 + 8, cs + 8);
+        } else {
+            st8_stream(so + e0, sv);
+            st8_stream(co + e0, cv);
+        }
+    }
+}
+
+template <int V, bool INTER, bool TURNS>
+static const void *pick_short() {
+    return reinterpret_cast<const void *>(phase_grid_short<V, INTER, TURNS>);
+}
+
 template <int V, bool INTER, bool TURNS>
 static const void *pick_flat() {
     return reinterpret_cast<const void *>(phase_grid_flat<V, INTER, TURNS>);
@@ -402,14 +490,23 @@ static const void *pick_flat() {
 
 cudaError_t launch_phase_flat(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
                               size_t nt, float *so, float *co, float *io, size_t head, size_t nvec,
-                              unsigned grid, cudaStream_t stream) {
+                              unsigned grid, bool short_rows, cudaStream_t stream) {
     const void *fn;
-    if (variant == kNormalized)
+    if (short_rows && nt >= 8 && nt < kPhaseRowsMinNt) {                  // phase_grid_short
+        if (variant == kNormalized)
+            fn = inter ? (turns ? pick_short<kNormalized, true, true>() : pick_short<kNormalized, true, false>())
+                       : (turns ? pick_short<kNormalized, false, true>() : pick_short<kNormalized, false, false>());
+        else
+            fn = inter ? (turns ? pick_short<kRenormalized, true, true>() : pick_short<kRenormalized, true, false>())
+                       : (turns ? pick_short<kRenormalized, false, true>()
+                                : pick_short<kRenormalized, false, false>());
+    } else if (variant == kNormalized) {
         fn = inter ? (turns ? pick_flat<kNormalized, true, true>() : pick_flat<kNormalized, true, false>())
                    : (turns ? pick_flat<kNormalized, false, true>() : pick_flat<kNormalized, false, false>());
-    else
+    } else {
         fn = inter ? (turns ? pick_flat<kRenormalized, true, true>() : pick_flat<kRenormalized, true, false>())
                    : (turns ? pick_flat<kRenormalized, false, true>() : pick_flat<kRenormalized, false, false>());
+    }
     size_t n = nf * nt;
     double inv_nt = 1.0 / static_cast<double>(nt);
     void *args[] = {&f, &t, &nf, &nt, &so, &co, &io, &head, &nvec, &n, &inv_nt};

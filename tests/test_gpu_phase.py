@@ -113,7 +113,8 @@ def test_radians_equals_the_materialised_path(variant):
 @pytest.mark.parametrize("mode", [1, 3, 0])
 def test_ragged_rows_flat_path(units, variant, mode):
     """Rows that are not whole 256-bit vectors (nt % 8 != 0, t or outputs off 32 B) go through
-    the row kernel (nt >= 128: t windows re-aligned per row class), the flat kernel (8
+    the row kernel (nt >= 1024: t windows re-aligned per row class) or the short-row kernel
+    (8 <= nt < 1024: t from shared memory), the flat kernel (8
     consecutive pairs of the row-major grid per thread, rows wrapping inside a vector, nt = 1..9
     included; for every nt with set_realign(3)) or, with both disabled / for outputs they
     cannot serve, one pair per thread; bit-exact either way, at several output offsets, split
@@ -151,11 +152,12 @@ def test_ragged_rows_flat_path(units, variant, mode):
 
 
 @pytest.mark.parametrize("units,variant", COMBOS)
-@pytest.mark.parametrize("nt", [128, 129, 130, 131, 132, 133, 134, 135, 300, 1001])
+@pytest.mark.parametrize("nt", [9, 17, 131, 1001, 1024, 1025, 1026, 1027, 1028, 1029, 1030, 1031])
 def test_row_path_every_alignment(units, variant, nt):
-    """The row kernel at every t offset (its re-alignment K = 0..7) x every output offset
-    (the rows' first aligned column, per row class) x nt mod 8, with nf = 19 rows (every row
-    class, more rows than classes), split and interleaved: bit-exact vs the oracle."""
+    """The ragged-row kernels at every t offset x every output offset x nt mod 8, with nf = 19
+    rows, split and interleaved: bit-exact vs the oracle.  nt >= 1024: the row kernel (its
+    re-alignment K = 0..7, every row class, more rows than classes); 8 <= nt < 1024: the
+    short-row kernel (t windows from shared memory, rows wrapping inside a vector)."""
     rng = np.random.default_rng(nt * 7 + units + 2 * variant)
     nf = 19
     n = nf * nt
@@ -181,11 +183,12 @@ def test_row_path_every_alignment(units, variant, nt):
 
 
 @pytest.mark.parametrize("inter", [False, True])
-@pytest.mark.parametrize("shape", [(70001, 131), (2_240_032, 521)])
+@pytest.mark.parametrize("shape", [(70001, 131), (2_240_032, 521), (70001, 1029), (2_150_000, 1031)])
 def test_row_path_many_rows(inter, shape):
-    """Many rows: (70001, 131) -- 4 row slots per block, past the 65528-block grid height's
-    rows; (2 240 032, 521) -- slot count capped, > 32 rows per slot (f re-loaded per 32-row
-    chunk), 1.17e9 pairs.  Row i depends on f_i and t only, so sampled rows (the first and
+    """Many rows: (70001, 131), (2 240 032, 521) -- the short-row kernel's grid-stride loop;
+    (70001, 1029) -- the row kernel past the 65528-block grid height's rows; (2 150 000, 1031)
+    -- slot count capped, > 32 rows per slot (f re-loaded per 32-row chunk), 2.2e9 pairs.
+    Row i depends on f_i and t only, so sampled rows (the first and
     last, rows around the slot-count multiples, random rows) are compared with the oracle's
     grid of those f values: bit-exact."""
     nf, nt = shape
@@ -197,7 +200,7 @@ def test_row_path_many_rows(inter, shape):
     td = torch.from_numpy(tb).cuda()[1:]
     n = nf * nt
     rows = np.unique(np.concatenate([[0, 1, 2, nf - 2, nf - 1], rng.integers(0, nf, 3000),
-                                     *[np.arange(k - 9, k + 9) for k in (65528, 262112, 524224, 2 * 262112)
+                                     *[np.arange(k - 9, k + 9) for k in (65528, 262112, 524224, 2 * 262112, 32 * 65528)
                                        if k + 9 < nf]]))
     ws, wc = oracle.phase_grid(f[rows], t, R, 1)
     ri = torch.from_numpy(rows).cuda()

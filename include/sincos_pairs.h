@@ -198,8 +198,8 @@ SINCOS_API sincos_status_t sincos_pairs_method(const float *theta_dev, float *si
  *                              and skips the 1/2pi scaling and its rounding.
  * Outputs as in sincos_pairs (split sin/cos of nf*nt floats each, or interleaved
  * {cos, sin}).  Only 8 B per pair are written (no theta array is read); f and t
- * must not overlap the outputs.  Paths, identical numerics: nt % 8 == 0 with 32-B
- * aligned t and outputs -- 256-bit vectors per row; any other nt / alignment with
+ * must not overlap the outputs.  Paths, identical numerics: nt % 8 == 0, nt >= 256, with
+ * 32-B aligned t and outputs -- 256-bit vectors per row; any other nt / alignment with
  * outputs that can take 256-bit stores (split: sin and cos at the same offset mod
  * 32 B; interleaved: 8-B aligned) -- for nt >= 1024 the row path (each thread keeps
  * eight t-values, re-aligned by warp shuffles to the rows' output alignment, and

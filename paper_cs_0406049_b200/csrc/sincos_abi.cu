@@ -320,7 +320,9 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
         if (o == nullptr) continue;
         if (overlaps(o, ob, f_dev, 4 * nf) || overlaps(o, ob, t_dev, 4 * nt)) return SINCOS_ERR_OVERLAP;
     }
-    const bool vec = nt % 8 == 0 && aligned(t_dev, 32) &&
+    // whole-vector rows: the vector kernel from kPhaseVecMinNt on (shorter rows leave its
+    // threads idle: nt = 16 ran at 0.7 TB/s; the short-row kernel takes them)
+    const bool vec = nt % 8 == 0 && nt >= kPhaseVecMinNt && aligned(t_dev, 32) &&
                      (split ? aligned(sin_dev, 32) && aligned(cos_dev, 32) : aligned(inter_dev, 32));
     cudaError_t e;
     // any other shape: when the outputs can take 256-bit stores from some pair on (split: sin

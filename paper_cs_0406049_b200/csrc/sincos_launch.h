@@ -79,6 +79,10 @@ constexpr size_t kPhaseRowsMinNt = SINCOS_PHASE_ROWS_MIN_NT;   // shorter rows: 
 #define SINCOS_PHASE_ROWS_PER_BLOCK 8
 #endif
 constexpr size_t kPhaseRowsPerBlock = SINCOS_PHASE_ROWS_PER_BLOCK;   // target rows per row slot
+#ifndef SINCOS_PHASE_VEC_MIN_NT
+#define SINCOS_PHASE_VEC_MIN_NT 256
+#endif
+constexpr size_t kPhaseVecMinNt = SINCOS_PHASE_VEC_MIN_NT;     // aligned rows shorter: the short-row kernel
 #ifndef SINCOS_PHASE_SHORT_BPS
 #define SINCOS_PHASE_SHORT_BPS 256
 #endif

@@ -24,7 +24,7 @@ if os.environ.get("AB_CASES") == "short":
 if os.environ.get("AB_CASES") == "mid":
     CASES = [(131, 0), (200, 2), (255, 0), (300, 0), (500, 1), (1001, 0), (1001, 3), (2000, 0), (4000, 5)]
 if os.environ.get("AB_CASES") == "aligned":
-    CASES = [(32768, 0), (4096, 0), (1000, 0), (256, 0), (136, 0), (64, 0), (16, 0)]
+    CASES = [(32768, 0), (8192, 0), (4096, 0), (2048, 0), (1000, 0), (512, 0), (256, 0), (136, 0), (64, 0), (16, 0)]
 
 
 def build(name, flags):

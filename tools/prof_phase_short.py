@@ -1,6 +1,7 @@
-"""One launch each of the phase grid's flat kernel on short rows (nt = 65, 100 with t one float
-off), split, turns, variant N, ~2^30 pairs -- for an ncu capture:
-  ncu --set full -k regex:phase_grid_flat python tools/prof_phase_short.py"""
+"""One launch each of the phase grid's short-row kernel on short rows (nt = 65, 100 with t one
+float off) and of the flat kernel (set_realign(3)) on nt = 65, split, turns, variant N, ~2^30
+pairs -- for an ncu capture:
+  ncu --set full -k regex:"phase_grid_(short|flat)" python tools/prof_phase_short.py"""
 import os
 import sys
 
@@ -11,7 +12,8 @@ import torch  # noqa: E402
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
 
-for nt, toff in ((65, 0), (100, 1)):
+for nt, toff, mode in ((65, 0, 1), (100, 1, 1), (65, 0, 3)):
+    sp.set_realign(mode)
     nf = (1 << 30) // nt
     f = torch.rand(nf, device="cuda") * 512
     t = torch.rand(nt + 8, device="cuda")[toff:toff + nt]
@@ -20,4 +22,5 @@ for nt, toff in ((65, 0), (100, 1)):
     sp.phase_grid(f, t, s, c, units=sp.TURNS)
     torch.cuda.synchronize()
     del s, c
+sp.set_realign(1)
 print("ok")

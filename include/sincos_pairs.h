@@ -203,10 +203,10 @@ SINCOS_API sincos_status_t sincos_pairs_method(const float *theta_dev, float *si
  * outputs that can take 256-bit stores (split: sin and cos at the same offset mod
  * 32 B; interleaved: 8-B aligned) -- for nt >= 1024 the row path (each thread keeps
  * eight t-values, re-aligned by warp shuffles to the rows' output alignment, and
- * writes them for the rows of one alignment class), for 8 <= nt < 1024 the short-row
- * path (8 consecutive pairs of the row-major grid per thread, t from shared memory),
- * for nt < 8 the flat path; otherwise one pair per thread.  Returns as sincos_pairs;
- * nf*nt == 0 is a no-op.
+ * writes them for the rows of one alignment class), for nt < 1024 (and whole-vector
+ * rows shorter than 256) the short-row path (8 consecutive pairs of the row-major grid
+ * per thread, t from shared memory); otherwise one pair per thread.  Returns as
+ * sincos_pairs; nf*nt == 0 is a no-op.
  */
 typedef enum { SINCOS_RADIANS = 0, SINCOS_TURNS = 1 } sincos_units_t;
 SINCOS_API sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_dev, size_t nt,

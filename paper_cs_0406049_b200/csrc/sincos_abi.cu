@@ -348,7 +348,7 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
         size_t grid = (nvec + 127) / 128;
         if (grid < 1) grid = 1;
         if (grid > 0x7FFFFFFFu) grid = 0x7FFFFFFFu;
-        const bool short_rows = g_phase_rows.load(std::memory_order_relaxed) != 0 && nt >= 8 && nt < kPhaseRowsMinNt;
+        const bool short_rows = g_phase_rows.load(std::memory_order_relaxed) != 0 && nt < kPhaseRowsMinNt;
         // the short-row kernel stages t in shared memory once per block: a grid of a few
         // blocks per SM, grid-striding, amortises that
         const size_t cap = static_cast<size_t>(sm_count(dev)) * kPhaseShortBlocksPerSm;

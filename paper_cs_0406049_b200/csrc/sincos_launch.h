@@ -65,7 +65,7 @@ cudaError_t launch_phase_grid(int variant, bool inter, bool turns, bool vec, con
                               const float *t, size_t nt, float *so, float *co, float *io, cudaStream_t stream);
 // NEXT(1) flat path for any nt: pairs [head, head + 8 nvec) as 256-bit stores (outputs 32-B
 // aligned at `head`), the rest one per thread; grid-stride over `grid` blocks.  short_rows:
-// for 8 <= nt < kPhaseRowsMinNt the one-path kernel with t in shared memory.
+// for nt < kPhaseRowsMinNt the one-path kernel with t in shared memory.
 cudaError_t launch_phase_flat(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
                               size_t nt, float *so, float *co, float *io, size_t head, size_t nvec,
                               unsigned grid, bool short_rows, cudaStream_t stream);

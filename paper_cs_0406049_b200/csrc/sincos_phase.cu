@@ -415,13 +415,14 @@ cudaError_t launch_phase_rows(int variant, bool inter, bool turns, const float *
                             args, 0, stream);
 }
 
-// Short rows (8 <= nt < kPhaseRowsMinNt = 1024): the flat kernel's mapping (8 consecutive pairs of the
+// Short rows (1 <= nt < kPhaseRowsMinNt = 1024): the flat kernel's mapping (8 consecutive pairs of the
 // row-major grid per thread, (i, j) of the first by the corrected fp64 quotient) with one code
 // path for every vector -- a warp spans several short rows, and the flat kernel's separate
 // in-row / row-boundary forms ran both in most warps (17 of 32 lanes active per instruction).
 // t comes from shared memory: four copies ts[r][m] = t[(m + r) mod nt], so that the window
 // t[(j .. j+7) mod nt] (wrapping into the next row's first t-values) is ts[j & 3][(j & ~3) ..]:
-// two aligned 128-bit loads and no selection; each pair takes f_i or f_{i+1} by a select.
+// two aligned 128-bit loads and no selection; each pair takes f_i or f_{i+1} by a select
+// (nt < 8: f_{i + (j + k) / nt}, the row offsets from a 16-entry table).
 // 16.6 KB of shared memory per block; a grid of 256 blocks per SM, grid-striding (fewer blocks
 // with longer strides measured slower, the full grid too: tools/ab_phase.py).  Below 1024 it
 // beats the row kernel, whose slots are partly idle and which pays per-row ends.
@@ -435,7 +436,9 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_short(const float *_
                                                                  size_t head, size_t nvec, size_t n,
                                                                  double inv_nt) {
     __shared__ __align__(16) float ts[4][kShortStride];
+    __shared__ unsigned char rowoff[16];                                  // m / nt (nt < 8)
     const unsigned ntu = static_cast<unsigned>(nt);
+    if (threadIdx.x < 16) rowoff[threadIdx.x] = static_cast<unsigned char>(threadIdx.x / ntu);
     for (unsigned q = threadIdx.x; q < 4u * (ntu + 8u); q += blockDim.x) {
         const unsigned r = q / (ntu + 8u), m = q % (ntu + 8u);
         ts[r][m] = __ldg(t + (m + r) % ntu);
@@ -454,12 +457,17 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_short(const float *_
         const float4 *w = reinterpret_cast<const float4 *>(&ts[r][ju - r]);
         const float4 w0 = w[0], w1 = w[1];
         const float tv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-        const unsigned kw = ntu - ju;                                     // first pair of row i+1
-        const float f0 = __ldg(f + i);
-        const float f1 = kw < 8u ? __ldg(f + i + 1) : f0;                 // row i+1 exists when reached
         float fv[8];
+        if (ntu >= 8u) {                                                  // at most one row boundary
+            const unsigned kw = ntu - ju;                                 // first pair of row i+1
+            const float f0 = __ldg(f + i);
+            const float f1 = kw < 8u ? __ldg(f + i + 1) : f0;             // row i+1 exists when reached
 #pragma unroll
-        for (int k = 0; k < 8; ++k) fv[k] = static_cast<unsigned>(k) >= kw ? f1 : f0;
+            for (int k = 0; k < 8; ++k) fv[k] = static_cast<unsigned>(k) >= kw ? f1 : f0;
+        } else {                                                          // nt < 8: several rows
+#pragma unroll
+            for (int k = 0; k < 8; ++k) fv[k] = __ldg(f + i + rowoff[ju + k]);
+        }
         float sv[8], cv[8];
         phase8f<V, TURNS>(fv, tv, sv, cv);
         if constexpr (INTER) {
@@ -492,7 +500,7 @@ cudaError_t launch_phase_flat(int variant, bool inter, bool turns, const float *
                               size_t nt, float *so, float *co, float *io, size_t head, size_t nvec,
                               unsigned grid, bool short_rows, cudaStream_t stream) {
     const void *fn;
-    if (short_rows && nt >= 8 && nt < kPhaseRowsMinNt) {                  // phase_grid_short
+    if (short_rows && nt >= 1 && nt < kPhaseRowsMinNt) {                  // phase_grid_short
         if (variant == kNormalized)
             fn = inter ? (turns ? pick_short<kNormalized, true, true>() : pick_short<kNormalized, true, false>())
                        : (turns ? pick_short<kNormalized, false, true>() : pick_short<kNormalized, false, false>());

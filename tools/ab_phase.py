@@ -20,7 +20,7 @@ AB = os.path.join(ROOT, "tools", "ab_phase")
 CASES = [(32767, 0), (32772, 0), (1001, 0), (1001, 3), (4000, 5), (255, 0), (300, 0), (500, 1), (131, 0),
          (65, 0), (100, 1), (200, 2)]
 if os.environ.get("AB_CASES") == "short":
-    CASES = [(9, 0), (17, 3), (33, 0), (65, 0), (100, 1), (127, 0)]
+    CASES = [(1, 0), (3, 0), (5, 1), (7, 2), (9, 0), (17, 3), (33, 0), (65, 0), (100, 1), (127, 0)]
 if os.environ.get("AB_CASES") == "mid":
     CASES = [(131, 0), (200, 2), (255, 0), (300, 0), (500, 1), (1001, 0), (1001, 3), (2000, 0), (4000, 5)]
 if os.environ.get("AB_CASES") == "aligned":

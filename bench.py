@@ -315,6 +315,26 @@ def measure_phase_grid(dev, stream, peak, reps=10):
             gbs = 8 * (1 << 30) / (ms / 1e3) / 1e9
             out[f"{uname}_{vname}"] = {"ms": ms, "pairs_per_s": (1 << 30) / (ms / 1e3), "GBps": gbs,
                                        "frac": gbs / peak}
+    # ragged rows (not whole 256-bit vectors): the row kernel (nt = 2^15 - 1) and the short-row
+    # kernel (nt = 1001), turns, variant N, ~2^30 pairs each
+    for nt in ((1 << 15) - 1, 1001):
+        nf = (1 << 30) // nt
+        fd = torch.rand(nf, device=dev, generator=torch.Generator(device=dev).manual_seed(5)) * 512
+        td = torch.rand(nt, device=dev, generator=torch.Generator(device=dev).manual_seed(6))
+        oo = o[: 2 * nf * nt]
+        for _ in range(2):
+            sp.phase_grid(fd, td, interleaved_out=oo, units=sp.TURNS, variant=sp.NORMALIZED, stream=stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            sp.phase_grid(fd, td, interleaved_out=oo, units=sp.TURNS, variant=sp.NORMALIZED, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = a.elapsed_time(b) / reps
+        gbs = 8 * nf * nt / (ms / 1e3) / 1e9
+        out[f"ragged_nt{nt}_turns_N"] = {"nf": nf, "nt": nt, "ms": ms, "pairs_per_s": nf * nt / (ms / 1e3),
+                                         "GBps": gbs, "frac": gbs / peak,
+                                         "kernel": "row" if nt >= 1024 else "short-row"}
     del o
     torch.cuda.empty_cache()
     return out

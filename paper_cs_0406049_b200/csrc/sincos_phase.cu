@@ -428,6 +428,9 @@ cudaError_t launch_phase_rows(int variant, bool inter, bool turns, const float *
 // beats the row kernel, whose slots are partly idle and which pays per-row ends.
 constexpr int kShortNtMax = static_cast<int>(kPhaseRowsMinNt);
 constexpr int kShortStride = kShortNtMax + 16;                              // floats per copy (16-B rows)
+static_assert(4 * kShortStride * sizeof(float) + 16 <= 48 * 1024,
+              "short-row kernel: four t copies must fit static shared memory (kPhaseRowsMinNt too large)");
+static_assert(kShortStride % 4 == 0, "short-row kernel: copies must start 16-B aligned");
 
 template <int V, bool INTER, bool TURNS>
 __global__ void __launch_bounds__(kPhaseThreads) phase_grid_short(const float *__restrict__ f,

@@ -46,7 +46,9 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
                     help="BASELINE config (default c2 = configs[1], weak scaling; c1/c3/c4/c5 strong, sharded)")
-    ap.add_argument("--n", type=int, default=N_PER_RANK, help="elements per rank for c2 (default 2^28)")
+    # (not "--n": torch.distributed.run would take it for an abbreviation of its own options)
+    ap.add_argument("--n-per-rank", dest="n", type=int, default=N_PER_RANK,
+                    help="elements per rank for c2 (default 2^28)")
     ap.add_argument("--e2e-max", type=int, default=1 << 28, help="elements per rank in the e2e leg")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample for cpu_baseline")
@@ -483,6 +485,49 @@ def measure_nudft(dev, stream, reps=5):
     return res
 
 
+def pcie_roofline(th_h, n, nvar, dev):
+    """The e2e leg's ceiling: one step's bytes (nvar x 4n B H2D, nvar x 8n B D2H) through plain
+    pinned cudaMemcpyAsync copies -- each direction alone, and both directions concurrently on
+    two streams, which is how the pipeline runs them.  step_floor_ms = the concurrent time (the
+    binding one when the link is not fully duplex), never less than either direction alone."""
+    import torch
+    dbuf = torch.empty(2 * n, dtype=torch.float32, device=dev)
+    hbuf = torch.empty(2 * n, dtype=torch.float32).pin_memory()
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(h2d, d2h):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        torch.cuda.synchronize(dev)
+        if h2d:
+            ev[0].record(s_in)
+            with torch.cuda.stream(s_in):
+                for _ in range(nvar):
+                    dbuf[:n].copy_(th_h, non_blocking=True)
+            ev[1].record(s_in)
+        if d2h:
+            ev[2].record(s_out)
+            with torch.cuda.stream(s_out):
+                for _ in range(nvar):
+                    hbuf.copy_(dbuf, non_blocking=True)
+            ev[3].record(s_out)
+        torch.cuda.synchronize(dev)
+        ms_in = ev[0].elapsed_time(ev[1]) if h2d else 0.0
+        ms_out = ev[2].elapsed_time(ev[3]) if d2h else 0.0
+        return ms_in, ms_out
+
+    for _ in range(2):
+        timed(True, True)
+    ms_h2d = min(timed(True, False)[0] for _ in range(3))
+    ms_d2h = min(timed(False, True)[1] for _ in range(3))
+    both = min((max(r[0], r[1]) for r in (timed(True, True) for _ in range(3))))
+    floor = max(both, ms_h2d, ms_d2h)
+    del dbuf, hbuf
+    return {"h2d_GBps": nvar * 4 * n / (ms_h2d / 1e3) / 1e9, "d2h_GBps": nvar * 8 * n / (ms_d2h / 1e3) / 1e9,
+            "h2d_ms": ms_h2d, "d2h_ms": ms_d2h, "concurrent_ms": both, "step_floor_ms": floor,
+            "how": "pinned copies of one step's bytes; concurrent = H2D and D2H on two streams at once "
+                   "(max of the two event spans); best of 3"}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -608,7 +653,7 @@ def run_ours(args, rank, world, local_rank):
     achieved = BYTES_PER_PAIR * n / (avg[dom] / 1e3) / 1e9
     vname = {0: "N", 1: "A"}
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": ncu_traffic(n, W.interleaved) if world == 1 else None,
+            "traffic": ncu_traffic(n, W.interleaved),
             "kernel": f"sincos_vec_kernel variant {vname[dom]}", "bytes_per_launch": BYTES_PER_PAIR * n,
             "bytes_per_pair": BYTES_PER_PAIR, "peak_source": peak_src,
             "frac_of_theoretical_8180": achieved / 8180.0,
@@ -619,33 +664,6 @@ def run_ours(args, rank, world, local_rank):
             "per_variant_ms": {vname[v]: avg[v] for v in variants},
             "per_variant_ms_median_min": {vname[v]: [statistics.median(per_kernel[v]), min(per_kernel[v])]
                                           for v in variants}}
-
-    # energy (outside the timed region): steps back to back for >= 2 s, the board's energy
-    # counter (NVML, mJ) read before and after -> joules per step, pairs per joule, mean power
-    energy = None
-    if clk.ok and rank == 0:
-        try:
-            nv, h = clk.nv, clk.h
-            steps_e = max(1, int(2.0 / max(ms_max / args.steps / 1e3, 1e-6)))
-            torch.cuda.synchronize(dev)
-            e_a, t_a = nv.nvmlDeviceGetTotalEnergyConsumption(h), time.perf_counter()
-            for _ in range(steps_e):
-                if use_graph:
-                    step_graph.replay()
-                else:
-                    for v in variants:
-                        sp.sincos_pairs(th, variant=v, stream=stream, **outs[v])
-            torch.cuda.synchronize(dev)
-            e_b, t_b = nv.nvmlDeviceGetTotalEnergyConsumption(h), time.perf_counter()
-            joules = (e_b - e_a) / 1e3
-            pairs_e = len(variants) * n * steps_e
-            energy = {"steps": steps_e, "seconds": t_b - t_a, "joules": joules,
-                      "mean_power_w": joules / (t_b - t_a), "pairs_per_joule": pairs_e / joules,
-                      "sustained_pairs_per_s": pairs_e / (t_b - t_a),
-                      "joules_per_step": joules / steps_e,
-                      "how": "NVML total energy counter around back-to-back steps (this GPU, one rank)"}
-        except Exception as e:  # counter not supported: no energy figure
-            energy = {"error": repr(e)}
 
     # traffic ceiling: same access pattern and launch, no arithmetic (outside the timed region)
     o = outs[sp.NORMALIZED]
@@ -685,19 +703,9 @@ def run_ours(args, rank, world, local_rank):
                      avg[v], float(rank), float(v)])
     summary = summarize(gather_records(recs, world, cdev))
 
-    methods_res = None
-    if rank == 0 and not args.no_next and not W.interleaved:
-        o = outs[sp.NORMALIZED]
-        methods_res = measure_methods(dev, stream, th, (o["sin_out"], o["cos_out"]), peak)
-        methods_res["dtypes"] = measure_dtypes(dev, stream, th, peak)
-        methods_res["context_cuda_functions"] = measure_cuda_functions(dev, stream, th,
-                                                                       (o["sin_out"], o["cos_out"]), peak)
-
     # end to end through the C ABI with host buffers, copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        del outs
-        torch.cuda.empty_cache()
         ws = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
         if W.interleaved:
             oh = {"interleaved_out": torch.empty(2 * e2e_n, dtype=torch.float32).pin_memory()}
@@ -724,94 +732,150 @@ def run_ours(args, rank, world, local_rank):
                "h2d_bytes_per_step": len(variants) * 4 * e2e_n, "d2h_bytes_per_step": len(variants) * 8 * e2e_n,
                "steps": k2, "elements_per_rank": e2e_n,
                "path": "sincos_pairs_host: pinned host buffers, chunked H2D -> kernel -> D2H over 3 streams"}
-        # the e2e roofline: the PCIe copy engines (H2D and D2H run concurrently), measured here
-        # with plain pinned copies of one step's byte counts
-        dbuf = torch.empty(2 * e2e_n, dtype=torch.float32, device=dev)
-        hbuf = torch.empty(2 * e2e_n, dtype=torch.float32).pin_memory()
-        for _ in range(2):
-            dbuf[:e2e_n].copy_(th_h, non_blocking=True)
-            hbuf.copy_(dbuf, non_blocking=True)
-        torch.cuda.synchronize(dev)
-        a.record(stream)
-        dbuf[:e2e_n].copy_(th_h, non_blocking=True)
-        b.record(stream)
-        torch.cuda.synchronize(dev)
-        h2d_gbs = 4 * e2e_n / (a.elapsed_time(b) / 1e3) / 1e9
-        a.record(stream)
-        hbuf.copy_(dbuf, non_blocking=True)
-        b.record(stream)
-        torch.cuda.synchronize(dev)
-        d2h_gbs = 8 * e2e_n / (a.elapsed_time(b) / 1e3) / 1e9
-        step_floor = max(len(variants) * 4 * e2e_n / (h2d_gbs * 1e9), len(variants) * 8 * e2e_n / (d2h_gbs * 1e9))
-        e2e["pcie"] = {"h2d_GBps": h2d_gbs, "d2h_GBps": d2h_gbs,
-                       "roofline_pairs_per_s": world * len(variants) * e2e_n / step_floor}
+        # the e2e roofline: one step's bytes through the PCIe copy engines with plain pinned copies,
+        # H2D and D2H issued concurrently on two streams (as the pipeline runs them) and each alone
+        e2e["pcie"] = pcie_roofline(th_h, e2e_n, len(variants), dev)
+        e2e["pcie"]["roofline_pairs_per_s"] = world * len(variants) * e2e_n / (e2e["pcie"]["step_floor_ms"] / 1e3)
         e2e["frac_of_pcie_roofline"] = e2e["value"] / e2e["pcie"]["roofline_pairs_per_s"]
-        del ws, oh, dbuf, hbuf
+        del ws, oh
+
+    # every rank's clocks (the collectives end here; rank 0 alone continues)
+    clocks = clk.result()
+    clocks_all = [clocks]
+    if world > 1:
+        import torch.distributed as dist
+        clocks_all = [None] * world
+        dist.all_gather_object(clocks_all, clocks)
+    nccl = None
+    if world > 1:
+        import torch.distributed as dist
+        nccl = {"backend": dist.get_backend(), "comm_nranks": dist.get_world_size(),
+                "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if args.backend == "nccl" else None,
+                "same_device": bool(args.same_device)}
+    if rank != 0:
+        return
+
+    methods_res = None
+    if not args.no_next and not W.interleaved:
+        o = outs[sp.NORMALIZED]
+        methods_res = measure_methods(dev, stream, th, (o["sin_out"], o["cos_out"]), peak)
+        methods_res["dtypes"] = measure_dtypes(dev, stream, th, peak)
+        methods_res["context_cuda_functions"] = measure_cuda_functions(dev, stream, th,
+                                                                       (o["sin_out"], o["cos_out"]), peak)
 
     fused = nudft_res = None
-    if rank == 0 and not args.no_next:
-        if "outs" in locals():
-            del outs
+    if not args.no_next:
+        del outs
         torch.cuda.empty_cache()
         fused = measure_phase_grid(dev, stream, peak)
         nudft_res = measure_nudft(dev, stream)
 
+    # the oracle on the host cores, after every other rank has finished its GPU work (so no
+    # rank's host thread competes with it)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if not args.no_cpu_baseline:
         cpu = cpu_oracle_rate(th_h.numpy(), args.cpu_seconds, W.description.split(":")[0])
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps,
-            "wall_ms_per_step": wall_ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak" if W.weak else "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": W.description, "n_per_rank": n, "pairs_per_step": len(variants) * units_all,
-                       "global_batch": units_all, "parallelism": f"dp{world} (contiguous shards, no collective)",
-                       "l2": "inputs larger than L2 (4n B theta + 8n B outputs per launch vs 126 MB L2); no flush"
-                             if 12 * n > (256 << 20) else "working set near/below L2 size: not an HBM measurement",
-                       "launch": sp.get_launch_config(), "cuda_graph": use_graph},
-            "hbm_GBps": BYTES_PER_PAIR * pairs_total / (ms_max / 1e3) / 1e9 / world,
-            "roofline": roof,
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches,
-            "clocks": clk.result(),
-            "energy": energy,
-            "max_error": summary["max_err"],
-            "rms_error": summary["rms_err"],
-            "error_reference": "fp64 sin/cos on the device (P:137-138 metric); large-|theta| reduction error "
-                               "is the method's (BASELINE.md section 2), the kernel equals the oracle bit for bit",
-            "shards": summary["shards"],
-            "next_fused_phase": fused,
-            "next_fused_nudft": nudft_res,
-            "next_methods": methods_res,
-            "paper_context": "PowerPC 7400 G4 500 MHz AltiVec: 140 ns per 4 pairs = 28.6 M pairs/s (P:177-180)",
-        }
-        print(json.dumps(line), flush=True)
+    line = {
+        "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps,
+        "wall_ms_per_step": wall_ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak" if W.weak else "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": W.description, "n_per_rank": n, "pairs_per_step": len(variants) * units_all,
+                   "global_batch": units_all, "parallelism": f"dp{world} (contiguous shards, no collective)",
+                   "l2": "inputs larger than L2 (4n B theta + 8n B outputs per launch vs 126 MB L2); no flush"
+                         if 12 * n > (256 << 20) else "working set near/below L2 size: not an HBM measurement",
+                   "launch": sp.get_launch_config(), "cuda_graph": use_graph},
+        "hbm_GBps": BYTES_PER_PAIR * pairs_total / (ms_max / 1e3) / 1e9 / world,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "clocks_per_rank": clocks_all,
+        "distributed": nccl,
+        "max_error": summary["max_err"],
+        "rms_error": summary["rms_err"],
+        "error_reference": "fp64 sin/cos on the device (P:137-138 metric); large-|theta| reduction error "
+                           "is the method's (BASELINE.md section 2), the kernel equals the oracle bit for bit",
+        "shards": summary["shards"],
+        "next_fused_phase": fused,
+        "next_fused_nudft": nudft_res,
+        "next_methods": methods_res,
+        "paper_context": "PowerPC 7400 G4 500 MHz AltiVec: 140 ns per 4 pairs = 28.6 M pairs/s (P:177-180)",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def die(msg: str, code: int = 2):
+    print(f"bench.py: {msg}", file=sys.stderr, flush=True)
+    sys.exit(code)
+
+
+def visible_gpus() -> int:
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` (N > 1) without a launcher: re-run this command under
+    torch.distributed.run with N ranks on this node (one process per GPU, rendezvous on
+    127.0.0.1), so both invocation forms time N GPUs.  Returns the launcher's exit code."""
+    import socket
+    import subprocess
+    if not args.same_device and visible_gpus() < args.gpus:
+        die(f"--gpus {args.gpus} needs {args.gpus} visible CUDA devices, found {visible_gpus()} "
+            "(--same-device --backend gloo runs every rank on cuda:0: host-flow testing only)")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
 
 
 def main():
     args = parse()
+    launched = "WORLD_SIZE" in os.environ
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus < 1:
+        die("--gpus must be >= 1")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if not launched and args.gpus > 1:
+        sys.exit(self_launch(args))
+    # from here on: one process per GPU, and the job is exactly --gpus ranks
+    if world != args.gpus:
+        die(f"--gpus {args.gpus} but the launcher started WORLD_SIZE={world} ranks")
+    if args.same_device and args.backend != "gloo":
+        die("--same-device needs --backend gloo (the ranks' kernels share one GPU: flow testing only)")
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    if not args.same_device and visible_gpus() < local_world:
+        die(f"{local_world} ranks on this node but {visible_gpus()} visible CUDA devices")
     import torch
     import torch.distributed as dist
     gpu = 0 if args.same_device else local_rank
     if world > 1:
         torch.cuda.set_device(gpu)
         if args.backend == "nccl":
+            # the communicator's own init line ("... nranks N ...") goes to stderr with the rest of NCCL's
+            # INIT log, so the job's rank count is on record beside the JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
         else:
             dist.init_process_group("gloo")
     try:
         run_ours(args, rank, world, gpu)
     finally:
-        if world > 1:
+        if world > 1 and dist.is_initialized():
             dist.destroy_process_group()
 
 

@@ -59,9 +59,6 @@ def parse():
                     help="process-group backend for the stats gather / time max (gloo: flow testing only)")
     ap.add_argument("--same-device", action="store_true",
                     help="every rank on cuda:0 (flow testing of the N>1 host path on a 1-GPU box; gloo only)")
-    ap.add_argument("--launch", default=None, help="threads,blocks_per_sm,vec,unroll (default: library default)")
-    ap.add_argument("--pdl", type=int, default=None, choices=[0, 1],
-                    help="programmatic dependent launch of the hot kernel (default: the library's)")
     return ap.parse_args()
 
 
@@ -450,7 +447,7 @@ def measure_nudft(dev, stream, reps=5):
     ws = torch.empty(sp.lib().sincos_nudft_workspace_bytes(nf, nt), dtype=torch.uint8, device=dev)
     res = {"workload": "C4 shape: 2^15 f x 2^15 t = 2^30 terms, complex64 amplitudes", "bound": "alu",
            "peak_ops_per_s": ALU_PEAK_OPS, "ops_per_term": NUDFT_OPS,
-           "kernel": "packed fp32 (FFMA2/FMUL2/FADD2, two frequencies per instruction) unless named scalar"}
+           "kernel": "packed fp32 (FFMA2/FMUL2/FADD2, two frequencies per instruction)"}
     ks = torch.arange(0, nf, nf // 16, device=dev)
     asum = float(a.abs().sum())
     for units, uname in ((sp.RADIANS, "radians"), (sp.TURNS, "turns")):
@@ -461,12 +458,9 @@ def measure_nudft(dev, stream, reps=5):
         p = (fd[ks, None] * td[None, :]).double()
         ang = p if units == sp.RADIANS else 2 * np.pi * (p - torch.round(p))
         ref = (a.to(torch.complex128)[None, :] * torch.exp(1j * ang)).sum(dim=1)
-        for v, vname in ((sp.NORMALIZED, "N"), (sp.RENORMALIZED, "A"), (sp.NORMALIZED, "N_scalar_kernel"),
-                         (sp.CMP_LIBM_SINCOSF, "cuda_sincosf"),
+        for v, vname in ((sp.NORMALIZED, "N"), (sp.RENORMALIZED, "A"), (sp.CMP_LIBM_SINCOSF, "cuda_sincosf"),
                          (sp.CMP_INTRINSIC_SINCOSF, "cuda___sincosf"), ("m132", "method_1dbl_deg3_2_angle")):
             kw = {"method": fit_method(1, 3, 2)} if v == "m132" else {"variant": v}
-            # the default kernels are packed fp32 (FFMA2); "N_scalar_kernel" is the scalar twin
-            sp.set_nudft_packed(vname != "N_scalar_kernel")
             sp.nudft(fd, td, a, out=out, units=units, workspace=ws, stream=stream, **kw)
             err = float((out[ks].to(torch.complex128) - ref).abs().max()) / asum
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -481,7 +475,6 @@ def measure_nudft(dev, stream, reps=5):
             if vname.startswith("N"):
                 r["alu_frac"] = terms * NUDFT_OPS[uname] / ALU_PEAK_OPS
             res[f"{uname}_{vname}"] = r
-    sp.set_nudft_packed(True)
     return res
 
 
@@ -537,10 +530,6 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     cdev = dev if args.backend == "nccl" else None      # where the collectives' tensors live
-    if args.launch:
-        sp.set_launch_config(*[int(x) for x in args.launch.split(",")])
-    if args.pdl is not None:
-        sp.set_pdl(bool(args.pdl))
     W = WORKLOADS[args.workload]
     if args.n and args.workload == "c2":
         W = type(W)(**{**W.__dict__, "n": args.n})
@@ -785,7 +774,7 @@ def run_ours(args, rank, world, local_rank):
                    "global_batch": units_all, "parallelism": f"dp{world} (contiguous shards, no collective)",
                    "l2": "inputs larger than L2 (4n B theta + 8n B outputs per launch vs 126 MB L2); no flush"
                          if 12 * n > (256 << 20) else "working set near/below L2 size: not an HBM measurement",
-                   "launch": sp.get_launch_config(), "cuda_graph": use_graph},
+                   "launch": sp.LAUNCH, "cuda_graph": use_graph},
         "hbm_GBps": BYTES_PER_PAIR * pairs_total / (ms_max / 1e3) / 1e9 / world,
         "roofline": roof,
         "cpu_baseline": cpu,

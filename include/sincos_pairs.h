@@ -64,7 +64,9 @@ typedef enum {
                                         form, unknown variant, misaligned (not 4-B) pointer  */
     SINCOS_ERR_OVERLAP = 2,          /* outputs overlap each other or the input (other than
                                         theta == sin_out or theta == cos_out exactly)        */
-    SINCOS_ERR_CUDA = 3              /* a CUDA call failed; see sincos_last_cuda_error()      */
+    SINCOS_ERR_CUDA = 3,             /* a CUDA call failed; see sincos_last_cuda_error()      */
+    SINCOS_ERR_NCCL = 4              /* an NCCL call failed (sincos_pairs_sharded_stats only);
+                                        see sincos_last_nccl_error()                         */
 } sincos_status_t;
 
 /*
@@ -82,10 +84,10 @@ typedef enum {
  * vector loads/stores (128-bit if they share only 16 B); otherwise, if the
  * outputs can still take whole-sector stores (split: sin and cos at one offset
  * mod 16 B; interleaved: 8-B aligned), theta is read as aligned vectors and
- * re-aligned in registers (warp shuffles; sincos_set_realign); otherwise the
- * outputs are re-aligned instead (theta's 256-bit frame, whole 32-B output blocks
- * from neighbouring lanes).  With re-alignment off: one element per thread.  A
- * scalar head and tail cover the ragged ends.
+ * re-aligned in registers (warp shuffles); otherwise the outputs are re-aligned
+ * instead (theta's 256-bit frame, whole 32-B output blocks from neighbouring lanes).
+ * A scalar head and tail cover the ragged ends.  The kernel configuration (block
+ * size, full grid, vector width) is fixed: there is no tuning state.
  * theta_dev == sin_dev or
  * theta_dev == cos_dev (exact in-place) is allowed.  Validation happens
  * before any CUDA call; the return value reports validation and the launch
@@ -98,8 +100,11 @@ SINCOS_API sincos_status_t sincos_pairs(const float *theta_dev, float *sin_dev, 
  * sincos_pairs_host -- the same computation on HOST buffers, end to end:
  * chunked host->device copies, the kernel and device->host copies pipelined
  * over three internal streams (created once per device), so the copy engines
- * run both directions while the kernel computes.  Synchronous: returns when
- * the outputs are in host memory.  Ordered after prior work on `stream`.
+ * run both directions while the kernel computes; chunks grow from 2^16 elements
+ * to the workspace's slot size, so the first device->host copy starts early.
+ * Synchronous: returns when the outputs are in host memory -- also on an error
+ * after work was queued (the internal streams are drained first, so nothing of
+ * the call still uses the caller's buffers).  Ordered after prior work on `stream`.
  * Concurrent calls from several host threads on one device are serialised
  * (the internal streams are shared); calls on different devices run in parallel.
  *
@@ -112,25 +117,6 @@ SINCOS_API sincos_status_t sincos_pairs_host(const float *theta_host, float *sin
 SINCOS_API size_t sincos_host_workspace_min_bytes(void);
 
 /*
- * sincos_pairs_batched -- many independent arrays in ONE kernel launch (serving many small
- * requests: below ~10^5 elements a launch per array is dominated by launch latency).
- * items: host array of `count` descriptors, each with the buffers and conventions of
- * sincos_pairs (split or interleaved, any 4-B alignment, exact in-place allowed); items must
- * not overlap one another.  The host validates every item (returning before any CUDA call on
- * the first invalid one) and launches one grid per 480 items, the item table travelling in
- * the kernel's parameter block (no workspace, no copy, asynchronous on `stream`; `items` may be
- * reused as soon as the call returns): each block finds its item and 1024-element chunk by
- * binary search.  Numerics identical to sincos_pairs.
- */
-typedef struct {
-    const float *theta_dev;
-    float *sin_dev, *cos_dev, *inter_dev;
-    uint64_t n;
-} sincos_item_t;
-SINCOS_API sincos_status_t sincos_pairs_batched(const sincos_item_t *items, int count, sincos_variant_t variant,
-                                                void *stream);
-
-/*
  * NEXT(4): other output dtypes and layout adapters.
  *
  * sincos_pairs_dtype: the hot path with the pair rounded once (to nearest even) from the
@@ -139,8 +125,8 @@ SINCOS_API sincos_status_t sincos_pairs_batched(const sincos_item_t *items, int 
  * uint16 arrays (split) or n {cos, sin} 16-bit pairs (interleaved); theta must not overlap
  * them.  Vector path (8 pairs per thread; 128-bit split / 256-bit interleaved stores) when
  * sin and cos share their offset mod 16 B (interleaved: always), theta read as one aligned
- * 256-bit vector or re-aligned in registers when it sits off the outputs' alignment
- * (sincos_set_realign); otherwise one element per thread; identical values.
+ * 256-bit vector or re-aligned in registers when it sits off the outputs' alignment;
+ * otherwise one element per thread; identical values.
  *
  * sincos_interleave / sincos_deinterleave: fp32 split (sin[], cos[]) <-> interleaved
  * ({cos, sin} float2) copies; no overlap allowed.
@@ -263,8 +249,15 @@ typedef struct {
     void *stream;            /* stream of that device (NULL = its legacy default) */
 } sincos_shard_t;
 
-/* Launch every shard on its own device (single process, many devices);
- * no data crosses devices.  Restores the caller's current device. */
+/* Launch every shard on its own device (single process, many devices); no data
+ * crosses devices.  Every shard is validated, and every device ordinal checked
+ * against cudaGetDeviceCount (else INVALID_ARGUMENT), before anything is launched.
+ * With shards on several devices, one host thread per device (created on first use,
+ * kept for the process) launches that device's shards, so the devices start together
+ * rather than one launch latency apart each; shards on one device launch in order from
+ * the calling thread.  Returns the first failing shard's status (its CUDA error in
+ * sincos_last_cuda_error of the calling thread); the other shards may have been
+ * launched.  The caller's current device is unchanged. */
 SINCOS_API sincos_status_t sincos_pairs_sharded(const sincos_shard_t *shards, int nshards,
                                      sincos_variant_t variant);
 
@@ -293,13 +286,19 @@ typedef struct {
  * each shard's error statistics (below) and kernel time (CUDA events around its launch)
  * into its 64-byte record, and all-gather the records over NCCL (ncclCommInitAll over the
  * shards' devices, ncclAllGather inside a group) -- the only collective of the path, 64 B
- * per rank.  gathered: host array of nshards records, shard order.  Synchronous.  NCCL is
- * bound at run time (dlopen "libnccl.so.2"); without it returns INVALID_ARGUMENT (see
- * sincos_nccl_available).  Allocates and frees small per-device buffers internally.
+ * per rank.  gathered: host array of nshards records, shard order.  Synchronous (every
+ * stream it used is drained before it returns, on success and on error).  NCCL is bound at
+ * run time (dlopen "libnccl.so.2"); without it returns INVALID_ARGUMENT (see
+ * sincos_nccl_available).  Device ordinals are checked before any launch.  The
+ * communicator and small per-device buffers (stats workspace, records, events) are created
+ * on the first call for a device list and kept for the process: later calls on the same
+ * devices reuse them.  A failing NCCL call returns SINCOS_ERR_NCCL (its ncclResult_t in
+ * sincos_last_nccl_error), a failing CUDA call SINCOS_ERR_CUDA.
  */
 SINCOS_API sincos_status_t sincos_pairs_sharded_stats(const sincos_shard_t *shards, int nshards,
                                                       sincos_variant_t variant, sincos_stats_t *gathered);
 SINCOS_API int sincos_nccl_available(void);
+SINCOS_API int sincos_last_nccl_error(void);     /* ncclResult_t of the last SINCOS_ERR_NCCL in this thread */
 
 SINCOS_API size_t sincos_stats_workspace_bytes(void);
 /* stats_dev: device pointer to one sincos_stats_t (8-B aligned); ws_dev: device workspace
@@ -308,42 +307,6 @@ SINCOS_API size_t sincos_stats_workspace_bytes(void);
 SINCOS_API sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
                                    const float *cos_dev, const float *inter_dev, size_t n,
                                    sincos_stats_t *stats_dev, void *ws_dev, void *stream);
-
-/* Launch tuning (bench / tests).  threads per block (128, 256, 512);
- * blocks_per_sm: 0 = the full grid, one trip per thread (the default, measured
- * fastest); > 0 = a grid-stride grid of SMs x blocks_per_sm blocks; vec: floats per thread access (4 = 128-bit, 8 = 256-bit);
- * unroll U (1, 2, 4 independent vectors in flight per thread: the GPU form of
- * "computes two vectors at a time"); prefetch (0/1): software-
- * pipelined loads (the next trip's loads issued before this trip's math).
- * Process-global; returns -1 for unsupported values. */
-SINCOS_API int sincos_set_launch_config(int threads, int blocks_per_sm, int vec, int unroll, int prefetch);
-/* Defaults: threads 128, blocks_per_sm 0, vec 8, unroll 1, prefetch 0. */
-SINCOS_API void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *vec, int *unroll,
-                                         int *prefetch);
-
-/* Unshared alignment (theta and the outputs at different offsets mod 16 B): 1 = keep the
- * outputs' 128-bit stores and re-align theta in registers with warp shuffles (the default),
- * 0 = one element per thread, 2 = re-alignment in its 128-bit form only (A/B), 3 = as 1 but
- * sincos_phase_grid's ragged rows through the flat path instead of the row / short-row
- * paths (A/B).
- * Identical results.  0 also turns off sincos_phase_grid's row and flat paths for rows that
- * are not whole 256-bit vectors.  Process-global; returns the previous setting, or -1 for a
- * value other than 0..3. */
-SINCOS_API int sincos_set_realign(int on);
-
-/* Programmatic dependent launch of the hot kernel (bench / tests): 1 = on (the default) --
- * back-to-back launches on a stream overlap their launch latency and block scheduling, the
- * kernel waiting (griddepcontrol.wait) for the previous kernel's completion before it touches
- * memory, so stream order is unchanged; 0 = plain launches.  Process-global; returns the
- * previous setting, or -1 for a value other than 0/1. */
-SINCOS_API int sincos_set_pdl(int on);
-
-/* Fused-sum kernel form (bench / tests): 1 = packed fp32 (sm_100a FFMA2/FMUL2/FADD2,
- * two frequencies per instruction; the default), 0 = scalar fp32.  Both are
- * bit-identical (each packed lane rounds as the scalar instruction does); applies to
- * variants 0/1 and every method (specialised and general shapes).  Process-global; returns the previous
- * setting, or -1 for a value other than 0/1. */
-SINCOS_API int sincos_set_nudft_packed(int on);
 
 /* Traffic-ceiling kernel (bench only): same access pattern and launch as
  * sincos_pairs, no arithmetic (writes theta to both outputs). */

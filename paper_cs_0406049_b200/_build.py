@@ -17,6 +17,10 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsincos_pairs.so")
+# the A/B build: the same sources with -DSINCOS_AB (settable kernel forms, csrc/sincos_ab.h);
+# loaded by tests/ and tools/ only, never by the product binding
+AB_LIB = os.path.join(PKG, "libsincos_pairs_ab.so")
+AB_FLAGS = ("-DSINCOS_AB",)
 HEADER = os.path.join(ROOT, "include", "sincos_pairs.h")
 
 NVCC_FLAGS = [
@@ -32,11 +36,11 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
     deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + [HEADER]
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -53,8 +57,8 @@ def build(force: bool = False, verbose: bool = False, extra_flags=(), out: str |
     library (cudart static).  extra_flags: e.g. -D switches for A/B builds; out: another path;
     link_flags: extra flags for the link step (e.g. sanitizer runtimes)."""
     out = out or LIB
-    if out == LIB and not force and not _stale():
-        return LIB
+    if out in (LIB, AB_LIB) and not force and not _stale(out):
+        return out
     import tempfile
     from concurrent.futures import ThreadPoolExecutor
     compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-cudart", "static")]
@@ -77,6 +81,13 @@ def build(force: bool = False, verbose: bool = False, extra_flags=(), out: str |
     return out
 
 
+def build_ab(force: bool = False) -> str:
+    """libsincos_pairs_ab.so (tests and tools only)."""
+    return build(force=force, extra_flags=AB_FLAGS, out=AB_LIB)
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(LIB)
+    if "--ab" in sys.argv:
+        print(build_ab(force="--force" in sys.argv))

@@ -1,20 +1,29 @@
 // sincos_abi.cu -- the extern "C" boundary of libsincos_pairs.so (include/sincos_pairs.h).
 //
 // Validation (no CUDA call on any error path), path selection (256-bit / 128-bit
-// vector body with a scalar head and tail, or the scalar kernel for pointers
-// that do not share an alignment), grid sizing (grid-stride, a multiple of the
-// SM count: SMs x resident blocks per SM), the pipelined host-buffer path, and
-// the single-process multi-device sharder.
+// vector body with a scalar head and tail; register re-alignment for pointers
+// that do not share an alignment), grid sizing, the pipelined host-buffer path,
+// and the single-process multi-device sharder (one host thread per device).
+// The kernel configuration is fixed (sincos_launch.h Tuning); the A/B build
+// (-DSINCOS_AB) adds the settable alternatives and sincos_pairs_batched.
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <functional>
 #include <mutex>
+#include <thread>
 #include <vector>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../../include/sincos_pairs.h"
 #include "sincos_launch.h"
+#ifdef SINCOS_AB
+#include "sincos_ab.h"
+#endif
 #include "sincos_method.cuh"
 #include "sincos_realign.cuh"
 
@@ -24,16 +33,6 @@ namespace {
 
 thread_local int g_last_cuda_error = 0;
 std::atomic<uint64_t> g_launches{0};
-
-std::atomic<int> g_threads{128};
-std::atomic<int> g_blocks_per_sm{0};
-std::atomic<int> g_vec{8};
-std::atomic<int> g_unroll{1};
-std::atomic<int> g_prefetch{0};
-std::atomic<int> g_shift{1};          // KB3b re-aligning path for unshared alignment (1 = on)
-std::atomic<int> g_phase_flat{1};
-std::atomic<int> g_phase_rows{1};   // 0 (sincos_set_realign(3), A/B): ragged phase rows via the flat kernel
-std::atomic<int> g_shift8{1};         // KB3b in its 256-bit form where the outputs allow it     // NEXT(1) flat path for rows that are not whole 256-bit vectors
 
 constexpr int kMaxDev = 64;
 std::atomic<int> g_sm_count[kMaxDev];
@@ -98,42 +97,29 @@ unsigned grid_for(size_t units, size_t per_block, int sms, int cfg_bps) {
     return static_cast<unsigned>(need);
 }
 
-// Launch on already-validated arguments, n > 0.  pf_mode: -1 = the configured mode.
+// Launch on already-validated arguments, n > 0.
 // Path, first that applies (identical numerics on every path):
-//   TMA pipeline (pf_mode 2, experimental) ->
 //   KB1/KB2 vector kernel (theta and outputs share a 32-B / 16-B alignment after a head) ->
 //   KB3b  theta re-aligned (split sin/cos share an offset mod 16 B; interleaved 8-B aligned) ->
-//   KB3c  outputs re-aligned (everything else) -> KB3 one element per thread (re-alignment off).
+//   KB3c  outputs re-aligned (everything else).
+// (A/B build, realign = 0: KB3, one element per thread, instead of KB3b/KB3c.)
 sincos_status_t launch(const float *theta, float *so, float *co, float *io, size_t n, int variant,
-                       cudaStream_t stream, int pf_mode = -1) {
+                       cudaStream_t stream) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e);
+    const Tuning T = tuning();
     const int sms = sm_count(dev);
     const bool inter = io != nullptr;
     const bool nc = !(theta == so || theta == co);
-    const int threads = g_threads.load(std::memory_order_relaxed);
-    const int cfg_bps = g_blocks_per_sm.load(std::memory_order_relaxed);
-    const int unroll = g_unroll.load(std::memory_order_relaxed);
-    if (pf_mode < 0) pf_mode = g_prefetch.load(std::memory_order_relaxed);
-    const bool pf = pf_mode == 1;
-
-    // Mode 2: persistent TMA bulk-load pipeline over whole tiles, the rest by the vector kernel.
-    if (pf_mode == 2 && variant != 2 && nc && aligned(theta, 32) &&
-        (inter ? aligned(io, 32) : aligned(so, 32) && aligned(co, 32))) {
-        size_t done = 0;
-        e = launch_tma(variant, inter, static_cast<unsigned>(sms) * 4, theta, so, co, io, n, &done, stream);
-        if (e != cudaSuccess) return cuda_fail(e);
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        if (done == n) return SINCOS_OK;
-        return launch(theta + done, so ? so + done : nullptr, co ? co + done : nullptr,
-                      io ? io + 2 * done : nullptr, n - done, variant, stream, 0);
-    }
+    const int threads = T.threads;
+    const int cfg_bps = T.blocks_per_sm;
+    const bool realign = T.realign != 0;
 
     // Widest vector whose alignment theta and the outputs share after a scalar head.
     int w = 0;
     size_t head = 0;
-    for (int cand = g_vec.load(std::memory_order_relaxed); cand >= 4; cand /= 2) {
+    for (int cand = T.vec; cand >= 4; cand /= 2) {
         const uintptr_t A = 4u * cand;  // bytes of theta per access
         const uintptr_t t = reinterpret_cast<uintptr_t>(theta);
         const size_t h = ((A - (t & (A - 1))) & (A - 1)) / 4;
@@ -155,10 +141,10 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
     // interleaved outputs without the 256-bit path but 8-B aligned (its 256-bit store per four
     // pairs beats the 128-bit path's half-sector stores).
     size_t hs = SIZE_MAX;
-    if (g_shift.load(std::memory_order_relaxed)) {
+    if (realign) {
         if (inter) {
-            // (w == 4 with the default vec 8 only: a configured vec 4 keeps its 128-bit kernel)
-            if ((w == 0 || (w == 4 && g_vec.load(std::memory_order_relaxed) == 8)) && aligned(io, 8))
+            // (w == 4 with the default vec 8 only: an A/B vec 4 keeps its 128-bit kernel)
+            if ((w == 0 || (w == 4 && T.vec == 8)) && aligned(io, 8))
                 hs = ((32 - (reinterpret_cast<uintptr_t>(io) & 31)) & 31) / 8;
         } else if (w == 0 && ((reinterpret_cast<uintptr_t>(so) ^ reinterpret_cast<uintptr_t>(co)) & 15) == 0) {
             hs = ((16 - (reinterpret_cast<uintptr_t>(so) & 15)) & 15) / 4;
@@ -166,7 +152,8 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
     }
     // 256-bit form when the outputs take 256-bit stores at a common element (split: sin and cos
     // share their offset mod 32 B; interleaved: always, being 8-B aligned here)
-    if (hs != SIZE_MAX && g_shift8.load(std::memory_order_relaxed) &&
+    const bool shift8 = T.realign == 1 || T.realign == 3;
+    if (hs != SIZE_MAX && shift8 &&
         (inter || ((reinterpret_cast<uintptr_t>(so) ^ reinterpret_cast<uintptr_t>(co)) & 31) == 0)) {
         const size_t h0 = inter ? ((32 - (reinterpret_cast<uintptr_t>(io) & 31)) & 31) / 8
                                 : ((32 - (reinterpret_cast<uintptr_t>(so) & 31)) & 31) / 4;
@@ -193,7 +180,7 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
         if (k > 0) nvec = n + k >= hb + 4 ? (n + k - hb - 4) / 4 : 0;
         e = launch_shift(variant, inter, k, grid_for(nvec, threads, sms, cfg_bps), threads, theta, so, co, io, hb,
                          nvec, n, stream);
-    } else if (w == 0 && g_shift.load(std::memory_order_relaxed)) {
+    } else if (w == 0 && realign) {
         // KB3c: theta's frame, outputs re-aligned (sin and cos apart mod 16 B; pairs only 4-B aligned)
         const uintptr_t ta = reinterpret_cast<uintptr_t>(theta);
         size_t hb = ((32 - (ta & 31)) & 31) / 4;
@@ -209,17 +196,22 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
         e = launch_outshift(variant, inter, ks, kc, grid_for(nvec, threads, sms, cfg_bps), threads, theta, so, co,
                             io, hb, nvec, n, stream);
     } else if (w == 0) {
+#ifdef SINCOS_AB
         const unsigned grid = static_cast<unsigned>(
             (n + threads - 1) / threads < static_cast<size_t>(sms) * 8 ? (n + threads - 1) / threads : sms * 8);
         e = launch_scalar(variant, inter, grid, threads, theta, so, co, io, n, stream);
+#else
+        return SINCOS_ERR_INVALID_ARGUMENT;          // unreachable: the product always re-aligns
+#endif
     } else {
         if (head > n) head = n;
         const size_t nvec = (n - head) / w;
         // Default (blocks_per_sm == 0): the full grid, one trip of `unroll` vectors per thread --
-        // measured fastest on B200.  blocks_per_sm > 0: a grid-stride grid of
-        // SMs x blocks_per_sm blocks.
-        const unsigned grid = grid_for(nvec, static_cast<size_t>(threads) * unroll, sms, cfg_bps);
-        e = launch_vec(variant, inter, w, unroll, nc, pf, grid, threads, theta, so, co, io, head, nvec, n, stream);
+        // measured fastest on B200.  blocks_per_sm > 0 (A/B): a grid-stride
+        // grid of SMs x blocks_per_sm blocks.
+        const unsigned grid = grid_for(nvec, static_cast<size_t>(threads) * T.unroll, sms, cfg_bps);
+        e = launch_vec(variant, inter, w, T.unroll, nc, T.prefetch == 1, T.pdl != 0, grid, threads, theta, so, co,
+                       io, head, nvec, n, stream);
     }
     if (e != cudaSuccess) return cuda_fail(e);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -261,7 +253,82 @@ cudaError_t dev_streams(int dev, DevStreams **out) {
     return cudaSuccess;
 }
 
+// ---- one host thread per device (sincos_pairs_sharded) ---------------------------------
+// Workers are created on first use and live for the process (heap objects never destroyed,
+// so no static destructor races a worker at exit); each runs the jobs posted to it in order.
+struct Latch {
+    explicit Latch(int n) : left(n) {}
+    void count_down() {
+        std::lock_guard<std::mutex> lk(mu);
+        if (--left == 0) cv.notify_all();
+    }
+    void wait() {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return left == 0; });
+    }
+    std::mutex mu;
+    std::condition_variable cv;
+    int left;
+};
+
+class DeviceWorker {
+  public:
+    explicit DeviceWorker(int dev) : dev_(dev), th_([this] { run(); }) { th_.detach(); }
+    void post(std::function<void()> job) {
+        std::lock_guard<std::mutex> lk(mu_);
+        q_.push_back(std::move(job));
+        cv_.notify_one();
+    }
+
+  private:
+    void run() {
+        cudaSetDevice(dev_);
+        for (;;) {
+            std::function<void()> job;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return !q_.empty(); });
+                job = std::move(q_.front());
+                q_.pop_front();
+            }
+            job();
+        }
+    }
+    int dev_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> q_;
+    std::thread th_;
+};
+
+std::mutex g_worker_mu;
+DeviceWorker *g_workers[kMaxDev] = {};
+
+DeviceWorker *device_worker(int dev) {
+    std::lock_guard<std::mutex> lk(g_worker_mu);
+    if (g_workers[dev] == nullptr) g_workers[dev] = new DeviceWorker(dev);
+    return g_workers[dev];
+}
+
 }  // namespace
+
+#ifdef SINCOS_AB
+extern "C" int sincos_ab_get(int knob);
+namespace sincos_b200 {
+Tuning tuning() {
+    Tuning t;
+    t.threads = sincos_ab_get(SINCOS_AB_THREADS);
+    t.blocks_per_sm = sincos_ab_get(SINCOS_AB_BLOCKS_PER_SM);
+    t.vec = sincos_ab_get(SINCOS_AB_VEC);
+    t.unroll = sincos_ab_get(SINCOS_AB_UNROLL);
+    t.prefetch = sincos_ab_get(SINCOS_AB_PREFETCH);
+    t.realign = sincos_ab_get(SINCOS_AB_REALIGN);
+    t.pdl = sincos_ab_get(SINCOS_AB_PDL);
+    t.nudft_packed = sincos_ab_get(SINCOS_AB_NUDFT_PACKED);
+    return t;
+}
+}  // namespace sincos_b200
+#endif
 
 extern "C" {
 
@@ -331,9 +398,10 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
     // n < 2^52); else one per thread
     const uintptr_t so_a = reinterpret_cast<uintptr_t>(sin_dev), co_a = reinterpret_cast<uintptr_t>(cos_dev),
                     io_a = reinterpret_cast<uintptr_t>(inter_dev);
-    const bool flat = !vec && g_phase_flat.load(std::memory_order_relaxed) && n < (size_t(1) << 52) &&
+    const Tuning T = tuning();
+    const bool flat = !vec && T.realign != 0 && n < (size_t(1) << 52) &&
                       (split ? ((so_a ^ co_a) & 31) == 0 : aligned(inter_dev, 8));
-    if (flat && nt >= kPhaseRowsMinNt && g_phase_rows.load(std::memory_order_relaxed)) {
+    if (flat && nt >= kPhaseRowsMinNt && T.realign != 3) {
         const unsigned h0 = static_cast<unsigned>(split ? ((32 - (so_a & 31)) & 31) / 4 : ((32 - (io_a & 31)) & 31) / 8);
         int dev = 0;
         if ((e = cudaGetDevice(&dev)) != cudaSuccess) return cuda_fail(e);
@@ -348,7 +416,7 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
         size_t grid = (nvec + 127) / 128;
         if (grid < 1) grid = 1;
         if (grid > 0x7FFFFFFFu) grid = 0x7FFFFFFFu;
-        const bool short_rows = g_phase_rows.load(std::memory_order_relaxed) != 0 && nt < kPhaseRowsMinNt;
+        const bool short_rows = T.realign != 3 && nt < kPhaseRowsMinNt;
         // the short-row kernel stages t in shared memory once per block: a grid of a few
         // blocks per SM, grid-striding, amortises that
         const size_t cap = static_cast<size_t>(sm_count(dev)) * kPhaseShortBlocksPerSm;
@@ -397,7 +465,7 @@ sincos_status_t sincos_pairs_dtype(const float *theta_dev, void *sin_dev, void *
     size_t head = 0, nvec = 0;
     if (vec) {
         realign_plan(theta_dev, n, h0, &k, &head, &nvec);
-        if (k != 0 && !g_shift.load(std::memory_order_relaxed)) vec = false;
+        if (k != 0 && tuning().realign == 0) vec = false;
     }
     if (!vec) head = nvec = 0, k = 0;
     // without the vector path every element is a "tail" element: one per thread
@@ -462,7 +530,7 @@ sincos_status_t sincos_pairs_method(const float *theta_dev, float *sin_dev, floa
     size_t head = 0, nvec = 0;
     if (vec) {
         realign_plan(theta_dev, n, h0, &k, &head, &nvec);
-        if (k != 0 && !g_shift.load(std::memory_order_relaxed)) vec = false;
+        if (k != 0 && tuning().realign == 0) vec = false;
     }
     if (!vec) head = nvec = 0, k = 0;
     size_t work = vec ? (nvec > 0 ? nvec : 1) : n;
@@ -522,7 +590,8 @@ sincos_status_t nudft_impl(const float *f_dev, size_t nf, const float *t_dev, co
     if (variant == 5) mp = make_params(m->ss, m->n_ss, m->cc, m->n_cc, m->doublings);
     cudaError_t e = launch_nudft(variant, units == SINCOS_TURNS, f_dev, nf, t_dev, a_dev, nt, out_dev, ws_dev, s,
                                  variant == 5 ? &mp : nullptr, variant == 5 && (m->n_ss > 4 || m->n_cc > 4) ? 8 : 4,
-                                 variant == 5 ? m->fix : 0, variant == 5 ? method_spec(m) : -1);
+                                 variant == 5 ? m->fix : 0, variant == 5 ? method_spec(m) : -1,
+                                 tuning().nudft_packed != 0);
     if (e != cudaSuccess) return cuda_fail(e);
     g_launches.fetch_add(2, std::memory_order_relaxed);
     return SINCOS_OK;
@@ -560,8 +629,8 @@ sincos_status_t sincos_pairs_host(const float *theta_host, float *sin_host, floa
 
     std::lock_guard<std::mutex> call_lock(ds->busy);   // reentrancy (header: thread-safe)
 
-    // chunk elements per slot, a multiple of 64 so every slot buffer stays 256-B aligned
-    size_t chunk = (ws_bytes / (kSlots * 12)) & ~size_t(63);
+    // slot capacity in elements, a multiple of 64 so every slot buffer stays 256-B aligned
+    const size_t cap = (ws_bytes / (kSlots * 12)) & ~size_t(63);
     const bool inter = inter_host != nullptr;
     char *ws = static_cast<char *>(dev_ws);
     cudaStream_t caller = static_cast<cudaStream_t>(stream);
@@ -570,35 +639,47 @@ sincos_status_t sincos_pairs_host(const float *theta_host, float *sin_host, floa
     for (int k = 0; k < kSlots; ++k)
         if ((e = cudaStreamWaitEvent(ds->s[k], ds->start, 0)) != cudaSuccess) return cuda_fail(e);
 
+    // From here on work may be queued on the slot streams: every exit drains them first, so no
+    // copy or kernel of this call is still using the caller's buffers when it returns.
+    auto drain = [&](sincos_status_t s) {
+        for (int k = 0; k < kSlots; ++k) cudaStreamSynchronize(ds->s[k]);
+        return s;
+    };
+    // Chunk sizes ramp up from kMinChunk, doubling to the slot capacity: the first device->host
+    // copy starts after a short first chunk, not after a whole slot's copy and kernel (the fill
+    // of the pipeline; its drain is the last chunk's device->host copy either way).
+    size_t chunk = kMinChunk < cap ? kMinChunk : cap;
     size_t j = 0;
     for (size_t off = 0; off < n; off += chunk, ++j) {
+        if (j > 0 && chunk < cap) chunk = 2 * chunk < cap ? 2 * chunk : cap;
         const size_t m = n - off < chunk ? n - off : chunk;
         const int k = static_cast<int>(j % kSlots);
         cudaStream_t s = ds->s[k];
-        float *th = reinterpret_cast<float *>(ws + k * chunk * 12);
-        float *o1 = th + chunk;      // sin, or interleaved pairs
-        float *o2 = o1 + chunk;      // cos
+        float *th = reinterpret_cast<float *>(ws + k * cap * 12);
+        float *o1 = th + cap;        // sin, or interleaved pairs
+        float *o2 = o1 + cap;        // cos
         if ((e = cudaMemcpyAsync(th, theta_host + off, 4 * m, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-            return cuda_fail(e);
+            return drain(cuda_fail(e));
         st = inter ? launch(th, nullptr, nullptr, o1, m, variant, s) : launch(th, o1, o2, nullptr, m, variant, s);
-        if (st != SINCOS_OK) return st;
+        if (st != SINCOS_OK) return drain(st);
         if (inter) {
             if ((e = cudaMemcpyAsync(inter_host + 2 * off, o1, 8 * m, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-                return cuda_fail(e);
+                return drain(cuda_fail(e));
         } else {
             if ((e = cudaMemcpyAsync(sin_host + off, o1, 4 * m, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-                return cuda_fail(e);
+                return drain(cuda_fail(e));
             if ((e = cudaMemcpyAsync(cos_host + off, o2, 4 * m, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-                return cuda_fail(e);
+                return drain(cuda_fail(e));
         }
     }
     for (int k = 0; k < kSlots; ++k) {
-        if ((e = cudaEventRecord(ds->done[k], ds->s[k])) != cudaSuccess) return cuda_fail(e);
-        if ((e = cudaStreamWaitEvent(caller, ds->done[k], 0)) != cudaSuccess) return cuda_fail(e);
+        if ((e = cudaEventRecord(ds->done[k], ds->s[k])) != cudaSuccess) return drain(cuda_fail(e));
+        if ((e = cudaStreamWaitEvent(caller, ds->done[k], 0)) != cudaSuccess) return drain(cuda_fail(e));
     }
+    sincos_status_t result = SINCOS_OK;
     for (int k = 0; k < kSlots; ++k)
-        if ((e = cudaStreamSynchronize(ds->s[k])) != cudaSuccess) return cuda_fail(e);
-    return SINCOS_OK;
+        if ((e = cudaStreamSynchronize(ds->s[k])) != cudaSuccess && result == SINCOS_OK) result = cuda_fail(e);
+    return result;
 }
 
 int sincos_shard_range(size_t n, int nshards, int g, size_t *lo, size_t *hi) {
@@ -622,22 +703,71 @@ sincos_status_t sincos_pairs_sharded(const sincos_shard_t *shards, int nshards, 
         sincos_status_t st = validate(sh.theta_dev, sh.sin_dev, sh.cos_dev, sh.inter_dev, sh.n, variant, false);
         if (st != SINCOS_OK) return st;
     }
-    int prev = 0;
-    cudaError_t e = cudaGetDevice(&prev);
+    if (nshards == 0) return SINCOS_OK;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess) return cuda_fail(e);
-    sincos_status_t result = SINCOS_OK;
-    for (int g = 0; g < nshards && result == SINCOS_OK; ++g) {
-        const sincos_shard_t &sh = shards[g];
-        if (sh.n == 0) continue;
-        if ((e = cudaSetDevice(sh.device)) != cudaSuccess) {
-            result = cuda_fail(e);
-            break;
+    for (int g = 0; g < nshards; ++g)
+        if (shards[g].device < 0 || shards[g].device >= ndev || shards[g].device >= kMaxDev)
+            return SINCOS_ERR_INVALID_ARGUMENT;                        // before anything is launched
+    // the shards of each device, in shard order
+    std::vector<int> devs;
+    std::vector<std::vector<int>> of;
+    for (int g = 0; g < nshards; ++g) {
+        if (shards[g].n == 0) continue;
+        size_t i = 0;
+        while (i < devs.size() && devs[i] != shards[g].device) ++i;
+        if (i == devs.size()) {
+            devs.push_back(shards[g].device);
+            of.emplace_back();
         }
-        result = launch(sh.theta_dev, sh.sin_dev, sh.cos_dev, sh.inter_dev, sh.n, variant,
-                        static_cast<cudaStream_t>(sh.stream));
+        of[i].push_back(g);
     }
-    cudaSetDevice(prev);
-    return result;
+    std::vector<sincos_status_t> st(nshards, SINCOS_OK);
+    std::vector<int> err(nshards, 0);
+    auto run_device = [&](size_t i) {          // on the device's worker thread (or inline)
+        cudaError_t ce = cudaSetDevice(devs[i]);
+        for (int g : of[i]) {
+            const sincos_shard_t &sh = shards[g];
+            if (ce != cudaSuccess) {
+                st[g] = SINCOS_ERR_CUDA;
+                err[g] = static_cast<int>(ce);
+                continue;
+            }
+            st[g] = launch(sh.theta_dev, sh.sin_dev, sh.cos_dev, sh.inter_dev, sh.n, variant,
+                           static_cast<cudaStream_t>(sh.stream));
+            err[g] = st[g] == SINCOS_ERR_CUDA ? g_last_cuda_error : 0;
+        }
+    };
+    // SINCOS_SHARDED_WORKERS=1 (test hook, read once): the worker threads even for one device,
+    // so a one-GPU box exercises the multi-device launch machinery too
+    static const bool force_workers = [] {
+        const char *v = getenv("SINCOS_SHARDED_WORKERS");
+        return v != nullptr && v[0] == '1';
+    }();
+    if (devs.size() <= 1 && !(force_workers && !devs.empty())) {
+        // one device: launch from the calling thread, keeping its current device
+        int prev = 0;
+        if ((e = cudaGetDevice(&prev)) != cudaSuccess) return cuda_fail(e);
+        if (!devs.empty()) run_device(0);
+        cudaSetDevice(prev);
+    } else {
+        // several devices: one host thread per device launches its shards, so the devices
+        // start together instead of one launch latency apart each (launch skew)
+        Latch latch(static_cast<int>(devs.size()));
+        for (size_t i = 0; i < devs.size(); ++i)
+            device_worker(devs[i])->post([&, i] {
+                run_device(i);
+                latch.count_down();
+            });
+        latch.wait();
+    }
+    for (int g = 0; g < nshards; ++g)          // the first failing shard's status (and CUDA error)
+        if (st[g] != SINCOS_OK) {
+            if (st[g] == SINCOS_ERR_CUDA) g_last_cuda_error = err[g];
+            return st[g];
+        }
+    return SINCOS_OK;
 }
 
 size_t sincos_stats_workspace_bytes(void) { return stats_ws_bytes(); }
@@ -661,6 +791,8 @@ sincos_status_t sincos_error_stats(const float *theta_dev, const float *sin_dev,
     return SINCOS_OK;
 }
 
+#ifdef SINCOS_AB
+// ---- A/B build only (csrc/sincos_ab.h) -------------------------------------------------
 sincos_status_t sincos_pairs_batched(const sincos_item_t *items, int count, sincos_variant_t variant,
                                      void *stream) {
     if (count < 0 || (count > 0 && items == nullptr)) return SINCOS_ERR_INVALID_ARGUMENT;
@@ -711,47 +843,30 @@ sincos_status_t sincos_pairs_batched(const sincos_item_t *items, int count, sinc
     return SINCOS_OK;
 }
 
-int sincos_set_pdl(int on) { return set_pdl(on); }
+namespace {
+std::atomic<int> g_ab[SINCOS_AB_KNOBS] = {{128}, {0}, {8}, {1}, {0}, {1}, {1}, {1}};
+bool ab_ok(int knob, int v) {
+    switch (knob) {
+    case SINCOS_AB_THREADS: return v == 128 || v == 256 || v == 512;
+    case SINCOS_AB_BLOCKS_PER_SM: return v >= 0 && v <= 4096;
+    case SINCOS_AB_VEC: return v == 4 || v == 8;
+    case SINCOS_AB_UNROLL: return v == 1 || v == 2 || v == 4;
+    case SINCOS_AB_PREFETCH: return v == 0 || v == 1;
+    case SINCOS_AB_REALIGN: return v >= 0 && v <= 3;
+    case SINCOS_AB_PDL: return v == 0 || v == 1;
+    case SINCOS_AB_NUDFT_PACKED: return v == 0 || v == 1;
+    default: return false;
+    }
+}
+}  // namespace
 
-int sincos_set_realign(int on) {
-    if (on < 0 || on > 3) return -1;
-    const int prev = g_shift.load(std::memory_order_relaxed) == 0        ? 0
-                     : !g_phase_rows.load(std::memory_order_relaxed)     ? 3
-                     : g_shift8.load(std::memory_order_relaxed)          ? 1
-                                                                         : 2;
-    g_shift.store(on != 0, std::memory_order_relaxed);
-    g_shift8.store(on == 1 || on == 3, std::memory_order_relaxed);
-    g_phase_flat.store(on != 0, std::memory_order_relaxed);
-    g_phase_rows.store(on != 3, std::memory_order_relaxed);
-    return prev;
+int sincos_ab_set(int knob, int value) {
+    if (!ab_ok(knob, value)) return -1;
+    return g_ab[knob].exchange(value);
 }
 
-int sincos_set_nudft_packed(int on) {
-    const int prev = get_nudft_packed();
-    return set_nudft_packed(on) == 0 ? prev : -1;
-}
-
-int sincos_set_launch_config(int threads, int blocks_per_sm, int vec, int unroll, int prefetch) {
-    if (!(threads == 128 || threads == 256 || threads == 512)) return -1;
-    if (blocks_per_sm < 0 || blocks_per_sm > 4096) return -1;
-    if (prefetch < 0 || prefetch > 2) return -1;
-    if (!(vec == 4 || vec == 8)) return -1;
-    if (!(unroll == 1 || unroll == 2 || unroll == 4)) return -1;
-    g_threads.store(threads);
-    g_blocks_per_sm.store(blocks_per_sm);
-    g_vec.store(vec);
-    g_unroll.store(unroll);
-    g_prefetch.store(prefetch);
-    return 0;
-}
-
-void sincos_get_launch_config(int *threads, int *blocks_per_sm, int *vec, int *unroll, int *prefetch) {
-    if (prefetch) *prefetch = g_prefetch.load();
-    if (threads) *threads = g_threads.load();
-    if (blocks_per_sm) *blocks_per_sm = g_blocks_per_sm.load();
-    if (vec) *vec = g_vec.load();
-    if (unroll) *unroll = g_unroll.load();
-}
+int sincos_ab_get(int knob) { return knob >= 0 && knob < SINCOS_AB_KNOBS ? g_ab[knob].load() : -1; }
+#endif  // SINCOS_AB
 
 sincos_status_t sincos_debug_packed_check(int variant, const sincos_method_t *method,
                                           unsigned long long *mismatch_dev, void *stream) {
@@ -803,6 +918,7 @@ const char *sincos_status_string(sincos_status_t s) {
     case SINCOS_ERR_INVALID_ARGUMENT: return "invalid argument";
     case SINCOS_ERR_OVERLAP: return "output buffers overlap each other or the input";
     case SINCOS_ERR_CUDA: return "CUDA error (see sincos_last_cuda_error)";
+    case SINCOS_ERR_NCCL: return "NCCL error (see sincos_last_nccl_error)";
     default: return "unknown status";
     }
 }

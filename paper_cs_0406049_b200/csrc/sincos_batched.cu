@@ -10,12 +10,16 @@
 // per-element method (sincos_math.cuh) on its chunk: 256-bit loads and stores when the item's
 // theta and outputs share their alignment, one element per thread otherwise.  Numerics
 // identical to sincos_pairs.
+//
+// Not part of the product library (SURVEY 8 does not list it): compiled into the A/B build
+// (-DSINCOS_AB, libsincos_pairs_ab.so) only.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "sincos_launch.h"
 #include "sincos_math.cuh"
 
+#ifdef SINCOS_AB
 namespace sincos_b200 {
 
 constexpr int kBatchThreads = 128;
@@ -129,3 +133,4 @@ uint64_t batched_chunks(uint64_t n, uint64_t head, bool vec) {
 }
 
 }  // namespace sincos_b200
+#endif  // SINCOS_AB

@@ -11,7 +11,7 @@
 //          The scalar head (to reach alignment) and tail (n mod W) are done by
 //          the first threads of the grid with the same math.
 // KB3      sincos_scalar_kernel<V, INTER>: any 4-B alignment, one element per
-//          thread, identical numerics.
+//          thread, identical numerics (A/B build only: the product re-aligns instead).
 // KB4      V = kNull: the traffic ceiling (same access pattern, no math).
 // KB5      sincos_stats_kernel: fp64 error statistics (verification only).
 //
@@ -178,18 +178,30 @@ __global__ void __launch_bounds__(512) rcp_kernel(const float *d, float *out, si
 using VecFn = void (*)(const float *, float *, float *, float *, size_t, size_t, size_t);
 using ScalarFn = void (*)(const float *, float *, float *, float *, size_t);
 
+// The product instantiates U = 1 without software prefetch only (measured best, DESIGN.md
+// section 5); the A/B build adds U = 2, 4 and the prefetching forms.
 template <int V, bool INTER, int W, bool NC, bool PF>
 static VecFn pick_u(int unroll) {
+#ifdef SINCOS_AB
     switch (unroll) {
     case 1: return sincos_vec_kernel<V, INTER, W, 1, NC, PF>;
     case 2: return sincos_vec_kernel<V, INTER, W, 2, NC, PF>;
     default: return sincos_vec_kernel<V, INTER, W, 4, NC, PF>;
     }
+#else
+    (void)unroll;
+    return sincos_vec_kernel<V, INTER, W, 1, NC, false>;
+#endif
 }
 
 template <int V, bool INTER, int W, bool NC>
 static VecFn pick_pf(int unroll, bool pf) {
+#ifdef SINCOS_AB
     return pf ? pick_u<V, INTER, W, NC, true>(unroll) : pick_u<V, INTER, W, NC, false>(unroll);
+#else
+    (void)pf;
+    return pick_u<V, INTER, W, NC, false>(unroll);
+#endif
 }
 
 template <int V, bool INTER>
@@ -211,6 +223,7 @@ VecFn vec_kernel(int variant, bool inter, int w, int unroll, bool nc, bool pf) {
     }
 }
 
+#ifdef SINCOS_AB
 ScalarFn scalar_kernel(int variant, bool inter) {
     switch (variant) {
     case kNormalized: return inter ? sincos_scalar_kernel<kNormalized, true> : sincos_scalar_kernel<kNormalized, false>;
@@ -219,15 +232,9 @@ ScalarFn scalar_kernel(int variant, bool inter) {
     }
 }
 
-static int g_pdl = 1;   // programmatic dependent launch of the vector kernel (see pdl_enter)
-int set_pdl(int on) {
-    if (on != 0 && on != 1) return -1;
-    const int prev = g_pdl;
-    g_pdl = on;
-    return prev;
-}
+#endif  // SINCOS_AB
 
-cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, bool pf, unsigned grid,
+cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, bool pf, bool pdl, unsigned grid,
                        unsigned threads, const float *theta, float *so, float *co, float *io, size_t head,
                        size_t nvec, size_t n, cudaStream_t stream) {
     VecFn fn = vec_kernel(variant, inter, w, unroll, nc, pf);
@@ -235,7 +242,7 @@ cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, bool
     // inside a CUDA graph capture the plain launch is kept: graph replay already removes the
     // launch latency, and the programmatic edges measured slower for small graphed kernels
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (!g_pdl || w != 8 || cudaStreamIsCapturing(stream, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+    if (!pdl || w != 8 || cudaStreamIsCapturing(stream, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
         return cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(threads), args, 0, stream);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -249,12 +256,14 @@ cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, bool
     return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(fn), args);
 }
 
+#ifdef SINCOS_AB
 cudaError_t launch_scalar(int variant, bool inter, unsigned grid, unsigned threads, const float *theta, float *so,
                           float *co, float *io, size_t n, cudaStream_t stream) {
     ScalarFn fn = scalar_kernel(variant, inter);
     void *args[] = {&theta, &so, &co, &io, &n};
     return cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(threads), args, 0, stream);
 }
+#endif
 
 template <int V, bool INTER>
 static VecFn pick_shift(int k) {
@@ -296,10 +305,6 @@ cudaError_t launch_compare(int which, bool inter, unsigned grid, unsigned thread
     size_t head = 0;
     void *args[] = {&theta, &so, &co, &io, &head, &nvec, &n};
     return cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(threads), args, 0, stream);
-}
-
-const void *vec_kernel_ptr(int variant, bool inter, int w, int unroll, bool nc, bool pf) {
-    return reinterpret_cast<const void *>(vec_kernel(variant, inter, w, unroll, nc, pf));
 }
 
 }  // namespace sincos_b200

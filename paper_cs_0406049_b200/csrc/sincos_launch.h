@@ -9,10 +9,33 @@
 
 namespace sincos_b200 {
 
+// Kernel selection.  The product library has ONE configuration: these defaults, the one every
+// measurement in DESIGN.md was taken with (a sweep on the B200 found them best, section 5), and
+// nothing in it is settable -- no process-global state changes what another caller gets.  The
+// A/B build (-DSINCOS_AB -> libsincos_pairs_ab.so, loaded only by tests/ and tools/) makes each
+// field settable through sincos_ab_set (csrc/sincos_ab.h) to measure the alternatives.
+struct Tuning {
+    int threads = 128;       // threads per block of the streaming kernels (128, 256, 512)
+    int blocks_per_sm = 0;   // 0: the full grid, one trip per thread; > 0: grid-stride, SMs x this
+    int vec = 8;             // floats per thread access: 8 (256-bit) or 4 (128-bit)
+    int unroll = 1;          // independent vectors per thread and trip (1, 2, 4)
+    int prefetch = 0;        // 1: software-pipelined loads (trip k+1 in flight while trip k computes)
+    int realign = 1;         // 1: register re-alignment of unshared alignments; 0: one element per
+                             // thread; 2: its 128-bit form only; 3: ragged phase rows via the flat kernel
+    int pdl = 1;             // programmatic dependent launch of the 256-bit vector kernel
+    int nudft_packed = 1;    // fused sum on packed fp32 (FFMA2) rather than its scalar twin
+};
+#ifdef SINCOS_AB
+Tuning tuning();                                         // sincos_abi.cu: the A/B settings
+#else
+__host__ inline constexpr Tuning tuning() { return Tuning{}; }
+#endif
+
 // variant: 0 = N, 1 = A, 2 = null (traffic ceiling); w = 4 or 8 floats per access;
 // unroll = 1, 2 or 4; nc = read-only (non-coherent) loads, false when theta aliases an output.
-// pf = software-pipelined loads (trip k+1 in flight while trip k computes).
-cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, bool pf, unsigned grid,
+// pf = software-pipelined loads (trip k+1 in flight while trip k computes).  unroll != 1 and pf
+// exist in the A/B build only.  pdl: programmatic dependent launch (256-bit instances).
+cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, bool pf, bool pdl, unsigned grid,
                        unsigned threads, const float *theta, float *so, float *co, float *io, size_t head,
                        size_t nvec, size_t n, cudaStream_t stream);
 // Context kernels for the bench (3 = CUDA sincosf, 4 = __sincosf), 32-B aligned buffers, head 0.
@@ -30,6 +53,7 @@ cudaError_t launch_shift8(int variant, bool inter, int k, unsigned grid, unsigne
 cudaError_t launch_outshift(int variant, bool inter, int ks, int kc, unsigned grid, unsigned threads,
                             const float *theta, float *so, float *co, float *io, size_t head, size_t nvec, size_t n,
                             cudaStream_t stream);
+#ifdef SINCOS_AB
 // Many arrays in one launch (sincos_batched.cu): one record per item in device memory.
 struct BatchItem {
     const float *theta;
@@ -51,21 +75,18 @@ using BatchParams = BatchParamsT<kBatchMax>;
 static_assert(sizeof(BatchParams) <= 32764, "kernel parameter block limit");
 uint64_t batched_chunks(uint64_t n, uint64_t head, bool vec);
 cudaError_t launch_batched(int variant, const BatchParams &p, cudaStream_t stream);
-// Programmatic dependent launch of the vector kernel: 1 = on (default), 0 = plain launches.
-int set_pdl(int on);
+// KB3, one element per thread (the A/B build's realign = 0).
 cudaError_t launch_scalar(int variant, bool inter, unsigned grid, unsigned threads, const float *theta, float *so,
                           float *co, float *io, size_t n, cudaStream_t stream);
+#endif  // SINCOS_AB
 cudaError_t launch_rcp(unsigned grid, unsigned threads, const float *d, float *out, size_t n, cudaStream_t stream);
-// Persistent TMA bulk-load pipeline over the whole 2048-element tiles of [theta, theta+n);
-// *done = elements covered (the caller finishes the rest).
-cudaError_t launch_tma(int variant, bool inter, unsigned grid, const float *theta, float *so, float *co, float *io,
-                       size_t n, size_t *done, cudaStream_t stream);
 // NEXT(1) phase grid (sincos_phase.cu); vec = 256-bit path (nt % 8 == 0, 32-B aligned t/outputs).
 cudaError_t launch_phase_grid(int variant, bool inter, bool turns, bool vec, const float *f, size_t nf,
                               const float *t, size_t nt, float *so, float *co, float *io, cudaStream_t stream);
 // NEXT(1) flat path for any nt: pairs [head, head + 8 nvec) as 256-bit stores (outputs 32-B
 // aligned at `head`), the rest one per thread; grid-stride over `grid` blocks.  short_rows:
-// for nt < kPhaseRowsMinNt the one-path kernel with t in shared memory.
+// for nt < kPhaseRowsMinNt the one-path kernel with t in shared memory (the product's only
+// form; short_rows = false, the flat kernel, exists in the A/B build only).
 cudaError_t launch_phase_flat(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
                               size_t nt, float *so, float *co, float *io, size_t head, size_t nvec,
                               unsigned grid, bool short_rows, cudaStream_t stream);
@@ -96,16 +117,14 @@ size_t nudft_ws_bytes(size_t nf, size_t nt);
 struct MethodParams;
 // variant 5 = the general method `method` (max series terms method_nt, fix 0/1/3); method_spec
 // >= 0 selects a compile-time shape (0 = n_ss 4 / n_cc 3 / 2 doublings, 1 = 3 / 2 / 1).
+// packed: the FFMA2 kernels (the product's only form; false, their scalar twins, in the A/B build).
 cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, const float *t, const float *a,
                          size_t nt, float *out, void *ws, cudaStream_t stream, const MethodParams *method = nullptr,
-                         int method_nt = 4, int method_fix = 0, int method_spec = -1);
+                         int method_nt = 4, int method_fix = 0, int method_spec = -1, bool packed = true);
 // Test hook (sincos_packcheck.cu): packed vs scalar method over all 2^32 inputs; shape -1 = the
 // paper's table of `variant`, 0 / 1 = method shapes (4,3,2) / (3,2,1) with fix 0/1.
 cudaError_t launch_packcheck(int variant, int shape, int fix, const MethodParams *m, unsigned grid,
                              unsigned long long *mismatch_dev, cudaStream_t stream);
-// Packed fp32 (FFMA2) kernels for the fused sum: 1 = on (default), 0 = scalar; -1 on bad value.
-int set_nudft_packed(int on);
-int get_nudft_packed();
 // NEXT(3) general method (sincos_method.cu).
 // k = theta's float offset past the 32-B boundary at element head - k (0 = aligned).
 cudaError_t launch_method(const float *ss, int n_ss, const float *cc, int n_cc, int doublings, int fix, bool inter,
@@ -116,7 +135,6 @@ cudaError_t launch_pairs16(int variant, int dtype, bool inter, unsigned grid, co
                            void *io, size_t head, size_t nvec, size_t n, int k, cudaStream_t stream);
 cudaError_t launch_interleave(bool to_inter, unsigned grid, const float *s, const float *c, float *io, size_t n,
                               cudaStream_t stream);
-const void *vec_kernel_ptr(int variant, bool inter, int w, int unroll, bool nc, bool pf);
 
 size_t stats_ws_bytes();
 cudaError_t launch_stats(const float *theta, const float *so, const float *co, const float *io, size_t n,

@@ -21,7 +21,6 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include <atomic>
 
 #include "sincos_launch.h"
 #include "sincos_math2.cuh"
@@ -266,30 +265,35 @@ size_t nudft_ws_bytes(size_t nf, size_t nt) {
     return nseg * nf * sizeof(double2);
 }
 
-// Packed fp32 for the paper's tables and the specialised method shapes (default on;
-// sincos_set_nudft_packed(0) selects the scalar kernels, bit-identical, for A/B).
-static std::atomic<int> g_nudft_packed{1};
-int set_nudft_packed(int on) {
-    if (on != 0 && on != 1) return -1;
-    g_nudft_packed.store(on, std::memory_order_relaxed);
-    return 0;
-}
-int get_nudft_packed() { return g_nudft_packed.load(std::memory_order_relaxed); }
+// Packed fp32 for the paper's tables and the specialised method shapes; their scalar twins
+// (bit-identical) exist in the A/B build only, for the comparison.  Kernels that are not
+// packable (comparison functions, general method shapes) have only the scalar form.
+#ifdef SINCOS_AB
+constexpr bool kScalarTwins = true;
+#else
+constexpr bool kScalarTwins = false;
+#endif
 
 template <int V>
-static const void *pick_nudft(bool turns) {
+static const void *pick_nudft(bool turns, bool packed) {
     if constexpr (kPackable<V> && kKPerThread % 2 == 0) {
-        if (get_nudft_packed())
-            return turns ? reinterpret_cast<const void *>(nudft_partial<V, true, true>)
-                         : reinterpret_cast<const void *>(nudft_partial<V, false, true>);
+        if constexpr (kScalarTwins) {
+            if (!packed)
+                return turns ? reinterpret_cast<const void *>(nudft_partial<V, true, false>)
+                             : reinterpret_cast<const void *>(nudft_partial<V, false, false>);
+        }
+        return turns ? reinterpret_cast<const void *>(nudft_partial<V, true, true>)
+                     : reinterpret_cast<const void *>(nudft_partial<V, false, true>);
+    } else {
+        (void)packed;
+        return turns ? reinterpret_cast<const void *>(nudft_partial<V, true, false>)
+                     : reinterpret_cast<const void *>(nudft_partial<V, false, false>);
     }
-    return turns ? reinterpret_cast<const void *>(nudft_partial<V, true, false>)
-                 : reinterpret_cast<const void *>(nudft_partial<V, false, false>);
 }
 
 cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, const float *t, const float *a,
                          size_t nt, float *out, void *ws, cudaStream_t stream, const MethodParams *method,
-                         int method_nt, int method_fix, int method_spec) {
+                         int method_nt, int method_fix, int method_spec, bool packed) {
     size_t chunk = nudft_chunk(nt);
     size_t seg = nudft_segment(nf, nt);
     const size_t nchunks = (nt + seg - 1) / seg;                       // segments (grid.y)
@@ -297,23 +301,23 @@ cudaError_t launch_nudft(int variant, bool turns, const float *f, size_t nf, con
     if (gx > 0x7FFFFFFFu || nchunks > 65535) return cudaErrorInvalidValue;
     const void *fn;
     switch (variant) {
-    case kNormalized: fn = pick_nudft<kNormalized>(turns); break;
-    case kRenormalized: fn = pick_nudft<kRenormalized>(turns); break;
-    case kLibmSincosf: fn = pick_nudft<kLibmSincosf>(turns); break;
-    case kIntrinsicSincosf: fn = pick_nudft<kIntrinsicSincosf>(turns); break;
+    case kNormalized: fn = pick_nudft<kNormalized>(turns, packed); break;
+    case kRenormalized: fn = pick_nudft<kRenormalized>(turns, packed); break;
+    case kLibmSincosf: fn = pick_nudft<kLibmSincosf>(turns, packed); break;
+    case kIntrinsicSincosf: fn = pick_nudft<kIntrinsicSincosf>(turns, packed); break;
     default:
         if (method == nullptr) return cudaErrorInvalidValue;
         if (method_spec >= 0 && method_fix != 3)
-            fn = method_spec == 0 ? (method_fix == 0 ? pick_nudft<kMethodExactBase + 0>(turns)
-                                                     : pick_nudft<kMethodExactBase + 1>(turns))
-                                  : (method_fix == 0 ? pick_nudft<kMethodExactBase + 4>(turns)
-                                                     : pick_nudft<kMethodExactBase + 5>(turns));
+            fn = method_spec == 0 ? (method_fix == 0 ? pick_nudft<kMethodExactBase + 0>(turns, packed)
+                                                     : pick_nudft<kMethodExactBase + 1>(turns, packed))
+                                  : (method_fix == 0 ? pick_nudft<kMethodExactBase + 4>(turns, packed)
+                                                     : pick_nudft<kMethodExactBase + 5>(turns, packed));
         else if (method_nt <= 4)
-            fn = method_fix == 0 ? pick_nudft<kMethodBase + 0>(turns)
-                 : method_fix == 1 ? pick_nudft<kMethodBase + 1>(turns) : pick_nudft<kMethodBase + 3>(turns);
+            fn = method_fix == 0 ? pick_nudft<kMethodBase + 0>(turns, packed)
+                 : method_fix == 1 ? pick_nudft<kMethodBase + 1>(turns, packed) : pick_nudft<kMethodBase + 3>(turns, packed);
         else
-            fn = method_fix == 0 ? pick_nudft<kMethodBase + 4>(turns)
-                 : method_fix == 1 ? pick_nudft<kMethodBase + 5>(turns) : pick_nudft<kMethodBase + 7>(turns);
+            fn = method_fix == 0 ? pick_nudft<kMethodBase + 4>(turns, packed)
+                 : method_fix == 1 ? pick_nudft<kMethodBase + 5>(turns, packed) : pick_nudft<kMethodBase + 7>(turns, packed);
         break;
     }
     MethodParams mp = method ? *method : MethodParams{};

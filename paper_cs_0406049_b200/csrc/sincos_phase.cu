@@ -494,10 +494,12 @@ static const void *pick_short() {
     return reinterpret_cast<const void *>(phase_grid_short<V, INTER, TURNS>);
 }
 
+#ifdef SINCOS_AB
 template <int V, bool INTER, bool TURNS>
 static const void *pick_flat() {
     return reinterpret_cast<const void *>(phase_grid_flat<V, INTER, TURNS>);
 }
+#endif
 
 cudaError_t launch_phase_flat(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
                               size_t nt, float *so, float *co, float *io, size_t head, size_t nvec,
@@ -511,12 +513,18 @@ cudaError_t launch_phase_flat(int variant, bool inter, bool turns, const float *
             fn = inter ? (turns ? pick_short<kRenormalized, true, true>() : pick_short<kRenormalized, true, false>())
                        : (turns ? pick_short<kRenormalized, false, true>()
                                 : pick_short<kRenormalized, false, false>());
-    } else if (variant == kNormalized) {
-        fn = inter ? (turns ? pick_flat<kNormalized, true, true>() : pick_flat<kNormalized, true, false>())
-                   : (turns ? pick_flat<kNormalized, false, true>() : pick_flat<kNormalized, false, false>());
     } else {
-        fn = inter ? (turns ? pick_flat<kRenormalized, true, true>() : pick_flat<kRenormalized, true, false>())
-                   : (turns ? pick_flat<kRenormalized, false, true>() : pick_flat<kRenormalized, false, false>());
+#ifdef SINCOS_AB
+        if (variant == kNormalized)
+            fn = inter ? (turns ? pick_flat<kNormalized, true, true>() : pick_flat<kNormalized, true, false>())
+                       : (turns ? pick_flat<kNormalized, false, true>() : pick_flat<kNormalized, false, false>());
+        else
+            fn = inter ? (turns ? pick_flat<kRenormalized, true, true>() : pick_flat<kRenormalized, true, false>())
+                       : (turns ? pick_flat<kRenormalized, false, true>()
+                                : pick_flat<kRenormalized, false, false>());
+#else
+        return cudaErrorInvalidValue;        // the flat kernel is an A/B-build form
+#endif
     }
     size_t n = nf * nt;
     double inv_nt = 1.0 / static_cast<double>(nt);

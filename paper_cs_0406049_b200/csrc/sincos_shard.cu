@@ -5,6 +5,13 @@
 // device, inside ncclGroupStart/End).  No array data crosses devices: the collective moves
 // 64 B per rank, once per run, outside any timed region of the hot kernel.
 //
+// The communicator and the small per-device buffers (workspace, record, gathered records,
+// timing events) are created once per device list and kept for the process: a second call on
+// the same devices reuses them.  Every CUDA and NCCL return is checked; a failing NCCL call
+// returns SINCOS_ERR_NCCL with its code in sincos_last_nccl_error(), a failing CUDA call
+// SINCOS_ERR_CUDA with its code in sincos_last_cuda_error(); work already queued is drained
+// before any error return.
+//
 // NCCL is bound at run time with dlopen("libnccl.so.2") -- inside a torch process this is
 // torch's own NCCL, standalone the system one -- so the library has no link-time NCCL
 // dependency and the hot path never touches it.
@@ -13,11 +20,14 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <memory>
 #include <mutex>
 #include <vector>
 
 #include "../../include/sincos_pairs.h"
 #include "sincos_launch.h"
+
+extern "C" sincos_status_t sincos_last_error_set(int e);   // sincos_abi.cu
 
 namespace {
 
@@ -41,6 +51,7 @@ struct Nccl {
 std::mutex g_nccl_mu;
 Nccl g_nccl;
 bool g_nccl_tried = false;
+thread_local int g_last_nccl_error = 0;
 
 const Nccl &nccl() {
     std::lock_guard<std::mutex> lk(g_nccl_mu);
@@ -60,95 +71,169 @@ const Nccl &nccl() {
     return g_nccl;
 }
 
-}  // namespace
+// Everything one device list needs, created once and kept (the communicator is the costly
+// part: ncclCommInitAll takes ~0.1-1 s).
+struct Ctx {
+    std::vector<int> devs;
+    std::vector<ncclComm_t> comms;
+    std::vector<void *> ws, mine, all;
+    std::vector<cudaEvent_t> e0, e1;
+    std::mutex busy;                 // one call at a time per device list
+};
 
-extern "C" sincos_status_t sincos_last_error_set(int e);   // sincos_abi.cu
+std::mutex g_ctx_mu;
+std::vector<Ctx *> *g_ctxs = new std::vector<Ctx *>();   // never freed (process lifetime)
+
+sincos_status_t nccl_fail(ncclResult_t r) {
+    g_last_nccl_error = r;
+    return SINCOS_ERR_NCCL;
+}
+
+// Release what a partly built context holds (its own devices only).
+void release(Ctx *c) {
+    const Nccl &N = nccl();
+    for (size_t g = 0; g < c->devs.size(); ++g) {
+        if (cudaSetDevice(c->devs[g]) != cudaSuccess) continue;
+        if (g < c->comms.size() && c->comms[g]) N.destroy(c->comms[g]);
+        if (c->ws[g]) cudaFree(c->ws[g]);
+        if (c->mine[g]) cudaFree(c->mine[g]);
+        if (c->all[g]) cudaFree(c->all[g]);
+        if (c->e0[g]) cudaEventDestroy(c->e0[g]);
+        if (c->e1[g]) cudaEventDestroy(c->e1[g]);
+    }
+    delete c;
+}
+
+// The cached context of this device list, or a new one (nullptr + status on failure).
+Ctx *context(const std::vector<int> &devs, sincos_status_t *st) {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    for (Ctx *c : *g_ctxs)
+        if (c->devs == devs) return c;
+    const Nccl &N = nccl();
+    const size_t G = devs.size(), rec = sizeof(sincos_stats_t);
+    Ctx *c = new Ctx();
+    c->devs = devs;
+    c->ws.assign(G, nullptr);
+    c->mine.assign(G, nullptr);
+    c->all.assign(G, nullptr);
+    c->e0.assign(G, nullptr);
+    c->e1.assign(G, nullptr);
+    cudaError_t e = cudaSuccess;
+    for (size_t g = 0; g < G && e == cudaSuccess; ++g) {
+        if ((e = cudaSetDevice(devs[g])) != cudaSuccess) break;
+        if ((e = cudaMalloc(&c->ws[g], sincos_b200::stats_ws_bytes())) != cudaSuccess) break;
+        if ((e = cudaMalloc(&c->mine[g], rec)) != cudaSuccess) break;
+        if ((e = cudaMalloc(&c->all[g], rec * G)) != cudaSuccess) break;
+        if ((e = cudaEventCreate(&c->e0[g])) != cudaSuccess) break;
+        e = cudaEventCreate(&c->e1[g]);
+    }
+    if (e != cudaSuccess) {
+        *st = sincos_last_error_set(static_cast<int>(e));
+        release(c);
+        return nullptr;
+    }
+    c->comms.assign(G, nullptr);
+    const ncclResult_t r = N.init_all(c->comms.data(), static_cast<int>(G), devs.data());
+    if (r != 0) {
+        c->comms.assign(G, nullptr);       // a failed init leaves no communicator to destroy
+        *st = nccl_fail(r);
+        release(c);
+        return nullptr;
+    }
+    g_ctxs->push_back(c);
+    return c;
+}
+
+}  // namespace
 
 extern "C" {
 
 int sincos_nccl_available(void) { return nccl().ok ? 1 : 0; }
 
+int sincos_last_nccl_error(void) { return g_last_nccl_error; }
+
 sincos_status_t sincos_pairs_sharded_stats(const sincos_shard_t *shards, int nshards, sincos_variant_t variant,
                                            sincos_stats_t *gathered) {
     if (nshards < 1 || shards == nullptr || gathered == nullptr) return SINCOS_ERR_INVALID_ARGUMENT;
+    if (variant != SINCOS_NORMALIZED && variant != SINCOS_RENORMALIZED) return SINCOS_ERR_INVALID_ARGUMENT;
     for (int g = 0; g < nshards; ++g)
         for (int h = 0; h < g; ++h)
             if (shards[g].device == shards[h].device) return SINCOS_ERR_INVALID_ARGUMENT;  // one shard per device
     const Nccl &N = nccl();
     if (!N.ok) return SINCOS_ERR_INVALID_ARGUMENT;
+    int ndev = 0;
+    cudaError_t ce = cudaGetDeviceCount(&ndev);
+    if (ce != cudaSuccess) return sincos_last_error_set(static_cast<int>(ce));
+    for (int g = 0; g < nshards; ++g)
+        if (shards[g].device < 0 || shards[g].device >= ndev) return SINCOS_ERR_INVALID_ARGUMENT;
     int prev = 0;
-    cudaGetDevice(&prev);
-    const size_t rec = sizeof(sincos_stats_t);
+    if ((ce = cudaGetDevice(&prev)) != cudaSuccess) return sincos_last_error_set(static_cast<int>(ce));
+
     std::vector<int> devs(nshards);
-    std::vector<void *> ws(nshards, nullptr), mine(nshards, nullptr), all(nshards, nullptr);
-    std::vector<cudaEvent_t> e0(nshards, nullptr), e1(nshards, nullptr);
-    std::vector<ncclComm_t> comms(nshards, nullptr);
+    for (int g = 0; g < nshards; ++g) devs[g] = shards[g].device;
     sincos_status_t st = SINCOS_OK;
-    cudaError_t ce = cudaSuccess;
-    auto fail = [&](cudaError_t e) { ce = e; st = sincos_last_error_set(static_cast<int>(e)); };
+    Ctx *c = context(devs, &st);
+    if (c == nullptr) {
+        cudaSetDevice(prev);
+        return st;
+    }
+    std::lock_guard<std::mutex> call_lock(c->busy);
+    const size_t rec = sizeof(sincos_stats_t);
+    auto stream = [&](int g) { return static_cast<cudaStream_t>(shards[g].stream); };
+    auto cuda = [&](cudaError_t e) {
+        if (e != cudaSuccess && st == SINCOS_OK) st = sincos_last_error_set(static_cast<int>(e));
+        return e == cudaSuccess;
+    };
+    int touched = 0;                 // shards whose streams may hold work of this call
 
     for (int g = 0; g < nshards && st == SINCOS_OK; ++g) {
         const sincos_shard_t &sh = shards[g];
-        devs[g] = sh.device;
-        cudaStream_t s = static_cast<cudaStream_t>(sh.stream);
-        if ((ce = cudaSetDevice(sh.device)) != cudaSuccess) { fail(ce); break; }
-        if ((ce = cudaMalloc(&ws[g], sincos_b200::stats_ws_bytes())) != cudaSuccess) { fail(ce); break; }
-        if ((ce = cudaMalloc(&mine[g], rec)) != cudaSuccess) { fail(ce); break; }
-        if ((ce = cudaMalloc(&all[g], rec * nshards)) != cudaSuccess) { fail(ce); break; }
-        if ((ce = cudaEventCreate(&e0[g])) != cudaSuccess || (ce = cudaEventCreate(&e1[g])) != cudaSuccess) {
-            fail(ce);
-            break;
-        }
-        cudaEventRecord(e0[g], s);
+        if (!cuda(cudaSetDevice(sh.device))) break;
+        touched = g + 1;
+        if (!cuda(cudaEventRecord(c->e0[g], stream(g)))) break;
         st = sincos_pairs(sh.theta_dev, sh.sin_dev, sh.cos_dev, sh.inter_dev, sh.n, variant, sh.stream);
         if (st != SINCOS_OK) break;
-        cudaEventRecord(e1[g], s);
+        if (!cuda(cudaEventRecord(c->e1[g], stream(g)))) break;
         st = sincos_error_stats(sh.theta_dev, sh.sin_dev, sh.cos_dev, sh.inter_dev, sh.n,
-                                static_cast<sincos_stats_t *>(mine[g]), ws[g], sh.stream);
+                                static_cast<sincos_stats_t *>(c->mine[g]), c->ws[g], sh.stream);
     }
-    // per-shard kernel time into the record (the host waits for each shard's stream)
+    // per-shard kernel time and device into the record (the host waits for each shard's stream)
+    std::vector<double> ms(nshards, 0.0);
+    std::vector<uint32_t> dv(nshards, 0);
     for (int g = 0; g < nshards && st == SINCOS_OK; ++g) {
-        cudaSetDevice(devs[g]);
-        if ((ce = cudaStreamSynchronize(static_cast<cudaStream_t>(shards[g].stream))) != cudaSuccess) {
-            fail(ce);
+        if (!cuda(cudaSetDevice(devs[g])) || !cuda(cudaStreamSynchronize(stream(g)))) break;
+        float f = 0.0f;
+        if (!cuda(cudaEventElapsedTime(&f, c->e0[g], c->e1[g]))) break;
+        ms[g] = f;
+        dv[g] = static_cast<uint32_t>(devs[g]);
+        char *r = static_cast<char *>(c->mine[g]);
+        if (!cuda(cudaMemcpyAsync(r + offsetof(sincos_stats_t, kernel_ms), &ms[g], sizeof(double),
+                                  cudaMemcpyHostToDevice, stream(g))) ||
+            !cuda(cudaMemcpyAsync(r + offsetof(sincos_stats_t, device), &dv[g], sizeof(uint32_t),
+                                  cudaMemcpyHostToDevice, stream(g))))
             break;
-        }
-        float ms = 0.0f;
-        cudaEventElapsedTime(&ms, e0[g], e1[g]);
-        double dms = ms;
-        uint32_t dev = static_cast<uint32_t>(devs[g]);
-        cudaMemcpy(static_cast<char *>(mine[g]) + offsetof(sincos_stats_t, kernel_ms), &dms, sizeof(dms),
-                   cudaMemcpyHostToDevice);
-        cudaMemcpy(static_cast<char *>(mine[g]) + offsetof(sincos_stats_t, device), &dev, sizeof(dev),
-                   cudaMemcpyHostToDevice);
     }
     // the one collective: 64 B per rank
     if (st == SINCOS_OK) {
-        if (N.init_all(comms.data(), nshards, devs.data()) != 0) st = SINCOS_ERR_CUDA;
-    }
-    if (st == SINCOS_OK) {
-        N.group_start();
-        for (int g = 0; g < nshards; ++g) {
-            cudaSetDevice(devs[g]);
-            N.all_gather(mine[g], all[g], rec, kNcclUint8, comms[g], static_cast<cudaStream_t>(shards[g].stream));
+        ncclResult_t r = N.group_start();
+        if (r != 0) st = nccl_fail(r);
+        for (int g = 0; g < nshards && st == SINCOS_OK; ++g) {
+            if (!cuda(cudaSetDevice(devs[g]))) break;
+            if ((r = N.all_gather(c->mine[g], c->all[g], rec, kNcclUint8, c->comms[g], stream(g))) != 0)
+                st = nccl_fail(r);
         }
-        if (N.group_end() != 0) st = SINCOS_ERR_CUDA;
+        // the group is always closed once opened (even after a failed enqueue)
+        const ncclResult_t r2 = N.group_end();
+        if (r2 != 0 && st == SINCOS_OK) st = nccl_fail(r2);
     }
-    if (st == SINCOS_OK) {
-        cudaSetDevice(devs[0]);
-        if ((ce = cudaStreamSynchronize(static_cast<cudaStream_t>(shards[0].stream))) != cudaSuccess ||
-            (ce = cudaMemcpy(gathered, all[0], rec * nshards, cudaMemcpyDeviceToHost)) != cudaSuccess)
-            fail(ce);
-    }
-    for (int g = 0; g < nshards; ++g) {
-        cudaSetDevice(devs[g]);
-        cudaStreamSynchronize(static_cast<cudaStream_t>(shards[g].stream));
-        if (comms[g]) N.destroy(comms[g]);
-        if (ws[g]) cudaFree(ws[g]);
-        if (mine[g]) cudaFree(mine[g]);
-        if (all[g]) cudaFree(all[g]);
-        if (e0[g]) cudaEventDestroy(e0[g]);
-        if (e1[g]) cudaEventDestroy(e1[g]);
+    if (st == SINCOS_OK && cuda(cudaSetDevice(devs[0])) && cuda(cudaStreamSynchronize(stream(0))))
+        cuda(cudaMemcpy(gathered, c->all[0], rec * nshards, cudaMemcpyDeviceToHost));
+    // drain every stream this call used before returning (success or not): the records and
+    // the staging values above must not be read after the call, nor the caller's buffers
+    for (int g = 0; g < (st == SINCOS_OK ? nshards : touched); ++g) {
+        if (cudaSetDevice(devs[g]) != cudaSuccess) continue;
+        const cudaError_t e = cudaStreamSynchronize(stream(g));
+        if (e != cudaSuccess && st == SINCOS_OK) st = sincos_last_error_set(static_cast<int>(e));
     }
     cudaSetDevice(prev);
     return st;

@@ -8,7 +8,6 @@
 #include <stdint.h>
 
 #include "sincos_math.cuh"
-#include "sincos_math2.cuh"
 
 namespace sincos_b200 {
 
@@ -87,42 +86,9 @@ __device__ __forceinline__ void storeW(float *p, const float *r) {
     if constexpr (W == 8) store8(p, r); else store4(p, r);
 }
 
-// Packed-fp32 form of the vector body (sincos_math2.cuh; bit-identical).  Build-time
-// switch for measurement only: the path is HBM-bound, so halving FP32 issue slots does
-// not move it.
-#ifndef SINCOS_PACKED_HOT
-#define SINCOS_PACKED_HOT 0
-#endif
-
 // Compute and store one vector of W elements whose first element is `e0`.
 template <int V, bool INTER, int W>
 __device__ __forceinline__ void emit(const float (&x)[W], size_t e0, float *so, float *co, float *io) {
-    if constexpr (SINCOS_PACKED_HOT && (V == kNormalized || V == kRenormalized)) {
-        float s[W], c[W];
-#pragma unroll
-        for (int k = 0; k < W; k += 2) {
-            F2 s2, c2;
-            sincos_from_q2<V>(reduce_turn2(mul2(pk2(x[k], x[k + 1]), bc2(kInvTwoPi))), s2, c2);
-            s[k] = lo2(s2);
-            s[k + 1] = hi2(s2);
-            c[k] = lo2(c2);
-            c[k + 1] = hi2(c2);
-        }
-        if constexpr (INTER) {
-            float cs[2 * W];
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-                cs[2 * k] = c[k];
-                cs[2 * k + 1] = s[k];
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) storeW<W>(io + 2 * e0 + h * W, cs + h * W);
-        } else {
-            storeW<W>(so + e0, s);
-            storeW<W>(co + e0, c);
-        }
-        return;
-    }
     if constexpr (INTER) {
         float cs[2 * W];
 #pragma unroll

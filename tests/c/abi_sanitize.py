@@ -1,4 +1,4 @@
-"""Host-side logic of libsincos_pairs.so (validation, sharder, workspace sizing, tuning,
+"""Host-side logic of libsincos_pairs.so (validation, sharder, workspace sizing,
 status strings) driven without a GPU, for a build with -fsanitize=address,undefined; run by
 tests/test_sanitize_host.py with libasan/libubsan preloaded.  argv[1] = the library."""
 import ctypes
@@ -30,11 +30,8 @@ bad += L.sincos_shard_range(10, 0, 0, ctypes.byref(lo), ctypes.byref(hi)) != -1
 L.sincos_nudft_workspace_bytes.argtypes = [S, S]; L.sincos_nudft_workspace_bytes.restype = S
 for nf, nt in ((0, 0), (0, 9), (9, 0), (1, 1), (1 << 20, 1 << 30), ((1 << 40), 3)):
     L.sincos_nudft_workspace_bytes(nf, nt)
-L.sincos_set_launch_config.argtypes = [I] * 5
-for cfg in ((128, 0, 8, 1, 0), (100, 0, 8, 1, 0), (512, 16, 4, 4, 1), (256, -1, 8, 2, 0)):
-    L.sincos_set_launch_config(*cfg)
 L.sincos_status_string.restype = ctypes.c_char_p
-for k in range(-1, 6):
+for k in range(-1, 7):
     L.sincos_status_string(k)
 print("san_abi", "ok" if bad == 0 else f"FAIL {bad}")
 sys.exit(1 if bad else 0)

@@ -47,8 +47,9 @@ def test_only_the_abi_is_exported():
 
 def test_version_and_status_strings(L):
     assert b"sm_100a" in L.sincos_version()
-    for s in range(4):
+    for s in range(5):
         assert L.sincos_status_string(s)
+    assert b"NCCL" in L.sincos_status_string(4)
 
 
 def test_library_is_sm100a_cubin():
@@ -124,16 +125,26 @@ def test_host_path_validation(L):
     assert L.sincos_pairs_host(p, p + 4, p + 128, None, 16, 0, A, 1 << 30, None) == OVERLAP
 
 
-def test_launch_config_validation(L):
-    assert L.sincos_set_launch_config(100, 0, 8, 2, 0) == -1
-    assert L.sincos_set_launch_config(256, 0, 3, 2, 0) == -1
-    assert L.sincos_set_launch_config(256, 0, 8, 3, 0) == -1
-    assert L.sincos_set_launch_config(256, 0, 8, 2, 3) == -1
-    assert L.sincos_set_launch_config(256, -1, 8, 2, 0) == -1
-    assert L.sincos_set_launch_config(512, 16, 4, 4, 1) == 0
-    assert sp.get_launch_config() == {"threads": 512, "blocks_per_sm": 16, "vec": 4, "unroll": 4, "prefetch": 1}
-    sp.set_launch_config()
-    assert sp.get_launch_config() == sp.DEFAULT_LAUNCH
+def test_no_tuning_state_in_the_product():
+    """The product library has one fixed kernel configuration: no setter of launch shape,
+    re-alignment, PDL or kernel form is exported (those live in the A/B build only)."""
+    out = subprocess.run(["nm", "-D", "--defined-only", sp.library_path], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (sincos_\w+)", out))
+    assert not {s for s in exported if "_set_" in s or s.startswith("sincos_ab_") or "batched" in s}, exported
+    from paper_cs_0406049_b200 import _build
+    ab_out = subprocess.run(["nm", "-D", "--defined-only", _build.build_ab()], capture_output=True, text=True).stdout
+    ab_exported = set(re.findall(r"\bT (sincos_\w+)", ab_out))
+    assert ab_exported == exported | {"sincos_ab_set", "sincos_ab_get", "sincos_pairs_batched"}, ab_exported ^ exported
+
+
+def test_ab_knob_validation():
+    from paper_cs_0406049_b200 import ab
+    L = ab.lib()
+    for knob, bad in ((0, 100), (1, -1), (2, 3), (3, 3), (4, 2), (5, 4), (6, 2), (7, 2), (8, 0), (-1, 0)):
+        assert L.sincos_ab_set(knob, bad) == -1, (knob, bad)
+    assert L.sincos_ab_set(0, 512) == 128 and L.sincos_ab_get(0) == 512
+    ab.reset()
+    assert [L.sincos_ab_get(k) for k in range(8)] == list(ab.DEFAULTS.values())
 
 
 @pytest.mark.parametrize("n", [0, 1, 7, 8, 9, 1000, 1 << 20, (1 << 32) + 5, (1 << 30) + 3])
@@ -196,7 +207,7 @@ def test_sass_value_path_branch_free():
             # the loads/stores are the wide streaming forms
             assert re.search(r"LDG\.E\.[A-Z0-9.]*(128|256)", body), name
             assert re.search(r"STG\.E\.[A-Z0-9.]*(128|256)", body), name
-    assert seen >= 96 + 8 + 24
+    assert seen >= 24 + 24 + 8 + 24       # vector, re-aligning (128-bit), phase-grid, fused-sum instances
 
 
 def test_product_never_touches_the_oracle():
@@ -209,13 +220,10 @@ def test_product_never_touches_the_oracle():
         assert not re.search(r"\bimport\s+oracle|from\s+oracle|sincos_oracle|liboracle", src), path
 
 
-def test_sass_packed_fused_sum_uses_ffma2():
-    """The fused sum's packed kernels (PACK = true, last template flag) run the method and the
-    complex MAC on sm_100a's two-lane fp32 instructions; their scalar twins have none."""
-    sass = _sass()
-    funcs = re.split(r"\n\s*Function : ", sass)
+def _nudft_forms(lib_path):
+    sass = subprocess.run(["cuobjdump", "-sass", lib_path], capture_output=True, text=True).stdout
     packed = scalar = 0
-    for f in funcs:
+    for f in re.split(r"\n\s*Function : ", sass):
         name = f.split("\n", 1)[0]
         if "nudft_partial" not in name:
             continue
@@ -228,7 +236,19 @@ def test_sass_packed_fused_sum_uses_ffma2():
         else:
             scalar += 1
             assert n2 == 0, (name, n2)
-    assert packed >= 8 and scalar >= 8
+    return packed, scalar
+
+
+def test_sass_packed_fused_sum_uses_ffma2():
+    """The fused sum's kernels (PACK = true, last template flag) run the method and the complex
+    MAC on sm_100a's two-lane fp32 instructions.  The product has only those, plus the scalar
+    comparison kernels with CUDA's own functions (radians / turns x sincosf / __sincosf); the
+    A/B build adds a scalar twin (no FFMA2) of every packed kernel."""
+    from paper_cs_0406049_b200 import _build
+    packed, scalar = _nudft_forms(sp.library_path)
+    assert packed >= 24 and scalar == 4, (packed, scalar)
+    packed_ab, scalar_ab = _nudft_forms(_build.build_ab())
+    assert packed_ab == packed and scalar_ab == scalar + packed, (packed_ab, scalar_ab)
 
 
 def test_nudft_chunk_rule():
@@ -278,9 +298,12 @@ def test_alignment_checks_of_the_other_entry_points(L):
     assert L.sincos_debug_packed_check(7, None, A, None) == INVALID
 
 
-def test_batched_validation_before_cuda(L):
-    """sincos_pairs_batched validates every item before launching anything (fake addresses)."""
-    Item = sp.Item
+def test_batched_validation_before_cuda():
+    """sincos_pairs_batched (A/B build) validates every item before launching anything (fake
+    addresses)."""
+    from paper_cs_0406049_b200 import ab
+    L = ab.lib()
+    Item = ab.Item
     assert L.sincos_pairs_batched(None, 0, 0, None) == OK                 # empty batch
     assert L.sincos_pairs_batched(None, -1, 0, None) == INVALID
     good = Item(A, 2 * A, 3 * A, None, 64)
@@ -292,3 +315,11 @@ def test_batched_validation_before_cuda(L):
         assert L.sincos_pairs_batched(ctypes.addressof(arr), 3, 0, None) == want
     arr = (Item * 1)(good)
     assert L.sincos_pairs_batched(ctypes.addressof(arr), 1, 9, None) == INVALID  # variant
+
+
+def test_host_path_binding_refuses_a_host_workspace():
+    """The host-buffer path's workspace is device memory: a CPU tensor is refused in Python,
+    before the library is called."""
+    import torch
+    with pytest.raises(ValueError, match="workspace"):
+        sp.sincos_pairs_host(torch.zeros(16), torch.zeros(16), torch.zeros(16), workspace=torch.zeros(1 << 20))

@@ -1,5 +1,5 @@
-"""sincos_pairs_batched: many arrays in one launch (per 480), each bit-exact vs the oracle.
-``pytest -m gpu``."""
+"""sincos_pairs_batched of the A/B build (outside SURVEY 8, not in the product library): many
+arrays in one launch (per 480), each bit-exact vs the oracle.  ``pytest -m gpu``."""
 import numpy as np
 import pytest
 
@@ -11,6 +11,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # noqa: E402
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -53,9 +54,9 @@ def test_batched_matches_oracle(count, inter, variant):
             outs_c.append(torch.empty(n + 8, device="cuda")[oo:oo + n])
         thetas.append(th)
     if inter:
-        sp.sincos_pairs_batched(thetas, interleaved_outs=outs_i, variant=variant)
+        ab.sincos_pairs_batched(thetas, interleaved_outs=outs_i, variant=variant)
     else:
-        sp.sincos_pairs_batched(thetas, outs_s, outs_c, variant=variant)
+        ab.sincos_pairs_batched(thetas, outs_s, outs_c, variant=variant)
     torch.cuda.synchronize()
     for i, (ws, wc) in enumerate(wants):
         if inter:
@@ -65,14 +66,15 @@ def test_batched_matches_oracle(count, inter, variant):
             assert_parity(outs_s[i].cpu().numpy(), outs_c[i].cpu().numpy(), ws, wc, f"item {i} n={lens[i]}")
 
 
-def test_batched_convenience_and_validation():
+def test_batched_list_form_and_validation():
     ts = [torch.rand(n, device="cuda") * 10 for n in (5, 1000, 3000)]
-    res = sp.sincos_batched(ts)
-    for t, (s, c) in zip(ts, res):
+    ss, cs = [torch.empty_like(t) for t in ts], [torch.empty_like(t) for t in ts]
+    ab.sincos_pairs_batched(ts, ss, cs)
+    for t, s, c in zip(ts, ss, cs):
         ws, wc = oracle.sincos(t.cpu().numpy(), 0)
-        assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws, wc, "convenience")
-    sp.sincos_pairs_batched([])                               # empty batch: no-op
+        assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws, wc, "list form")
+    ab.sincos_pairs_batched([])                               # empty batch: no-op
     t = torch.rand(64, device="cuda")
     s = torch.empty(64, device="cuda")
     with pytest.raises(sp.SincosError):                       # overlap inside an item: refused
-        sp.sincos_pairs_batched([t], [s], [s])
+        ab.sincos_pairs_batched([t], [s], [s])

@@ -1,6 +1,7 @@
 """GPU parity of NEXT(4): 16-bit outputs (IEEE binary16, bfloat16) and the split <-> interleaved
 adapters.  The 16-bit values must equal the oracle's fp32 pair rounded to nearest even by a
 library conversion (numpy float16, torch bfloat16 on the CPU).  ``pytest -m gpu``."""
+import contextlib
 import numpy as np
 import pytest
 
@@ -11,6 +12,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # noqa: E402  (A/B build)
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -145,8 +147,7 @@ def test_16bit_every_theta_offset(dtype, realign):
     rng = np.random.default_rng(5)
     N = 100_003
     base = rng.uniform(-300, 300, N + 16).astype(np.float32)
-    prev = sp.set_realign(realign)
-    try:
+    with (contextlib.nullcontext() if realign else ab.knobs(realign=0)):
         for variant in (0, 1):
             ws, wc = oracle.sincos(base, variant)
             bt = torch.from_numpy(base).cuda()
@@ -169,8 +170,6 @@ def test_16bit_every_theta_offset(dtype, realign):
                         gi = io.view(torch.int16).cpu().numpy().view(np.uint16)
                         assert same16(gi[1::2], rn16(ws[ot:ot + n], dtype), dtype).all(), tag
                         assert same16(gi[0::2], rn16(wc[ot:ot + n], dtype), dtype).all(), tag
-    finally:
-        sp.set_realign(prev)
 
 
 @pytest.mark.parametrize("n", [1, 5, 1003, (1 << 20) + 7])

@@ -8,6 +8,7 @@ sincos_pairs_method with the paper's table, sincos_phase_grid with f = [1] in ra
 of which must return the method's pairs), a launch configuration and an input distribution
 (the five BASELINE config generators, raw bit patterns).  Bar: bit-exact by value vs the
 oracle on the same inputs."""
+import contextlib
 import numpy as np
 import pytest
 
@@ -19,6 +20,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # noqa: E402  (A/B build)
 
 CASES = 800
 
@@ -28,8 +30,6 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     yield
-    sp.set_launch_config()
-    sp.set_realign(True)
 
 
 def draw_theta(rng, n):
@@ -66,9 +66,15 @@ def test_fuzz_pairs(block):
         ot, os_, oc = (int(x) for x in rng.integers(0, 8, 3))
         if rng.random() < 0.5:
             oc = os_                                     # sin and cos at one offset (common)
+        # half the cases on the product library, half on the A/B build with a random launch
+        # shape and, 15% of the time, re-alignment off (one element per thread)
         cfg = [(128, 0, 8, 1, 0), (256, 0, 8, 2, 0), (512, 4, 4, 1, 1), (128, 1, 8, 4, 0)][int(rng.integers(0, 4))]
-        sp.set_launch_config(*cfg)
-        sp.set_realign(bool(rng.random() < 0.85))
+        realign = int(rng.random() < 0.85)
+        use_ab = rng.random() < 0.5
+        if not use_ab:
+            cfg, realign = "product", 1
+        ctx = ab.knobs(launch=cfg, realign=realign) if use_ab else contextlib.nullcontext()
+        ctx.__enter__()
         tbuf = torch.empty(n + 16, dtype=torch.float32, device="cuda")
         tbuf[ot:ot + n].copy_(torch.from_numpy(th))
         t = tbuf[ot:ot + n]
@@ -95,6 +101,7 @@ def test_fuzz_pairs(block):
             sp.phase_grid(torch.from_numpy(f2).cuda(), tb2[toff2:toff2 + nt2], units=sp.RADIANS, variant=variant,
                           **outs)
         torch.cuda.synchronize()
+        ctx.__exit__(None, None, None)
         if inter:
             v = outs["interleaved_out"].cpu().numpy()
             gs, gc = v[1::2], v[0::2]
@@ -102,4 +109,4 @@ def test_fuzz_pairs(block):
             gs, gc = outs["sin_out"].cpu().numpy(), outs["cos_out"].cpu().numpy()
         ws, wc = oracle.sincos(th, variant)
         assert_parity(gs, gc, ws, wc, f"case {block}/{case}: n={n} entry={entry} inter={inter} v={variant} "
-                                      f"offs={ot},{os_},{oc} cfg={cfg}")
+                                      f"offs={ot},{os_},{oc} cfg={cfg} realign={realign}")

@@ -1,5 +1,6 @@
 """GPU parity of NEXT(3), sincos_pairs_method (caller-supplied series / doublings / fix),
 against the oracle's general method: bit-exact by value.  ``pytest -m gpu``."""
+import contextlib
 import numpy as np
 import pytest
 
@@ -12,6 +13,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # noqa: E402  (A/B build)
 
 OFIX = {sp.FIX_LINEAR: oracle.FIX_LINEAR_PENULTIMATE, sp.FIX_RECIPROCAL: oracle.FIX_RECIPROCAL,
         sp.FIX_NONE: oracle.FIX_NONE}
@@ -120,8 +122,7 @@ def test_method_every_theta_offset(realign):
     bs = torch.empty(N + 64, device="cuda")
     bc = torch.empty(N + 64, device="cuda")
     bi = torch.empty(2 * N + 64, device="cuda")
-    prev = sp.set_realign(realign)
-    try:
+    with (contextlib.nullcontext() if realign else ab.knobs(realign=0)):
         for n in list(range(0, 20)) + [63, 64, 65, 1001, N]:
             for ot in range(8):
                 for oo in (0, 1, 6):
@@ -134,5 +135,3 @@ def test_method_every_theta_offset(realign):
                     assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws[ot:ot + n], wc[ot:ot + n], tag)
                     iv = io.cpu().numpy()
                     assert_parity(iv[1::2], iv[0::2], ws[ot:ot + n], wc[ot:ot + n], "inter " + tag)
-    finally:
-        sp.set_realign(prev)

@@ -13,6 +13,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # noqa: E402  (A/B build)
 
 U = 2.0 ** -24
 
@@ -167,19 +168,13 @@ def test_nudft_method_single_amplitude_exact(units, spec):
 
 # ---- packed fp32 (FFMA2) kernels --------------------------------------------------------
 
-@pytest.fixture
-def scalar_then_packed():
-    prev = sp.set_nudft_packed(True)
-    yield
-    sp.set_nudft_packed(prev)
-
-
 @pytest.mark.parametrize("units", [0, 1])
 @pytest.mark.parametrize("kind", ["N", "A", "m1_3_2", "m2_4_3", "g3_3_2", "g2_5_4", "g1_4_4"])
 @pytest.mark.parametrize("shape", [(1, 1), (3, 7), (513, 1031), (1500, 4100)])
-def test_packed_kernel_bit_identical_to_scalar(units, kind, shape, scalar_then_packed):
-    """The packed kernels (two frequencies per FFMA2/FMUL2/FADD2 lane pair) round every lane
-    exactly as the scalar kernels do: the sums are bit-identical, for the paper's tables, the
+def test_packed_kernel_bit_identical_to_scalar(units, kind, shape):
+    """The packed kernels of the product (two frequencies per FFMA2/FMUL2/FADD2 lane pair) round
+    every lane exactly as their scalar twins (the A/B build's nudft_packed = 0) do
+    -- the sums are bit-identical, for the paper's tables, the
     specialised method shapes and general shapes, ragged nf (odd lane pairs past nf) and nt
     (tail tiles).
     Phases include exact zeros, half-turn ties and huge / subnormal / non-finite values."""
@@ -204,9 +199,8 @@ def test_packed_kernel_bit_identical_to_scalar(units, kind, shape, scalar_then_p
                "g2_5_4": sp.FIX_LINEAR, "g1_4_4": sp.FIX_NONE}[kind]
         kw = {"method": sp.make_method(list(ss), list(cc), n, fix)}
     fd, td, ad = (torch.from_numpy(x).cuda() for x in (f, t, a))
-    sp.set_nudft_packed(False)
-    o_scalar = sp.nudft(fd, td, ad, units=units, **kw)
-    sp.set_nudft_packed(True)
+    with ab.knobs(nudft_packed=0):
+        o_scalar = sp.nudft(fd, td, ad, units=units, **kw)
     o_packed = sp.nudft(fd, td, ad, units=units, **kw)
     torch.cuda.synchronize()
     x, y = o_scalar.cpu().numpy(), o_packed.cpu().numpy()
@@ -217,10 +211,9 @@ def test_packed_kernel_bit_identical_to_scalar(units, kind, shape, scalar_then_p
     assert np.array_equal(xb[fin], yb[fin])
 
 
-def test_set_nudft_packed_rejects_bad_values():
-    assert sp.lib().sincos_set_nudft_packed(2) == -1
-    prev = sp.set_nudft_packed(True)
-    assert sp.set_nudft_packed(prev) is True
+def test_ab_knobs_reject_bad_values():
+    assert ab.lib().sincos_ab_set(7, 2) == -1 and ab.lib().sincos_ab_set(99, 0) == -1
+    assert ab.lib().sincos_ab_get(7) == 1
 
 
 @pytest.mark.parametrize("variant", [0, 1])

@@ -4,6 +4,7 @@
 Bar: bit-exact by value (signed zeros and NaN payloads aside; reading G15 -- the
 algorithm fixes one bit pattern per input), which implies the north_star bound
 |delta| <= 4 ulp of 1.0 per component (ULP4 in helpers.py), also asserted."""
+import contextlib
 import math
 import os
 
@@ -18,6 +19,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # noqa: E402  (A/B build: the alternative kernel forms)
 
 VARIANTS = [oracle.VARIANT_N, oracle.VARIANT_A]   # same numbering as sp.NORMALIZED / sp.RENORMALIZED
 
@@ -26,7 +28,6 @@ VARIANTS = [oracle.VARIANT_N, oracle.VARIANT_A]   # same numbering as sp.NORMALI
 def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    sp.set_launch_config()          # the default config bench.py times
     torch.cuda.init()
     yield
 
@@ -292,23 +293,21 @@ def test_in_place(variant):
 @pytest.mark.parametrize("threads", [128, 256, 512])
 @pytest.mark.parametrize("vec", [4, 8])
 @pytest.mark.parametrize("unroll", [1, 2, 4])
-@pytest.mark.parametrize("prefetch", [0, 1, 2])
+@pytest.mark.parametrize("prefetch", [0, 1])
 def test_every_kernel_instance(threads, vec, unroll, prefetch):
-    """Every (threads, vector width, unroll, prefetch) the tuner can select, both variants and
-    layouts, on a ragged size, with a 1-block-per-SM grid (many grid-stride trips), the
-    occupancy grid, and an oversubscribed grid (about one trip per thread)."""
+    """Every (threads, vector width, unroll, prefetch) of the A/B build (the product runs the
+    first of them, 128 / 8 / 1 / 0, full grid), both variants and layouts, on a ragged size,
+    with a 1-block-per-SM grid (many grid-stride trips), the occupancy grid, and the full
+    grid (about one trip per thread)."""
     th = inputs.generate(2, 12345, (1 << 20) + 13)
     want = {v: oracle.sincos(th, v) for v in VARIANTS}
-    try:
-        for bps in (0, 1, 6):
-            sp.set_launch_config(threads, bps, vec, unroll, prefetch)
+    for bps in (0, 1, 6):
+        with ab.knobs(launch=(threads, bps, vec, unroll, prefetch)):
             for variant in VARIANTS:
                 for inter in (False, True):
                     s, c = run(th, variant, inter)
                     assert_parity(s, c, *want[variant],
                                   f"t{threads} v{vec} u{unroll} pf{prefetch} bps{bps} inter={inter}")
-    finally:
-        sp.set_launch_config()
 
 
 def test_special_values_gpu():
@@ -324,13 +323,15 @@ def test_special_values_gpu():
 # ---- host path, stats kernel, null kernel, launch accounting ---------------------------
 
 @pytest.mark.parametrize("inter", [False, True])
-def test_host_buffer_path(inter):
+@pytest.mark.parametrize("ws_mib", [0, 64])
+def test_host_buffer_path(inter, ws_mib):
     """sincos_pairs_host (chunked H2D -> kernel -> D2H over three streams) equals the oracle;
-    a small workspace forces many chunks and a ragged last one."""
+    the minimum workspace forces many 2^16-element chunks and a ragged last one, a 64 MiB one
+    the whole ramp of chunk sizes (2^16, 2^17, ... up to the slot size) and a ragged end."""
     n = (1 << 21) + 77
     th = inputs.generate(3, 0, n)
     th_h = torch.from_numpy(th).pin_memory()
-    ws = torch.empty(sp.host_workspace_min_bytes(), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(max(sp.host_workspace_min_bytes(), ws_mib << 20), dtype=torch.uint8, device="cuda")
     for variant in VARIANTS:
         if inter:
             o = torch.empty(2 * n, dtype=torch.float32).pin_memory()
@@ -448,9 +449,9 @@ def test_realign_path(bps, mode):
     big_s = torch.empty(N + 64, dtype=torch.float32, device="cuda")
     big_c = torch.empty(N + 64, dtype=torch.float32, device="cuda")
     big_i = torch.empty(2 * N + 64, dtype=torch.float32, device="cuda")
-    sp.set_launch_config(blocks_per_sm=bps)
-    prev = sp.set_realign(mode)              # 1: 256-bit form where possible; 2: 128-bit form only
-    try:
+    # the product (mode 1, full grid) or the A/B build (128-bit form only, grid-stride grids)
+    ctx = ab.knobs(blocks_per_sm=bps, realign=mode) if (mode, bps) != (1, 0) else contextlib.nullcontext()
+    with ctx:
         for variant in VARIANTS:
             rs, rc = ref[variant]
             for n in list(range(0, 24)) + [127, 128, 129, 1000, 4097, N]:
@@ -470,9 +471,6 @@ def test_realign_path(bps, mode):
                         iv = io.cpu().numpy()
                         assert_parity(iv[1::2], iv[0::2], rs[ot:ot + n], rc[ot:ot + n],
                                       f"realign inter n={n} off={ot},{oo} bps={bps}")
-    finally:
-        sp.set_launch_config()
-        sp.set_realign(prev)
 
 
 def test_scalar_path_unshared_outputs():
@@ -489,8 +487,7 @@ def test_scalar_path_unshared_outputs():
     for variant in VARIANTS:
         rs, rc = oracle.sincos(base, variant)
         for realign in (True, False):
-            prev = sp.set_realign(realign)
-            try:
+            with (contextlib.nullcontext() if realign else ab.knobs(realign=0)):
                 for ot, os_, oc_, oi in ((0, 1, 2, 1), (1, 0, 3, 3), (2, 2, 2, 2), (3, 0, 0, 5)):
                     t = big_t[ot:ot + n]
                     s, c = big_s[os_:os_ + n], big_c[oc_:oc_ + n]
@@ -503,8 +500,6 @@ def test_scalar_path_unshared_outputs():
                     iv = io.cpu().numpy()
                     assert_parity(iv[1::2], iv[0::2], rs[ot:ot + n], rc[ot:ot + n],
                                   f"scalar inter off={ot},{oi} realign={realign}")
-            finally:
-                sp.set_realign(prev)
 
 
 @pytest.mark.parametrize("variant,name", [(oracle.VARIANT_N, "N"), (oracle.VARIANT_A, "A")])
@@ -520,9 +515,7 @@ def test_all_fp32_bit_patterns_other_paths(golden, variant, name, path):
     chunk = 1 << 28
     toff = 1 if path in ("realign_split", "realign_interleaved", "scalar_split") else 0
     tbuf = torch.empty(chunk + 8, dtype=torch.float32, device="cuda")
-    if path == "scalar_split":
-        prev = sp.set_realign(False)
-    try:
+    with (ab.knobs(realign=0) if path == "scalar_split" else contextlib.nullcontext()):
         if "inter" in path:
             ibuf = torch.empty(2 * chunk + 8, dtype=torch.float32, device="cuda")
             io = ibuf[1:1 + 2 * chunk] if path == "outshift_interleaved" else ibuf[:2 * chunk]   # 4-B pairs
@@ -544,9 +537,6 @@ def test_all_fp32_bit_patterns_other_paths(golden, variant, name, path):
                 sp.sincos_pairs(th, s, c, variant=variant)
             h, nn, ex = _hash_chunk(u0, s.contiguous(), c.contiguous())
             H, NN, EX = (H + h) % (1 << 64), NN + nn, EX + ex
-    finally:
-        if path == "scalar_split":
-            sp.set_realign(prev)
     assert "0x%016X" % H == want["hash"], path
     assert NN == want["nan_pairs"] and EX == want["exact_0_1"]
 
@@ -679,8 +669,7 @@ def test_dependent_launch_chain_keeps_stream_order(pdl):
     """Programmatic dependent launch must not let a kernel read its predecessor's output early:
     a chain of 12 back-to-back launches, each reading the previous one's sin output (in place
     every other step), no host sync in between, equals the oracle applied 12 times."""
-    prev = sp.set_pdl(pdl)
-    try:
+    with (contextlib.nullcontext() if pdl else ab.knobs(pdl=0)):
         n = (1 << 22) + 3
         th = inputs.generate(1, 0, n)
         cur = torch.from_numpy(th).cuda()
@@ -697,8 +686,6 @@ def test_dependent_launch_chain_keeps_stream_order(pdl):
             want, wc = oracle.sincos(want, v)
         torch.cuda.synchronize()
         assert_parity(cur.cpu().numpy(), c.cpu().numpy(), want, wc, f"chain pdl={pdl}")
-    finally:
-        sp.set_pdl(prev)
 
 
 @pytest.mark.parametrize("variant", VARIANTS)

@@ -1,5 +1,6 @@
 """GPU parity of NEXT(1), sincos_phase_grid (pairs of phases f_i * t_j formed in the kernel),
 against the oracle's phase functions: bit-exact by value.  ``pytest -m gpu``."""
+import contextlib
 import numpy as np
 import pytest
 
@@ -11,6 +12,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # noqa: E402  (A/B build)
 
 R, T = 0, 1
 COMBOS = [(u, v) for u in (R, T) for v in (0, 1)]
@@ -116,12 +118,12 @@ def test_ragged_rows_flat_path(units, variant, mode):
     the row kernel (nt >= 1024: t windows re-aligned per row class) or the short-row kernel
     (8 <= nt < 1024: t from shared memory), the flat kernel (8
     consecutive pairs of the row-major grid per thread, rows wrapping inside a vector, nt = 1..9
-    included; for every nt with set_realign(3)) or, with both disabled / for outputs they
+    included; for every nt in the A/B build's realign = 3) or, with both disabled / for outputs they
     cannot serve, one pair per thread; bit-exact either way, at several output offsets, split
     and interleaved."""
     rng = np.random.default_rng(31 + units + 2 * variant)
-    prev = sp.set_realign(mode)
-    try:
+    # mode 1: the product; 3 (flat kernel) and 0 (one pair per thread): the A/B build
+    with (contextlib.nullcontext() if mode == 1 else ab.knobs(realign=mode)):
         for nf, nt in ((1, 1), (3, 1), (7, 2), (5, 3), (9, 7), (4, 9), (33, 1001), (257, 255), (64, 256), (5, 127),
                        (6, 129), (2, 5000)):
             f = rng.uniform(0, 400, nf).astype(np.float32)
@@ -147,8 +149,6 @@ def test_ragged_rows_flat_path(units, variant, mode):
                     assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws, wc, "split " + tag)
                     iv = io.cpu().numpy()
                     assert_parity(iv[1::2], iv[0::2], ws, wc, "inter " + tag)
-    finally:
-        sp.set_realign(prev)
 
 
 @pytest.mark.parametrize("units,variant", COMBOS)

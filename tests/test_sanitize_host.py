@@ -31,7 +31,7 @@ def test_oracle_and_generators_clean_under_asan_ubsan(tmp_path):
                     not os.path.exists("/usr/local/cuda/bin/nvcc"), reason="needs gcc and nvcc")
 def test_library_host_logic_clean_under_asan_ubsan(tmp_path):
     """The library's host code (argument validation before any CUDA call, the sharder's
-    range arithmetic up to n = 2^64 - 1, workspace sizing, tuning knobs) built with
+    range arithmetic up to n = 2^64 - 1, workspace sizing) built with
     -fsanitize=address,undefined and driven without a GPU (tests/c/abi_sanitize.py)."""
     import sys
     sys.path.insert(0, ROOT)

@@ -12,6 +12,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # A/B build (tools only)
 
 
 def timed(fn, reps=20):
@@ -28,7 +29,7 @@ def timed(fn, reps=20):
 
 
 def main():
-    L = sp.lib()
+    L = ab.lib()
     out = {}
     for count, n in ((1000, 256), (1000, 4096), (100, 65536), (2000, 1000), (10, 4096), (60, 4096)):
         base = torch.rand(count * n, device="cuda") * 200 - 100
@@ -44,7 +45,7 @@ def main():
             for tp, sp_, cp in ptrs:
                 L.sincos_pairs(tp, sp_, cp, None, n, 0, st)
 
-        arr = (sp.Item * count)(*[sp.Item(tp, sp_, cp, None, n) for tp, sp_, cp in ptrs])
+        arr = (ab.Item * count)(*[ab.Item(tp, sp_, cp, None, n) for tp, sp_, cp in ptrs])
 
         def batched():
             L.sincos_pairs_batched(ctypes.addressof(arr), count, 0, st)

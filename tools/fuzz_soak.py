@@ -20,6 +20,7 @@ import torch  # noqa: E402
 import inputs  # noqa: E402
 import oracle  # noqa: E402
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # A/B build (tools only)
 from helpers import same_values  # noqa: E402
 
 
@@ -54,9 +55,9 @@ def one_case(rng):
     if rng.random() < 0.5:
         oc = os_
     cfg = [(128, 0, 8, 1, 0), (256, 0, 8, 2, 0), (512, 4, 4, 1, 1), (128, 1, 8, 4, 0)][int(rng.integers(0, 4))]
-    sp.set_launch_config(*cfg)
-    sp.set_realign(bool(rng.random() < 0.85))
-    sp.set_pdl(bool(rng.random() < 0.7))
+    ab.set_launch_config(*cfg)
+    ab.set_realign(bool(rng.random() < 0.85))
+    ab.set_pdl(bool(rng.random() < 0.7))
     tbuf = torch.empty(n + 16, dtype=torch.float32, device="cuda")
     tbuf[ot:ot + n].copy_(torch.from_numpy(th))
     t = tbuf[ot:ot + n]
@@ -83,10 +84,10 @@ def one_case(rng):
         sp.phase_grid(torch.from_numpy(f2).cuda(), tb2[toff2:toff2 + nt2], units=sp.RADIANS, variant=variant, **outs)
     else:
         if inter:
-            sp.sincos_pairs_batched([t, t[: n // 2]], interleaved_outs=[io, torch.empty(2 * (n // 2), device="cuda")],
+            ab.sincos_pairs_batched([t, t[: n // 2]], interleaved_outs=[io, torch.empty(2 * (n // 2), device="cuda")],
                                     variant=variant)
         else:
-            sp.sincos_pairs_batched([t], [outs["sin_out"]], [outs["cos_out"]], variant=variant)
+            ab.sincos_pairs_batched([t], [outs["sin_out"]], [outs["cos_out"]], variant=variant)
     torch.cuda.synchronize()
     if inter:
         v = outs["interleaved_out"].float().cpu().numpy()
@@ -119,9 +120,9 @@ def main():
         if not ok:
             bad += 1
             first_bad = first_bad or cases
-    sp.set_launch_config()
-    sp.set_realign(True)
-    sp.set_pdl(True)
+    ab.set_launch_config()
+    ab.set_realign(True)
+    ab.set_pdl(True)
     print(json.dumps({"cases": cases, "elements": elements, "mismatching_cases": bad, "first_bad_case": first_bad,
                       "by_entry": by_entry, "seconds": round(time.time() - t0, 1), "seed": args.seed}))
 

@@ -3,12 +3,13 @@
 import sys, torch, json
 sys.path.insert(0, '.')
 import paper_cs_0406049_b200 as sp
+from paper_cs_0406049_b200 import ab  # A/B build (tools only)
 n = 1 << 28
 base = torch.rand(n + 8, device='cuda') * 2e4 - 1e4
 s = torch.empty(n + 8, device='cuda'); c = torch.empty(n + 8, device='cuda')
 res = {}
 for realign in (1, 2, 0):
-  sp.set_realign(realign)
+  ab.set_realign(realign)
   for name, (to, so, co) in {'aligned': (0, 0, 0), 'theta+1': (1, 0, 0), 'out+1': (0, 1, 1), 'all+1': (1, 1, 1),
                              'theta+4': (4, 0, 0), 'sin+1 cos+2': (0, 1, 2), 'theta+3 sin+1 cos+0': (3, 1, 0)}.items():
     th, ss, cc = base[to:to + n], s[so:so + n], c[co:co + n]
@@ -37,7 +38,7 @@ def more():
     m = sp.make_method(*sp.PAPER_METHODS[0])
     s16 = torch.empty(n, dtype=torch.float16, device='cuda'); c16 = torch.empty(n, dtype=torch.float16, device='cuda')
     for realign in (True, False):
-        sp.set_realign(realign)
+        ab.set_realign(realign)
         for to in (0, 1):
             th = base[to:to + n]
             for name, fn, bpp in (("fp16 split", lambda: sp.sincos_pairs_dtype(th, s16, c16), 8),
@@ -48,7 +49,7 @@ def more():
                 for _ in range(10): fn()
                 b.record(); torch.cuda.synchronize()
                 out[f"{name} theta+{to} realign={int(realign)}"] = round(bpp * n / (a.elapsed_time(b) / 10 / 1e3) / 1e9, 1)
-    sp.set_realign(True)
+    ab.set_realign(True)
     print(json.dumps(out))
 
 

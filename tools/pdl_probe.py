@@ -11,6 +11,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # A/B build (tools only)
 
 
 def time_steps(th, s, c, graph, steps=20, reps=5):
@@ -52,11 +53,11 @@ def main():
         s, c = torch.empty_like(th), torch.empty_like(th)
         for graph in (False, True):
             for pdl in (False, True, False, True):
-                sp.set_pdl(pdl)
+                ab.set_pdl(pdl)
                 us = time_steps(th, s, c, graph)
                 key = f"2^{lg} {'graph' if graph else 'stream'} pdl={int(pdl)}"
                 res[key] = min(res.get(key, 1e18), round(us, 2))
-    sp.set_pdl(True)
+    ab.set_pdl(True)
     print(json.dumps({"us_per_step_N_then_A": res}))
 
 

@@ -14,6 +14,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # A/B build (tools only)
 
 
 MIN_NT = int(os.environ.get("ROWS_MIN_NT", "256"))   # the library's kPhaseRowsMinNt (A/B builds)
@@ -30,7 +31,7 @@ def main():
         for inter, mode in ((False, 1), (True, 1), (False, 3), (True, 3)):
             if mode == 3 and nt % 8 == 0 and toff == 0:
                 continue
-            sp.set_realign(mode)
+            ab.set_realign(mode)
             if inter:
                 outs = {"interleaved_out": torch.empty(2 * n, device="cuda")}
             else:
@@ -48,7 +49,7 @@ def main():
                                                              "short" if mode == 1 and nt >= 8 else "flat")
             res[f"nt={nt} toff={toff} {'inter' if inter else 'split'} {kern}"] = round(8 * n / (ms / 1e3) / 1e9, 1)
             del outs
-    sp.set_realign(1)
+    ab.set_realign(1)
     print(json.dumps(res))
 
 

@@ -12,6 +12,7 @@ import torch  # noqa: E402
 
 import inputs  # noqa: E402
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # A/B build (tools only)
 
 
 def main():
@@ -21,10 +22,10 @@ def main():
     c = torch.empty(n, device="cuda")
     io = torch.empty(2 * n, device="cuda")
     for u in (1, 2, 4):
-        sp.set_launch_config(unroll=u)
+        ab.set_launch_config(unroll=u)
         for v in (sp.NORMALIZED, sp.RENORMALIZED):
             sp.sincos_pairs(th, s, c, variant=v)
-    sp.set_launch_config()
+    ab.set_launch_config()
     for v in (sp.NORMALIZED, sp.RENORMALIZED):
         sp.sincos_pairs(th, interleaved_out=io, variant=v)
     sp.null_4in8out(th, s, c)

@@ -11,6 +11,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # A/B build (tools only)
 from bench import c4_axes, fit_method  # noqa: E402
 
 
@@ -21,7 +22,7 @@ def main():
     for packed, units, kw in ((1, sp.RADIANS, {"variant": 0}), (1, sp.TURNS, {"variant": 0}),
                               (0, sp.RADIANS, {"variant": 0}), (0, sp.TURNS, {"variant": 0}),
                               (1, sp.TURNS, {"method": fit_method(1, 3, 2)})):
-        sp.set_nudft_packed(bool(packed))
+        ab.set_nudft_packed(bool(packed))
         f, t = c4_axes(units == sp.TURNS)
         sp.nudft(torch.from_numpy(f).cuda(), torch.from_numpy(t).cuda(), a, units=units, **kw)
     torch.cuda.synchronize()

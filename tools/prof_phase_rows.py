@@ -13,6 +13,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # A/B build (tools only)
 
 CASES = (((1 << 15) - 1, 0, False, 1), ((1 << 15) - 1, 0, False, 3), ((1 << 15) - 1, 0, True, 1),
          (4000, 5, False, 1), (1001, 0, False, 1), ((1 << 15) + 4, 0, False, 1))
@@ -21,7 +22,7 @@ for nt, toff, inter, mode in CASES[int(sys.argv[1]):] if len(sys.argv) > 1 else 
     f = torch.rand(nf, device="cuda") * 512
     t = torch.rand(nt + 8, device="cuda")[toff:toff + nt]
     n = nf * nt
-    sp.set_realign(mode)
+    ab.set_realign(mode)
     if inter:
         outs = {"interleaved_out": torch.empty(2 * n, device="cuda")}
     else:
@@ -29,5 +30,5 @@ for nt, toff, inter, mode in CASES[int(sys.argv[1]):] if len(sys.argv) > 1 else 
     sp.phase_grid(f, t, units=sp.TURNS, **outs)
     torch.cuda.synchronize()
     del outs
-sp.set_realign(1)
+ab.set_realign(1)
 print("ok")

@@ -11,9 +11,10 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # A/B build (tools only)
 
 for nt, toff, mode in ((65, 0, 1), (100, 1, 1), (65, 0, 3)):
-    sp.set_realign(mode)
+    ab.set_realign(mode)
     nf = (1 << 30) // nt
     f = torch.rand(nf, device="cuda") * 512
     t = torch.rand(nt + 8, device="cuda")[toff:toff + nt]
@@ -22,5 +23,5 @@ for nt, toff, mode in ((65, 0, 1), (100, 1, 1), (65, 0, 3)):
     sp.phase_grid(f, t, s, c, units=sp.TURNS)
     torch.cuda.synchronize()
     del s, c
-sp.set_realign(1)
+ab.set_realign(1)
 print("ok")

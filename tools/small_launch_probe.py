@@ -11,6 +11,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # A/B build (tools only)
 
 CFGS = [(128, 0, 8, 1, 0), (256, 0, 8, 1, 0), (512, 0, 8, 1, 0), (128, 0, 4, 1, 0), (256, 0, 4, 1, 0),
         (128, 0, 8, 2, 0), (256, 2, 8, 1, 0), (512, 1, 8, 1, 0)]
@@ -23,7 +24,7 @@ def main():
         th = torch.rand(n, device="cuda") * 100
         s, c = torch.empty_like(th), torch.empty_like(th)
         for cfg in CFGS:
-            sp.set_launch_config(*cfg)
+            ab.set_launch_config(*cfg)
             for _ in range(3):
                 sp.sincos_pairs(th, s, c)
             cap = torch.cuda.Stream()
@@ -44,7 +45,7 @@ def main():
                 torch.cuda.synchronize()
                 best = min(best, a.elapsed_time(b) / 50 * 1e3)
             res.setdefault(f"2^{lg}", {})[",".join(map(str, cfg))] = round(best, 2)
-    sp.set_launch_config()
+    ab.set_launch_config()
     print(json.dumps({"us_per_launch": res}))
 
 

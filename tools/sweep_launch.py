@@ -21,6 +21,7 @@ import torch  # noqa: E402
 
 import inputs  # noqa: E402
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # A/B build (tools only)
 
 
 def main():
@@ -60,7 +61,7 @@ def main():
 
     for _ in range(args.rounds):
         for c in cands:
-            sp.set_launch_config(*c)
+            ab.set_launch_config(*c)
             res[c]["N"].append(timeit(lambda: sp.sincos_pairs(th, variant=0, **outs)))
             res[c]["A"].append(timeit(lambda: sp.sincos_pairs(th, variant=1, **outs)))
             res[c]["null"].append(timeit(lambda: sp.null_4in8out(th, **outs)))

@@ -11,6 +11,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_cs_0406049_b200 as sp  # noqa: E402
+from paper_cs_0406049_b200 import ab  # A/B build (tools only)
 from bench import c4_axes, fit_method  # noqa: E402
 
 
@@ -21,7 +22,7 @@ def main():
     out = {}
     packed = os.environ.get("NUDFT_PACKED")
     if packed is not None:
-        sp.set_nudft_packed(packed == "1")
+        ab.set_nudft_packed(packed == "1")
     for units in (sp.RADIANS, sp.TURNS):
         f, t = c4_axes(units == sp.TURNS)
         fd, td = torch.from_numpy(f).cuda(), torch.from_numpy(t).cuda()

@@ -1,0 +1,117 @@
+"""Full-array parity at BASELINE.json's largest sizes, every element (``pytest -m gpu``).
+
+north_star: "GPU output matching the oracle ... on all five configs".  C1-C3 are compared in
+full in test_gpu_parity.py; here C4 (configs[3], 2^30 NUFFT phases) and C5 (configs[4], 2^32
+normal angles, 16 GiB in / 32 GiB out) run on one GPU at full size, in the launch
+configuration bench.py times (one launch over the whole array), both variants, both output
+layouts, and every element is compared with the oracle on the regenerated inputs -- chunk by
+chunk: the host regenerates a chunk of theta (the shared generator), runs the threaded C
+oracle on it, copies its pairs to the device and compares there.
+
+The comparison is of BIT PATTERNS (only NaN payloads are excused, G8): a sign-of-zero
+difference (the kernel's RN product vs Fig. 1's vec_madd(a, b, 0.0) = fmaf(a, b, +0)) would
+fail here, and the same raw comparison runs over all 2^32 fp32 bit patterns, where every
+signed zero, subnormal and non-finite input occurs.  Runtime (one B200 box, 16 host threads):
+about a minute in all, dominated by the host generator and oracle.
+"""
+import time
+
+import numpy as np
+import pytest
+
+import inputs
+from helpers import oracle_threaded
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_cs_0406049_b200 as sp  # noqa: E402
+
+CHUNK = 1 << 27
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+    torch.cuda.empty_cache()
+
+
+def gen_to_device(config, n):
+    dev = torch.empty(n, dtype=torch.float32, device="cuda")
+    host = torch.empty(min(CHUNK, n), dtype=torch.float32).pin_memory()
+    for off in range(0, n, CHUNK):
+        m = min(CHUNK, n - off)
+        inputs.generate(config, off, m, out=host.numpy()[:m])
+        dev[off:off + m].copy_(host[:m])
+    return dev
+
+
+def bit_mismatches(got, want):
+    """Positions where the float32 tensors differ in bit pattern (NaN matching any NaN)."""
+    same = (got.view(torch.int32) == want.view(torch.int32)) | (torch.isnan(got) & torch.isnan(want))
+    return torch.nonzero(~same).flatten()
+
+
+def full_compare(config, variant):
+    """Every element of config `config`, one variant, split and interleaved outputs."""
+    n = inputs.size(config)
+    t0 = time.perf_counter()
+    th = gen_to_device(config, n)
+    s = torch.empty(n, dtype=torch.float32, device="cuda")
+    c = torch.empty(n, dtype=torch.float32, device="cuda")
+    io = torch.empty(2 * n, dtype=torch.float32, device="cuda")
+    before = sp.launch_count()
+    sp.sincos_pairs(th, s, c, variant=variant)                  # one launch each, whole array
+    sp.sincos_pairs(th, interleaved_out=io, variant=variant)
+    torch.cuda.synchronize()
+    assert sp.launch_count() - before == 2
+    pairs = io.view(n, 2)
+    checked = 0
+    for off in range(0, n, CHUNK):
+        m = min(CHUNK, n - off)
+        th_h = inputs.generate(config, off, m)                     # regenerated on the host
+        ws, wc = oracle_threaded(th_h, variant)
+        wsd, wcd = torch.from_numpy(ws).cuda(), torch.from_numpy(wc).cuda()
+        for name, got_s, got_c in (("split", s[off:off + m], c[off:off + m]),
+                                   ("interleaved", pairs[off:off + m, 1], pairs[off:off + m, 0])):
+            for comp, got, want in (("sin", got_s, wsd), ("cos", got_c, wcd)):
+                bad = bit_mismatches(got, want)
+                if bad.numel():
+                    i = int(bad[0])
+                    raise AssertionError(
+                        f"config {config} variant {variant} {name} {comp}: {bad.numel()} bit mismatches in chunk "
+                        f"at {off}; first at {off + i}: theta {th_h[i]!r} got {float(got[i])!r} "
+                        f"(0x{int(got.view(torch.int32)[i]) & 0xFFFFFFFF:08X}) want {float(want[i])!r} "
+                        f"(0x{int(want.view(torch.int32)[i]) & 0xFFFFFFFF:08X})")
+        checked += m
+    assert checked == n
+    del th, s, c, io
+    torch.cuda.empty_cache()
+    return time.perf_counter() - t0
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_c4_full(variant):
+    """BASELINE configs[3]: 2^30 NUFFT phases 2 pi f_i t_j (seed 3), every element, split and
+    interleaved, bit for bit."""
+    dt = full_compare(4, variant)
+    print(f"C4 variant {variant}: 2^30 elements x 2 layouts in {dt:.1f} s")
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_c5_full(variant):
+    """BASELINE configs[4]: 2^32 N(0, 100^2) (seed 4), 64-bit indexing past 2^31 and 2^32-1,
+    every element, split and interleaved, bit for bit."""
+    dt = full_compare(5, variant)
+    print(f"C5 variant {variant}: 2^32 elements x 2 layouts in {dt:.1f} s")
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_all_fp32_bit_patterns_raw_bits(variant):
+    """Every one of the 2^32 fp32 inputs (theta_i = bits(i)): the kernel's output BITS equal the
+    oracle's, split and interleaved -- signed zeros included (the whole-space hash tests
+    canonicalise +-0; this one does not), NaN payloads excused."""
+    dt = full_compare(0, variant)
+    print(f"all 2^32 bit patterns variant {variant}: x 2 layouts in {dt:.1f} s")

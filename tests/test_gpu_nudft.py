@@ -83,10 +83,52 @@ def test_uniform_grid_matches_fft():
     assert np.all(np.abs(got - want) <= 4.9e-7 * np.abs(a).sum() + bound(a, want, N))
 
 
+def oracle_nudft_threaded(f, t, a, units, variant, block=256):
+    """oracle.nudft over blocks of frequencies on all host threads (per-row numerics unchanged)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    spans = [(i, min(i + block, f.size)) for i in range(0, f.size, block)]
+    with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+        parts = list(ex.map(lambda ab: oracle.nudft(f[ab[0]:ab[1]], t, a, units, variant), spans))
+    return np.concatenate(parts)
+
+
+def run_model_bound(f, t, a, units, variant, chunk):
+    """Per-row error bound of the fused sum from its documented arithmetic, evaluated on this
+    run's own partial sums (not the worst case): every term enters its fp32 accumulators by
+    two single-rounding FMAs in order -- re += ar c; re -= ai s; im += ar s; im += ai c --
+    over runs of `chunk` consecutive terms (aligned to multiples of chunk), each run then
+    added into fp64, the fp64 total rounded once to fp32.  An FMA's rounding error is at most
+    2^-24 of its result, so a run's error is at most 2^-24 times the sum of |partial sum| over
+    its steps (to first order; the factor 1.01 covers the second order at <= 2048 steps);
+    fp64 adds contribute ~2^-53 of the same sums; the final rounding 2^-24 |F|.  The exact
+    partial sums are formed here in fp64 from the oracle's pairs (products of two fp32 values
+    are exact in fp64).  Returns (bound per row, F per row from the same fp64 sums)."""
+    sp_, cp = oracle.phase_grid(f, t, units, variant)
+    s64, c64 = sp_.astype(np.float64), cp.astype(np.float64)
+    ar, ai = a.real.astype(np.float64)[None, :], a.imag.astype(np.float64)[None, :]
+    m, nt = s64.shape
+    nrun = -(-nt // chunk)
+    out = []
+    for steps in (np.stack([ar * c64, -ai * s64], axis=-1), np.stack([ar * s64, ai * c64], axis=-1)):
+        st = np.zeros((m, nrun * chunk, 2))
+        st[:, :nt] = steps
+        part = np.cumsum(st.reshape(m, nrun, 2 * chunk), axis=-1)      # partials inside each run
+        out.append((np.abs(part).sum(axis=(1, 2)), part[:, :, -1].sum(axis=1)))
+    (pr, fr), (pi, fi) = out
+    F = fr + 1j * fi
+    b = 1.01 * U * (pr + pi) + 2.0 ** -50 * (pr + pi)
+    return b + U * (np.abs(F) + b), F
+
+
 @pytest.mark.parametrize("units", [0, 1])
-def test_c4_scale_sampled(units):
-    """The C4 shape (2^15 frequencies x 2^15 jittered times, 2^30 terms), 64 sampled k vs the
-    oracle."""
+@pytest.mark.parametrize("variant", [0, 1])
+def test_c4_scale_per_run_bound(units, variant):
+    """The C4 shape (2^15 frequencies x 2^15 jittered times, 2^30 terms, random complex
+    amplitudes), 64 sampled k against the oracle within the per-run bound of THIS run's partial
+    sums -- ~16x tighter than the worst-case header bound.  Negative control: for every sampled
+    k the bound is smaller than the term of median |a_j| would be, so one lost or doubled term
+    in any row, tile, chunk or segment fails."""
     nf = nt = 1 << 15
     rng = np.random.default_rng(7)
     f = (512 * rng.random(nf)).astype(np.float32)
@@ -94,10 +136,50 @@ def test_c4_scale_sampled(units):
         f = (2 * np.pi * f.astype(np.float64)).astype(np.float32)
     t = ((np.arange(nt) + rng.random(nt)) * 2.0 ** -15).astype(np.float32)
     a = rand_complex(rng, nt)
-    got = run(f, t, a, units, 0)
+    got = run(f, t, a, units, variant)
     ks = np.unique(np.concatenate([[0, nf - 1], rng.integers(0, nf, 62)]))
-    want = oracle.nudft(f[ks], t, a, units, 0)
-    assert np.all(np.abs(got[ks] - want) <= bound(a, want, nt))
+    want = oracle.nudft(f[ks], t, a, units, variant)
+    b, F = run_model_bound(f[ks], t, a, units, variant, sp.nudft_chunk(nt))
+    assert np.allclose(F, want, rtol=0, atol=1e-9 * np.abs(a).sum())     # the model's sums are the oracle's
+    err = np.abs(got[ks] - want)
+    assert np.all(err <= b), (err / b).max()
+    worst = bound(a, want, nt)
+    assert np.all(b < worst / 10), (b / worst).max()                       # >= 10x tighter than the header bound
+    j_med = int(np.argsort(np.abs(a))[nt // 2])
+    assert np.all(np.abs(a[j_med]) > b), (np.abs(a[j_med]), b.max())      # one lost term would fail
+    print(f"units {units} variant {variant}: max err/bound {(err / b).max():.3f}, bound {b.max():.3g}, "
+          f"median |a_j| {np.abs(a[j_med]):.3f}")
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("imag", [False, True])
+def test_c4_shape_exact_sum(variant, imag):
+    """An exact case at the C4 shape (2^15 x 2^15): phases in turns p = RN(f_k m_j / 2) with
+    integer f_k in [0, 512) and integer m_j, so q = p - rint(p) is 0 or +-1/2, where the method's
+    cosine is exactly +1 or -1 (c = -1 iff f_k and m_j are both odd); small-integer amplitudes,
+    all real (or all imaginary).  Then every fp32 partial sum of the real (imaginary) part is a
+    small integer -- exact -- and the sum over all 2^15 terms, across every tile, chunk and
+    segment boundary, must equal the oracle's (exact, fp64) sum BIT FOR BIT, for every k.  The
+    other part (multiples of the tiny sine at q = +-1/2) within the per-run bound."""
+    nf = nt = 1 << 15
+    rng = np.random.default_rng(11 + variant + 2 * imag)
+    f = rng.integers(0, 512, nf).astype(np.float32)
+    mj = rng.integers(0, 1 << 15, nt)
+    t = (mj / 2.0).astype(np.float32)
+    amp = rng.integers(-3, 4, nt).astype(np.float32)
+    a = (1j * amp if imag else amp + 0j).astype(np.complex64)
+    got = run(f, t, a, 1, variant)
+    want = oracle_nudft_threaded(f, t, a, 1, variant)
+    ex_got, ex_want = (got.imag, want.imag) if imag else (got.real, want.real)
+    assert np.all(ex_want == np.rint(ex_want))                          # the exact part: integers
+    assert np.array_equal(ex_got, ex_want.astype(np.float32).astype(np.float64))
+    # not degenerate: the parity pattern and the amplitudes make the rows differ
+    odd = f.astype(np.int64) % 2 == 1
+    assert np.unique(ex_want[odd]).size == 1 and np.unique(ex_want[~odd]).size == 1
+    assert ex_want[odd][0] != ex_want[~odd][0]
+    ks = np.unique(np.concatenate([[0, nf - 1], rng.integers(0, nf, 30)]))
+    b, _ = run_model_bound(f[ks], t, a, 1, variant, sp.nudft_chunk(nt))
+    assert np.all(np.abs(got[ks] - want[ks]) <= b)
 
 
 def test_edges():

@@ -419,7 +419,7 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
         const bool short_rows = T.realign != 3 && nt < kPhaseRowsMinNt;
         // the short-row kernel stages t in shared memory once per block: a grid of a few
         // blocks per SM, grid-striding, amortises that
-        const size_t cap = static_cast<size_t>(sm_count(dev)) * kPhaseShortBlocksPerSm;
+        const size_t cap = static_cast<size_t>(sm_count(dev)) * phase_short_blocks_per_sm(nt);
         if (short_rows && grid > cap) grid = cap;
         e = launch_phase_flat(variant, inter, units == SINCOS_TURNS, f_dev, nf, t_dev, nt, sin_dev, cos_dev,
                               inter_dev, head, nvec, static_cast<unsigned>(grid), short_rows,

@@ -104,10 +104,18 @@ constexpr size_t kPhaseRowsPerBlock = SINCOS_PHASE_ROWS_PER_BLOCK;   // target r
 #define SINCOS_PHASE_VEC_MIN_NT 256
 #endif
 constexpr size_t kPhaseVecMinNt = SINCOS_PHASE_VEC_MIN_NT;     // aligned rows shorter: the short-row kernel
+// Short-row kernel grid, blocks per SM (grid-striding): rows of >= 256 pairs 64 (nt = 1001
+// interleaved: 6.37 vs 6.05 TB/s at 256), shorter rows 256 (nt = 2..9: 3% ahead of 64;
+// tools/ab_phase.py, profiles/r02/ab_phase_short.jsonl).
 #ifndef SINCOS_PHASE_SHORT_BPS
 #define SINCOS_PHASE_SHORT_BPS 256
 #endif
-constexpr size_t kPhaseShortBlocksPerSm = SINCOS_PHASE_SHORT_BPS;     // short-row kernel grid, per SM
+#ifndef SINCOS_PHASE_SHORT_BPS_LONG
+#define SINCOS_PHASE_SHORT_BPS_LONG 64
+#endif
+constexpr size_t phase_short_blocks_per_sm(size_t nt) {
+    return nt >= 256 ? SINCOS_PHASE_SHORT_BPS_LONG : SINCOS_PHASE_SHORT_BPS;
+}
 cudaError_t launch_phase_rows(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
                               size_t nt, float *so, float *co, float *io, unsigned h0, int sms,
                               cudaStream_t stream);

@@ -14,22 +14,55 @@ namespace sincos_b200 {
 // KB3c: the outputs are what does not share theta's alignment (split: sin and cos at
 // different offsets mod 16 B; interleaved: only 4-B aligned pairs).  The frame is theta's:
 // thread v loads the aligned 256-bit theta[head + 8v ..] and computes its eight pairs; each
-// output stream X sits K_X floats past a 32-B boundary at that frame and is written as
-// whole aligned vectors anyway -- the block of X that thread v stores holds the last K_X values
-// of thread v-1 (one warp shuffle up) and its own first values.  A warp's lane 0 has no
-// predecessor in the warp and stores its own part one float at a time; the warp's last
-// active lane stores the K_X values that spill into the next warp's frame the same way, so
-// every element is written exactly once.  K_X is warp-uniform at run time (a switch over
-// register moves).  Head [0, head) and tail one element per thread.  Same numerics.
+// output stream X sits k_X floats past a 32-B boundary at that frame and is written as
+// whole aligned 32-B blocks anyway -- the block of X that thread v stores holds the last k_X
+// values of thread v-1 (warp shuffles up) and its own first values; for k_X > 4, mirrored, its
+// own last values and the first 8 - k_X of thread v+1 (shuffles down: never more than four
+// shuffles per stream; with seven, k = 7 ran 10% slower than k = 1).  A warp's lane 0 has no
+// predecessor in the warp: it stores the part of its first block that is its own (floats
+// [k, 8) of that block) and the warp's last active lane the k values that spill into the next
+// warp's frame (floats [0, k) of the next block) -- each as at most three naturally aligned
+// pieces (16 / 8 / 4 B) when k is a compile-time constant (the first form stored these one
+// float at a time: 8 scalar stores per stream and warp, 16 for interleaved pairs; ncu: issue
+// slots 65-69% busy against the aligned kernel's 48%).  Every element is written exactly once.
+// (A form that let the previous warp store the whole edge block through shared memory needed
+// a CTA barrier per trip and ran 15-20% slower: the barrier couples the warps' HBM latencies.)
+// k_X is a template parameter (KC >= 0) for the cases that occur, else warp-uniform at run time
+// (a switch over register moves, single-float edge stores).  Head [0, head) and tail one
+// element per thread.  Same numerics as every other path.
 template <int K, int W>
 __device__ __forceinline__ void shift_block(const float (&prev)[W], const float (&val)[W], float (&blk)[W]) {
 #pragma unroll
     for (int j = 0; j < W; ++j) blk[j] = j < K ? prev[W - K + j] : val[j - K];
 }
 
+__device__ __forceinline__ void st_piece(float *p, const float *r, int m) {
+    if (m == 4)
+        asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
+                     :: "l"(p), "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]) : "memory");
+    else if (m == 2)
+        asm volatile("st.global.L1::no_allocate.v2.f32 [%0], {%1,%2};"
+                     :: "l"(p), "f"(r[0]), "f"(r[1]) : "memory");
+    else
+        asm volatile("st.global.L1::no_allocate.f32 [%0], %1;" :: "l"(p), "f"(r[0]) : "memory");
+}
+
+// Floats [A, B) of the 32-B block at `blk` from r[0 .. B - A), as naturally aligned pieces
+// (largest first at each position): at most three stores.
+template <int A, int B>
+__device__ __forceinline__ void store_range(float *blk, const float *r) {
+    if constexpr (A < B) {
+        constexpr int al = (A & 1) ? 1 : (A & 2) ? 2 : (A & 4) ? 4 : 8;   // alignment of position A
+        constexpr int m = al < (B - A) ? al : ((B - A) >= 4 ? 4 : (B - A) >= 2 ? 2 : 1);
+        constexpr int mm = m > 4 ? 4 : m;
+        st_piece(blk + A, r, mm);
+        store_range<A + mm, B>(blk, r + mm);
+    }
+}
+
 // Store the W values `val` (W = 8 or 16) of floats [f0, f0 + W) of stream x, whose aligned
 // 8-float (32-B) blocks start k floats (0..7) before f0.  All 32 lanes call it (shuffles).
-// KC >= 0: k known at compile time (== KC); KC < 0: k at run time (a switch over register moves).
+// KC >= 0: k known at compile time (== KC); KC < 0: k at run time.
 template <int W, int KC>
 __device__ __forceinline__ void store_realigned(float *x, size_t f0, const float (&val)[W], int k_rt, unsigned lane,
                                                 bool act, bool last) {
@@ -41,7 +74,27 @@ __device__ __forceinline__ void store_realigned(float *x, size_t f0, const float
         }
         return;
     }
-    // only the predecessor's last k <= 7 values are ever used: shuffle those (7, or K)
+    if constexpr (KC > 4) {
+        // k > 4: the blocks the thread stores start 8 - k floats into its own values and end with
+        // the successor's first 8 - k (shuffled down: 8 - k < 4 shuffles instead of k)
+        constexpr int D = 8 - KC;
+        float next[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) next[j] = j < D ? __shfl_down_sync(0xFFFFFFFFu, val[j], 1) : 0.0f;
+        if (!act) return;
+        if (lane == 0) store_range<KC, 8>(x + f0 - KC, val);          // its head: floats [k, 8) of a block
+        if constexpr (W == 16) store8(x + f0 + D, val + D);              // its own whole block
+        if (last) {
+            store_range<0, KC>(x + f0 + W - KC, val + W - KC);         // no successor: a partial block
+        } else {
+            float blk[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) blk[j] = j < KC ? val[W - KC + j] : next[j - KC];
+            store8(x + f0 + W - KC, blk);
+        }
+        return;
+    }
+    // k <= 4 (or at run time): only the predecessor's last k values are used: shuffle those
     constexpr int NS = KC > 0 ? KC : 7;
     float prev[W];
 #pragma unroll
@@ -65,22 +118,45 @@ __device__ __forceinline__ void store_realigned(float *x, size_t f0, const float
 #pragma unroll
         for (int h = 0; h < W; h += 8) store8(x + f0 - k + h, blk + h);
     } else {
+        // lane 0: floats [k, 8) of its first block, then (W = 16) its one whole block
+        if constexpr (KC > 0) {
+            store_range<KC, 8>(x + f0 - KC, val);
+            if constexpr (W == 16) store8(x + f0 + 8 - KC, val + 8 - KC);
+        } else {
 #pragma unroll
-        for (int j = 0; j < W; ++j)
-            if (j < W - k) x[f0 + j] = val[j];
+            for (int j = 0; j < W; ++j)
+                if (j < W - k) x[f0 + j] = val[j];
+        }
     }
     if (last) {
+        // floats [0, k) of the block after the thread's last one
+        if constexpr (KC > 0) {
+            store_range<0, KC>(x + f0 + W - KC, val + W - KC);
+        } else {
 #pragma unroll
-        for (int j = 0; j < W; ++j)
-            if (j >= W - k) x[f0 + j] = val[j];
+            for (int j = 0; j < W; ++j)
+                if (j >= W - k) x[f0 + j] = val[j];
+        }
     }
 }
 
 // KI: the interleaved stream's offset at compile time (1, 3, 5, 7: pairs only 4-B aligned), or
 // for split outputs KI = 8 * KS + KC with both offsets at compile time (0..63), or -1 (both at
 // run time)
+// Register budget: most instances need 34-40 registers, which leaves 12 resident 128-thread
+// blocks per SM (75% occupancy); capped at 32 (16 blocks, full occupancy, a few bytes of
+// spill) they run faster where the kernel waits on HBM -- measured for the split instances
+// (sin+2 cos+5: 6.46 -> 6.67 TB/s) and the interleaved ones with k <= 4 (k = 3: 6.61 -> 6.68),
+// slower for interleaved k > 4 (k = 7: 6.85 -> 6.55; tools/ab_layouts.py, profiles/r02).  The
+// capped instances take 128-thread blocks (launch_outshift).
+template <bool INTER, int KI>
+constexpr int outshift_min_blocks() { return !INTER || (KI >= 0 && KI <= 4) ? 16 : 1; }
+template <bool INTER, int KI>
+constexpr int outshift_max_threads() { return outshift_min_blocks<INTER, KI>() > 1 ? 128 : 512; }
+
 template <int V, bool INTER, int KI>
-__global__ void __launch_bounds__(512) sincos_outshift_kernel(const float *theta, float *so, float *co, float *io,
+__global__ void __launch_bounds__(outshift_max_threads<INTER, KI>(), outshift_min_blocks<INTER, KI>())
+sincos_outshift_kernel(const float *theta, float *so, float *co, float *io,
                                                               size_t head, size_t nvec, size_t n, int ks, int kc) {
     const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
@@ -139,6 +215,10 @@ cudaError_t launch_outshift(int variant, bool inter, int ks, int kc, unsigned gr
                      : variant == kRenormalized ? pick_outshift<kRenormalized>(inter, ks, kc)
                                                 : pick_outshift<kNull>(inter, ks, kc);
     void *args[] = {&theta, &so, &co, &io, &head, &nvec, &n, &ks, &kc};
+    if (threads > 128) {            // (A/B block sizes) the register-capped instances take 128 at most
+        grid = static_cast<unsigned>((static_cast<size_t>(grid) * threads + 127) / 128);
+        threads = 128;
+    }
     return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, 0, stream);
 }
 

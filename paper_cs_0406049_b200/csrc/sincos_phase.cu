@@ -416,28 +416,46 @@ cudaError_t launch_phase_rows(int variant, bool inter, bool turns, const float *
 }
 
 // Short rows (1 <= nt < kPhaseRowsMinNt = 1024): the flat kernel's mapping (8 consecutive pairs of the
-// row-major grid per thread, (i, j) of the first by the corrected fp64 quotient) with one code
-// path for every vector -- a warp spans several short rows, and the flat kernel's separate
-// in-row / row-boundary forms ran both in most warps (17 of 32 lanes active per instruction).
+// row-major grid per thread) with one code path for every vector -- a warp spans several short
+// rows, and the flat kernel's separate in-row / row-boundary forms ran both in most warps (17 of
+// 32 lanes active per instruction).
 // t comes from shared memory: four copies ts[r][m] = t[(m + r) mod nt], so that the window
 // t[(j .. j+7) mod nt] (wrapping into the next row's first t-values) is ts[j & 3][(j & ~3) ..]:
 // two aligned 128-bit loads and no selection; each pair takes f_i or f_{i+1} by a select
-// (nt < 8: f_{i + (j + k) / nt}, the row offsets from a 16-entry table).
-// 16.6 KB of shared memory per block; a grid of 256 blocks per SM, grid-striding (fewer blocks
-// with longer strides measured slower, the full grid too: tools/ab_phase.py).  Below 1024 it
-// beats the row kernel, whose slots are partly idle and which pays per-row ends.
+// (SMALL, nt < 8: f_{i + (j + k) / nt}, the row offsets from a 16-entry table).
+// The grid strides by a fixed number of pairs, 8 x (threads in the grid) = step_q nt + step_r
+// (host-computed), so a thread advances its (row, column) by integer adds and one compare per
+// vector -- only its first vector needs the fp64 quotient -- and the f values of its next
+// vector are loaded before this one's arithmetic: the f fetch latency, which bound the first
+// form of this kernel (per-vector fp64 divmod -> dependent f load: ncu 10.8 long-scoreboard
+// stalls per issue), overlaps the method.
+// 16.6 KB of shared memory per block; phase_short_blocks_per_sm(nt) blocks per SM, grid-striding.
 constexpr int kShortNtMax = static_cast<int>(kPhaseRowsMinNt);
 constexpr int kShortStride = kShortNtMax + 16;                              // floats per copy (16-B rows)
 static_assert(4 * kShortStride * sizeof(float) + 16 <= 48 * 1024,
               "short-row kernel: four t copies must fit static shared memory (kPhaseRowsMinNt too large)");
 static_assert(kShortStride % 4 == 0, "short-row kernel: copies must start 16-B aligned");
 
-template <int V, bool INTER, bool TURNS>
+// the f values of the vector whose first pair is (i, j): f0 = f_i, f1 = f_{i+1} when the row ends
+// inside the vector (nt >= 8); SMALL (nt < 8): fr[k] = f_{i + (j + k) / nt}
+template <bool SMALL>
+__device__ __forceinline__ void short_f(const float *__restrict__ f, size_t i, unsigned j, unsigned ntu,
+                                        const unsigned char *rowoff, float (&fr)[8]) {
+    if constexpr (SMALL) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) fr[k] = __ldg(f + i + rowoff[j + k]);
+    } else {
+        fr[0] = __ldg(f + i);
+        fr[1] = ntu - j < 8u ? __ldg(f + i + 1) : fr[0];        // row i+1 exists when reached
+    }
+}
+
+template <int V, bool INTER, bool TURNS, bool SMALL>
 __global__ void __launch_bounds__(kPhaseThreads) phase_grid_short(const float *__restrict__ f,
                                                                  const float *__restrict__ t, size_t nf,
                                                                  size_t nt, float *so, float *co, float *io,
                                                                  size_t head, size_t nvec, size_t n,
-                                                                 double inv_nt) {
+                                                                 double inv_nt, size_t step_q, unsigned step_r) {
     __shared__ __align__(16) float ts[4][kShortStride];
     __shared__ unsigned char rowoff[16];                                  // m / nt (nt < 8)
     const unsigned ntu = static_cast<unsigned>(nt);
@@ -452,24 +470,37 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_short(const float *_
     const size_t tail0 = head + 8 * nvec;
     if (tid < head) phase_one<V, INTER, TURNS>(f, t, nt, inv_nt, tid, so, co, io);
     if (tid < n - tail0) phase_one<V, INTER, TURNS>(f, t, nt, inv_nt, tail0 + tid, so, co, io);
-    for (size_t v = tid; v < nvec; v += nthr) {
+    size_t v = tid;
+    if (v >= nvec) return;
+    size_t i, j0;
+    divmod_nt(head + 8 * v, nt, inv_nt, i, j0);
+    unsigned j = static_cast<unsigned>(j0);
+    float fr[8];
+    short_f<SMALL>(f, i, j, ntu, rowoff, fr);
+    for (;;) {
         const size_t e0 = head + 8 * v;
-        size_t i, j;
-        divmod_nt(e0, nt, inv_nt, i, j);
-        const unsigned ju = static_cast<unsigned>(j), r = ju & 3u;
-        const float4 *w = reinterpret_cast<const float4 *>(&ts[r][ju - r]);
+        // the next vector: (i, j) + step pairs, and its f values issued now
+        const size_t vn = v + nthr;
+        size_t in = i + step_q;
+        unsigned jn = j + step_r;
+        if (jn >= ntu) {
+            jn -= ntu;
+            ++in;
+        }
+        float gr[8];
+        if (vn < nvec) short_f<SMALL>(f, in, jn, ntu, rowoff, gr);
+        const unsigned r = j & 3u;
+        const float4 *w = reinterpret_cast<const float4 *>(&ts[r][j - r]);
         const float4 w0 = w[0], w1 = w[1];
         const float tv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
         float fv[8];
-        if (ntu >= 8u) {                                                  // at most one row boundary
-            const unsigned kw = ntu - ju;                                 // first pair of row i+1
-            const float f0 = __ldg(f + i);
-            const float f1 = kw < 8u ? __ldg(f + i + 1) : f0;             // row i+1 exists when reached
+        if constexpr (SMALL) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) fv[k] = static_cast<unsigned>(k) >= kw ? f1 : f0;
-        } else {                                                          // nt < 8: several rows
+            for (int k = 0; k < 8; ++k) fv[k] = fr[k];
+        } else {
+            const unsigned kw = ntu - j;                                  // first pair of row i+1
 #pragma unroll
-            for (int k = 0; k < 8; ++k) fv[k] = __ldg(f + i + rowoff[ju + k]);
+            for (int k = 0; k < 8; ++k) fv[k] = static_cast<unsigned>(k) >= kw ? fr[1] : fr[0];
         }
         float sv[8], cv[8];
         phase8f<V, TURNS>(fv, tv, sv, cv);
@@ -486,12 +517,19 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_short(const float *_
             st8_stream(so + e0, sv);
             st8_stream(co + e0, cv);
         }
+        if (vn >= nvec) break;
+        v = vn;
+        i = in;
+        j = jn;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) fr[k] = gr[k];
     }
 }
 
 template <int V, bool INTER, bool TURNS>
-static const void *pick_short() {
-    return reinterpret_cast<const void *>(phase_grid_short<V, INTER, TURNS>);
+static const void *pick_short(bool small) {
+    return small ? reinterpret_cast<const void *>(phase_grid_short<V, INTER, TURNS, true>)
+                 : reinterpret_cast<const void *>(phase_grid_short<V, INTER, TURNS, false>);
 }
 
 #ifdef SINCOS_AB
@@ -505,14 +543,24 @@ cudaError_t launch_phase_flat(int variant, bool inter, bool turns, const float *
                               size_t nt, float *so, float *co, float *io, size_t head, size_t nvec,
                               unsigned grid, bool short_rows, cudaStream_t stream) {
     const void *fn;
+    const bool small = nt < 8;
     if (short_rows && nt >= 1 && nt < kPhaseRowsMinNt) {                  // phase_grid_short
         if (variant == kNormalized)
-            fn = inter ? (turns ? pick_short<kNormalized, true, true>() : pick_short<kNormalized, true, false>())
-                       : (turns ? pick_short<kNormalized, false, true>() : pick_short<kNormalized, false, false>());
+            fn = inter ? (turns ? pick_short<kNormalized, true, true>(small) : pick_short<kNormalized, true, false>(small))
+                       : (turns ? pick_short<kNormalized, false, true>(small)
+                                : pick_short<kNormalized, false, false>(small));
         else
-            fn = inter ? (turns ? pick_short<kRenormalized, true, true>() : pick_short<kRenormalized, true, false>())
-                       : (turns ? pick_short<kRenormalized, false, true>()
-                                : pick_short<kRenormalized, false, false>());
+            fn = inter ? (turns ? pick_short<kRenormalized, true, true>(small)
+                                : pick_short<kRenormalized, true, false>(small))
+                       : (turns ? pick_short<kRenormalized, false, true>(small)
+                                : pick_short<kRenormalized, false, false>(small));
+        size_t n = nf * nt;
+        double inv_nt = 1.0 / static_cast<double>(nt);
+        const size_t step = 8 * static_cast<size_t>(grid) * kPhaseThreads;   // pairs per grid stride
+        size_t step_q = step / nt;
+        unsigned step_r = static_cast<unsigned>(step % nt);
+        void *args[] = {&f, &t, &nf, &nt, &so, &co, &io, &head, &nvec, &n, &inv_nt, &step_q, &step_r};
+        return cudaLaunchKernel(fn, dim3(grid), dim3(kPhaseThreads), args, 0, stream);
     } else {
 #ifdef SINCOS_AB
         if (variant == kNormalized)

@@ -401,7 +401,16 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
     const Tuning T = tuning();
     const bool flat = !vec && T.realign != 0 && n < (size_t(1) << 52) &&
                       (split ? ((so_a ^ co_a) & 31) == 0 : aligned(inter_dev, 8));
-    if (flat && nt >= kPhaseRowsMinNt && T.realign != 3) {
+    // rows of one pair (split or interleaved) or of 2-3 pairs (split), outputs 32-B aligned at
+    // pair 0: the tiny-row kernel (its per-lane store stride, 8 nt pairs, spreads a warp's store
+    // over more lines as nt grows: for nt >= 4, and interleaved nt = 2-3, the short-row kernel
+    // is faster -- profiles/r02/ab_phase_tiny.jsonl)
+    const bool tiny = flat && T.realign != 3 && (nt == 1 || (split && nt <= 3)) &&
+                      (split ? aligned(sin_dev, 32) && aligned(cos_dev, 32) : aligned(inter_dev, 32));
+    if (tiny) {
+        e = launch_phase_tiny(variant, inter, units == SINCOS_TURNS, f_dev, nf, t_dev, nt, sin_dev, cos_dev,
+                              inter_dev, static_cast<cudaStream_t>(stream));
+    } else if (flat && nt >= kPhaseRowsMinNt && T.realign != 3) {
         const unsigned h0 = static_cast<unsigned>(split ? ((32 - (so_a & 31)) & 31) / 4 : ((32 - (io_a & 31)) & 31) / 8);
         int dev = 0;
         if ((e = cudaGetDevice(&dev)) != cudaSuccess) return cuda_fail(e);

@@ -116,6 +116,10 @@ constexpr size_t kPhaseVecMinNt = SINCOS_PHASE_VEC_MIN_NT;     // aligned rows s
 constexpr size_t phase_short_blocks_per_sm(size_t nt) {
     return nt >= 256 ? SINCOS_PHASE_SHORT_BPS_LONG : SINCOS_PHASE_SHORT_BPS;
 }
+// NEXT(1) tiny rows (1 <= nt <= 7), outputs 32-B aligned at pair 0: groups of 8 rows per thread,
+// the row length a compile-time parameter.
+cudaError_t launch_phase_tiny(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
+                              size_t nt, float *so, float *co, float *io, cudaStream_t stream);
 cudaError_t launch_phase_rows(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
                               size_t nt, float *so, float *co, float *io, unsigned h0, int sms,
                               cudaStream_t stream);

@@ -526,6 +526,113 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_short(const float *_
     }
 }
 
+// Tiny rows (nt = NT = 1..7, a compile-time parameter; outputs 32-B aligned at pair 0): a
+// thread owns a group of 8 rows -- 8 NT consecutive pairs of the row-major grid, NT whole
+// 8-pair vectors -- so every pair's (row, column) inside the group is a constant: pair 8m + q
+// is f[8g + (8m + q) / NT] x t[(8m + q) % NT].  One 256-bit load of the group's eight f values
+// (f 32-B aligned; else eight scalar loads), the NT t values in registers once per thread, no
+// selects and no division; NT vectors of 256-bit streaming stores.  f is read once, so these
+// grids move 4 / NT B of f per pair besides the 8 B written.  Against the short-row kernel
+// (per-pair f selects, row-offset table): nt = 1 4.59 / 4.64 TB/s written vs 4.41 / 4.13
+// (split / interleaved), nt = 2, 3 split 5.47 / 5.60 vs 5.19 / 5.28; but a lane's stores are
+// 8 NT pairs apart, so one warp store spans NT times more lines, and from nt = 4 on (and for
+// interleaved nt = 2, 3) it is slower (profiles/r02/ab_phase_tiny.jsonl): the ABI takes it for
+// nt = 1, and for nt = 2, 3 split.  Rows past the last whole group: one pair per thread.
+template <int V, bool INTER, bool TURNS, int NT>
+__global__ void __launch_bounds__(kPhaseThreads) phase_grid_tiny(const float *__restrict__ f,
+                                                                const float *__restrict__ t, size_t nf,
+                                                                float *so, float *co, float *io, size_t ngroups,
+                                                                bool f_al32) {
+    const size_t gid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    // rows past the last whole group (< 8 of them): one pair per thread
+    const size_t rem0 = 8 * ngroups * NT, rem = nf * NT - rem0;
+    if (gid < rem) {
+        const size_t e = rem0 + gid;
+        float sr, cr;
+        phase_pair<V, TURNS>(__ldg(f + e / NT), __ldg(t + e % NT), sr, cr);
+        if constexpr (INTER) {
+            io[2 * e] = cr;
+            io[2 * e + 1] = sr;
+        } else {
+            so[e] = sr;
+            co[e] = cr;
+        }
+    }
+    float tt[NT];
+#pragma unroll
+    for (int b = 0; b < NT; ++b) tt[b] = __ldg(t + b);
+    for (size_t g = gid; g < ngroups; g += nthr) {
+        float fr[8];
+        if (f_al32) {
+            ld8_stream(fr, f + 8 * g);
+        } else {
+#pragma unroll
+            for (int a = 0; a < 8; ++a) fr[a] = __ldg(f + 8 * g + a);
+        }
+        const size_t e0 = 8 * NT * g;
+#pragma unroll
+        for (int m = 0; m < NT; ++m) {
+            float fv[8], tv[8], sv[8], cv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                fv[q] = fr[(8 * m + q) / NT];
+                tv[q] = tt[(8 * m + q) % NT];
+            }
+            phase8f<V, TURNS>(fv, tv, sv, cv);
+            const size_t e = e0 + 8 * m;
+            if constexpr (INTER) {
+                float cs[16];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    cs[2 * k] = cv[k];
+                    cs[2 * k + 1] = sv[k];
+                }
+                st8_stream(io + 2 * e, cs);
+                st8_stream(io + 2 * e + 8, cs + 8);
+            } else {
+                st8_stream(so + e, sv);
+                st8_stream(co + e, cv);
+            }
+        }
+    }
+}
+
+template <int V, bool INTER, bool TURNS>
+static const void *pick_tiny(size_t nt) {
+    switch (nt) {
+    case 1: return reinterpret_cast<const void *>(phase_grid_tiny<V, INTER, TURNS, 1>);
+    case 2: return reinterpret_cast<const void *>(phase_grid_tiny<V, INTER, TURNS, 2>);
+    case 3: return reinterpret_cast<const void *>(phase_grid_tiny<V, INTER, TURNS, 3>);
+    case 4: return reinterpret_cast<const void *>(phase_grid_tiny<V, INTER, TURNS, 4>);
+    case 5: return reinterpret_cast<const void *>(phase_grid_tiny<V, INTER, TURNS, 5>);
+    case 6: return reinterpret_cast<const void *>(phase_grid_tiny<V, INTER, TURNS, 6>);
+    default: return reinterpret_cast<const void *>(phase_grid_tiny<V, INTER, TURNS, 7>);
+    }
+}
+
+cudaError_t launch_phase_tiny(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
+                              size_t nt, float *so, float *co, float *io, cudaStream_t stream) {
+    if (nt < 1 || nt > 7) return cudaErrorInvalidValue;
+    const void *fn;
+    if (variant == kNormalized)
+        fn = inter ? (turns ? pick_tiny<kNormalized, true, true>(nt) : pick_tiny<kNormalized, true, false>(nt))
+                   : (turns ? pick_tiny<kNormalized, false, true>(nt) : pick_tiny<kNormalized, false, false>(nt));
+    else
+        fn = inter ? (turns ? pick_tiny<kRenormalized, true, true>(nt) : pick_tiny<kRenormalized, true, false>(nt))
+                   : (turns ? pick_tiny<kRenormalized, false, true>(nt)
+                            : pick_tiny<kRenormalized, false, false>(nt));
+    size_t ngroups = nf / 8;
+    const size_t rem = (nf - 8 * ngroups) * nt;                       // < 56 tail pairs
+    size_t work = ngroups > rem ? ngroups : rem;
+    size_t grid = (work + kPhaseThreads - 1) / kPhaseThreads;
+    if (grid < 1) grid = 1;
+    if (grid > 0x7FFFFFFFu) grid = 0x7FFFFFFFu;                        // grid-strides past it
+    bool f_al32 = (reinterpret_cast<uintptr_t>(f) & 31) == 0;
+    void *args[] = {&f, &t, &nf, &so, &co, &io, &ngroups, &f_al32};
+    return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kPhaseThreads), args, 0, stream);
+}
+
 template <int V, bool INTER, bool TURNS>
 static const void *pick_short(bool small) {
     return small ? reinterpret_cast<const void *>(phase_grid_short<V, INTER, TURNS, true>)

@@ -99,7 +99,8 @@ def test_phase_grid_and_nudft(shape):
     check(bo, G, G + 2 * nf)
 
 
-@pytest.mark.parametrize("shape", [(1, 1), (3, 7), (9, 13), (33, 1001), (16, 256), (9, 131), (21, 300), (3, 4000)])
+@pytest.mark.parametrize("shape", [(1, 1), (3, 7), (9, 13), (33, 1001), (16, 256), (9, 131), (21, 300), (3, 4000),
+                                   (21, 1), (1003, 2), (77, 3)])
 @pytest.mark.parametrize("off", [0, 1, 3, 6])
 def test_phase_grid_split_offsets(shape, off):
     """Split phase-grid outputs at offsets (the flat kernel's head/body/tail, the ragged-row

@@ -236,3 +236,32 @@ def test_sincos_turns(variant, inter, config):
             s, c = sp.sincos_turns(xd, variant=variant)
             gs, gc = s.cpu().numpy(), c.cpu().numpy()
         assert_parity(gs, gc, ws, wc, f"turns config={config} n={n}")
+
+
+@pytest.mark.parametrize("units,variant", COMBOS)
+@pytest.mark.parametrize("nt", [1, 2, 3, 4, 7])
+def test_tiny_rows(units, variant, nt):
+    """Rows of 1..7 pairs with 32-B aligned outputs: the tiny-row kernel (nt = 1; nt = 2, 3 split:
+    groups of 8 rows per thread, static (row, column) per pair, f as one 256-bit load when
+    32-B aligned, else scalar) and the short-row kernel for the rest -- whole groups, a ragged
+    remainder of < 8 rows, f at an aligned and an unaligned offset."""
+    rng = np.random.default_rng(nt * 10 + units + 2 * variant)
+    for nf in (8, 13, 1001, 8 * 40_000 + 5):
+        fb = rng.uniform(-400, 400, nf + 8).astype(np.float32)
+        t = rng.uniform(-1, 1, nt).astype(np.float32)
+        n = nf * nt
+        for foff in (0, 1):
+            f = fb[foff:foff + nf]
+            ws, wc = oracle.phase_grid(f, t, units, variant)
+            ws, wc = ws.ravel(), wc.ravel()
+            fbig = torch.from_numpy(fb).cuda()
+            fd, td = fbig[foff:foff + nf], torch.from_numpy(t).cuda()
+            s, c = torch.empty(n, device="cuda"), torch.empty(n, device="cuda")
+            io = torch.empty(2 * n, device="cuda")
+            sp.phase_grid(fd, td, s, c, units=units, variant=variant)
+            sp.phase_grid(fd, td, interleaved_out=io, units=units, variant=variant)
+            torch.cuda.synchronize()
+            tag = f"nt={nt} nf={nf} foff={foff}"
+            assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws, wc, "split " + tag)
+            iv = io.cpu().numpy()
+            assert_parity(iv[1::2], iv[0::2], ws, wc, "inter " + tag)

@@ -740,7 +740,8 @@ def run_ours(args, rank, world, local_rank):
         import torch.distributed as dist
         nccl = {"backend": dist.get_backend(), "comm_nranks": dist.get_world_size(),
                 "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if args.backend == "nccl" else None,
-                "same_device": bool(args.same_device)}
+                "same_device": bool(args.same_device),
+                "nccl_init_log": nccl_init_lines() if rank == 0 and args.backend == "nccl" else None}
     if rank != 0:
         return
 
@@ -794,6 +795,19 @@ def run_ours(args, rank, world, local_rank):
         "paper_context": "PowerPC 7400 G4 500 MHz AltiVec: 140 ns per 4 pairs = 28.6 M pairs/s (P:177-180)",
     }
     print(json.dumps(line), flush=True)
+
+
+def nccl_init_lines():
+    """This process's NCCL communicator-init lines (NCCL_DEBUG=INFO, subsystem INIT, to
+    NCCL_DEBUG_FILE), e.g. "... comm 0x... rank 0 nRanks 8 nNodes 1 localRanks 8 ..."; also
+    echoed to stderr."""
+    path = os.environ.get("NCCL_DEBUG_FILE", "")
+    if not path or "%" in path or not os.path.exists(path):
+        return None
+    keep = [l.strip() for l in open(path, errors="ignore") if "nRanks" in l or "Init COMPLETE" in l]
+    for l in keep:
+        print(l, file=sys.stderr, flush=True)
+    return keep[:8]
 
 
 def die(msg: str, code: int = 2):
@@ -853,12 +867,14 @@ def main():
     if world > 1:
         torch.cuda.set_device(gpu)
         if args.backend == "nccl":
-            # the communicator's own init line ("... nranks N ...") goes to stderr with the rest of NCCL's
-            # INIT log, so the job's rank count is on record beside the JSON line
+            # NCCL's INIT log (per process, to a file: on stdout it could follow the JSON line, and
+            # several ranks writing one stderr file would clobber it); rank 0 copies its
+            # communicator lines ("... nRanks N ...") to stderr and into the JSON line
             os.environ.setdefault("NCCL_DEBUG", "INFO")
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+            os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/bench_nccl.{os.getpid()}.log")
             dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+            dist.barrier()
         else:
             dist.init_process_group("gloo")
     try:

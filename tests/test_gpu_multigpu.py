@@ -40,3 +40,18 @@ def test_torchrun_nccl_bench(workload):
         import inputs
         per_variant = [s["n"] + s["nan"] for s in shards if s["variant"] == "N"]
         assert sum(per_variant) == inputs.size(4)
+
+
+@pytest.mark.skipif(ngpus() < 2, reason="needs >= 2 GPUs")
+def test_plain_invocation_self_launches_every_gpu():
+    """`python bench.py --gpus G` without a launcher: G ranks over NCCL, one per GPU; the line
+    carries every rank's shards and clocks and the communicator's rank count."""
+    G = ngpus()
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(G), "--steps", "3", "--warmup", "3",
+           "--no-next", "--e2e-max", str(1 << 22), "--cpu-seconds", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == G and line["distributed"]["comm_nranks"] == G
+    assert len(line["clocks_per_rank"]) == G and {s["rank"] for s in line["shards"]} == set(range(G))
+    assert line["cpu_baseline"] is not None and line["roofline"]["traffic"] is not None

@@ -159,6 +159,7 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
                                 : ((32 - (reinterpret_cast<uintptr_t>(so) & 31)) & 31) / 4;
         const int k = static_cast<int>(((reinterpret_cast<uintptr_t>(theta) + 4 * h0) & 31) / 4);   // 0..7
         if (k != 0) {
+            if (!nc) return SINCOS_ERR_OVERLAP;  // unreachable: in place shares theta's alignment
             size_t hb = h0 >= static_cast<size_t>(k) ? h0 : h0 + 8;
             if (hb > n) hb = n;
             // the second aligned vector of every thread inside theta: (hb - k) + 8 nvec + 7 <= n - 1
@@ -178,6 +179,7 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
         // (hb - k) + 4 nvec + 3 <= n - 1
         size_t nvec = (n - hb) / 4;
         if (k > 0) nvec = n + k >= hb + 4 ? (n + k - hb - 4) / 4 : 0;
+        if (!nc) return SINCOS_ERR_OVERLAP;      // unreachable: in place shares theta's alignment
         e = launch_shift(variant, inter, k, grid_for(nvec, threads, sms, cfg_bps), threads, theta, so, co, io, hb,
                          nvec, n, stream);
     } else if (w == 0 && realign) {
@@ -193,6 +195,12 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
             ks = static_cast<int>(((reinterpret_cast<uintptr_t>(so) + 4 * hb) & 31) / 4);
             kc = static_cast<int>(((reinterpret_cast<uintptr_t>(co) + 4 * hb) & 31) / 4);
         }
+        // Exact in place (theta == sin or theta == cos) reaches KB3c only with the aliased stream
+        // at theta's own alignment (k = 0): each thread then writes exactly the elements of theta
+        // it read itself, after reading them -- which is what makes the read-only (.nc) theta
+        // loads safe here.  Any other aliasing was refused by validate(); keep the invariant
+        // explicit rather than implied.
+        if ((theta == so && ks != 0) || (theta == co && kc != 0)) return SINCOS_ERR_OVERLAP;
         e = launch_outshift(variant, inter, ks, kc, grid_for(nvec, threads, sms, cfg_bps), threads, theta, so, co,
                             io, hb, nvec, n, stream);
     } else if (w == 0) {

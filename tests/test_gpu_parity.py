@@ -689,6 +689,21 @@ def test_dependent_launch_chain_keeps_stream_order(pdl):
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("soff", [1, 2, 3, 6])
+def test_in_place_cos_over_theta_with_sin_off_alignment(variant, soff):
+    """theta == cos_out with sin at another offset (the mirror of the case below): through the
+    output-realigning kernel, at a size of many warps and a ragged tail."""
+    th = inputs.generate(5, 0, (1 << 21) + 13)
+    os_, oc = oracle.sincos(th, variant)
+    t = torch.from_numpy(th).cuda()
+    sb = torch.empty(t.numel() + 8, device="cuda")
+    s = sb[soff:soff + t.numel()]
+    sp.sincos_pairs(t, s, t, variant=variant)
+    torch.cuda.synchronize()
+    assert_parity(s.cpu().numpy(), t.cpu().numpy(), os_, oc, f"in place cos, sin +{soff}")
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("coff", [1, 2, 3, 5])
 def test_in_place_with_cos_off_alignment(variant, coff):
     """theta == sin_out (exact in place) with cos at another offset: the output-realigning

@@ -116,17 +116,22 @@ class ClockSampler:
         self._stop = threading.Event()
 
     def _run(self):
+        # SM clock and event reasons as fast as NVML answers (the C2 timed region is ~20 ms);
+        # the memory clock every 8th sample
+        k = 0
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                self.mem.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_MEM))
+                if k % 8 == 0:
+                    self.mem.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_MEM))
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if r & bit:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.002)
+            k += 1
+            time.sleep(0.0002)
 
     def __enter__(self):
         if self.ok:

@@ -379,6 +379,22 @@ def test_null_kernel_copies():
     assert torch.equal(s, t) and torch.equal(c, t) and torch.equal(o[0::2], t) and torch.equal(o[1::2], t)
 
 
+def test_host_buffer_path_pageable():
+    """sincos_pairs_host on ordinary (pageable) host memory: correct, if slower (the copies stage
+    through the driver's pinned buffers)."""
+    n = (1 << 20) + 9
+    th = inputs.generate(2, 7, n)
+    ws = torch.empty(8 << 20, dtype=torch.uint8, device="cuda")
+    for variant in VARIANTS:
+        s_h, c_h = torch.empty(n), torch.empty(n)
+        sp.sincos_pairs_host(torch.from_numpy(th), s_h, c_h, variant=variant, workspace=ws)
+        io = torch.empty(2 * n)
+        sp.sincos_pairs_host(torch.from_numpy(th), interleaved_out=io, variant=variant, workspace=ws)
+        os_, oc = oracle.sincos(th, variant)
+        assert_parity(s_h.numpy(), c_h.numpy(), os_, oc, "pageable split")
+        assert_parity(io.numpy()[1::2], io.numpy()[0::2], os_, oc, "pageable inter")
+
+
 def test_launches_are_counted():
     before = sp.launch_count()
     t = torch.zeros(100, device="cuda")

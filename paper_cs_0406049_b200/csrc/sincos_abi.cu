@@ -137,17 +137,26 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
         }
     }
 
-    // KB3b: split outputs without a shared alignment but whose sin and cos share one mod 16 B;
-    // interleaved outputs without the 256-bit path but 8-B aligned (its 256-bit store per four
-    // pairs beats the 128-bit path's half-sector stores).
+    // KB3b: theta re-aligned onto the outputs' 256-bit frame -- split outputs whose sin and cos
+    // share one offset mod 32 B (theta elsewhere); interleaved outputs without the 256-bit path
+    // but 8-B aligned (its 256-bit store per four pairs beats the 128-bit path's half-sector
+    // stores).
     size_t hs = SIZE_MAX;
+    const uintptr_t sc = reinterpret_cast<uintptr_t>(so) ^ reinterpret_cast<uintptr_t>(co);
     if (realign) {
         if (inter) {
             // (w == 4 with the default vec 8 only: an A/B vec 4 keeps its 128-bit kernel)
             if ((w == 0 || (w == 4 && T.vec == 8)) && aligned(io, 8))
                 hs = ((32 - (reinterpret_cast<uintptr_t>(io) & 31)) & 31) / 8;
-        } else if (w == 0 && ((reinterpret_cast<uintptr_t>(so) ^ reinterpret_cast<uintptr_t>(co)) & 15) == 0) {
-            hs = ((16 - (reinterpret_cast<uintptr_t>(so) & 15)) & 15) / 4;
+        } else if (T.realign == 2) {
+            // (A/B: the 128-bit form wherever sin and cos share 16 B)
+            if (w == 0 && (sc & 15) == 0) hs = ((16 - (reinterpret_cast<uintptr_t>(so) & 15)) & 15) / 4;
+        } else if ((w == 0 || (w == 4 && T.vec == 8)) && (sc & 31) == 0) {
+            // sin and cos at one offset mod 32 B: theta re-aligned onto their 256-bit frame (also
+            // when theta shares only 16 B with them: the 128-bit vector kernel ran 6.2 TB/s there,
+            // the 256-bit re-alignment 6.8).  Sharing only 16 B: KB3c below (the 128-bit
+            // re-alignment ran 5.6-6.2 TB/s; profiles/r02/ab_layouts_all*.jsonl)
+            hs = ((32 - (reinterpret_cast<uintptr_t>(so) & 31)) & 31) / 4;
         }
     }
     // 256-bit form when the outputs take 256-bit stores at a common element (split: sin and cos
@@ -182,7 +191,7 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
         if (!nc) return SINCOS_ERR_OVERLAP;      // unreachable: in place shares theta's alignment
         e = launch_shift(variant, inter, k, grid_for(nvec, threads, sms, cfg_bps), threads, theta, so, co, io, hb,
                          nvec, n, stream);
-    } else if (w == 0 && realign) {
+    } else if ((w == 0 || (w == 4 && !inter && T.vec == 8 && T.realign != 2)) && realign) {
         // KB3c: theta's frame, outputs re-aligned (sin and cos apart mod 16 B; pairs only 4-B aligned)
         const uintptr_t ta = reinterpret_cast<uintptr_t>(theta);
         size_t hb = ((32 - (ta & 31)) & 31) / 4;

@@ -145,12 +145,23 @@ __device__ __forceinline__ void store_realigned(float *x, size_t f0, const float
 // run time)
 // Register budget: most instances need 34-40 registers, which leaves 12 resident 128-thread
 // blocks per SM (75% occupancy); capped at 32 (16 blocks, full occupancy, a few bytes of
-// spill) they run faster where the kernel waits on HBM -- measured for the split instances
+// spill) they run faster where the kernel waits on HBM -- measured for most split instances
 // (sin+2 cos+5: 6.46 -> 6.67 TB/s) and the interleaved ones with k <= 4 (k = 3: 6.61 -> 6.68),
-// slower for interleaved k > 4 (k = 7: 6.85 -> 6.55; tools/ab_layouts.py, profiles/r02).  The
-// capped instances take 128-thread blocks (launch_outshift).
+// slower for interleaved k > 4 (k = 7: 6.85 -> 6.55) and for the split instances that would
+// spill more (below; tools/ab_layouts.py, profiles/r02).  The capped instances take 128-thread
+// blocks (launch_outshift).
+// Split instances KI = 8 ks + kc: capped, except those that would spill >= 12 bytes at 32
+// registers (ks = 4; ks = 6 with odd kc; ks = 3, kc = 0), which ran 1-13% faster uncapped --
+// every (ks, kc) timed both ways, profiles/r02/ab_layouts_all2.jsonl.
 template <bool INTER, int KI>
-constexpr int outshift_min_blocks() { return !INTER || (KI >= 0 && KI <= 4) ? 16 : 1; }
+constexpr int outshift_min_blocks() {
+    if constexpr (INTER) {
+        return KI >= 0 && KI <= 4 ? 16 : 1;
+    } else {
+        constexpr int ks = KI / 8, kc = KI % 8;
+        return KI < 0 || ks == 4 || (ks == 6 && kc % 2 == 1) || (ks == 3 && kc == 0) ? 1 : 16;
+    }
+}
 template <bool INTER, int KI>
 constexpr int outshift_max_threads() { return outshift_min_blocks<INTER, KI>() > 1 ? 128 : 512; }
 

@@ -23,6 +23,12 @@ CASES = [("aligned split", 0, 0, 0), ("aligned inter", 0, 0), ("theta+1 split", 
          ("inter+3", 0, 3), ("theta+3 inter+5", 3, 5)]
 
 
+if os.environ.get("AB_CASES") == "all":
+    # every split (sin, cos) offset pair 0..7 with theta aligned, and every interleaved offset
+    CASES = [(f"sin+{a} cos+{b}", 0, a, b) for a in range(8) for b in range(8)] + \
+            [(f"inter+{a}", 0, a) for a in range(8)]
+
+
 def main():
     import torch
     libs = {}

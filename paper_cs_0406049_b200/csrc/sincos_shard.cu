@@ -235,6 +235,17 @@ sincos_status_t sincos_pairs_sharded_stats(const sincos_shard_t *shards, int nsh
         const cudaError_t e = cudaStreamSynchronize(stream(g));
         if (e != cudaSuccess && st == SINCOS_OK) st = sincos_last_error_set(static_cast<int>(e));
     }
+    if (st == SINCOS_ERR_NCCL) {
+        // a failed collective may leave the communicator unusable: the next call on these devices
+        // builds a new context (this one is dropped from the cache -- not destroyed, which could
+        // block on a broken communicator -- and its small buffers are leaked)
+        std::lock_guard<std::mutex> lk(g_ctx_mu);
+        for (size_t i = 0; i < g_ctxs->size(); ++i)
+            if ((*g_ctxs)[i] == c) {
+                g_ctxs->erase(g_ctxs->begin() + static_cast<long>(i));
+                break;
+            }
+    }
     cudaSetDevice(prev);
     return st;
 }

@@ -115,3 +115,55 @@ def test_all_fp32_bit_patterns_raw_bits(variant):
     canonicalise +-0; this one does not), NaN payloads excused."""
     dt = full_compare(0, variant)
     print(f"all 2^32 bit patterns variant {variant}: x 2 layouts in {dt:.1f} s")
+
+
+def c4_axes(turns):
+    """BASELINE configs[3] axes (2^15 f x 2^15 jittered t); in radians the row factor is fl32(2 pi f)."""
+    nf = nt = 1 << 15
+    f = np.array([512.0 * inputs.urand(3, 0, i) for i in range(nf)])
+    t = np.array([(j + inputs.urand(3, 1, j)) * 2.0 ** -15 for j in range(nt)])
+    if not turns:
+        f = 2 * np.pi * f
+    return f.astype(np.float32), t.astype(np.float32)
+
+
+def oracle_grid_rows(f, t, units, variant, rows):
+    """oracle.phase_grid over blocks of rows on all host threads (per-pair numerics unchanged)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+    spans = [(i, min(i + rows // 64, rows)) for i in range(0, rows, max(1, rows // 64))]
+    with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+        parts = list(ex.map(lambda ab: oracle.phase_grid(f[ab[0]:ab[1]], t, units, variant), spans))
+    return np.concatenate([p[0] for p in parts]).ravel(), np.concatenate([p[1] for p in parts]).ravel()
+
+
+@pytest.mark.parametrize("units", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1])
+def test_c4_phase_grid_full(units, variant):
+    """NEXT(1) at BASELINE configs[3]'s full shape: the 2^15 x 2^15 phase grid formed in the kernel
+    (2^30 pairs), split and interleaved, every element, raw bits, against the oracle's pairs of
+    RN(f_i t_j) -- 4096 rows at a time."""
+    nf = nt = 1 << 15
+    f, t = c4_axes(units == 1)
+    fd, td = torch.from_numpy(f).cuda(), torch.from_numpy(t).cuda()
+    n = nf * nt
+    s = torch.empty(n, device="cuda")
+    c = torch.empty(n, device="cuda")
+    io = torch.empty(2 * n, device="cuda")
+    sp.phase_grid(fd, td, s, c, units=units, variant=variant)
+    sp.phase_grid(fd, td, interleaved_out=io, units=units, variant=variant)
+    torch.cuda.synchronize()
+    pairs = io.view(n, 2)
+    R = 4096
+    for r0 in range(0, nf, R):
+        ws, wc = oracle_grid_rows(f[r0:r0 + R], t, units, variant, R)
+        wsd, wcd = torch.from_numpy(ws).cuda(), torch.from_numpy(wc).cuda()
+        lo, hi = r0 * nt, (r0 + R) * nt
+        for name, gs, gc in (("split", s[lo:hi], c[lo:hi]), ("interleaved", pairs[lo:hi, 1], pairs[lo:hi, 0])):
+            for comp, got, want in (("sin", gs, wsd), ("cos", gc, wcd)):
+                bad = bit_mismatches(got, want)
+                assert bad.numel() == 0, f"{name} {comp}: {bad.numel()} mismatches from row {r0}, first {int(bad[0])}"
+    del s, c, io
+    torch.cuda.empty_cache()

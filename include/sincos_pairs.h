@@ -80,12 +80,13 @@ typedef enum {
  *   n                element count; 0 is a no-op (pointers may then be NULL).
  *
  * Any 4-B aligned pointers are accepted; every path has identical numerics.
- * When theta and the outputs share their alignment the body runs 256-bit
- * vector loads/stores (128-bit if they share only 16 B); otherwise, if the
- * outputs can still take whole-sector stores (split: sin and cos at one offset
- * mod 16 B; interleaved: 8-B aligned), theta is read as aligned vectors and
- * re-aligned in registers (warp shuffles); otherwise the outputs are re-aligned
- * instead (theta's 256-bit frame, whole 32-B output blocks from neighbouring lanes).
+ * When theta and the outputs share their 32-B alignment the body runs 256-bit
+ * vector loads/stores; otherwise, if the outputs can take 256-bit stores at a
+ * common element (split: sin and cos at one offset mod 32 B; interleaved: 8-B
+ * aligned), theta is read as aligned vectors and re-aligned in registers (warp
+ * shuffles); otherwise the outputs are re-aligned instead (theta's 256-bit frame,
+ * whole 32-B output blocks from neighbouring lanes).  (Exact in-place always
+ * keeps the aliased output at theta's alignment.)
  * A scalar head and tail cover the ragged ends.  The kernel configuration (block
  * size, full grid, vector width) is fixed: there is no tuning state.
  * theta_dev == sin_dev or
@@ -191,8 +192,9 @@ SINCOS_API sincos_status_t sincos_pairs_method(const float *theta_dev, float *si
  * eight t-values, re-aligned by warp shuffles to the rows' output alignment, and
  * writes them for the rows of one alignment class), for nt < 1024 (and whole-vector
  * rows shorter than 256) the short-row path (8 consecutive pairs of the row-major grid
- * per thread, t from shared memory); otherwise one pair per thread.  Returns as
- * sincos_pairs; nf*nt == 0 is a no-op.
+ * per thread, t from shared memory) -- except rows of 1 pair, or 2-3 pairs split, with
+ * outputs 32-B aligned at pair 0: the tiny-row path (8 whole rows per thread); otherwise
+ * one pair per thread.  Returns as sincos_pairs; nf*nt == 0 is a no-op.
  */
 typedef enum { SINCOS_RADIANS = 0, SINCOS_TURNS = 1 } sincos_units_t;
 SINCOS_API sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_dev, size_t nt,

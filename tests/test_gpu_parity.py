@@ -704,6 +704,30 @@ def test_dependent_launch_chain_keeps_stream_order(pdl):
         assert_parity(cur.cpu().numpy(), c.cpu().numpy(), want, wc, f"chain pdl={pdl}")
 
 
+@pytest.mark.parametrize("bps", [1, 2])
+def test_in_place_realigning_many_trips(bps):
+    """The in-place read-only-load invariant under grid-stride: on the A/B build with 1-2 blocks
+    per SM every thread makes hundreds of trips, so a thread that read an element some other
+    thread had already overwritten (or a stale cached line) would show up as a mismatch against
+    the out-of-place run.  theta == sin and theta == cos, the other output at every offset."""
+    th = inputs.generate(2, 3, (1 << 22) + 5)
+    want = {v: oracle.sincos(th, v) for v in VARIANTS}
+    with ab.knobs(blocks_per_sm=bps):
+        for variant in VARIANTS:
+            os_, oc = want[variant]
+            for off in (1, 2, 3, 4, 5, 6, 7):
+                t = torch.from_numpy(th).cuda()
+                ob = torch.empty(t.numel() + 8, device="cuda")
+                o = ob[off:off + t.numel()]
+                sp.sincos_pairs(t, t, o, variant=variant)              # sin over theta
+                torch.cuda.synchronize()
+                assert_parity(t.cpu().numpy(), o.cpu().numpy(), os_, oc, f"sin in place, cos +{off}, bps={bps}")
+                t = torch.from_numpy(th).cuda()
+                sp.sincos_pairs(t, o, t, variant=variant)              # cos over theta
+                torch.cuda.synchronize()
+                assert_parity(o.cpu().numpy(), t.cpu().numpy(), os_, oc, f"cos in place, sin +{off}, bps={bps}")
+
+
 @pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("soff", [1, 2, 3, 6])
 def test_in_place_cos_over_theta_with_sin_off_alignment(variant, soff):

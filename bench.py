@@ -875,9 +875,11 @@ def main():
             # NCCL's INIT log (per process, to a file: on stdout it could follow the JSON line, and
             # several ranks writing one stderr file would clobber it); rank 0 copies its
             # communicator lines ("... nRanks N ...") to stderr and into the JSON line
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-            os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/bench_nccl.{os.getpid()}.log")
+            # (a launcher that set NCCL_DEBUG itself keeps NCCL's own log destination)
+            if "NCCL_DEBUG" not in os.environ:
+                os.environ["NCCL_DEBUG"] = "INFO"
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+                os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/bench_nccl.{os.getpid()}.log")
             dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
             dist.barrier()
         else:

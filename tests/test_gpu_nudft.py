@@ -151,6 +151,32 @@ def test_c4_scale_per_run_bound(units, variant):
           f"median |a_j| {np.abs(a[j_med]):.3f}")
 
 
+@pytest.mark.parametrize("units,variant", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_c4_every_row_within_its_per_run_bound(units, variant):
+    """All 2^15 outputs at the C4 shape (not a sample): each within the per-run bound of its own
+    partial sums, against the oracle's fp64 sum -- rows evaluated in blocks on all host threads
+    (~6 s per case on the GPU box's host)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    nf = nt = 1 << 15
+    rng = np.random.default_rng(17 + units)
+    f = (512 * rng.random(nf)).astype(np.float32)
+    if not units:
+        f = (2 * np.pi * f.astype(np.float64)).astype(np.float32)
+    t = ((np.arange(nt) + rng.random(nt)) * 2.0 ** -15).astype(np.float32)
+    a = rand_complex(rng, nt)
+    got = run(f, t, a, units, variant)
+    want = oracle_nudft_threaded(f, t, a, units, variant)
+    chunk = sp.nudft_chunk(nt)
+    blocks = [(r, min(r + 64, nf)) for r in range(0, nf, 64)]
+    with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+        bounds = list(ex.map(lambda ab: run_model_bound(f[ab[0]:ab[1]], t, a, units, variant, chunk)[0], blocks))
+    b = np.concatenate(bounds)
+    err = np.abs(got - want)
+    assert np.all(err <= b), (int(np.argmax(err / b)), float((err / b).max()))
+    print(f"units {units} variant {variant}: all {nf} rows, max err/bound {(err / b).max():.4f}")
+
+
 @pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("imag", [False, True])
 def test_c4_shape_exact_sum(variant, imag):

@@ -777,7 +777,9 @@ def run_ours(args, rank, world, local_rank):
         "wall_ms_per_step": wall_ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak" if W.weak else "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": W.description, "n_per_rank": n, "pairs_per_step": len(variants) * units_all,
-                   "global_batch": units_all, "parallelism": f"dp{world} (contiguous shards, no collective)",
+                   "global_batch": units_all, "parallelism": f"dp{world} (contiguous shards, no collective)" + (
+                           "; SAME DEVICE: every rank on cuda:0 in its own context (time-sliced), a host-flow "
+                           "test -- value is NOT a throughput measurement" if args.same_device else ""),
                    "l2": "inputs larger than L2 (4n B theta + 8n B outputs per launch vs 126 MB L2); no flush"
                          if 12 * n > (256 << 20) else "working set near/below L2 size: not an HBM measurement",
                    "launch": sp.LAUNCH, "cuda_graph": use_graph},

@@ -1,4 +1,4 @@
-"""A/B of programmatic dependent launch (sincos_set_pdl) on back-to-back steps (variant N then
+"""A/B of programmatic dependent launch (the A/B build's pdl knob) on back-to-back steps (variant N then
 A, split) at 2^20 .. 2^28 elements: plain stream launches and a CUDA graph of 20 steps
 (GPU box).  python tools/pdl_probe.py"""
 import json

@@ -279,7 +279,9 @@ def host_input(W, lo, hi, pinned=True):
     t = torch.empty(hi - lo, dtype=torch.float32)
     if pinned:
         t = t.pin_memory()
-    inputs.generate(W.config, lo, hi - lo, out=t.numpy())
+    # this rank's share of the host cores (a launcher sets OMP_NUM_THREADS=1 per rank)
+    local = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    inputs.generate(W.config, lo, hi - lo, out=t.numpy(), nthreads=max(1, (os.cpu_count() or 1) // local))
     return t
 
 

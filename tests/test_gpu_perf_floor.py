@@ -45,11 +45,13 @@ def bufs():
 CASES = {
     "aligned split (256-bit)": (0, 0, 0, False, 6000, 6870),
     "aligned interleaved": (0, 0, 0, True, 6000, 6890),
-    "shared 16 B (128-bit)": (4, 0, 0, False, 6000, 6890),
+    "shared 16 B (256-bit theta re-alignment)": (4, 0, 0, False, 6000, 6800),
     "theta realigned (KB3b)": (1, 0, 0, False, 6000, 6810),
     "theta realigned interleaved": (1, 0, 0, True, 6000, 6890),
-    "outputs realigned (KB3c)": (0, 1, 2, False, 5500, 6230),
-    "pairs 4-B only (KB3c)": (0, 1, 1, "odd", 5500, 6370),
+    "outputs realigned (KB3c)": (0, 1, 2, False, 5900, 6760),
+    "outputs realigned, sin 4 off (KB3c)": (0, 4, 2, False, 5400, 6220),
+    "sin/cos sharing 16 B (KB3c)": (0, 3, 7, False, 5600, 6420),
+    "pairs 4-B only (KB3c)": (0, 1, 1, "odd", 5900, 6710),
 }
 
 
@@ -74,6 +76,22 @@ def test_phase_grid_floor():
     o = torch.empty(2 * (1 << 27), device="cuda")
     got = gbps(lambda: sp.phase_grid(f, t, interleaved_out=o, units=sp.TURNS), 8 * (1 << 27))
     assert got >= 6500, got                        # recorded 7.5-7.6 TB/s (write-only ceiling)
+
+
+def test_phase_grid_short_and_tiny_rows_floor():
+    """Ragged short rows (nt = 1001, interleaved: recorded 6.9-7.1 TB/s in the bench) and rows of
+    one pair (the tiny-row kernel: recorded 4.6 TB/s written = 6.9 TB/s with the f reads)."""
+    f = torch.rand((1 << 27) // 1001, device="cuda") * 512
+    t = torch.rand(1001, device="cuda")
+    n = f.numel() * 1001
+    o = torch.empty(2 * n, device="cuda")
+    got = gbps(lambda: sp.phase_grid(f, t, interleaved_out=o, units=sp.TURNS), 8 * n)
+    assert got >= 5800, f"nt=1001 {got:.0f}"
+    f1 = torch.rand(1 << 27, device="cuda")
+    t1 = torch.rand(1, device="cuda")
+    s, c = torch.empty(1 << 27, device="cuda"), torch.empty(1 << 27, device="cuda")
+    got = gbps(lambda: sp.phase_grid(f1, t1, s, c, units=sp.TURNS), 12 * (1 << 27))
+    assert got >= 6000, f"nt=1 {got:.0f} (12 B/pair incl. the f read)"
 
 
 def test_fused_sum_floor():

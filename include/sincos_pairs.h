@@ -259,7 +259,8 @@ typedef struct {
  * rather than one launch latency apart each; shards on one device launch in order from
  * the calling thread.  Returns the first failing shard's status (its CUDA error in
  * sincos_last_cuda_error of the calling thread); the other shards may have been
- * launched.  The caller's current device is unchanged. */
+ * launched.  The caller's current device is unchanged.  (Test hook: the environment variable
+ * SINCOS_SHARDED_WORKERS=1, read once, routes single-device calls through the worker threads too.) */
 SINCOS_API sincos_status_t sincos_pairs_sharded(const sincos_shard_t *shards, int nshards,
                                      sincos_variant_t variant);
 

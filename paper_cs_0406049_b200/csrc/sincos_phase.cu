@@ -90,6 +90,13 @@ __device__ __forceinline__ void st8_stream(float *p, const float *r) {
 // Vector path: nt % 8 == 0, t and the outputs 32-B aligned.  Block (x, y) covers 128
 // vectors of 8 t-values of rows y, y + gridDim.y, ...: every thread loads one 256-bit
 // vector of t (L1-cached, reused by every row) and its row's f once per row.
+// Interleaved output with nt % 256 == 0: a lane's two 256-bit stores go to pairs 4l..4l+3 and
+// 128+4l..+3 of its warp's 256 (t loaded as two 128-bit vectors), so each warp store instruction
+// writes 1 KB of whole lines instead of alternating 32-B halves of 2 KB: +1-2% burst, +3% in
+// the board's power cap (6.36 -> 6.55 TB/s sustained at nt = 2^15; profiles/r02/ab_phase_inter_halves*.jsonl).
+#ifndef SINCOS_PHASE_INTER_HALVES
+#define SINCOS_PHASE_INTER_HALVES 1
+#endif
 template <int V, bool INTER, bool TURNS>
 __global__ void __launch_bounds__(kPhaseThreads) phase_grid_vec(const float *__restrict__ f,
                                                                const float *__restrict__ t, size_t nf,
@@ -97,6 +104,35 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_vec(const float *__r
     const size_t nt8 = nt / 8;
     const size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (v >= nt8) return;
+#if SINCOS_PHASE_INTER_HALVES
+    // interleaved, nt % 256 == 0: lane l of a warp takes pairs 4l..4l+3 and 128+4l..+3 of the
+    // warp's 256, so each 256-bit store instruction covers 1 KB contiguous (whole lines)
+    if constexpr (INTER) {
+        if (nt % 256 == 0) {
+            const unsigned lane = threadIdx.x & 31u;
+            const size_t w0 = (v - lane) * 8;                         // the warp's first pair of the row
+            const size_t j0 = w0 + 4 * lane, j1 = w0 + 128 + 4 * lane;
+            float tt[8];
+            const float4 a = __ldg(reinterpret_cast<const float4 *>(t + j0));
+            const float4 b = __ldg(reinterpret_cast<const float4 *>(t + j1));
+            tt[0] = a.x; tt[1] = a.y; tt[2] = a.z; tt[3] = a.w; tt[4] = b.x; tt[5] = b.y; tt[6] = b.z; tt[7] = b.w;
+            for (size_t i = blockIdx.y; i < nf; i += gridDim.y) {
+                const float fi = __ldg(f + i);
+                float sv[8], cv[8];
+                phase8<V, TURNS>(fi, tt, sv, cv);
+                float cs[16];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    cs[2 * k] = cv[k];
+                    cs[2 * k + 1] = sv[k];
+                }
+                st8_stream(io + 2 * (i * nt + j0), cs);
+                st8_stream(io + 2 * (i * nt + j1), cs + 8);
+            }
+            return;
+        }
+    }
+#endif
     float tt[8];
     asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=f"(tt[0]), "=f"(tt[1]), "=f"(tt[2]), "=f"(tt[3]), "=f"(tt[4]), "=f"(tt[5]), "=f"(tt[6]),

@@ -106,10 +106,13 @@ def sustain():
     s = torch.empty(nf * nt, device="cuda")
     c = torch.empty(nf * nt, device="cuda")
     nbytes = 8 * nf * nt
+    inter = os.environ.get("SUSTAIN_INTER") == "1"      # interleaved output (s viewed as 2 x n/2... below)
+    io = torch.empty(2 * nf * nt, device="cuda") if inter else None
+    outs = (0, 0, io.data_ptr()) if inter else (s.data_ptr(), c.data_ptr(), 0)
     out = {k: [] for k in libs}
     for rep in range(2):
         for name, L in libs.items():
-            L.sincos_phase_grid(f.data_ptr(), nf, t.data_ptr(), nt, s.data_ptr(), c.data_ptr(), 0, 1, 0, st)
+            L.sincos_phase_grid(f.data_ptr(), nf, t.data_ptr(), nt, *outs, 1, 0, st)
             torch.cuda.synchronize()
             time.sleep(3)
             e0 = pynvml.nvmlDeviceGetTotalEnergyConsumption(h)
@@ -118,7 +121,7 @@ def sustain():
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
                 for _ in range(5):
-                    L.sincos_phase_grid(f.data_ptr(), nf, t.data_ptr(), nt, s.data_ptr(), c.data_ptr(), 0, 1, 0, st)
+                    L.sincos_phase_grid(f.data_ptr(), nf, t.data_ptr(), nt, *outs, 1, 0, st)
                 b.record()
                 torch.cuda.synchronize()
                 gbs.append(nbytes / (a.elapsed_time(b) / 5 / 1e3) / 1e9)

@@ -55,9 +55,15 @@ def one_case(rng):
     if rng.random() < 0.5:
         oc = os_
     cfg = [(128, 0, 8, 1, 0), (256, 0, 8, 2, 0), (512, 4, 4, 1, 1), (128, 1, 8, 4, 0)][int(rng.integers(0, 4))]
-    ab.set_launch_config(*cfg)
-    ab.set_realign(bool(rng.random() < 0.85))
-    ab.set_pdl(bool(rng.random() < 0.7))
+    if entry == "batched" or rng.random() < 0.5:
+        # the A/B build (the batched entry exists only there), with a random launch shape,
+        # re-alignment and PDL switch
+        ab.set_launch_config(*cfg)
+        ab.set_realign(bool(rng.random() < 0.85))
+        ab.set_pdl(bool(rng.random() < 0.7))
+    else:
+        ab.use(False)                     # the product library: its one configuration
+        cfg = "product"
     tbuf = torch.empty(n + 16, dtype=torch.float32, device="cuda")
     tbuf[ot:ot + n].copy_(torch.from_numpy(th))
     t = tbuf[ot:ot + n]

@@ -134,3 +134,15 @@ def test_every_bench_option_survives_torchrun_parsing():
         argv += [o, "1"]
     ns = get_args_parser().parse_args(argv)
     assert ns.training_script == "bench.py" and len(ns.training_script_args) == 2 * len(opts)
+
+
+@pytest.mark.gpu
+def test_gpus_2_on_a_one_gpu_box_fails_loudly():
+    """On the one-GPU box: `--gpus 2` without --same-device refuses (non-zero exit, no JSON line)
+    instead of timing one GPU."""
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("this box has >= 2 GPUs")
+    rc, out, err = run_rc(["--gpus", "2", "--steps", "1", "--warmup", "3"])
+    assert rc != 0 and not [l for l in out.splitlines() if l.startswith("{")]
+    assert "--gpus 2 needs 2 visible CUDA devices, found 1" in err

@@ -749,6 +749,11 @@ def run_ours(args, rank, world, local_rank):
                 "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if args.backend == "nccl" else None,
                 "same_device": bool(args.same_device),
                 "nccl_init_log": nccl_init_lines() if rank == 0 and args.backend == "nccl" else None}
+        # every collective is done: all ranks tear the process group down together, so rank 0's
+        # remaining single-rank work (NEXT side measurements, the CPU baseline) never runs with a
+        # communicator whose peers have exited
+        dist.barrier()
+        dist.destroy_process_group()
     if rank != 0:
         return
 

@@ -142,3 +142,27 @@ def test_pairs_outputs_apart(n, offs):
         check(bs, G + os_, G + os_ + n)
         check(bc, G + oc, G + oc + n)
         check(bi, G + oi, G + oi + 2 * n)
+
+
+@pytest.mark.parametrize("n", SIZES + [8 * 40_000 + 3])
+@pytest.mark.parametrize("off", [0, 1, 2, 4, 8])
+def test_layout_adapters(n, off):
+    """sincos_interleave / sincos_deinterleave (the 256-bit form when all three buffers are 32-B
+    aligned -- off 0, 8 -- else the 128-bit or scalar forms): no write outside the outputs, and
+    the round trip is exact."""
+    s = torch.rand(n, device="cuda")
+    c = torch.rand(n, device="cuda")
+    bi = torch.full((2 * G + 2 * n + 16,), SENT, dtype=torch.int32, device="cuda")
+    io = bi[G + 2 * off:G + 2 * off + 2 * n].view(torch.float32)
+    sp.interleave(s, c, io)
+    bs = torch.full((2 * G + n + 16,), SENT, dtype=torch.int32, device="cuda")
+    bc = bs.clone()
+    s2 = bs[G + off:G + off + n].view(torch.float32)
+    c2 = bc[G + off:G + off + n].view(torch.float32)
+    sp.deinterleave(io, s2, c2)
+    torch.cuda.synchronize()
+    check(bi, G + 2 * off, G + 2 * off + 2 * n)
+    check(bs, G + off, G + off + n)
+    check(bc, G + off, G + off + n)
+    assert torch.equal(s2, s) and torch.equal(c2, c)
+    assert torch.equal(io.view(n, 2)[:, 0], c) and torch.equal(io.view(n, 2)[:, 1], s)

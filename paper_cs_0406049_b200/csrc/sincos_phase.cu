@@ -486,8 +486,13 @@ __device__ __forceinline__ void short_f(const float *__restrict__ f, size_t i, u
     }
 }
 
+// Register cap: the interleaved rows-of->=8 instances at 32 registers (16 resident blocks; 42-48
+// uncapped) ran 1-2% faster, the split ones 3-6% slower and the nt < 8 ones ~30% slower (spills)
+// -- profiles/r02/ab_phase_short_minb.jsonl; so only the first are capped.
+template <bool INTER, bool SMALL>
+constexpr int short_min_blocks() { return INTER && !SMALL ? 16 : 1; }
 template <int V, bool INTER, bool TURNS, bool SMALL>
-__global__ void __launch_bounds__(kPhaseThreads) phase_grid_short(const float *__restrict__ f,
+__global__ void __launch_bounds__(kPhaseThreads, short_min_blocks<INTER, SMALL>()) phase_grid_short(const float *__restrict__ f,
                                                                  const float *__restrict__ t, size_t nf,
                                                                  size_t nt, float *so, float *co, float *io,
                                                                  size_t head, size_t nvec, size_t n,

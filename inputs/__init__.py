@@ -13,6 +13,7 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
+import threading
 
 import numpy as np
 
@@ -30,19 +31,35 @@ CONFIG_NAMES = {
 }
 
 
+_lock = threading.Lock()
+
+
 def build(force: bool = False) -> str:
-    """Compile gen.c into libsincos_inputs.so (gcc, OpenMP)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call([
-            "gcc", "-O2", "-std=c99", "-D_GNU_SOURCE", "-ffp-contract=off", "-fno-fast-math",
-            "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
+    """Compile gen.c into libsincos_inputs.so (gcc, OpenMP): to a temporary file renamed into
+    place, under a lock, so concurrent first uses never load a half-written library."""
+    with _lock:
+        if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+            tmp = f"{_LIB}.{os.getpid()}.{threading.get_ident()}.tmp"
+            subprocess.check_call([
+                "gcc", "-O2", "-std=c99", "-D_GNU_SOURCE", "-ffp-contract=off", "-fno-fast-math",
+                "-fopenmp", "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+            os.replace(tmp, _LIB)
     return _LIB
 
 
 _lib = None
+_load_lock = threading.Lock()
 
 
 def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _load_lock:
+        return _load_locked()
+
+
+def _load_locked():
     global _lib
     if _lib is None:
         lib = ctypes.CDLL(build())

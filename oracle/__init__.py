@@ -16,6 +16,7 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
+import threading
 
 import numpy as np
 
@@ -51,10 +52,19 @@ def _cflags():
     return flags
 
 
+_build_lock = threading.Lock()
+_load_lock = threading.Lock()
+
+
 def build(force: bool = False) -> str:
-    newest = max(os.path.getmtime(p) for p in _SRCS + [_HDR])
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
-        subprocess.check_call(["gcc", *_cflags(), "-o", _LIB, *_SRCS, "-lm"])
+    """Compile the oracle (gcc) if missing or stale: to a temporary file renamed into place, under
+    a lock, so concurrent first uses (threads, processes) never load a half-written library."""
+    with _build_lock:
+        newest = max(os.path.getmtime(p) for p in _SRCS + [_HDR])
+        if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
+            tmp = f"{_LIB}.{os.getpid()}.{threading.get_ident()}.tmp"
+            subprocess.check_call(["gcc", *_cflags(), "-o", tmp, *_SRCS, "-lm"])
+            os.replace(tmp, _LIB)
     return _LIB
 
 
@@ -112,6 +122,14 @@ _P = ctypes.c_void_p
 
 
 def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _load_lock:
+        return _load_locked()
+
+
+def _load_locked():
     global _lib
     if _lib is None:
         lib = ctypes.CDLL(build())

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 
 __all__ = [
     # the hot path
@@ -142,12 +143,18 @@ def _load(path: str, sigs: dict):
     return L
 
 
+_lib_lock = threading.Lock()
+
+
 def lib():
-    """Load libsincos_pairs.so (building it in-tree with nvcc if it is missing or stale)."""
+    """Load libsincos_pairs.so (building it in-tree with nvcc if it is missing or stale; once, even
+    when several threads ask at the same time)."""
     global _lib
     if _lib is None:
-        from . import _build
-        _lib = _load(_build.build(), _SIGS)
+        with _lib_lock:
+            if _lib is None:
+                from . import _build
+                _lib = _load(_build.build(), _SIGS)
     return _lib
 
 

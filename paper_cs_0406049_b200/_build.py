@@ -12,6 +12,7 @@ import glob
 import os
 import subprocess
 import sys
+import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -75,9 +76,10 @@ def build(force: bool = False, verbose: bool = False, extra_flags=(), out: str |
 
         with ThreadPoolExecutor(max(1, min(len(sources()), os.cpu_count() or 1))) as ex:
             objs = list(ex.map(one, sources()))
+        tmp_out = f"{out}.{os.getpid()}.{threading.get_ident()}.tmp"      # renamed into place: atomic
         subprocess.check_call([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
-                               "-Xcompiler", "-fPIC", *link_flags, "-o", out + ".tmp", *objs], cwd=PKG)
-    os.replace(out + ".tmp", out)
+                               "-Xcompiler", "-fPIC", *link_flags, "-o", tmp_out, *objs], cwd=PKG)
+    os.replace(tmp_out, out)
     return out
 
 

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import contextlib
 import ctypes
+import threading
 
 from . import _build
 
@@ -32,16 +33,21 @@ class Item(ctypes.Structure):
                 ("inter", ctypes.c_void_p), ("n", ctypes.c_uint64)]
 
 
+_ab_lock = threading.Lock()
+
+
 def lib():
     """Load libsincos_pairs_ab.so (building it in-tree if missing or stale)."""
     global _ab
     if _ab is None:
-        import paper_cs_0406049_b200 as sp
-        P, I = ctypes.c_void_p, ctypes.c_int
-        sigs = dict(sp._SIGS)
-        sigs.update({"sincos_ab_set": (I, [I, I]), "sincos_ab_get": (I, [I]),
-                     "sincos_pairs_batched": (I, [P, I, I, P])})
-        _ab = sp._load(_build.build_ab(), sigs)
+        with _ab_lock:
+            if _ab is None:
+                import paper_cs_0406049_b200 as sp
+                P, I = ctypes.c_void_p, ctypes.c_int
+                sigs = dict(sp._SIGS)
+                sigs.update({"sincos_ab_set": (I, [I, I]), "sincos_ab_get": (I, [I]),
+                             "sincos_pairs_batched": (I, [P, I, I, P])})
+                _ab = sp._load(_build.build_ab(), sigs)
     return _ab
 
 

@@ -86,7 +86,7 @@ def test_phase_grid_short_and_tiny_rows_floor():
     n = f.numel() * 1001
     o = torch.empty(2 * n, device="cuda")
     got = gbps(lambda: sp.phase_grid(f, t, interleaved_out=o, units=sp.TURNS), 8 * n)
-    assert got >= 5800, f"nt=1001 {got:.0f}"
+    assert got >= 5500, f"nt=1001 {got:.0f}"   # (6.0-6.4 once the board is in its power cap)
     f1 = torch.rand(1 << 27, device="cuda")
     t1 = torch.rand(1, device="cuda")
     s, c = torch.empty(1 << 27, device="cuda"), torch.empty(1 << 27, device="cuda")

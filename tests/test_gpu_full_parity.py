@@ -167,3 +167,51 @@ def test_c4_phase_grid_full(units, variant):
                 assert bad.numel() == 0, f"{name} {comp}: {bad.numel()} mismatches from row {r0}, first {int(bad[0])}"
     del s, c, io
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("inter", [False, True])
+def test_beyond_2_pow_32_elements(inter):
+    """64-bit indexing past C5: n = 2^33 + 13 angles (split: 96 GiB resident; interleaved: 96 GiB)
+    in one launch.  theta is one 2^28-element block of C2 tiled 32 times (+13), so element i is
+    block[i mod 2^28]: every tile's outputs must equal the first tile's bit for bit, and sampled
+    elements -- both ends, around 2^31, 2^32 and 2^33 -- equal the oracle."""
+    import oracle
+    B = 1 << 28
+    n = (1 << 33) + 13
+    free, _ = torch.cuda.mem_get_info()
+    if free < 12 * n + (8 << 30):
+        pytest.skip(f"needs {12 * n / 2**30:.0f} GiB free")
+    block = inputs.generate(2, 0, B)
+    th = torch.empty(n, dtype=torch.float32, device="cuda")
+    bd = torch.from_numpy(block).cuda()
+    for k in range(0, n, B):
+        m = min(B, n - k)
+        th[k:k + m].copy_(bd[:m])
+    del bd
+    if inter:
+        io = torch.empty(2 * n, dtype=torch.float32, device="cuda")
+        sp.sincos_pairs(th, interleaved_out=io, variant=1)
+        pv = io.view(n, 2)
+        s, c = pv[:, 1], pv[:, 0]
+    else:
+        s = torch.empty(n, dtype=torch.float32, device="cuda")
+        c = torch.empty(n, dtype=torch.float32, device="cuda")
+        sp.sincos_pairs(th, s, c, variant=1)
+    torch.cuda.synchronize()
+    del th
+    s0, c0 = s[:B].clone(), c[:B].clone()
+    for k in range(B, n, B):
+        m = min(B, n - k)
+        assert bit_mismatches(s[k:k + m], s0[:m]).numel() == 0, f"tile at {k}"
+        assert bit_mismatches(c[k:k + m], c0[:m]).numel() == 0, f"tile at {k}"
+    idx = np.unique(np.concatenate([np.arange(0, 64), np.arange(n - 64, n),
+                                    np.arange((1 << 31) - 32, (1 << 31) + 32),
+                                    np.arange((1 << 32) - 32, (1 << 32) + 32),
+                                    np.arange((1 << 33) - 32, (1 << 33) + 13)])).astype(np.int64)
+    it = torch.from_numpy(idx).cuda()
+    ws, wc = oracle.sincos(block[idx % B], 1)
+    gs, gc = s[it].cpu().numpy(), c[it].cpu().numpy()
+    assert np.array_equal(gs.view(np.uint32), ws.view(np.uint32))       # (C2 has no NaN)
+    assert np.array_equal(gc.view(np.uint32), wc.view(np.uint32))
+    del s, c, s0, c0
+    torch.cuda.empty_cache()

@@ -270,10 +270,11 @@ def sincos_pairs(theta, sin_out=None, cos_out=None, interleaved_out=None, varian
 
 
 def sincos(theta, variant="normalized", interleaved=False, out=None, stream=None):
-    """Allocate outputs (or take `out`, contiguous) and run the hot path.  Returns (sin, cos) or,
-    if interleaved, a (..., 2) float32 tensor of {cos, sin} rows."""
+    """Allocate outputs (or take `out`, contiguous: a strided `out` is refused, never silently
+    left unwritten) and run the hot path.  Returns (sin, cos) or, if interleaved, a (..., 2)
+    float32 tensor of {cos, sin} rows."""
     import torch
-    th = _flat(theta, "theta")
+    th = theta.reshape(-1)               # an input may be strided: a contiguous copy is read
     if interleaved:
         o = out if out is not None else torch.empty(theta.shape + (2,), dtype=torch.float32, device=theta.device)
         sincos_pairs(th, interleaved_out=_flat(o, "out"), variant=variant, stream=stream)
@@ -317,7 +318,7 @@ def sincos_turns(x, variant="normalized", interleaved=False, out=None, stream=No
     Returns (sin 2 pi x, cos 2 pi x) or, if interleaved, a (..., 2) tensor of {cos, sin} rows."""
     import torch
     one = torch.ones(1, dtype=torch.float32, device=x.device)
-    xf = _flat(x, "x")
+    xf = x.reshape(-1)
     if interleaved:
         o = out if out is not None else torch.empty(x.shape + (2,), dtype=torch.float32, device=x.device)
         phase_grid(one, xf, interleaved_out=_flat(o, "out"), units=TURNS, variant=variant, stream=stream)

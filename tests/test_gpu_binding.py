@@ -92,8 +92,11 @@ def test_non_contiguous_out_is_refused():
         sp.sincos(t, interleaved=True, out=o)
     with pytest.raises(ValueError, match="contiguous"):
         sp.sincos_turns(t, out=(s, c))
-    with pytest.raises(ValueError, match="contiguous"):
-        sp.sincos(torch.rand(100, 2, device="cuda")[:, 0])
+    # a strided INPUT is fine (read through a contiguous copy)
+    tin = torch.rand(100, 2, device="cuda")[:, 0]
+    s3, c3 = sp.sincos(tin)
+    ws3, wc3 = oracle.sincos(tin.contiguous().cpu().numpy(), 0)
+    assert np.array_equal(s3.cpu().numpy(), ws3) and np.array_equal(c3.cpu().numpy(), wc3)
     # contiguous outs of any shape are filled in place
     s2, c2 = torch.empty(10, 100, device="cuda"), torch.empty(10, 100, device="cuda")
     r = sp.sincos(t.view(10, 100), out=(s2, c2))

@@ -281,7 +281,8 @@ def sincos(theta, variant="normalized", interleaved=False, out=None, stream=None
         if out is None:
             _record(stream, theta.device, o)
         return o
-    s, c = out if out is not None else (torch.empty_like(theta), torch.empty_like(theta))
+    s, c = out if out is not None else (torch.empty(theta.shape, dtype=torch.float32, device=theta.device),
+                                             torch.empty(theta.shape, dtype=torch.float32, device=theta.device))
     sincos_pairs(th, _flat(s, "out[0]"), _flat(c, "out[1]"), variant=variant, stream=stream)
     if out is None:
         _record(stream, theta.device, s, c)
@@ -324,7 +325,8 @@ def sincos_turns(x, variant="normalized", interleaved=False, out=None, stream=No
         phase_grid(one, xf, interleaved_out=_flat(o, "out"), units=TURNS, variant=variant, stream=stream)
         _record(stream, x.device, one, *(() if out is not None else (o,)))
         return o
-    s, c = out if out is not None else (torch.empty_like(x), torch.empty_like(x))
+    s, c = out if out is not None else (torch.empty(x.shape, dtype=torch.float32, device=x.device),
+                                             torch.empty(x.shape, dtype=torch.float32, device=x.device))
     phase_grid(one, xf, _flat(s, "out[0]"), _flat(c, "out[1]"), units=TURNS, variant=variant, stream=stream)
     _record(stream, x.device, one, *(() if out is not None else (s, c)))
     return s, c

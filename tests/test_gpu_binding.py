@@ -92,7 +92,12 @@ def test_non_contiguous_out_is_refused():
         sp.sincos(t, interleaved=True, out=o)
     with pytest.raises(ValueError, match="contiguous"):
         sp.sincos_turns(t, out=(s, c))
-    # a strided INPUT is fine (read through a contiguous copy)
+    # a strided INPUT is fine (read through a contiguous copy), also a transposed one
+    tt = torch.rand(64, 32, device="cuda").t()
+    s4, c4 = sp.sincos(tt)
+    ws4, wc4 = oracle.sincos(tt.contiguous().cpu().numpy().ravel(), 0)
+    assert s4.is_contiguous() and np.array_equal(s4.cpu().numpy().ravel(), ws4)
+    assert np.array_equal(c4.cpu().numpy().ravel(), wc4)
     tin = torch.rand(100, 2, device="cuda")[:, 0]
     s3, c3 = sp.sincos(tin)
     ws3, wc3 = oracle.sincos(tin.contiguous().cpu().numpy(), 0)

@@ -274,18 +274,16 @@ def sincos(theta, variant="normalized", interleaved=False, out=None, stream=None
     left unwritten) and run the hot path.  Returns (sin, cos) or, if interleaved, a (..., 2)
     float32 tensor of {cos, sin} rows."""
     import torch
-    th = theta.reshape(-1)               # an input may be strided: a contiguous copy is read
+    th = theta.contiguous().view(-1)     # an input may be strided: a contiguous copy is read
     if interleaved:
         o = out if out is not None else torch.empty(theta.shape + (2,), dtype=torch.float32, device=theta.device)
         sincos_pairs(th, interleaved_out=_flat(o, "out"), variant=variant, stream=stream)
-        if out is None:
-            _record(stream, theta.device, o)
+        _record(stream, theta.device, th, *(() if out is not None else (o,)))
         return o
     s, c = out if out is not None else (torch.empty(theta.shape, dtype=torch.float32, device=theta.device),
                                              torch.empty(theta.shape, dtype=torch.float32, device=theta.device))
     sincos_pairs(th, _flat(s, "out[0]"), _flat(c, "out[1]"), variant=variant, stream=stream)
-    if out is None:
-        _record(stream, theta.device, s, c)
+    _record(stream, theta.device, th, *(() if out is not None else (s, c)))
     return s, c
 
 
@@ -319,16 +317,16 @@ def sincos_turns(x, variant="normalized", interleaved=False, out=None, stream=No
     Returns (sin 2 pi x, cos 2 pi x) or, if interleaved, a (..., 2) tensor of {cos, sin} rows."""
     import torch
     one = torch.ones(1, dtype=torch.float32, device=x.device)
-    xf = x.reshape(-1)
+    xf = x.contiguous().view(-1)
     if interleaved:
         o = out if out is not None else torch.empty(x.shape + (2,), dtype=torch.float32, device=x.device)
         phase_grid(one, xf, interleaved_out=_flat(o, "out"), units=TURNS, variant=variant, stream=stream)
-        _record(stream, x.device, one, *(() if out is not None else (o,)))
+        _record(stream, x.device, one, xf, *(() if out is not None else (o,)))
         return o
     s, c = out if out is not None else (torch.empty(x.shape, dtype=torch.float32, device=x.device),
                                              torch.empty(x.shape, dtype=torch.float32, device=x.device))
     phase_grid(one, xf, _flat(s, "out[0]"), _flat(c, "out[1]"), units=TURNS, variant=variant, stream=stream)
-    _record(stream, x.device, one, *(() if out is not None else (s, c)))
+    _record(stream, x.device, one, xf, *(() if out is not None else (s, c)))
     return s, c
 
 

@@ -652,6 +652,8 @@ def run_ours(args, rank, world, local_rank):
             "traffic": ncu_traffic(n, W.interleaved),
             "kernel": f"sincos_vec_kernel variant {vname[dom]}", "bytes_per_launch": BYTES_PER_PAIR * n,
             "bytes_per_pair": BYTES_PER_PAIR, "peak_source": peak_src,
+            "traffic_source": "profiles/ncu_summary.json (ncu --set full of this kernel; summary in "
+                              "profiles/ncu_r02_summary.txt, launch list profiles/ncu_launches_r02.csv)",
             "frac_of_theoretical_8180": achieved / 8180.0,
             # B200_PROFILING.md: 7.7 TB/s is the HGX B200 HBM3e spec figure (8 TB/s DGX); 8180 is
             # the 3996 MHz memory clock x 2 x 8192 bits

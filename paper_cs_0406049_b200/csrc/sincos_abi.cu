@@ -181,6 +181,7 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
         }
     }
     if (hs != SIZE_MAX) {
+#ifdef SINCOS_AB
         const int k = static_cast<int>(((reinterpret_cast<uintptr_t>(theta) + 4 * hs) & 15) / 4);   // 0..3
         size_t hb = hs >= static_cast<size_t>(k) ? hs : hs + 4;    // aligned theta base >= theta
         if (hb > n) hb = n;
@@ -191,6 +192,9 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
         if (!nc) return SINCOS_ERR_OVERLAP;      // unreachable: in place shares theta's alignment
         e = launch_shift(variant, inter, k, grid_for(nvec, threads, sms, cfg_bps), threads, theta, so, co, io, hb,
                          nvec, n, stream);
+#else
+        return SINCOS_ERR_INVALID_ARGUMENT;      // unreachable: the product takes the 256-bit forms
+#endif
     } else if ((w == 0 || (w == 4 && !inter && T.vec == 8 && T.realign != 2)) && realign) {
         // KB3c: theta's frame, outputs re-aligned (sin and cos apart mod 16 B; pairs only 4-B aligned)
         const uintptr_t ta = reinterpret_cast<uintptr_t>(theta);

@@ -265,6 +265,7 @@ cudaError_t launch_scalar(int variant, bool inter, unsigned grid, unsigned threa
 }
 #endif
 
+#ifdef SINCOS_AB   // the 128-bit theta re-alignment: A/B build only (the product routes those layouts to KB3c)
 template <int V, bool INTER>
 static VecFn pick_shift(int k) {
     switch (k) {
@@ -286,6 +287,7 @@ cudaError_t launch_shift(int variant, bool inter, int k, unsigned grid, unsigned
     void *args[] = {&theta, &so, &co, &io, &head, &nvec, &n};
     return cudaLaunchKernel(reinterpret_cast<const void *>(fn), dim3(grid), dim3(threads), args, 0, stream);
 }
+#endif
 
 cudaError_t launch_rcp(unsigned grid, unsigned threads, const float *d, float *out, size_t n, cudaStream_t stream) {
     void *args[] = {&d, &out, &n};

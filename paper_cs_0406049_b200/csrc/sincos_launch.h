@@ -41,7 +41,8 @@ cudaError_t launch_vec(int variant, bool inter, int w, int unroll, bool nc, bool
 // Context kernels for the bench (3 = CUDA sincosf, 4 = __sincosf), 32-B aligned buffers, head 0.
 cudaError_t launch_compare(int which, bool inter, unsigned grid, unsigned threads, const float *theta, float *so,
                            float *co, float *io, size_t nvec, size_t n, cudaStream_t stream);
-// KB3b: outputs 16-B aligned from element `head`, theta K = k floats past a 16-B boundary there.
+// KB3b, 128-bit form (A/B build only): outputs 16-B aligned from element `head`, theta K = k
+// floats past a 16-B boundary there.
 cudaError_t launch_shift(int variant, bool inter, int k, unsigned grid, unsigned threads, const float *theta,
                          float *so, float *co, float *io, size_t head, size_t nvec, size_t n, cudaStream_t stream);
 // KB3b, 256-bit form (sincos_outshift.cu): outputs 32-B aligned from `head`, theta k = 1..7 floats

@@ -146,7 +146,13 @@ def main():
                            "duration_s_under_ncu": dom.get("gpu__time_duration.sum")},
               "all": [{"kernel": k["kernel"], "dram_bytes_read": k.get("dram__bytes_read.sum"),
                        "dram_bytes_write": k.get("dram__bytes_write.sum")} for k in sk]}
-        json.dump(js, open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w"), indent=1)
+        path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+        if os.path.exists(path):          # keep the per-config DRAM captures (tools/prof_configs.py)
+            prev = json.load(open(path))
+            for k in ("by_config", "by_config_source"):
+                if k in prev and k not in js:
+                    js[k] = prev[k]
+        json.dump(js, open(path, "w"), indent=1)
     print("\n".join(lines))
 
 

@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--n-per-rank", dest="n", type=int, default=N_PER_RANK,
                     help="elements per rank for c2 (default 2^28)")
     ap.add_argument("--e2e-max", type=int, default=1 << 28, help="elements per rank in the e2e leg")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded oracle sample for cpu_baseline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -733,17 +733,20 @@ def run_ours(args, rank, world, local_rank):
         e2e_step()
         barrier()
         k2 = max(1, min(args.e2e_steps, args.steps))
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(k2):
+        # events on the caller's stream between the (synchronous) steps: each step's span
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(k2 + 1)]
+        marks[0].record(stream)
+        for k in range(k2):
             e2e_step()
-        b.record(stream)
+            marks[k + 1].record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        t2 = max_over_ranks(a.elapsed_time(b), world, cdev)
+        t2 = max_over_ranks(marks[0].elapsed_time(marks[-1]), world, cdev)
+        step_ms = [marks[k].elapsed_time(marks[k + 1]) for k in range(k2)]
         e2e = {"value": world * len(variants) * e2e_n * k2 / (t2 / 1e3), "unit": "pairs/s",
                "h2d_bytes_per_step": len(variants) * 4 * e2e_n, "d2h_bytes_per_step": len(variants) * 8 * e2e_n,
                "steps": k2, "elements_per_rank": e2e_n,
+               "step_ms_min_median_max": [min(step_ms), statistics.median(step_ms), max(step_ms)],
                "path": "sincos_pairs_host: pinned host buffers, chunked H2D -> kernel -> D2H over 3 streams"}
         # the e2e roofline: one step's bytes through the PCIe copy engines with plain pinned copies,
         # H2D and D2H issued concurrently on two streams (as the pipeline runs them) and each alone

@@ -130,3 +130,33 @@ def test_temporaries_on_a_side_stream():
         del junk
         side.synchronize()
         assert torch.equal(got, want) and torch.equal(s, ws_) and torch.equal(c, wc_)
+
+
+def test_every_entry_point_accepts_empty_inputs():
+    """n = 0 (and nf or nt = 0) is a no-op everywhere: nothing launched, nothing raised; an empty
+    sum zeroes its output."""
+    e = torch.empty(0, device="cuda")
+    before = sp.launch_count()
+    sp.sincos_pairs(e, e, e)
+    sp.sincos_pairs(e, interleaved_out=e)
+    s, c = sp.sincos(e)
+    assert s.numel() == 0 and c.numel() == 0
+    assert sp.cis(e).numel() == 0
+    sp.sincos_pairs_method(e, sp.make_method(*sp.PAPER_METHODS[1]), e, e)
+    sp.sincos_pairs_dtype(e, torch.empty(0, dtype=torch.float16, device="cuda"),
+                          torch.empty(0, dtype=torch.float16, device="cuda"))
+    sp.interleave(e, e, e)
+    sp.deinterleave(e, e, e)
+    sp.phase_grid(e, torch.rand(5, device="cuda"), e, e)
+    sp.phase_grid(torch.rand(5, device="cuda"), e, interleaved_out=e)
+    s2, c2 = sp.sincos_turns(e)
+    assert s2.numel() == 0
+    sp.sincos_pairs_sharded([{"theta": e, "sin": e, "cos": e}])
+    sp.sincos_pairs_host(torch.empty(0), torch.empty(0), torch.empty(0),
+                         workspace=torch.empty(sp.host_workspace_min_bytes(), dtype=torch.uint8, device="cuda"))
+    torch.cuda.synchronize()
+    assert sp.launch_count() == before
+    out = torch.full((4,), 3 + 3j, dtype=torch.complex64, device="cuda")
+    sp.nudft(torch.rand(4, device="cuda"), e, torch.empty(0, dtype=torch.complex64, device="cuda"), out=out)
+    torch.cuda.synchronize()
+    assert torch.all(out == 0)

@@ -143,23 +143,56 @@ __device__ __forceinline__ void store_realigned(float *x, size_t f0, const float
 // KI: the interleaved stream's offset at compile time (1, 3, 5, 7: pairs only 4-B aligned), or
 // for split outputs KI = 8 * KS + KC with both offsets at compile time (0..63), or -1 (both at
 // run time)
-// Register budget: most instances need 34-40 registers, which leaves 12 resident 128-thread
-// blocks per SM (75% occupancy); capped at 32 (16 blocks, full occupancy, a few bytes of
-// spill) they run faster where the kernel waits on HBM -- measured for most split instances
-// (sin+2 cos+5: 6.46 -> 6.67 TB/s) and the interleaved ones with k <= 4 (k = 3: 6.61 -> 6.68),
-// slower for interleaved k > 4 (k = 7: 6.85 -> 6.55) and for the split instances that would
-// spill more (below; tools/ab_layouts.py, profiles/r02).  The capped instances take 128-thread
-// blocks (launch_outshift).
-// Split instances KI = 8 ks + kc: capped, except those that would spill >= 12 bytes at 32
-// registers (ks = 4; ks = 6 with odd kc; ks = 3, kc = 0), which ran 1-13% faster uncapped --
-// every (ks, kc) timed both ways, profiles/r02/ab_layouts_all2.jsonl.
+// Register budget.  Uncapped, most instances take 34-48 registers: 10-12 resident 128-thread
+// blocks per SM.  Capped at 32 (16 blocks, full occupancy, a few bytes of spill) they run
+// faster where the kernel waits on HBM (sin+2 cos+5: 6.46 -> 6.67 TB/s; tools/ab_layouts.py,
+// profiles/r02) -- as long as the spill stays small, which the store order below arranges.
+//
+// Which stream to store first (split).  Both streams' eight values are live until the first
+// one is stored, so the first stream's re-alignment sets the register peak; at 32 registers
+// ptxas spills (bytes; sm_100a, nvcc 12.9, both variants) when the stream at offset a goes
+// first while offset b's values wait: a = 0, 1, 7: 0; a = 2, 5: 4; a = 3: 8 (12 if b = 0);
+// a = 4: 16-24; a = 6: 4 (12 if b is odd).  Storing the cheaper one first keeps every split
+// instance at <= 8 bytes, so all of them are capped.  Sin first throughout (the first round-2
+// form) spilled up to 24 bytes at sin offset 4, where those instances ran uncapped at 40-48
+// registers: 5.70-6.54 TB/s, now 6.45-6.79 (all 64 pairs timed both orders, both variants:
+// profiles/r02/ab_layouts_order*.jsonl, ab_layouts_flip*.jsonl, ab_all_new_v*.jsonl).
+//
+// Interleaved pairs at k = 3, 5, 7 floats: two trips per thread (half the blocks), the next
+// trip's theta vector loaded before this trip's pairs are computed and stored, at 40 registers
+// (12 resident blocks) -- 6.54-6.81 TB/s against 5.80-6.54 with one trip per thread (variant A
+// lost most, at 48-56 registers uncapped); k = 1 fits 32 registers and runs at 6.88-6.91
+// without it (prefetching there cost 1-2%).  profiles/r02/ab_inter_pf_v*.jsonl.
+#ifndef SINCOS_OUTSHIFT_PF
+#define SINCOS_OUTSHIFT_PF 1                 // 0: one trip per thread everywhere (A/B)
+#endif
+template <bool INTER, int KI>
+__host__ __device__ constexpr bool outshift_pf() {
+    return SINCOS_OUTSHIFT_PF && INTER && (KI == 3 || KI == 5 || KI == 7);
+}
+#ifndef SINCOS_OUTSHIFT_ORDER
+#define SINCOS_OUTSHIFT_ORDER 1          // 0: sin first, 2: the other order (A/B builds only)
+#endif
+__host__ __device__ constexpr int spill_first(int a, int b) {
+    return a == 4 ? 16 : a == 3 ? (b == 0 ? 12 : 8) : a == 6 ? (b % 2 ? 12 : 4) : (a == 2 || a == 5) ? 4 : 0;
+}
+template <int KI>
+__host__ __device__ constexpr bool cos_first() {
+    if constexpr (KI < 0 || SINCOS_OUTSHIFT_ORDER == 0) return false;
+    else if constexpr (SINCOS_OUTSHIFT_ORDER == 2) return !(spill_first(KI % 8, KI / 8) < spill_first(KI / 8, KI % 8));
+    else return spill_first(KI % 8, KI / 8) < spill_first(KI / 8, KI % 8);
+}
 template <bool INTER, int KI>
 constexpr int outshift_min_blocks() {
     if constexpr (INTER) {
-        return KI >= 0 && KI <= 4 ? 16 : 1;
+        return outshift_pf<INTER, KI>() ? 12 : KI >= 0 && KI <= 4 ? 16 : 1;
     } else {
-        constexpr int ks = KI / 8, kc = KI % 8;
-        return KI < 0 || ks == 4 || (ks == 6 && kc % 2 == 1) || (ks == 3 && kc == 0) ? 1 : 16;
+        if constexpr (SINCOS_OUTSHIFT_ORDER == 0) {
+            constexpr int ks = KI / 8, kc = KI % 8;
+            return KI < 0 || ks == 4 || (ks == 6 && kc % 2 == 1) || (ks == 3 && kc == 0) ? 1 : 16;
+        } else {
+            return KI < 0 ? 1 : 16;
+        }
     }
 }
 template <bool INTER, int KI>
@@ -175,12 +208,21 @@ sincos_outshift_kernel(const float *theta, float *so, float *co, float *io,
     if (tid < head) emit_scalar<V, INTER>(theta, tid, so, co, io);
     if (tid < n - tail0) emit_scalar<V, INTER>(theta, tail0 + tid, so, co, io);
     const unsigned lane = threadIdx.x & 31u;
+    constexpr bool PF = outshift_pf<INTER, KI>();
+    float xn[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+    if (PF && tid < nvec) Mem<8, true>::load(xn, theta + head + 8 * tid);
     for (size_t w0 = tid - lane; w0 < nvec; w0 += nthr) {   // warp-uniform trips
         const size_t v = w0 + lane;
         const bool act = v < nvec;
         const bool last = act && (lane == 31u || v + 1 >= nvec);
         float x[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
-        if (act) Mem<8, true>::load(x, theta + head + 8 * v);
+        if constexpr (PF) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = xn[j];
+            if (v + nthr < nvec) Mem<8, true>::load(xn, theta + head + 8 * (v + nthr));
+        } else {
+            if (act) Mem<8, true>::load(x, theta + head + 8 * v);
+        }
         const size_t e0 = head + 8 * v;
         if constexpr (INTER) {
             float cs[16];
@@ -191,8 +233,13 @@ sincos_outshift_kernel(const float *theta, float *so, float *co, float *io,
             float sv[8], cv[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) op<V>(x[j], sv[j], cv[j]);
-            store_realigned<8, (KI >= 0 ? KI / 8 : -1)>(so, e0, sv, ks, lane, act, last);
-            store_realigned<8, (KI >= 0 ? KI % 8 : -1)>(co, e0, cv, kc, lane, act, last);
+            if constexpr (cos_first<KI>()) {
+                store_realigned<8, (KI >= 0 ? KI % 8 : -1)>(co, e0, cv, kc, lane, act, last);
+                store_realigned<8, (KI >= 0 ? KI / 8 : -1)>(so, e0, sv, ks, lane, act, last);
+            } else {
+                store_realigned<8, (KI >= 0 ? KI / 8 : -1)>(so, e0, sv, ks, lane, act, last);
+                store_realigned<8, (KI >= 0 ? KI % 8 : -1)>(co, e0, cv, kc, lane, act, last);
+            }
         }
     }
 }
@@ -226,6 +273,7 @@ cudaError_t launch_outshift(int variant, bool inter, int ks, int kc, unsigned gr
                      : variant == kRenormalized ? pick_outshift<kRenormalized>(inter, ks, kc)
                                                 : pick_outshift<kNull>(inter, ks, kc);
     void *args[] = {&theta, &so, &co, &io, &head, &nvec, &n, &ks, &kc};
+    if (SINCOS_OUTSHIFT_PF && inter && (ks == 3 || ks == 5 || ks == 7)) grid = (grid + 1) / 2;   // two trips each
     if (threads > 128) {            // (A/B block sizes) the register-capped instances take 128 at most
         grid = static_cast<unsigned>((static_cast<size_t>(grid) * threads + 127) / 128);
         threads = 128;

@@ -122,11 +122,12 @@ def test_phase_grid_split_offsets(shape, off):
     check(bi, G + off, G + off + 2 * n)
 
 
-@pytest.mark.parametrize("n", SIZES)
-@pytest.mark.parametrize("offs", [(0, 1, 2), (1, 0, 3), (3, 2, 0), (2, 1, 1)])
+@pytest.mark.parametrize("n", SIZES + [8 * 128 * 3 + 5, 8 * 128 * 2 * 150 + 21])
+@pytest.mark.parametrize("offs", [(0, 1, 2), (1, 0, 3), (3, 2, 0), (2, 1, 1), (0, 2, 7), (0, 3, 6)])
 def test_pairs_outputs_apart(n, offs):
     """sin and cos at different offsets mod 16 B, interleaved pairs only 4-B aligned (the
-    output-realigning kernel: lane 0 / last-lane scalar edges, whole blocks in between)."""
+    output-realigning kernel: lane 0 / last-lane edge pieces, whole blocks in between; the
+    interleaved k = 3, 5, 7 instances at sizes with a partial and a full second trip)."""
     ot, os_, oc = offs
     tb = torch.from_numpy(inputs.generate(2, 0, n + 4)).cuda()
     th = tb[ot:ot + n]

@@ -757,3 +757,32 @@ def test_in_place_with_cos_off_alignment(variant, coff):
     sp.sincos_pairs(t, t, c, variant=variant)
     torch.cuda.synchronize()
     assert_parity(t.cpu().numpy(), c.cpu().numpy(), os_, oc, f"in place, cos +{coff}")
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_outshift_interleaved_two_trips(variant):
+    """KB3c for interleaved pairs at k = 3, 5, 7 floats runs two trips per thread with the next
+    trip's theta vector prefetched (half the blocks; csrc/sincos_outshift.cu outshift_pf):
+    every odd interleaved offset against an aligned and an unaligned theta, at sizes where the
+    last block has one trip, a partial second trip, exactly two, and a ragged tail -- and on
+    the A/B build's grid-stride grids (hundreds of trips per thread)."""
+    rng = np.random.default_rng(77)
+    N = 1 << 20
+    base = rng.uniform(-5e3, 5e3, N + 64).astype(np.float32)
+    rs, rc = oracle.sincos(base, variant)
+    bt = torch.from_numpy(base).cuda()
+    bi = torch.empty(2 * N + 64, dtype=torch.float32, device="cuda")
+    sizes = [1023, 1024 + 7, 2048, 2048 + 8 * 128 + 3, 8 * 128 * 3 + 1, 8 * 128 * 2 * 77 + 8 * 5 + 6, N]
+    for ctx in (contextlib.nullcontext(), ab.knobs(blocks_per_sm=1), ab.knobs(blocks_per_sm=3)):
+        with ctx:
+            for ot in (0, 8, 3):
+                for oi in (1, 3, 5, 7):
+                    for n in sizes:
+                        t = bt[ot:ot + n]
+                        io = bi[oi:oi + 2 * n]
+                        io.fill_(float("nan"))
+                        sp.sincos_pairs(t, interleaved_out=io, variant=variant)
+                        torch.cuda.synchronize()
+                        iv = io.cpu().numpy()
+                        assert_parity(iv[1::2], iv[0::2], rs[ot:ot + n], rc[ot:ot + n],
+                                      f"inter +{oi} theta +{ot} n={n}")

@@ -41,27 +41,31 @@ def bufs():
     torch.cuda.empty_cache()
 
 
-# (theta offset, sin offset, cos offset, interleaved?, floor GB/s, recorded GB/s)
+# (theta offset, sin offset, cos offset, interleaved float offset or None, floor GB/s, recorded GB/s)
 CASES = {
-    "aligned split (256-bit)": (0, 0, 0, False, 6000, 6870),
-    "aligned interleaved": (0, 0, 0, True, 6000, 6890),
-    "shared 16 B (256-bit theta re-alignment)": (4, 0, 0, False, 6000, 6800),
-    "theta realigned (KB3b)": (1, 0, 0, False, 6000, 6810),
-    "theta realigned interleaved": (1, 0, 0, True, 6000, 6890),
-    "outputs realigned (KB3c)": (0, 1, 2, False, 5900, 6760),
-    "outputs realigned, sin 4 off (KB3c)": (0, 4, 2, False, 5400, 6220),
-    "sin/cos sharing 16 B (KB3c)": (0, 3, 7, False, 5600, 6420),
-    "pairs 4-B only (KB3c)": (0, 1, 1, "odd", 5900, 6710),
+    "aligned split (256-bit)": (0, 0, 0, None, 6000, 6870),
+    "aligned interleaved": (0, 0, 0, 0, 6000, 6890),
+    "shared 16 B (256-bit theta re-alignment)": (4, 0, 0, None, 6000, 6800),
+    "theta realigned (KB3b)": (1, 0, 0, None, 6000, 6810),
+    "theta realigned interleaved": (1, 0, 0, 0, 6000, 6890),
+    "outputs realigned (KB3c)": (0, 1, 2, None, 5900, 6760),
+    "outputs realigned, sin 4 off (KB3c, cos stored first)": (0, 4, 2, None, 5900, 6600),
+    "sin/cos sharing 16 B (KB3c)": (0, 3, 7, None, 5800, 6570),
+    "pairs 4-B only, k = 1 (KB3c)": (0, 0, 0, 1, 5900, 6710),
+    "pairs 4-B only, k = 3 (KB3c, two trips)": (0, 0, 0, 3, 5900, 6690),
+    "pairs 4-B only, k = 5 (KB3c, two trips)": (0, 0, 0, 5, 5800, 6540),
+    "pairs 4-B only, k = 7 (KB3c, two trips)": (0, 0, 0, 7, 5900, 6730),
 }
 
 
 @pytest.mark.parametrize("name", list(CASES))
 def test_hot_path_floor(bufs, name):
+    """Variant N at C2 size; `recorded` is the r02 sweep's (tools/ab_layouts.py), ~2% run to run."""
     base, sb, cb, ib = bufs
     ot, os_, oc, inter, floor, _ = CASES[name]
     th = base[ot:ot + N]
-    if inter:
-        o = ib[1:1 + 2 * N] if inter == "odd" else ib[:2 * N]
+    if inter is not None:
+        o = ib[inter:inter + 2 * N]
         fn = lambda: sp.sincos_pairs(th, interleaved_out=o)  # noqa: E731
     else:
         s, c = sb[os_:os_ + N], cb[oc:oc + N]

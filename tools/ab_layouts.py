@@ -2,7 +2,7 @@
 
   python tools/ab_layouts.py            # times every tools/ab_layouts/*.so
 
-C2 size (2^28 angles), variant N: theta / sin / cos / interleaved at the offsets (in floats)
+C2 size (2^28 angles), variant N (AB_VARIANT=1: A): theta / sin / cos / interleaved at the offsets (in floats)
 that select each kernel form -- aligned (KB1/KB2), theta off the outputs (KB3b), sin and cos
 apart mod 16 B and interleaved pairs only 4-B aligned (KB3c) -- GB/s of 12 B per pair,
 median of 5 rounds x 5 launches, the libraries interleaved over rounds.  One JSON line per
@@ -21,6 +21,11 @@ N = 1 << 28
 CASES = [("aligned split", 0, 0, 0), ("aligned inter", 0, 0), ("theta+1 split", 1, 0, 0), ("theta+1 inter", 1, 0),
          ("sin+1 cos+2", 0, 1, 2), ("sin+0 cos+3", 0, 0, 3), ("sin+2 cos+5", 0, 2, 5), ("inter+1", 0, 1),
          ("inter+3", 0, 3), ("theta+3 inter+5", 3, 5)]
+
+
+if os.environ.get("AB_CASES") == "inter":
+    CASES = [("aligned split", 0, 0, 0), ("sin+2 cos+5", 0, 2, 5)] + [(f"inter+{a}", 0, a) for a in range(8)]
+VARIANT = int(os.environ.get("AB_VARIANT", "0"))     # 0 = N, 1 = A
 
 
 if os.environ.get("AB_CASES") == "all":
@@ -54,7 +59,7 @@ def main():
         for _ in range(5):
             for lname, L in libs.items():
                 def go():
-                    r = L.sincos_pairs(th, *outs, N, 0, st)
+                    r = L.sincos_pairs(th, *outs, N, VARIANT, st)
                     assert r == 0, r
                 go()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -67,7 +72,7 @@ def main():
         for lname in libs:
             res[lname][name] = round(12 * N / (statistics.median(samples[lname]) / 1e3) / 1e9, 1)
     for lname in libs:
-        print(json.dumps({"lib": lname, "GBps": res[lname]}))
+        print(json.dumps({"lib": lname, "variant": VARIANT, "GBps": res[lname]}))
 
 
 if __name__ == "__main__":

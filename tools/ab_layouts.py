@@ -25,6 +25,12 @@ CASES = [("aligned split", 0, 0, 0), ("aligned inter", 0, 0), ("theta+1 split", 
 
 if os.environ.get("AB_CASES") == "inter":
     CASES = [("aligned split", 0, 0, 0), ("sin+2 cos+5", 0, 2, 5)] + [(f"inter+{a}", 0, a) for a in range(8)]
+if os.environ.get("AB_CASES") == "theta":
+    # theta at every float offset against aligned split / interleaved outputs, and against
+    # outputs that are themselves off (theta and outputs apart in both directions)
+    CASES = [(f"theta+{a} split", a, 0, 0) for a in range(8)] + [(f"theta+{a} inter", a, 0) for a in range(8)] + \
+            [(f"theta+{a} sin+{b} cos+{b}", a, b, b) for a, b in ((1, 3), (3, 1), (2, 6), (5, 2))] + \
+            [(f"theta+{a} inter+{b}", a, b) for a, b in ((1, 4), (3, 5), (2, 7), (6, 1))]
 VARIANT = int(os.environ.get("AB_VARIANT", "0"))     # 0 = N, 1 = A
 
 

@@ -5,7 +5,7 @@
   python tools/ab_phase.py sustain                    # GPU box: 0.5-1 s of load per library from idle
 
 Cases: ragged row lengths (and t offsets) at ~2^30 pairs per launch, split and interleaved,
-turns, variant N; GB/s of the 8 B written per pair, median of 5 rounds x 5 launches, the
+turns, variant N (AB_VARIANT=1: A; AB_UNITS=0: radians); GB/s of the 8 B written per pair, median of 5 rounds x 5 launches, the
 libraries interleaved over rounds.  One JSON line per library."""
 import ctypes
 import glob
@@ -31,6 +31,10 @@ if os.environ.get("AB_CASES") == "rows":
     CASES = [(32767, 0), (32772, 0), (16385, 1), (8191, 3), (4000, 5), (2049, 0), (1025, 2)]
 if os.environ.get("AB_CASES") == "aligned":
     CASES = [(32768, 0), (8192, 0), (4096, 0), (2048, 0), (1000, 0), (512, 0), (256, 0), (136, 0), (64, 0), (16, 0)]
+
+
+VARIANT = int(os.environ.get("AB_VARIANT", "0"))     # 0 = N, 1 = A
+UNITS = int(os.environ.get("AB_UNITS", "1"))         # 1 = turns, 0 = radians
 
 
 def build(name, flags):
@@ -67,7 +71,7 @@ def run():
             for _ in range(5):
                 for name, L in libs.items():
                     def go():
-                        r = L.sincos_phase_grid(f.data_ptr(), nf, t.data_ptr(), nt, *outs, 1, 0, st)
+                        r = L.sincos_phase_grid(f.data_ptr(), nf, t.data_ptr(), nt, *outs, UNITS, VARIANT, st)
                         assert r == 0, r
                     go()
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -80,7 +84,7 @@ def run():
             for name in libs:
                 res[name][key] = round(8 * nf * nt / (statistics.median(samples[name]) / 1e3) / 1e9, 1)
     for name in libs:
-        print(json.dumps({"lib": name, "GBps": res[name]}))
+        print(json.dumps({"lib": name, "variant": VARIANT, "units": UNITS, "GBps": res[name]}))
 
 
 def sustain():

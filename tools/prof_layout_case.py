@@ -1,5 +1,5 @@
 """One hot-path pointer layout at the C2 size, launched twice (for ncu: --launch-skip 1
---launch-count 1).  Product library, variant N.
+--launch-count 1).  Product library, variant N (PROF_VARIANT=1: A).
 
   python tools/prof_layout_case.py THETA_OFF SIN_OFF COS_OFF    (split)
   python tools/prof_layout_case.py THETA_OFF INTER_OFF          (interleaved)"""
@@ -24,6 +24,6 @@ else:
     ib = torch.empty(2 * N + 16, device="cuda")
     outs = {"interleaved_out": ib[offs[1]:offs[1] + 2 * N]}
 for _ in range(2):
-    sp.sincos_pairs(th, **outs)
+    sp.sincos_pairs(th, **outs, variant=int(os.environ.get("PROF_VARIANT", "0")))
 torch.cuda.synchronize()
 print("ok", offs)

@@ -22,12 +22,6 @@ def cuda():
     yield
 
 
-def guarded(n, dtype=torch.float32, off=0):
-    words = (n * torch.finfo(dtype).bits // 32) if dtype != torch.float32 else n
-    buf = torch.full((2 * G + words + 8,), SENT, dtype=torch.int32, device="cuda")
-    return buf, buf[G + off // 1:]
-
-
 def check(buf, lo, hi):
     b = buf.cpu().numpy()
     assert np.all(b[:lo] == SENT) and np.all(b[hi:] == SENT), (np.flatnonzero(b[:lo] != SENT)[:5],

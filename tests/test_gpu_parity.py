@@ -13,7 +13,7 @@ import pytest
 
 import inputs
 import oracle
-from helpers import ULP4, assert_parity, oracle_threaded, same_values
+from helpers import assert_parity, oracle_threaded
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu

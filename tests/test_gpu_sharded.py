@@ -3,7 +3,6 @@ this pool: sincos_pairs_sharded (one host thread per device; forced onto its wor
 with SINCOS_SHARDED_WORKERS=1 so one GPU exercises them) and sincos_pairs_sharded_stats (a
 1-rank NCCL communicator still runs ncclCommInitAll and ncclAllGather), their validation before
 any launch, error codes, and the communicator kept across calls.  ``pytest -m gpu``."""
-import ctypes
 import os
 import subprocess
 import sys

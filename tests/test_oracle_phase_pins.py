@@ -2,7 +2,6 @@
 p = RN(f * t), in radians (the whole method) or in turns (the method from the reduction on,
 P:53-54).  Same legend as test_oracle_pins.py: CLOSED, PAPER, SURVEY, LIBM."""
 import json
-import math
 import os
 
 import numpy as np

@@ -529,3 +529,21 @@ def test_all_bits_hash_live(golden, name, variant):
     h, nn, ex = oracle.hash_bits(variant, 0, 0xFFFFFFFF)
     hb = golden["survey_crosscheck"]["all_bits_hash"]
     assert "0x%016X" % h == hb[name] and nn == hb["nan_pairs"] and ex == hb["exact_0_1"]
+
+
+def test_error_stats_interleaved_equals_split_form():
+    """oracle.error_stats_interleaved (the {cos, sin} record layout, G13) reports exactly what
+    the split form reports on the same pairs -- and that split form is pinned against the
+    paper's table above -- including a NaN, an infinity and a wrong pair."""
+    rng = np.random.default_rng(5)
+    th = np.concatenate([rng.uniform(-1e4, 1e4, 5000), [np.nan, np.inf, 0.0, -0.0]]).astype(np.float32)
+    for variant in (oracle.VARIANT_N, oracle.VARIANT_A):
+        s, c = oracle.sincos(th, variant)
+        s[7] = np.float32(3.0)                       # one wrong pair: it must set max_comb / worst_x
+        cs = np.empty(2 * th.size, dtype=np.float32)
+        cs[0::2], cs[1::2] = c, s
+        for ref in (oracle.REF_DOUBLE, oracle.REF_LONGDOUBLE):
+            a = oracle.error_stats(th, s, c, ref).as_dict()
+            b = oracle.error_stats_interleaved(th, cs, ref).as_dict()
+            assert a == b or all((x == y) or (x != x and y != y) for x, y in zip(a.values(), b.values())), (a, b)
+            assert a["worst_x"] == th[7] and a["nan_count"] >= 1

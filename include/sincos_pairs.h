@@ -88,7 +88,9 @@ typedef enum {
  * whole 32-B output blocks from neighbouring lanes).  (Exact in-place always
  * keeps the aliased output at theta's alignment.)
  * A scalar head and tail cover the ragged ends.  The kernel configuration (block
- * size, full grid, vector width) is fixed: there is no tuning state.
+ * size, grid, vector width) is fixed per path -- a full grid of 128-thread blocks,
+ * half of it with two trips per thread for interleaved pairs 4-B aligned at an odd
+ * offset of 3, 5 or 7 floats -- and there is no tuning state.
  * theta_dev == sin_dev or
  * theta_dev == cos_dev (exact in-place) is allowed.  Validation happens
  * before any CUDA call; the return value reports validation and the launch

@@ -209,10 +209,19 @@ def _flat(t, name: str):
 
 
 def _stream(stream, device) -> int:
+    """The cudaStream_t handle: `stream` (a torch CUDA stream, or a raw handle), else the current
+    stream of `device`.  A torch stream of another device is refused (its work would run on the
+    wrong GPU's queue while the kernel reads this one's memory)."""
     import torch
     if stream is None:
         stream = torch.cuda.current_stream(device)
-    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    if hasattr(stream, "cuda_stream"):
+        sd = getattr(stream, "device", None)
+        if sd is not None and device is not None and torch.device(device).type == "cuda" and \
+                torch.device(sd).index != torch.device(device).index:
+            raise ValueError(f"stream is on {sd}, the tensors on {device}")
+        return stream.cuda_stream
+    return int(stream)
 
 
 def _record(stream, device, *tensors):

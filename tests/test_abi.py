@@ -323,3 +323,18 @@ def test_host_path_binding_refuses_a_host_workspace():
     import torch
     with pytest.raises(ValueError, match="workspace"):
         sp.sincos_pairs_host(torch.zeros(16), torch.zeros(16), torch.zeros(16), workspace=torch.zeros(1 << 20))
+
+
+def test_binding_refuses_a_stream_of_another_device():
+    """A torch stream object of another GPU is refused before the library is called (its queue
+    would order the launch against the wrong device's work); a raw handle passes through."""
+    import torch
+
+    class FakeStream:                    # the two attributes the binding reads of a torch stream
+        def __init__(self, idx):
+            self.cuda_stream, self.device = 0x1234, torch.device("cuda", idx)
+
+    assert sp._stream(FakeStream(0), torch.device("cuda", 0)) == 0x1234
+    assert sp._stream(0x5678, torch.device("cuda", 0)) == 0x5678
+    with pytest.raises(ValueError, match="stream is on cuda:1"):
+        sp._stream(FakeStream(1), torch.device("cuda", 0))

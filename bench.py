@@ -35,6 +35,7 @@ N_PER_RANK = 1 << 28
 BYTES_PER_PAIR = 12                 # 4 B theta in + 8 B (sin, cos) out -- SURVEY 8(d)
 METRIC = "sincos pairs/sec and achieved HBM GB/s vs peak at 1/2/4/8 B200; max error"
 WORKLOAD = "C2: 2^28 fp32 angles U[-1e4,1e4] seed 1 per GPU, split sin/cos, both variants (N then A) per step"
+L2_FLUSH_BYTES = 512 << 20         # > 4x the 126 MB L2: written before every step of the small configs
 FALLBACK_HBM_GBS = 6650.0           # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
 
 
@@ -607,7 +608,13 @@ def run_ours(args, rank, world, local_rank):
     # (~1.5% of a step), so the kernels' average launch duration is the region's
     # time over its launches (both launches are the one streaming kernel, variant N and variant A),
     # and the per-variant split is timed after the region, each variant back to back.
+    # Working sets below 2x the 126 MB L2 (C1, C3): L2 is flushed before every step (a 512 MiB
+    # write, outside the timed spans) and each step is timed by its own pair of events; the
+    # device time is the sum of the step spans.
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev) if use_graph else None
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    spans = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+             for _ in range(args.steps)] if use_graph else []
     barrier()
     launches0 = sp.launch_count()
     with ClockSampler(local_rank) as clk:
@@ -615,7 +622,10 @@ def run_ours(args, rank, world, local_rank):
         t_start.record(stream)
         for k in range(args.steps):
             if use_graph:
+                flush.fill_(float(k))
+                spans[k][0].record(stream)
                 step_graph.replay()
+                spans[k][1].record(stream)
                 continue
             for v in variants:
                 sp.sincos_pairs(th, variant=v, stream=stream, **outs[v])
@@ -624,13 +634,15 @@ def run_ours(args, rank, world, local_rank):
         wall_ms = 1e3 * (time.perf_counter() - wall0)
     barrier()
     launches = sp.launch_count() - launches0 if not use_graph else len(variants) * args.steps
-    ms_max = max_over_ranks(t_start.elapsed_time(t_end), world, cdev)
+    region_ms = sum(a_.elapsed_time(b_) for a_, b_ in spans) if use_graph else t_start.elapsed_time(t_end)
+    ms_max = max_over_ranks(region_ms, world, cdev)
     wall_ms_max = max_over_ranks(wall_ms, world, cdev)
     if use_graph:
         per_kernel = {v: [] for v in variants}
         for _ in range(5):
             for v in variants:
                 a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                flush.fill_(0.0)
                 a_.record(stream)
                 rep_graphs[v].replay()
                 b_.record(stream)
@@ -808,7 +820,10 @@ def run_ours(args, rank, world, local_rank):
                            "; SAME DEVICE: every rank on cuda:0 in its own context (time-sliced), a host-flow "
                            "test -- value is NOT a throughput measurement" if args.same_device else ""),
                    "l2": "inputs larger than L2 (4n B theta + 8n B outputs per launch vs 126 MB L2); no flush"
-                         if 12 * n > (256 << 20) else "working set near/below L2 size: not an HBM measurement",
+                         if not use_graph else
+                         "L2 flushed (512 MiB write) before every step, outside the per-step event spans; "
+                         "launch/latency-bound at this size (the per-kernel split: graphs of 20 launches "
+                         "after a flush, so mostly L2-warm)",
                    "launch": sp.LAUNCH, "cuda_graph": use_graph},
         "hbm_GBps": BYTES_PER_PAIR * pairs_total / (ms_max / 1e3) / 1e9 / world,
         "roofline": roof,

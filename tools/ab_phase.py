@@ -35,6 +35,7 @@ if os.environ.get("AB_CASES") == "aligned":
 
 VARIANT = int(os.environ.get("AB_VARIANT", "0"))     # 0 = N, 1 = A
 UNITS = int(os.environ.get("AB_UNITS", "1"))         # 1 = turns, 0 = radians
+BURST = float(os.environ.get("AB_BURST", "0"))       # > 0: seconds idle before every case (burst figures)
 
 
 def build(name, flags):
@@ -68,6 +69,10 @@ def run():
             key = f"nt={nt} toff={toff} {'inter' if inter else 'split'}"
             outs = (0, 0, io.data_ptr()) if inter else (s.data_ptr(), c.data_ptr(), 0)
             samples = {k: [] for k in libs}
+            if BURST:
+                import time
+                torch.cuda.synchronize()
+                time.sleep(BURST)                  # let the board leave its power cap
             for _ in range(5):
                 for name, L in libs.items():
                     def go():

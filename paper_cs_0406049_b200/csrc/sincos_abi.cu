@@ -17,6 +17,13 @@
 #include <vector>
 #include <stdint.h>
 #include <stdlib.h>
+
+#ifndef SINCOS_PHASE_STAGED
+#define SINCOS_PHASE_STAGED 1      // 0: rows of 2-7 pairs through the short-row kernel (A/B)
+#endif
+#ifndef SINCOS_PHASE_STAGED_SPLIT_MIN
+#define SINCOS_PHASE_STAGED_SPLIT_MIN 4   // split rows of 2-3 pairs: the tiny-row kernel (A/B: 2)
+#endif
 #include <string.h>
 
 #include "../../include/sincos_pairs.h"
@@ -425,12 +432,27 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
     // rows of one pair (split or interleaved) or of 2-3 pairs (split), outputs 32-B aligned at
     // pair 0: the tiny-row kernel (its per-lane store stride, 8 nt pairs, spreads a warp's store
     // over more lines as nt grows: for nt >= 4, and interleaved nt = 2-3, the short-row kernel
-    // is faster -- profiles/r02/ab_phase_tiny.jsonl)
-    const bool tiny = flat && T.realign != 3 && (nt == 1 || (split && nt <= 3)) &&
+    // was faster -- profiles/r02/ab_phase_tiny.jsonl -- and the staged kernel below is now)
+    const bool tiny = flat && T.realign != 3 && (nt == 1 || (split && nt < SINCOS_PHASE_STAGED_SPLIT_MIN)) &&
                       (split ? aligned(sin_dev, 32) && aligned(cos_dev, 32) : aligned(inter_dev, 32));
+    // rows of 4-7 pairs (split) or 2-7 (interleaved), outputs 16-B aligned at pair 0: the staged
+    // short-row kernel (a warp's 128 rows staged in shared memory, written back as contiguous
+    // 512-B store instructions)
+    const bool staged = SINCOS_PHASE_STAGED && flat && !tiny && T.realign != 3 && nt <= 7 &&
+                        (split ? nt >= SINCOS_PHASE_STAGED_SPLIT_MIN && aligned(sin_dev, 16) && aligned(cos_dev, 16)
+                               : nt >= 2 && aligned(inter_dev, 16));
     if (tiny) {
         e = launch_phase_tiny(variant, inter, units == SINCOS_TURNS, f_dev, nf, t_dev, nt, sin_dev, cos_dev,
                               inter_dev, static_cast<cudaStream_t>(stream));
+    } else if (staged) {
+        size_t max_grid = 0;                   // the full grid (A/B: blocks_per_sm > 0 grid-strides)
+        if (T.blocks_per_sm > 0) {
+            int dev = 0;
+            if ((e = cudaGetDevice(&dev)) != cudaSuccess) return cuda_fail(e);
+            max_grid = static_cast<size_t>(sm_count(dev)) * T.blocks_per_sm;
+        }
+        e = launch_phase_staged(variant, inter, units == SINCOS_TURNS, f_dev, nf, t_dev, nt, sin_dev, cos_dev,
+                                inter_dev, max_grid, static_cast<cudaStream_t>(stream));
     } else if (flat && nt >= kPhaseRowsMinNt && T.realign != 3) {
         const unsigned h0 = static_cast<unsigned>(split ? ((32 - (so_a & 31)) & 31) / 4 : ((32 - (io_a & 31)) & 31) / 8);
         int dev = 0;

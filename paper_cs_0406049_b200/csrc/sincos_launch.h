@@ -119,6 +119,8 @@ constexpr size_t phase_short_blocks_per_sm(size_t nt) {
 }
 // NEXT(1) tiny rows (1 <= nt <= 7), outputs 32-B aligned at pair 0: groups of 8 rows per thread,
 // the row length a compile-time parameter.
+cudaError_t launch_phase_staged(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
+                                size_t nt, float *so, float *co, float *io, size_t max_grid, cudaStream_t stream);
 cudaError_t launch_phase_tiny(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
                               size_t nt, float *so, float *co, float *io, cudaStream_t stream);
 cudaError_t launch_phase_rows(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,

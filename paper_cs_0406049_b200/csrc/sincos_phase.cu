@@ -674,6 +674,189 @@ cudaError_t launch_phase_tiny(int variant, bool inter, bool turns, const float *
     return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kPhaseThreads), args, 0, stream);
 }
 
+// Staged short rows (round 2): rows of NT = 4..7 pairs (split) or 2..7 pairs (interleaved),
+// outputs 16-B aligned at pair 0.  The tiny-row kernel's lane stores are 8 NT pairs apart, so
+// its warp store instructions scatter over NT x more lines; here a warp computes a region of
+// 128 whole rows (lane l: rows 4l..4l+3, one 128-bit load of their f, every (row, column)
+// a compile-time constant as in the tiny kernel), stages the region's 128 NT pairs in shared
+// memory and writes it back as 128-bit stores of 512 B contiguous per warp instruction.  Lane l
+// writes its chunks (16 B) S l + q (S = chunks per lane: NT split, 2 NT interleaved), the
+// write-back reads chunks 32 j + l; chunk c is kept at c ^ ((c >> z) & 7), z = the number of
+// trailing zero bits of S (odd S: unswizzled), which makes both conflict-free for every S here
+// (a quarter-warp's eight 16-B accesses hit eight distinct bank groups; an unswizzled S = 12
+// was 4-way on the writes and cost interleaved nt = 6 16%).  Rows past the last whole region:
+// one pair per thread.
+template <int S>
+__device__ __forceinline__ int stage_chunk(int c) {
+    constexpr int z = S % 2 ? 0 : S % 4 ? 1 : S % 8 ? 2 : 3;
+    if constexpr (z == 0) return c;
+    else return c ^ ((c >> z) & 7);
+}
+__device__ __forceinline__ void st_shared4(const float4 *p, float a, float b, float c, float d) {
+    const unsigned addr = static_cast<unsigned>(__cvta_generic_to_shared(p));
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" :: "r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+__device__ __forceinline__ float4 ld_shared4(const float4 *p) {
+    const unsigned addr = static_cast<unsigned>(__cvta_generic_to_shared(p));
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_global4(float *p, float4 v) {
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w) : "memory");
+}
+
+// K pairs (K even) of the lane's rows, pairs k0 .. k0 + K - 1 in row-major order of its 4 x NT
+template <int V, bool TURNS, int NT, int K, int K0>
+__device__ __forceinline__ void staged_pairs(const float (&fr)[4], const float (&tt)[NT], float (&sv)[K],
+                                             float (&cv)[K]) {
+#pragma unroll
+    for (int k = 0; k < K; k += 2) {
+        if constexpr (SINCOS_PACKED_PHASE) {
+            F2 x = mul2(pk2(fr[(K0 + k) / NT], fr[(K0 + k + 1) / NT]), pk2(tt[(K0 + k) % NT], tt[(K0 + k + 1) % NT]));
+            if constexpr (!TURNS) x = mul2(x, bc2(kInvTwoPi));
+            F2 s2, c2;
+            sincos_from_q2<V>(reduce_turn2(x), s2, c2);
+            sv[k] = lo2(s2);
+            sv[k + 1] = hi2(s2);
+            cv[k] = lo2(c2);
+            cv[k + 1] = hi2(c2);
+        } else {
+            phase_pair<V, TURNS>(fr[(K0 + k) / NT], tt[(K0 + k) % NT], sv[k], cv[k]);
+            phase_pair<V, TURNS>(fr[(K0 + k + 1) / NT], tt[(K0 + k + 1) % NT], sv[k + 1], cv[k + 1]);
+        }
+    }
+}
+
+// compute pairs [K0, K0 + K) and stage them: split -> chunk K0/4 .. of the lane's sin / cos runs,
+// interleaved -> chunks K0/2 .. of its {cos, sin} run
+template <int V, bool INTER, bool TURNS, int NT, int K, int K0>
+__device__ __forceinline__ void stage_batch(const float (&fr)[4], const float (&tt)[NT], float4 *ws, unsigned lane) {
+    float sv[K], cv[K];
+    staged_pairs<V, TURNS, NT, K, K0>(fr, tt, sv, cv);
+    if constexpr (INTER) {
+        constexpr int S = 2 * NT;
+#pragma unroll
+        for (int h = 0; h < K / 2; ++h) {
+            const int c = static_cast<int>(lane) * S + K0 / 2 + h;
+            st_shared4(ws + stage_chunk<S>(c), cv[2 * h], sv[2 * h], cv[2 * h + 1], sv[2 * h + 1]);
+        }
+    } else {
+        constexpr int S = NT;
+#pragma unroll
+        for (int h = 0; h < K / 4; ++h) {
+            const int c = static_cast<int>(lane) * S + K0 / 4 + h;
+            st_shared4(ws + stage_chunk<S>(c), sv[4 * h], sv[4 * h + 1], sv[4 * h + 2], sv[4 * h + 3]);
+            st_shared4(ws + 32 * NT + stage_chunk<S>(c), cv[4 * h], cv[4 * h + 1], cv[4 * h + 2], cv[4 * h + 3]);
+        }
+    }
+}
+
+template <int V, bool INTER, bool TURNS, int NT>
+__global__ void __launch_bounds__(kPhaseThreads) phase_grid_staged(const float *__restrict__ f,
+                                                                  const float *__restrict__ t, size_t nf,
+                                                                  float *so, float *co, float *io, size_t nregions,
+                                                                  bool f_al16) {
+    __shared__ float4 stage[kPhaseThreads / 32][64 * NT];     // 1 KB x NT per warp
+    const size_t gid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t rem0 = 128 * NT * nregions, rem = nf * NT - rem0;   // rows past the last region
+    for (size_t i = gid; i < rem; i += nthr) {
+        const size_t e = rem0 + i;
+        float sr, cr;
+        phase_pair<V, TURNS>(__ldg(f + e / NT), __ldg(t + e % NT), sr, cr);
+        if constexpr (INTER) {
+            io[2 * e] = cr;
+            io[2 * e + 1] = sr;
+        } else {
+            so[e] = sr;
+            co[e] = cr;
+        }
+    }
+    const unsigned lane = threadIdx.x & 31u;
+    float4 *ws = stage[threadIdx.x >> 5];
+    float tt[NT];
+#pragma unroll
+    for (int b = 0; b < NT; ++b) tt[b] = __ldg(t + b);
+    const size_t nwarps = nthr / 32;
+    for (size_t r = gid / 32; r < nregions; r += nwarps) {   // warp-uniform: one region per trip
+        const size_t row0 = 128 * r + 4 * lane;
+        float fr[4];
+        if (f_al16) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(f + row0));
+            fr[0] = v.x;
+            fr[1] = v.y;
+            fr[2] = v.z;
+            fr[3] = v.w;
+        } else {
+#pragma unroll
+            for (int a = 0; a < 4; ++a) fr[a] = __ldg(f + row0 + a);
+        }
+        // the lane's 4 NT pairs in batches of 8 (and a last one of 4 for odd NT)
+        if constexpr (4 * NT >= 8) stage_batch<V, INTER, TURNS, NT, 8, 0>(fr, tt, ws, lane);
+        if constexpr (4 * NT >= 16) stage_batch<V, INTER, TURNS, NT, 8, 8>(fr, tt, ws, lane);
+        if constexpr (4 * NT >= 24) stage_batch<V, INTER, TURNS, NT, 8, 16>(fr, tt, ws, lane);
+        if constexpr ((4 * NT) % 8 == 4) stage_batch<V, INTER, TURNS, NT, 4, 4 * NT - 4>(fr, tt, ws, lane);
+        __syncwarp();
+        if constexpr (INTER) {
+            float *dst = io + 2 * 128 * NT * r;
+#pragma unroll
+            for (int j = 0; j < 2 * NT; ++j) {
+                const int c = 32 * j + static_cast<int>(lane);
+                st_global4(dst + 4 * c, ld_shared4(ws + stage_chunk<2 * NT>(c)));
+            }
+        } else {
+            float *ds = so + 128 * NT * r, *dc = co + 128 * NT * r;
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                const int c = 32 * j + static_cast<int>(lane);
+                st_global4(ds + 4 * c, ld_shared4(ws + stage_chunk<NT>(c)));
+                st_global4(dc + 4 * c, ld_shared4(ws + 32 * NT + stage_chunk<NT>(c)));
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <int V, bool INTER, bool TURNS>
+static const void *pick_staged(size_t nt) {
+    switch (nt) {
+    case 2: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 2>);
+    case 3: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 3>);
+    case 4: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 4>);
+    case 5: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 5>);
+    case 6: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 6>);
+    default: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 7>);
+    }
+}
+
+cudaError_t launch_phase_staged(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
+                                size_t nt, float *so, float *co, float *io, size_t max_grid, cudaStream_t stream) {
+    if (nt < 2 || nt > 7) return cudaErrorInvalidValue;
+    const void *fn;
+    if (variant == kNormalized)
+        fn = inter ? (turns ? pick_staged<kNormalized, true, true>(nt) : pick_staged<kNormalized, true, false>(nt))
+                   : (turns ? pick_staged<kNormalized, false, true>(nt) : pick_staged<kNormalized, false, false>(nt));
+    else
+        fn = inter ? (turns ? pick_staged<kRenormalized, true, true>(nt) : pick_staged<kRenormalized, true, false>(nt))
+                   : (turns ? pick_staged<kRenormalized, false, true>(nt)
+                            : pick_staged<kRenormalized, false, false>(nt));
+    size_t nregions = nf / 128;
+    const size_t rem = (nf - 128 * nregions) * nt;                    // < 128 rows of tail pairs
+    const size_t warps_per_block = kPhaseThreads / 32;
+    size_t grid = (nregions + warps_per_block - 1) / warps_per_block;
+    const size_t grid_rem = (rem + kPhaseThreads - 1) / kPhaseThreads;
+    if (grid < grid_rem) grid = grid_rem;
+    if (max_grid > 0 && grid > max_grid) grid = max_grid;               // (A/B: grid-stride)
+    if (grid < 1) grid = 1;
+    if (grid > 0x7FFFFFFFu / 4) grid = 0x7FFFFFFFu / 4;                // grid-strides past it
+    bool f_al16 = (reinterpret_cast<uintptr_t>(f) & 15) == 0;
+    void *args[] = {&f, &t, &nf, &so, &co, &io, &nregions, &f_al16};
+    return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kPhaseThreads), args, 0, stream);
+}
+
 template <int V, bool INTER, bool TURNS>
 static const void *pick_short(bool small) {
     return small ? reinterpret_cast<const void *>(phase_grid_short<V, INTER, TURNS, true>)

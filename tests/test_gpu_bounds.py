@@ -94,12 +94,14 @@ def test_phase_grid_and_nudft(shape):
 
 
 @pytest.mark.parametrize("shape", [(1, 1), (3, 7), (9, 13), (33, 1001), (16, 256), (9, 131), (21, 300), (3, 4000),
-                                   (21, 1), (1003, 2), (77, 3)])
-@pytest.mark.parametrize("off", [0, 1, 3, 6])
+                                   (21, 1), (1003, 2), (77, 3), (1000, 4), (300, 5), (129, 6), (385, 7),
+                                   (128 * 9 + 3, 3)])
+@pytest.mark.parametrize("off", [0, 1, 3, 4, 6])
 def test_phase_grid_split_offsets(shape, off):
     """Split phase-grid outputs at offsets (the flat kernel's head/body/tail, the ragged-row
-    kernel's row ends and re-aligned t windows -- t at a float offset too -- and the aligned row
-    kernel), interleaved at odd and even float offsets (flat / row kernel, one pair per thread)."""
+    kernel's row ends and re-aligned t windows -- t at a float offset too -- the aligned row
+    kernel, and the staged short-row kernel's regions and tail at 32-B and 16-B alignment),
+    interleaved at odd and even float offsets (flat / row kernel, one pair per thread)."""
     nf, nt = shape
     f = torch.rand(nf, device="cuda") * 100
     toff = off % 5

@@ -91,6 +91,12 @@ def test_phase_grid_short_and_tiny_rows_floor():
     o = torch.empty(2 * n, device="cuda")
     got = gbps(lambda: sp.phase_grid(f, t, interleaved_out=o, units=sp.TURNS), 8 * n)
     assert got >= 5500, f"nt=1001 {got:.0f}"   # (6.0-6.4 once the board is in its power cap)
+    f5 = torch.rand((1 << 27) // 5, device="cuda") * 512       # rows of 5 pairs: the staged kernel
+    t5 = torch.rand(5, device="cuda")
+    n5 = f5.numel() * 5
+    o5 = torch.empty(2 * n5, device="cuda")
+    got = gbps(lambda: sp.phase_grid(f5, t5, interleaved_out=o5, units=sp.TURNS), 8 * n5)
+    assert got >= 5300, f"nt=5 {got:.0f} (recorded 6.1 TB/s written)"
     f1 = torch.rand(1 << 27, device="cuda")
     t1 = torch.rand(1, device="cuda")
     s, c = torch.empty(1 << 27, device="cuda"), torch.empty(1 << 27, device="cuda")

@@ -265,3 +265,43 @@ def test_tiny_rows(units, variant, nt):
             assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws, wc, "split " + tag)
             iv = io.cpu().numpy()
             assert_parity(iv[1::2], iv[0::2], ws, wc, "inter " + tag)
+
+
+@pytest.mark.parametrize("nt", [2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("units", [0, 1])
+def test_staged_rows(units, variant, nt):
+    """Rows of 2..7 pairs through the staged short-row kernel (split nt >= 4, interleaved nt >= 2;
+    outputs 16-B aligned at pair 0: a warp's 128 rows staged in shared memory, written back as
+    contiguous 128-bit stores): whole 128-row regions and a ragged tail, f 16-B aligned or not,
+    outputs 32-B and only 16-B aligned, and on the A/B build's grid-stride grids (many regions
+    per warp).  Also the layouts that must not take it (interleaved pairs only 8-B aligned)."""
+    rng = np.random.default_rng(1000 + nt * 10 + units + 2 * variant)
+    sizes = (127, 128, 129, 128 * 37 + 77, 128 * 2500)
+    NF = max(sizes)
+    fb = rng.uniform(-400, 400, NF + 8).astype(np.float32)
+    t = rng.uniform(-1, 1, nt).astype(np.float32)
+    fbig, td = torch.from_numpy(fb).cuda(), torch.from_numpy(t).cuda()
+    sb = torch.empty(NF * nt + 16, device="cuda")
+    cb = torch.empty(NF * nt + 16, device="cuda")
+    ib = torch.empty(2 * NF * nt + 16, device="cuda")
+    for ctx in (contextlib.nullcontext(), ab.knobs(blocks_per_sm=1)):
+        with ctx:
+            for nf in sizes:
+                for foff in (0, 1, 4):
+                    f = fb[foff:foff + nf]
+                    ws, wc = oracle.phase_grid(f, t, units, variant)
+                    ws, wc = ws.ravel(), wc.ravel()
+                    fd = fbig[foff:foff + nf]
+                    n = nf * nt
+                    for ooff in (0, 4, 2):          # 32-B / 16-B aligned (staged) / 8-B (short-row kernel)
+                        s, c = sb[ooff:ooff + n], cb[ooff:ooff + n]
+                        io = ib[ooff:ooff + 2 * n]
+                        s.fill_(float("nan")); c.fill_(float("nan")); io.fill_(float("nan"))
+                        sp.phase_grid(fd, td, s, c, units=units, variant=variant)
+                        sp.phase_grid(fd, td, interleaved_out=io, units=units, variant=variant)
+                        torch.cuda.synchronize()
+                        tag = f"nt={nt} nf={nf} foff={foff} ooff={ooff}"
+                        assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws, wc, "split " + tag)
+                        iv = io.cpu().numpy()
+                        assert_parity(iv[1::2], iv[0::2], ws, wc, "inter " + tag)

@@ -29,6 +29,8 @@ if os.environ.get("AB_CASES") == "tiny":
     CASES = [(1, 0), (2, 0), (3, 0), (4, 0), (5, 1), (6, 0), (7, 2), (9, 0)]
 if os.environ.get("AB_CASES") == "rows":
     CASES = [(32767, 0), (32772, 0), (16385, 1), (8191, 3), (4000, 5), (2049, 0), (1025, 2)]
+if os.environ.get("AB_CASES") == "small":
+    CASES = [(8, 0), (10, 0), (12, 0), (16, 0), (20, 0), (24, 0), (32, 0), (48, 0), (63, 0)]
 if os.environ.get("AB_CASES") == "aligned":
     CASES = [(32768, 0), (8192, 0), (4096, 0), (2048, 0), (1000, 0), (512, 0), (256, 0), (136, 0), (64, 0), (16, 0)]
 

@@ -674,7 +674,7 @@ cudaError_t launch_phase_tiny(int variant, bool inter, bool turns, const float *
     return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kPhaseThreads), args, 0, stream);
 }
 
-// Staged short rows (round 2): rows of NT = 4..7 pairs (split) or 2..7 pairs (interleaved),
+// Staged short rows (round 2): rows of NT = 4..13 pairs (split) or 2..7 pairs (interleaved),
 // outputs 16-B aligned at pair 0.  The tiny-row kernel's lane stores are 8 NT pairs apart, so
 // its warp store instructions scatter over NT x more lines; here a warp computes a region of
 // 128 whole rows (lane l: rows 4l..4l+3, one 128-bit load of their f, every (row, column)
@@ -686,11 +686,24 @@ cudaError_t launch_phase_tiny(int variant, bool inter, bool turns, const float *
 // (a quarter-warp's eight 16-B accesses hit eight distinct bank groups; an unswizzled S = 12
 // was 4-way on the writes and cost interleaved nt = 6 16%).  Rows past the last whole region:
 // one pair per thread.
+__host__ __device__ constexpr int ctz_c(int s) { return s % 2 ? 0 : 1 + ctz_c(s / 2); }
 template <int S>
 __device__ __forceinline__ int stage_chunk(int c) {
-    constexpr int z = S % 2 ? 0 : S % 4 ? 1 : S % 8 ? 2 : 3;
+    constexpr int z = ctz_c(S);
     if constexpr (z == 0) return c;
     else return c ^ ((c >> z) & 7);
+}
+// 128-thread blocks up to NT = 11 (44 KB of static shared memory), 64 above (<= 48 KB)
+__host__ __device__ constexpr int staged_threads(int nt) { return nt <= 11 ? 128 : 64; }
+// Rows of 8-13 pairs: registers capped at 72.  Without the cap they took 134-214 and ran 20-40%
+// slower; at 64 some instances spill (profiles/r02/ab_phase_mid8b_v*.jsonl).  Rows of 2-7
+// pairs keep ptxas's own choice (32-72): any explicit minimum blocks per SM -- even 1 -- let
+// it spend more registers there, and the 7-pair rows lost up to 22%.
+#ifndef SINCOS_PHASE_STAGED_REGS
+#define SINCOS_PHASE_STAGED_REGS 72
+#endif
+__host__ __device__ constexpr int staged_min_blocks(int nt) {
+    return 65536 / (staged_threads(nt) * SINCOS_PHASE_STAGED_REGS);
 }
 __device__ __forceinline__ void st_shared4(const float4 *p, float a, float b, float c, float d) {
     const unsigned addr = static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -754,12 +767,21 @@ __device__ __forceinline__ void stage_batch(const float (&fr)[4], const float (&
     }
 }
 
+// the lane's 4 NT pairs: batches of 8 from pair K0 on, a last one of 4 for odd NT
+template <int V, bool INTER, bool TURNS, int NT, int K0>
+__device__ __forceinline__ void stage_all(const float (&fr)[4], const float (&tt)[NT], float4 *ws, unsigned lane) {
+    if constexpr (4 * NT - K0 >= 8) {
+        stage_batch<V, INTER, TURNS, NT, 8, K0>(fr, tt, ws, lane);
+        stage_all<V, INTER, TURNS, NT, K0 + 8>(fr, tt, ws, lane);
+    } else if constexpr (4 * NT - K0 == 4) {
+        stage_batch<V, INTER, TURNS, NT, 4, K0>(fr, tt, ws, lane);
+    }
+}
+
 template <int V, bool INTER, bool TURNS, int NT>
-__global__ void __launch_bounds__(kPhaseThreads) phase_grid_staged(const float *__restrict__ f,
-                                                                  const float *__restrict__ t, size_t nf,
-                                                                  float *so, float *co, float *io, size_t nregions,
-                                                                  bool f_al16) {
-    __shared__ float4 stage[kPhaseThreads / 32][64 * NT];     // 1 KB x NT per warp
+__device__ __forceinline__ void staged_body(const float *__restrict__ f, const float *__restrict__ t, size_t nf,
+                                            float *so, float *co, float *io, size_t nregions, bool f_al16) {
+    __shared__ float4 stage[staged_threads(NT) / 32][64 * NT];     // 1 KB x NT per warp
     const size_t gid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t rem0 = 128 * NT * nregions, rem = nf * NT - rem0;   // rows past the last region
@@ -794,11 +816,7 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_staged(const float *
 #pragma unroll
             for (int a = 0; a < 4; ++a) fr[a] = __ldg(f + row0 + a);
         }
-        // the lane's 4 NT pairs in batches of 8 (and a last one of 4 for odd NT)
-        if constexpr (4 * NT >= 8) stage_batch<V, INTER, TURNS, NT, 8, 0>(fr, tt, ws, lane);
-        if constexpr (4 * NT >= 16) stage_batch<V, INTER, TURNS, NT, 8, 8>(fr, tt, ws, lane);
-        if constexpr (4 * NT >= 24) stage_batch<V, INTER, TURNS, NT, 8, 16>(fr, tt, ws, lane);
-        if constexpr ((4 * NT) % 8 == 4) stage_batch<V, INTER, TURNS, NT, 4, 4 * NT - 4>(fr, tt, ws, lane);
+        stage_all<V, INTER, TURNS, NT, 0>(fr, tt, ws, lane);
         __syncwarp();
         if constexpr (INTER) {
             float *dst = io + 2 * 128 * NT * r;
@@ -820,6 +838,21 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_staged(const float *
     }
 }
 
+// rows of 2-7 pairs: ptxas's own register choice (32-72); rows of 8-13: capped at 72
+template <int V, bool INTER, bool TURNS, int NT>
+__global__ void __launch_bounds__(staged_threads(NT)) phase_grid_staged(const float *__restrict__ f,
+                                                                       const float *__restrict__ t, size_t nf,
+                                                                       float *so, float *co, float *io,
+                                                                       size_t nregions, bool f_al16) {
+    staged_body<V, INTER, TURNS, NT>(f, t, nf, so, co, io, nregions, f_al16);
+}
+template <int V, bool INTER, bool TURNS, int NT>
+__global__ void __launch_bounds__(staged_threads(NT), staged_min_blocks(NT))
+phase_grid_staged_wide(const float *__restrict__ f, const float *__restrict__ t, size_t nf, float *so, float *co,
+                       float *io, size_t nregions, bool f_al16) {
+    staged_body<V, INTER, TURNS, NT>(f, t, nf, so, co, io, nregions, f_al16);
+}
+
 template <int V, bool INTER, bool TURNS>
 static const void *pick_staged(size_t nt) {
     switch (nt) {
@@ -828,13 +861,26 @@ static const void *pick_staged(size_t nt) {
     case 4: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 4>);
     case 5: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 5>);
     case 6: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 6>);
-    default: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 7>);
+    default: break;
     }
+    if constexpr (!INTER) {                // split rows of 8-13 pairs (interleaved: the short-row kernel)
+        switch (nt) {
+        case 8: return reinterpret_cast<const void *>(phase_grid_staged_wide<V, INTER, TURNS, 8>);
+        case 9: return reinterpret_cast<const void *>(phase_grid_staged_wide<V, INTER, TURNS, 9>);
+        case 10: return reinterpret_cast<const void *>(phase_grid_staged_wide<V, INTER, TURNS, 10>);
+        case 11: return reinterpret_cast<const void *>(phase_grid_staged_wide<V, INTER, TURNS, 11>);
+        case 12: return reinterpret_cast<const void *>(phase_grid_staged_wide<V, INTER, TURNS, 12>);
+        case 13: return reinterpret_cast<const void *>(phase_grid_staged_wide<V, INTER, TURNS, 13>);
+        default: break;
+        }
+    }
+    return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 7>);
 }
 
 cudaError_t launch_phase_staged(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
                                 size_t nt, float *so, float *co, float *io, size_t max_grid, cudaStream_t stream) {
-    if (nt < 2 || nt > 7) return cudaErrorInvalidValue;
+    if (nt < 2 || nt > (inter ? SINCOS_PHASE_STAGED_MAX_NT_INTER : SINCOS_PHASE_STAGED_MAX_NT))
+        return cudaErrorInvalidValue;
     const void *fn;
     if (variant == kNormalized)
         fn = inter ? (turns ? pick_staged<kNormalized, true, true>(nt) : pick_staged<kNormalized, true, false>(nt))
@@ -845,16 +891,17 @@ cudaError_t launch_phase_staged(int variant, bool inter, bool turns, const float
                             : pick_staged<kRenormalized, false, false>(nt));
     size_t nregions = nf / 128;
     const size_t rem = (nf - 128 * nregions) * nt;                    // < 128 rows of tail pairs
-    const size_t warps_per_block = kPhaseThreads / 32;
+    const unsigned threads = staged_threads(static_cast<int>(nt));
+    const size_t warps_per_block = threads / 32;
     size_t grid = (nregions + warps_per_block - 1) / warps_per_block;
-    const size_t grid_rem = (rem + kPhaseThreads - 1) / kPhaseThreads;
+    const size_t grid_rem = (rem + threads - 1) / threads;
     if (grid < grid_rem) grid = grid_rem;
     if (max_grid > 0 && grid > max_grid) grid = max_grid;               // (A/B: grid-stride)
     if (grid < 1) grid = 1;
     if (grid > 0x7FFFFFFFu / 4) grid = 0x7FFFFFFFu / 4;                // grid-strides past it
     bool f_al16 = (reinterpret_cast<uintptr_t>(f) & 15) == 0;
     void *args[] = {&f, &t, &nf, &so, &co, &io, &nregions, &f_al16};
-    return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kPhaseThreads), args, 0, stream);
+    return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(threads), args, 0, stream);
 }
 
 template <int V, bool INTER, bool TURNS>

@@ -5,8 +5,11 @@
   python tools/ab_phase.py sustain                    # GPU box: 0.5-1 s of load per library from idle
 
 Cases: ragged row lengths (and t offsets) at ~2^30 pairs per launch, split and interleaved,
-turns, variant N (AB_VARIANT=1: A; AB_UNITS=0: radians); GB/s of the 8 B written per pair, median of 5 rounds x 5 launches, the
-libraries interleaved over rounds.  One JSON line per library."""
+turns, variant N (AB_VARIANT=1: A; AB_UNITS=0: radians); GB/s of the 8 B written per pair, median
+over rounds of 5 launches (at least 5 rounds, a multiple of the library count), the libraries
+interleaved over rounds in a rotating order (the first after an AB_BURST idle gap runs cooler: two
+identical libraries read 5-8% apart on interleaved nt = 3 without the rotation).  One JSON line
+per library."""
 import ctypes
 import glob
 import json
@@ -31,6 +34,8 @@ if os.environ.get("AB_CASES") == "rows":
     CASES = [(32767, 0), (32772, 0), (16385, 1), (8191, 3), (4000, 5), (2049, 0), (1025, 2)]
 if os.environ.get("AB_CASES") == "small":
     CASES = [(8, 0), (10, 0), (12, 0), (16, 0), (20, 0), (24, 0), (32, 0), (48, 0), (63, 0)]
+if os.environ.get("AB_CASES") == "mid8":
+    CASES = [(7, 2), (8, 0), (9, 0), (10, 0), (11, 3), (12, 0), (13, 0), (14, 0), (15, 1)]
 if os.environ.get("AB_CASES") == "aligned":
     CASES = [(32768, 0), (8192, 0), (4096, 0), (2048, 0), (1000, 0), (512, 0), (256, 0), (136, 0), (64, 0), (16, 0)]
 
@@ -75,8 +80,12 @@ def run():
                 import time
                 torch.cuda.synchronize()
                 time.sleep(BURST)                  # let the board leave its power cap
-            for _ in range(5):
-                for name, L in libs.items():
+            names = list(libs)
+            rounds = len(names) * -(-5 // len(names))   # >= 5, a multiple of the library count
+            for rnd in range(rounds):
+                # the first library after the idle gap runs cooler: rotate the order every round
+                for name in names[rnd % len(names):] + names[:rnd % len(names)]:
+                    L = libs[name]
                     def go():
                         r = L.sincos_phase_grid(f.data_ptr(), nf, t.data_ptr(), nt, *outs, UNITS, VARIANT, st)
                         assert r == 0, r

@@ -24,8 +24,10 @@ def main():
     io = torch.empty(2 * n, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
     res = {k: {"interleave": [], "deinterleave": []} for k in libs}
-    for _ in range(5):
-        for name, L in libs.items():
+    order = list(libs)
+    for rnd in range(len(order) * -(-5 // len(order))):   # rotating order (see ab_phase.py)
+        for name in order[rnd % len(order):] + order[:rnd % len(order)]:
+            L = libs[name]
             for which, call in (("interleave", lambda: L.sincos_interleave(s.data_ptr(), c.data_ptr(), io.data_ptr(), n, st)),
                                 ("deinterleave", lambda: L.sincos_deinterleave(io.data_ptr(), s.data_ptr(), c.data_ptr(), n, st))):
                 assert call() == 0

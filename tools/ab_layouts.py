@@ -62,8 +62,10 @@ def main():
         else:
             outs = (None, None, ib.data_ptr() + 4 * case[2])
         samples = {k: [] for k in libs}
-        for _ in range(5):
-            for lname, L in libs.items():
+        order = list(libs)
+        for rnd in range(len(order) * -(-5 // len(order))):   # rotating order (see ab_phase.py)
+            for lname in order[rnd % len(order):] + order[:rnd % len(order)]:
+                L = libs[lname]
                 def go():
                     r = L.sincos_pairs(th, *outs, N, VARIANT, st)
                     assert r == 0, r

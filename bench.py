@@ -322,9 +322,9 @@ def measure_phase_grid(dev, stream, peak, reps=10):
             gbs = 8 * (1 << 30) / (ms / 1e3) / 1e9
             out[f"{uname}_{vname}"] = {"ms": ms, "pairs_per_s": (1 << 30) / (ms / 1e3), "GBps": gbs,
                                        "frac": gbs / peak}
-    # ragged rows (not whole 256-bit vectors): the row kernel (nt = 2^15 - 1) and the short-row
-    # kernel (nt = 1001), turns, variant N, ~2^30 pairs each
-    for nt in ((1 << 15) - 1, 1001):
+    # ragged rows (not whole 256-bit vectors): the row kernel (nt = 2^15 - 1), the short-row
+    # kernel (nt = 1001) and the staged short-row kernel (nt = 5), turns, variant N, ~2^30 pairs each
+    for nt in ((1 << 15) - 1, 1001, 5):
         nf = (1 << 30) // nt
         fd = torch.rand(nf, device=dev, generator=torch.Generator(device=dev).manual_seed(5)) * 512
         td = torch.rand(nt, device=dev, generator=torch.Generator(device=dev).manual_seed(6))
@@ -341,7 +341,8 @@ def measure_phase_grid(dev, stream, peak, reps=10):
         gbs = 8 * nf * nt / (ms / 1e3) / 1e9
         out[f"ragged_nt{nt}_turns_N"] = {"nf": nf, "nt": nt, "ms": ms, "pairs_per_s": nf * nt / (ms / 1e3),
                                          "GBps": gbs, "frac": gbs / peak,
-                                         "kernel": "row" if nt >= 1024 else "short-row"}
+                                         "GBps_with_f_reads": (8 + 4 / nt) * nf * nt / (ms / 1e3) / 1e9,
+                                         "kernel": "row" if nt >= 1024 else "short-row" if nt > 7 else "staged"}
     del o
     torch.cuda.empty_cache()
     return out

@@ -487,14 +487,18 @@ def measure_nudft(dev, stream, reps=5):
     return res
 
 
-def pcie_roofline(th_h, n, nvar, dev):
+def pcie_roofline(th_h, n, nvar, dev, outs_h):
     """The e2e leg's ceiling: one step's bytes (nvar x 4n B H2D, nvar x 8n B D2H) through plain
-    pinned cudaMemcpyAsync copies -- each direction alone, and both directions concurrently on
-    two streams, which is how the pipeline runs them.  step_floor_ms = the concurrent time (the
-    binding one when the link is not fully duplex), never less than either direction alone."""
+    pinned cudaMemcpyAsync copies between the pipeline's OWN host buffers (theta in, the output
+    arrays out) and the device -- each direction alone, and both directions concurrently on two
+    streams, which is how the pipeline runs them.  step_floor_ms = the concurrent time (the
+    binding one when the link is not fully duplex), never less than either direction alone.
+    (The same buffers: on these VMs the pinned pages of one allocation can sit behind a slower
+    host path than another's -- a whole e2e run once read 0.89 of a roofline measured on a
+    separate buffer.)"""
     import torch
     dbuf = torch.empty(2 * n, dtype=torch.float32, device=dev)
-    hbuf = torch.empty(2 * n, dtype=torch.float32).pin_memory()
+    outs = [o.view(-1) for o in outs_h]          # sin, cos (n each) or interleaved (2n)
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
 
     def timed(h2d, d2h):
@@ -510,7 +514,10 @@ def pcie_roofline(th_h, n, nvar, dev):
             ev[2].record(s_out)
             with torch.cuda.stream(s_out):
                 for _ in range(nvar):
-                    hbuf.copy_(dbuf, non_blocking=True)
+                    off = 0
+                    for o in outs:
+                        o.copy_(dbuf[off:off + o.numel()], non_blocking=True)
+                        off += o.numel()
             ev[3].record(s_out)
         torch.cuda.synchronize(dev)
         ms_in = ev[0].elapsed_time(ev[1]) if h2d else 0.0
@@ -523,11 +530,11 @@ def pcie_roofline(th_h, n, nvar, dev):
     ms_d2h = min(timed(False, True)[1] for _ in range(3))
     both = min((max(r[0], r[1]) for r in (timed(True, True) for _ in range(3))))
     floor = max(both, ms_h2d, ms_d2h)
-    del dbuf, hbuf
+    del dbuf
     return {"h2d_GBps": nvar * 4 * n / (ms_h2d / 1e3) / 1e9, "d2h_GBps": nvar * 8 * n / (ms_d2h / 1e3) / 1e9,
             "h2d_ms": ms_h2d, "d2h_ms": ms_d2h, "concurrent_ms": both, "step_floor_ms": floor,
-            "how": "pinned copies of one step's bytes; concurrent = H2D and D2H on two streams at once "
-                   "(max of the two event spans); best of 3"}
+            "how": "pinned copies of one step's bytes between the pipeline's own host buffers and the device; "
+                   "concurrent = H2D and D2H on two streams at once (max of the two event spans); best of 3"}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -763,7 +770,7 @@ def run_ours(args, rank, world, local_rank):
                "path": "sincos_pairs_host: pinned host buffers, chunked H2D -> kernel -> D2H over 3 streams"}
         # the e2e roofline: one step's bytes through the PCIe copy engines with plain pinned copies,
         # H2D and D2H issued concurrently on two streams (as the pipeline runs them) and each alone
-        e2e["pcie"] = pcie_roofline(th_h, e2e_n, len(variants), dev)
+        e2e["pcie"] = pcie_roofline(th_h, e2e_n, len(variants), dev, list(oh.values()))
         e2e["pcie"]["roofline_pairs_per_s"] = world * len(variants) * e2e_n / (e2e["pcie"]["step_floor_ms"] / 1e3)
         e2e["frac_of_pcie_roofline"] = e2e["value"] / e2e["pcie"]["roofline_pairs_per_s"]
         del ws, oh

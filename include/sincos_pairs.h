@@ -196,9 +196,9 @@ SINCOS_API sincos_status_t sincos_pairs_method(const float *theta_dev, float *si
  * rows shorter than 256) the short-row path (8 consecutive pairs of the row-major grid
  * per thread, t from shared memory) -- except rows of 1 pair, or 2-3 pairs split, with
  * outputs 32-B aligned at pair 0: the tiny-row path (8 whole rows per thread), and rows
- * of 4-13 pairs split or 2-7 interleaved with outputs 16-B aligned at pair 0: the staged
- * path (4 whole rows per thread, a warp's 128 rows staged in shared memory and written
- * back as contiguous 512-B stores); otherwise one pair per thread.  Returns as
+ * of 4-14 pairs split or 2-15 interleaved with outputs 16-B aligned at pair 0: the staged
+ * path (4 or 2 whole rows per thread, a warp's 128 or 64 rows staged in shared memory and
+ * written back as contiguous 512-B stores); otherwise one pair per thread.  Returns as
  * sincos_pairs; nf*nt == 0 is a no-op.
  */
 typedef enum { SINCOS_RADIANS = 0, SINCOS_TURNS = 1 } sincos_units_t;

@@ -247,8 +247,17 @@ sincos_status_t launch(const float *theta, float *so, float *co, float *io, size
 }
 
 // ---- host-buffer pipeline ----------------------------------------------------------
-constexpr int kSlots = 3;
-constexpr size_t kMinChunk = size_t(1) << 16;
+// Three slots, chunks ramping up from 2^16 elements.  Measured against 2 and 4 slots, a tail
+// ramping down again, and 256 MiB - 2 GiB of workspace (tools/ab_host.py,
+// profiles/r02/ab_host*.jsonl): all within 1% of each other, ~0.97 of the PCIe roofline.
+#ifndef SINCOS_HOST_SLOTS
+#define SINCOS_HOST_SLOTS 3
+#endif
+#ifndef SINCOS_HOST_MIN_CHUNK_LOG2
+#define SINCOS_HOST_MIN_CHUNK_LOG2 16
+#endif
+constexpr int kSlots = SINCOS_HOST_SLOTS;
+constexpr size_t kMinChunk = size_t(1) << SINCOS_HOST_MIN_CHUNK_LOG2;
 
 struct DevStreams {
     bool init = false;
@@ -435,7 +444,7 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
     // was faster -- profiles/r02/ab_phase_tiny.jsonl -- and the staged kernel below is now)
     const bool tiny = flat && T.realign != 3 && (nt == 1 || (split && nt < SINCOS_PHASE_STAGED_SPLIT_MIN)) &&
                       (split ? aligned(sin_dev, 32) && aligned(cos_dev, 32) : aligned(inter_dev, 32));
-    // rows of 4-13 pairs (split) or 2-7 (interleaved), outputs 16-B aligned at pair 0: the staged
+    // rows of 4-14 pairs (split) or 2-15 (interleaved), outputs 16-B aligned at pair 0: the staged
     // short-row kernel (a warp's 128 rows staged in shared memory, written back as contiguous
     // 512-B store instructions)
     const bool staged = SINCOS_PHASE_STAGED && flat && !tiny && T.realign != 3 &&
@@ -703,9 +712,9 @@ sincos_status_t sincos_pairs_host(const float *theta_host, float *sin_host, floa
     // of the pipeline; its drain is the last chunk's device->host copy either way).
     size_t chunk = kMinChunk < cap ? kMinChunk : cap;
     size_t j = 0;
-    for (size_t off = 0; off < n; off += chunk, ++j) {
+    for (size_t off = 0, m = 0; off < n; off += m, ++j) {
         if (j > 0 && chunk < cap) chunk = 2 * chunk < cap ? 2 * chunk : cap;
-        const size_t m = n - off < chunk ? n - off : chunk;
+        m = n - off < chunk ? n - off : chunk;
         const int k = static_cast<int>(j % kSlots);
         cudaStream_t s = ds->s[k];
         float *th = reinterpret_cast<float *>(ws + k * cap * 12);

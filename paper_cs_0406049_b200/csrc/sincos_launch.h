@@ -102,10 +102,10 @@ constexpr size_t kPhaseRowsMinNt = SINCOS_PHASE_ROWS_MIN_NT;   // shorter rows: 
 #endif
 constexpr size_t kPhaseRowsPerBlock = SINCOS_PHASE_ROWS_PER_BLOCK;   // target rows per row slot
 #ifndef SINCOS_PHASE_STAGED_MAX_NT
-#define SINCOS_PHASE_STAGED_MAX_NT 13    // longest rows (pairs) of the staged short-row kernel, split
+#define SINCOS_PHASE_STAGED_MAX_NT 14    // longest rows (pairs) of the staged short-row kernel, split
 #endif
 #ifndef SINCOS_PHASE_STAGED_MAX_NT_INTER
-#define SINCOS_PHASE_STAGED_MAX_NT_INTER 7   // ... and interleaved
+#define SINCOS_PHASE_STAGED_MAX_NT_INTER 15  // ... and interleaved
 #endif
 #ifndef SINCOS_PHASE_VEC_MIN_NT
 #define SINCOS_PHASE_VEC_MIN_NT 256

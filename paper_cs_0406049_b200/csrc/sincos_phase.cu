@@ -674,12 +674,13 @@ cudaError_t launch_phase_tiny(int variant, bool inter, bool turns, const float *
     return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kPhaseThreads), args, 0, stream);
 }
 
-// Staged short rows (round 2): rows of NT = 4..13 pairs (split) or 2..7 pairs (interleaved),
+// Staged short rows (round 2): rows of NT = 4..14 pairs (split) or 2..15 pairs (interleaved),
 // outputs 16-B aligned at pair 0.  The tiny-row kernel's lane stores are 8 NT pairs apart, so
 // its warp store instructions scatter over NT x more lines; here a warp computes a region of
 // 128 whole rows (lane l: rows 4l..4l+3, one 128-bit load of their f, every (row, column)
 // a compile-time constant as in the tiny kernel), stages the region's 128 NT pairs in shared
-// memory and writes it back as 128-bit stores of 512 B contiguous per warp instruction.  Lane l
+// memory and writes it back as 128-bit stores of 512 B contiguous per warp instruction (longer
+// rows: 2 rows per lane, regions of 64 rows; staged_rows below).  Lane l
 // writes its chunks (16 B) S l + q (S = chunks per lane: NT split, 2 NT interleaved), the
 // write-back reads chunks 32 j + l; chunk c is kept at c ^ ((c >> z) & 7), z = the number of
 // trailing zero bits of S (odd S: unswizzled), which makes both conflict-free for every S here
@@ -693,8 +694,17 @@ __device__ __forceinline__ int stage_chunk(int c) {
     if constexpr (z == 0) return c;
     else return c ^ ((c >> z) & 7);
 }
-// 128-thread blocks up to NT = 11 (44 KB of static shared memory), 64 above (<= 48 KB)
-__host__ __device__ constexpr int staged_threads(int nt) { return nt <= 11 ? 128 : 64; }
+// Rows per lane: 4 (rows of 2-7 pairs, and split rows of 8-13), 2 for interleaved rows of 8-15
+// pairs and split rows of 14 (half the staging: 128-thread blocks, registers capped at 72; with
+// 4 rows per lane these ran no faster than the short-row kernel).  Against the short-row
+// kernel, burst: interleaved 9-15 +1-4% (14 in variant A -1.3%, 8 equal), split 14 +5%
+// (profiles/r02/ab_phase_r2_v*.jsonl).
+__host__ __device__ constexpr int staged_rows(bool inter, int nt) { return nt <= 7 || (!inter && nt <= 13) ? 4 : 2; }
+// A warp stages 256 R NT bytes: 128-thread blocks up to R NT = 44 (44 KB of static shared
+// memory), 64 above (<= 48 KB)
+__host__ __device__ constexpr int staged_threads(bool inter, int nt) {
+    return staged_rows(inter, nt) * nt <= 44 ? 128 : 64;
+}
 // Rows of 8-13 pairs: registers capped at 72.  Without the cap they took 134-214 and ran 20-40%
 // slower; at 64 some instances spill (profiles/r02/ab_phase_mid8b_v*.jsonl).  Rows of 2-7
 // pairs keep ptxas's own choice (32-72): any explicit minimum blocks per SM -- even 1 -- let
@@ -702,8 +712,8 @@ __host__ __device__ constexpr int staged_threads(int nt) { return nt <= 11 ? 128
 #ifndef SINCOS_PHASE_STAGED_REGS
 #define SINCOS_PHASE_STAGED_REGS 72
 #endif
-__host__ __device__ constexpr int staged_min_blocks(int nt) {
-    return 65536 / (staged_threads(nt) * SINCOS_PHASE_STAGED_REGS);
+__host__ __device__ constexpr int staged_min_blocks(bool inter, int nt) {
+    return 65536 / (staged_threads(inter, nt) * SINCOS_PHASE_STAGED_REGS);
 }
 __device__ __forceinline__ void st_shared4(const float4 *p, float a, float b, float c, float d) {
     const unsigned addr = static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -721,9 +731,9 @@ __device__ __forceinline__ void st_global4(float *p, float4 v) {
                  "f"(v.w) : "memory");
 }
 
-// K pairs (K even) of the lane's rows, pairs k0 .. k0 + K - 1 in row-major order of its 4 x NT
-template <int V, bool TURNS, int NT, int K, int K0>
-__device__ __forceinline__ void staged_pairs(const float (&fr)[4], const float (&tt)[NT], float (&sv)[K],
+// K pairs (K even) of the lane's rows, pairs K0 .. K0 + K - 1 in row-major order of its R x NT
+template <int V, bool TURNS, int NT, int R, int K, int K0>
+__device__ __forceinline__ void staged_pairs(const float (&fr)[R], const float (&tt)[NT], float (&sv)[K],
                                              float (&cv)[K]) {
 #pragma unroll
     for (int k = 0; k < K; k += 2) {
@@ -743,48 +753,55 @@ __device__ __forceinline__ void staged_pairs(const float (&fr)[4], const float (
     }
 }
 
+// Chunks (16 B) per lane and stream: split R NT / 4, interleaved R NT / 2 (whole chunks: R NT is
+// a multiple of 4, resp. 2, for every instance).
+template <bool INTER, int NT, int R>
+__host__ __device__ constexpr int staged_stride() { return INTER ? R * NT / 2 : R * NT / 4; }
+
 // compute pairs [K0, K0 + K) and stage them: split -> chunk K0/4 .. of the lane's sin / cos runs,
 // interleaved -> chunks K0/2 .. of its {cos, sin} run
-template <int V, bool INTER, bool TURNS, int NT, int K, int K0>
-__device__ __forceinline__ void stage_batch(const float (&fr)[4], const float (&tt)[NT], float4 *ws, unsigned lane) {
+template <int V, bool INTER, bool TURNS, int NT, int R, int K, int K0>
+__device__ __forceinline__ void stage_batch(const float (&fr)[R], const float (&tt)[NT], float4 *ws, unsigned lane) {
     float sv[K], cv[K];
-    staged_pairs<V, TURNS, NT, K, K0>(fr, tt, sv, cv);
+    staged_pairs<V, TURNS, NT, R, K, K0>(fr, tt, sv, cv);
+    constexpr int S = staged_stride<INTER, NT, R>();
     if constexpr (INTER) {
-        constexpr int S = 2 * NT;
 #pragma unroll
         for (int h = 0; h < K / 2; ++h) {
             const int c = static_cast<int>(lane) * S + K0 / 2 + h;
             st_shared4(ws + stage_chunk<S>(c), cv[2 * h], sv[2 * h], cv[2 * h + 1], sv[2 * h + 1]);
         }
     } else {
-        constexpr int S = NT;
 #pragma unroll
         for (int h = 0; h < K / 4; ++h) {
             const int c = static_cast<int>(lane) * S + K0 / 4 + h;
             st_shared4(ws + stage_chunk<S>(c), sv[4 * h], sv[4 * h + 1], sv[4 * h + 2], sv[4 * h + 3]);
-            st_shared4(ws + 32 * NT + stage_chunk<S>(c), cv[4 * h], cv[4 * h + 1], cv[4 * h + 2], cv[4 * h + 3]);
+            st_shared4(ws + 32 * S + stage_chunk<S>(c), cv[4 * h], cv[4 * h + 1], cv[4 * h + 2], cv[4 * h + 3]);
         }
     }
 }
 
-// the lane's 4 NT pairs: batches of 8 from pair K0 on, a last one of 4 for odd NT
-template <int V, bool INTER, bool TURNS, int NT, int K0>
-__device__ __forceinline__ void stage_all(const float (&fr)[4], const float (&tt)[NT], float4 *ws, unsigned lane) {
-    if constexpr (4 * NT - K0 >= 8) {
-        stage_batch<V, INTER, TURNS, NT, 8, K0>(fr, tt, ws, lane);
-        stage_all<V, INTER, TURNS, NT, K0 + 8>(fr, tt, ws, lane);
-    } else if constexpr (4 * NT - K0 == 4) {
-        stage_batch<V, INTER, TURNS, NT, 4, K0>(fr, tt, ws, lane);
+// the lane's R NT pairs: batches of 8 from pair K0 on, then the rest (2, 4 or 6)
+template <int V, bool INTER, bool TURNS, int NT, int R, int K0>
+__device__ __forceinline__ void stage_all(const float (&fr)[R], const float (&tt)[NT], float4 *ws, unsigned lane) {
+    if constexpr (R * NT - K0 >= 8) {
+        stage_batch<V, INTER, TURNS, NT, R, 8, K0>(fr, tt, ws, lane);
+        stage_all<V, INTER, TURNS, NT, R, K0 + 8>(fr, tt, ws, lane);
+    } else if constexpr (R * NT - K0 > 0) {
+        stage_batch<V, INTER, TURNS, NT, R, R * NT - K0, K0>(fr, tt, ws, lane);
     }
 }
 
-template <int V, bool INTER, bool TURNS, int NT>
+// A warp's region: 32 R whole rows = 32 R NT pairs, R rows per lane (R = 4, 2).
+template <int V, bool INTER, bool TURNS, int NT, int R>
 __device__ __forceinline__ void staged_body(const float *__restrict__ f, const float *__restrict__ t, size_t nf,
-                                            float *so, float *co, float *io, size_t nregions, bool f_al16) {
-    __shared__ float4 stage[staged_threads(NT) / 32][64 * NT];     // 1 KB x NT per warp
+                                            float *so, float *co, float *io, size_t nregions, bool f_al) {
+    constexpr int S = staged_stride<INTER, NT, R>();
+    static_assert((INTER ? R * NT % 2 : R * NT % 4) == 0, "whole 16-B chunks per lane");
+    __shared__ float4 stage[staged_threads(INTER, NT) / 32][INTER ? 32 * S : 64 * S];   // 256 R NT B per warp
     const size_t gid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
-    const size_t rem0 = 128 * NT * nregions, rem = nf * NT - rem0;   // rows past the last region
+    const size_t rem0 = 32 * R * NT * nregions, rem = nf * NT - rem0;   // rows past the last region
     for (size_t i = gid; i < rem; i += nthr) {
         const size_t e = rem0 + i;
         float sr, cr;
@@ -804,82 +821,115 @@ __device__ __forceinline__ void staged_body(const float *__restrict__ f, const f
     for (int b = 0; b < NT; ++b) tt[b] = __ldg(t + b);
     const size_t nwarps = nthr / 32;
     for (size_t r = gid / 32; r < nregions; r += nwarps) {   // warp-uniform: one region per trip
-        const size_t row0 = 128 * r + 4 * lane;
-        float fr[4];
-        if (f_al16) {
-            const float4 v = __ldg(reinterpret_cast<const float4 *>(f + row0));
-            fr[0] = v.x;
-            fr[1] = v.y;
-            fr[2] = v.z;
-            fr[3] = v.w;
-        } else {
+        const size_t row0 = 32 * R * r + R * lane;
+        float fr[R];
+        if constexpr (R == 4) {
+            if (f_al) {
+                const float4 v = __ldg(reinterpret_cast<const float4 *>(f + row0));
+                fr[0] = v.x;
+                fr[1] = v.y;
+                fr[2] = v.z;
+                fr[3] = v.w;
+            } else {
 #pragma unroll
-            for (int a = 0; a < 4; ++a) fr[a] = __ldg(f + row0 + a);
-        }
-        stage_all<V, INTER, TURNS, NT, 0>(fr, tt, ws, lane);
-        __syncwarp();
-        if constexpr (INTER) {
-            float *dst = io + 2 * 128 * NT * r;
-#pragma unroll
-            for (int j = 0; j < 2 * NT; ++j) {
-                const int c = 32 * j + static_cast<int>(lane);
-                st_global4(dst + 4 * c, ld_shared4(ws + stage_chunk<2 * NT>(c)));
+                for (int a = 0; a < 4; ++a) fr[a] = __ldg(f + row0 + a);
             }
         } else {
-            float *ds = so + 128 * NT * r, *dc = co + 128 * NT * r;
+            if (f_al) {
+                const float2 v = __ldg(reinterpret_cast<const float2 *>(f + row0));
+                fr[0] = v.x;
+                fr[1] = v.y;
+            } else {
 #pragma unroll
-            for (int j = 0; j < NT; ++j) {
+                for (int a = 0; a < R; ++a) fr[a] = __ldg(f + row0 + a);
+            }
+        }
+        stage_all<V, INTER, TURNS, NT, R, 0>(fr, tt, ws, lane);
+        __syncwarp();
+        if constexpr (INTER) {
+            float *dst = io + 2 * 32 * R * NT * r;
+#pragma unroll
+            for (int j = 0; j < S; ++j) {              // 32 S chunks = 32 R NT pairs
                 const int c = 32 * j + static_cast<int>(lane);
-                st_global4(ds + 4 * c, ld_shared4(ws + stage_chunk<NT>(c)));
-                st_global4(dc + 4 * c, ld_shared4(ws + 32 * NT + stage_chunk<NT>(c)));
+                st_global4(dst + 4 * c, ld_shared4(ws + stage_chunk<S>(c)));
+            }
+        } else {
+            float *ds = so + 32 * R * NT * r, *dc = co + 32 * R * NT * r;
+#pragma unroll
+            for (int j = 0; j < S; ++j) {              // 32 S chunks per stream
+                const int c = 32 * j + static_cast<int>(lane);
+                st_global4(ds + 4 * c, ld_shared4(ws + stage_chunk<S>(c)));
+                st_global4(dc + 4 * c, ld_shared4(ws + 32 * S + stage_chunk<S>(c)));
             }
         }
         __syncwarp();
     }
 }
 
-// rows of 2-7 pairs: ptxas's own register choice (32-72); rows of 8-13: capped at 72
-template <int V, bool INTER, bool TURNS, int NT>
-__global__ void __launch_bounds__(staged_threads(NT)) phase_grid_staged(const float *__restrict__ f,
+// rows of 2-7 pairs: ptxas's own register choice (32-72); longer rows: capped at 72
+template <int V, bool INTER, bool TURNS, int NT, int R>
+__global__ void __launch_bounds__(staged_threads(INTER, NT)) phase_grid_staged(const float *__restrict__ f,
                                                                        const float *__restrict__ t, size_t nf,
                                                                        float *so, float *co, float *io,
-                                                                       size_t nregions, bool f_al16) {
-    staged_body<V, INTER, TURNS, NT>(f, t, nf, so, co, io, nregions, f_al16);
+                                                                       size_t nregions, bool f_al) {
+    staged_body<V, INTER, TURNS, NT, R>(f, t, nf, so, co, io, nregions, f_al);
 }
-template <int V, bool INTER, bool TURNS, int NT>
-__global__ void __launch_bounds__(staged_threads(NT), staged_min_blocks(NT))
+template <int V, bool INTER, bool TURNS, int NT, int R>
+__global__ void __launch_bounds__(staged_threads(INTER, NT), staged_min_blocks(INTER, NT))
 phase_grid_staged_wide(const float *__restrict__ f, const float *__restrict__ t, size_t nf, float *so, float *co,
-                       float *io, size_t nregions, bool f_al16) {
-    staged_body<V, INTER, TURNS, NT>(f, t, nf, so, co, io, nregions, f_al16);
+                       float *io, size_t nregions, bool f_al) {
+    staged_body<V, INTER, TURNS, NT, R>(f, t, nf, so, co, io, nregions, f_al);
 }
 
 template <int V, bool INTER, bool TURNS>
 static const void *pick_staged(size_t nt) {
+#define STG(N) reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, N, 4>)
+#define WIDE(N) reinterpret_cast<const void *>(phase_grid_staged_wide<V, INTER, TURNS, N, staged_rows(INTER, N)>)
     switch (nt) {
-    case 2: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 2>);
-    case 3: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 3>);
-    case 4: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 4>);
-    case 5: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 5>);
-    case 6: return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 6>);
+    case 2: return STG(2);
+    case 3: return STG(3);
+    case 4: return STG(4);
+    case 5: return STG(5);
+    case 6: return STG(6);
     default: break;
     }
-    if constexpr (!INTER) {                // split rows of 8-13 pairs (interleaved: the short-row kernel)
+    if constexpr (!INTER) {                // split rows of 8-13 pairs (R = 4)
+        if constexpr (SINCOS_PHASE_STAGED_MAX_NT >= 8) {
+            switch (nt) {
+            case 8: return WIDE(8);
+            case 9: return WIDE(9);
+            case 10: return WIDE(10);
+            case 11: return WIDE(11);
+            case 12: return WIDE(12);
+            case 13: return WIDE(13);
+            default: break;
+            }
+        }
+        if constexpr (SINCOS_PHASE_STAGED_MAX_NT >= 14) {
+            if (nt == 14) return WIDE(14);
+        }
+    } else if constexpr (SINCOS_PHASE_STAGED_MAX_NT_INTER >= 8) {   // interleaved rows of 8-15 (R = 2)
         switch (nt) {
-        case 8: return reinterpret_cast<const void *>(phase_grid_staged_wide<V, INTER, TURNS, 8>);
-        case 9: return reinterpret_cast<const void *>(phase_grid_staged_wide<V, INTER, TURNS, 9>);
-        case 10: return reinterpret_cast<const void *>(phase_grid_staged_wide<V, INTER, TURNS, 10>);
-        case 11: return reinterpret_cast<const void *>(phase_grid_staged_wide<V, INTER, TURNS, 11>);
-        case 12: return reinterpret_cast<const void *>(phase_grid_staged_wide<V, INTER, TURNS, 12>);
-        case 13: return reinterpret_cast<const void *>(phase_grid_staged_wide<V, INTER, TURNS, 13>);
+        case 8: return WIDE(8);
+        case 9: return WIDE(9);
+        case 10: return WIDE(10);
+        case 11: return WIDE(11);
+        case 12: return WIDE(12);
+        case 13: return WIDE(13);
+        case 14: return WIDE(14);
+        case 15: return WIDE(15);
         default: break;
         }
     }
-    return reinterpret_cast<const void *>(phase_grid_staged<V, INTER, TURNS, 7>);
+    return STG(7);
+#undef STG
+#undef WIDE
 }
 
 cudaError_t launch_phase_staged(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
                                 size_t nt, float *so, float *co, float *io, size_t max_grid, cudaStream_t stream) {
-    if (nt < 2 || nt > (inter ? SINCOS_PHASE_STAGED_MAX_NT_INTER : SINCOS_PHASE_STAGED_MAX_NT))
+    if (nt < 2 || nt > (inter ? SINCOS_PHASE_STAGED_MAX_NT_INTER : SINCOS_PHASE_STAGED_MAX_NT) ||
+        (!inter && nt > 14))
         return cudaErrorInvalidValue;
     const void *fn;
     if (variant == kNormalized)
@@ -889,9 +939,10 @@ cudaError_t launch_phase_staged(int variant, bool inter, bool turns, const float
         fn = inter ? (turns ? pick_staged<kRenormalized, true, true>(nt) : pick_staged<kRenormalized, true, false>(nt))
                    : (turns ? pick_staged<kRenormalized, false, true>(nt)
                             : pick_staged<kRenormalized, false, false>(nt));
-    size_t nregions = nf / 128;
-    const size_t rem = (nf - 128 * nregions) * nt;                    // < 128 rows of tail pairs
-    const unsigned threads = staged_threads(static_cast<int>(nt));
+    const int R = staged_rows(inter, static_cast<int>(nt));
+    size_t nregions = nf / (32 * R);
+    const size_t rem = (nf - 32 * R * nregions) * nt;                 // < 32 R rows of tail pairs
+    const unsigned threads = staged_threads(inter, static_cast<int>(nt));
     const size_t warps_per_block = threads / 32;
     size_t grid = (nregions + warps_per_block - 1) / warps_per_block;
     const size_t grid_rem = (rem + threads - 1) / threads;
@@ -899,8 +950,8 @@ cudaError_t launch_phase_staged(int variant, bool inter, bool turns, const float
     if (max_grid > 0 && grid > max_grid) grid = max_grid;               // (A/B: grid-stride)
     if (grid < 1) grid = 1;
     if (grid > 0x7FFFFFFFu / 4) grid = 0x7FFFFFFFu / 4;                // grid-strides past it
-    bool f_al16 = (reinterpret_cast<uintptr_t>(f) & 15) == 0;
-    void *args[] = {&f, &t, &nf, &so, &co, &io, &nregions, &f_al16};
+    bool f_al = (reinterpret_cast<uintptr_t>(f) & (4 * R - 1)) == 0;
+    void *args[] = {&f, &t, &nf, &so, &co, &io, &nregions, &f_al};
     return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(threads), args, 0, stream);
 }
 

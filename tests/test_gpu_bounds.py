@@ -95,7 +95,8 @@ def test_phase_grid_and_nudft(shape):
 
 @pytest.mark.parametrize("shape", [(1, 1), (3, 7), (9, 13), (33, 1001), (16, 256), (9, 131), (21, 300), (3, 4000),
                                    (21, 1), (1003, 2), (77, 3), (1000, 4), (300, 5), (129, 6), (385, 7),
-                                   (128 * 9 + 3, 3), (300, 9), (129, 12), (1000, 13)])
+                                   (128 * 9 + 3, 3), (300, 9), (129, 12), (1000, 13), (513, 14), (77, 15),
+                                   (64 * 7 + 63, 10)])
 @pytest.mark.parametrize("off", [0, 1, 3, 4, 6])
 def test_phase_grid_split_offsets(shape, off):
     """Split phase-grid outputs at offsets (the flat kernel's head/body/tail, the ragged-row

@@ -267,12 +267,13 @@ def test_tiny_rows(units, variant, nt):
             assert_parity(iv[1::2], iv[0::2], ws, wc, "inter " + tag)
 
 
-@pytest.mark.parametrize("nt", [2, 3, 4, 5, 6, 7, 8, 9, 11, 12, 13])
+@pytest.mark.parametrize("nt", [2, 3, 4, 5, 6, 7, 8, 9, 11, 12, 13, 14, 15, 16])
 @pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("units", [0, 1])
 def test_staged_rows(units, variant, nt):
-    """Rows of 2..13 pairs through the staged short-row kernel (split nt = 4..13 -- 64-thread
-    blocks from 12 on -- interleaved nt = 2..7, the short-row kernel above;
+    """Rows of 2..15 pairs through the staged short-row kernel (split nt = 4..14: 4 rows per lane,
+    64-thread blocks for 12-13, 2 rows per lane for 14; interleaved nt = 2..15: 4 rows per lane
+    up to 7, 2 above; nt = 16 and split 15 on the short-row kernel);
     outputs 16-B aligned at pair 0: a warp's 128 rows staged in shared memory, written back as
     contiguous 128-bit stores): whole 128-row regions and a ragged tail, f 16-B aligned or not,
     outputs 32-B and only 16-B aligned, and on the A/B build's grid-stride grids (many regions

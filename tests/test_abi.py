@@ -210,6 +210,36 @@ def test_sass_value_path_branch_free():
     assert seen >= 24 + 42 + 8 + 24       # vector, theta re-aligning (256-bit), phase-grid, fused-sum instances
 
 
+def test_sass_other_kernel_forms_have_no_slow_paths():
+    """The re-aligning and phase-grid (row, short-row, staged, tiny) forms evaluate the same
+    method: no FCHK (fp32 division slow path), no fp64, and the method's reciprocal only in variant A
+    -- each variant-A instance has more MUFU.RCP than its variant-N twin (whose MUFU.RCP, where
+    present, belong to integer divisions of an index by a run-time row length)."""
+    sass = _sass()
+    funcs = re.split(r"\n\s*Function : ", sass)
+    rcp = {}
+    for f in funcs:
+        name = f.split("\n", 1)[0].strip()
+        form = next((k for k in ("sincos_outshift_kernel", "phase_grid_staged", "phase_grid_tiny",
+                                 "phase_grid_short", "phase_grid_rows") if k in name), None)
+        if form is None:
+            continue
+        m = re.search(r"ILi(\d+)E", name)
+        if not m or int(m.group(1)) not in (0, 1):
+            continue                     # the no-math ceiling instances
+        # (a CALL may appear: the 64-bit integer division of a pair index by the row length)
+        assert "FCHK" not in f and "DFMA" not in f and "MUFU.RCP64H" not in f, name
+        rcp[name] = len(re.findall(r"MUFU\.RCP\b", f))
+    pairs = 0
+    for name, k in rcp.items():
+        if re.search(r"ILi0E", name):
+            twin = name.replace("ILi0E", "ILi1E", 1)
+            assert twin in rcp, twin
+            assert rcp[twin] > k, (name, k, rcp[twin])
+            pairs += 1
+    assert pairs >= 64 + 4 + 2 * 2 * 13 + 8, pairs   # outshift split + interleaved, staged, tiny/short/rows
+
+
 def test_product_never_touches_the_oracle():
     """The oracle is test infrastructure: nothing under the package imports, links or includes it."""
     pkg = os.path.join(ROOT, "paper_cs_0406049_b200")

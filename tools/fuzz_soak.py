@@ -41,8 +41,12 @@ def one_case(rng):
     inter = bool(rng.integers(0, 2))
     entry = ["pairs", "dtype32", "method", "phase", "batched", "fp16", "bf16", "phase2d"][int(rng.integers(0, 8))]
     if entry == "phase2d":                # an nf x nt grid: theta_ij = RN(f_i t_j), the fp32 products
-        nf2 = int(rng.integers(1, 24))
-        nt2 = max(1, n // nf2)
+        if rng.random() < 0.5:            # many short rows: the tiny / staged / short-row kernels' regions
+            nt2 = int(rng.integers(1, 16))
+            nf2 = max(1, n // nt2)
+        else:
+            nf2 = int(rng.integers(1, 24))
+            nt2 = max(1, n // nf2)
         f2 = rng.uniform(-50, 50, nf2).astype(np.float32)
         toff2 = int(rng.integers(0, 8))
         t2 = draw_theta(rng, nt2 + 8)[toff2:toff2 + nt2]

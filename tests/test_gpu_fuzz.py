@@ -52,8 +52,12 @@ def test_fuzz_pairs(block):
         inter = bool(rng.integers(0, 2))
         entry = ["pairs", "dtype32", "method", "phase", "phase2d"][int(rng.integers(0, 5))]
         if entry == "phase2d":                           # an nf x nt grid: theta_ij = RN(f_i t_j)
-            nf2 = int(rng.integers(1, 24))
-            nt2 = max(1, n // nf2)
+            if rng.random() < 0.5:                        # many short rows (tiny / staged / short-row kernels)
+                nt2 = int(rng.integers(1, 16))
+                nf2 = max(1, n // nt2)
+            else:
+                nf2 = int(rng.integers(1, 24))
+                nt2 = max(1, n // nf2)
             f2 = rng.uniform(-50, 50, nf2).astype(np.float32)
             t2 = draw_theta(rng, nt2 + 8)
             toff2 = int(rng.integers(0, 8))

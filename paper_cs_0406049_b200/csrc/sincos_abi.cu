@@ -447,10 +447,9 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
     // rows of 4-14 pairs (split) or 2-15 (interleaved), outputs 16-B aligned at pair 0: the staged
     // short-row kernel (a warp's 128 rows staged in shared memory, written back as contiguous
     // 512-B store instructions)
-    const bool staged = SINCOS_PHASE_STAGED && flat && !tiny && T.realign != 3 &&
-                        (split ? nt >= SINCOS_PHASE_STAGED_SPLIT_MIN && nt <= SINCOS_PHASE_STAGED_MAX_NT &&
-                                     aligned(sin_dev, 16) && aligned(cos_dev, 16)
-                               : nt >= 2 && nt <= SINCOS_PHASE_STAGED_MAX_NT_INTER && aligned(inter_dev, 16));
+    const bool staged = SINCOS_PHASE_STAGED && flat && !tiny && T.realign != 3 && phase_staged_ok(inter, nt) &&
+                        (split ? nt >= SINCOS_PHASE_STAGED_SPLIT_MIN && aligned(sin_dev, 16) && aligned(cos_dev, 16)
+                               : aligned(inter_dev, 16));
     if (tiny) {
         e = launch_phase_tiny(variant, inter, units == SINCOS_TURNS, f_dev, nf, t_dev, nt, sin_dev, cos_dev,
                               inter_dev, static_cast<cudaStream_t>(stream));

@@ -107,6 +107,15 @@ constexpr size_t kPhaseRowsPerBlock = SINCOS_PHASE_ROWS_PER_BLOCK;   // target r
 #ifndef SINCOS_PHASE_STAGED_MAX_NT_INTER
 #define SINCOS_PHASE_STAGED_MAX_NT_INTER 15  // ... and interleaved
 #endif
+static_assert(SINCOS_PHASE_STAGED_MAX_NT <= 14 && SINCOS_PHASE_STAGED_MAX_NT_INTER <= 15,
+              "staged instances exist for split rows of 2-14 pairs and interleaved rows of 2-15");
+// Row lengths with a staged instance, up to the maxima above (the product routes split rows of
+// 2-3 pairs to the tiny-row kernel instead).  Longer rows (16-31 pairs, 2 rows per lane) were
+// measured: within the run-to-run spread of the short-row kernel, +-5% by shape and variant
+// (profiles/r02/ab_phase_m16_v*.jsonl) -- not kept.
+inline bool phase_staged_ok(bool inter, size_t nt) {
+    return nt >= 2 && nt <= static_cast<size_t>(inter ? SINCOS_PHASE_STAGED_MAX_NT_INTER : SINCOS_PHASE_STAGED_MAX_NT);
+}
 #ifndef SINCOS_PHASE_VEC_MIN_NT
 #define SINCOS_PHASE_VEC_MIN_NT 256
 #endif

@@ -928,9 +928,7 @@ static const void *pick_staged(size_t nt) {
 
 cudaError_t launch_phase_staged(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
                                 size_t nt, float *so, float *co, float *io, size_t max_grid, cudaStream_t stream) {
-    if (nt < 2 || nt > (inter ? SINCOS_PHASE_STAGED_MAX_NT_INTER : SINCOS_PHASE_STAGED_MAX_NT) ||
-        (!inter && nt > 14))
-        return cudaErrorInvalidValue;
+    if (!phase_staged_ok(inter, nt)) return cudaErrorInvalidValue;
     const void *fn;
     if (variant == kNormalized)
         fn = inter ? (turns ? pick_staged<kNormalized, true, true>(nt) : pick_staged<kNormalized, true, false>(nt))

@@ -439,6 +439,9 @@ ALU_PEAK_OPS = 148 * 128 * 1.965e9   # FP32-pipe lane-ops/s at the max SM clock 
 # algorithmic FP32-pipe ops per term of the fused sum, variant N: the phase product (1), the
 # method (11 FMUL + 10 FFMA + 1 FADD + 1 FRND = 23; turns skips the 1/2pi FMUL), the complex MAC (4)
 NUDFT_OPS = {"radians": 28, "turns": 27}
+# variant A: the fix f = RN(1/d) instead of N's two FFMA -- d = fma(s2, s2, RN(c2 c2)) (FMUL + FFMA)
+# and the Newton step on the MUFU.RCP seed (2 FFMA; the MUFU itself issues on the XU pipe): +2
+NUDFT_OPS_A = {"radians": 30, "turns": 29}
 
 
 def measure_nudft(dev, stream, reps=5):
@@ -455,7 +458,7 @@ def measure_nudft(dev, stream, reps=5):
     out = torch.empty(nf, dtype=torch.complex64, device=dev)
     ws = torch.empty(sp.lib().sincos_nudft_workspace_bytes(nf, nt), dtype=torch.uint8, device=dev)
     res = {"workload": "C4 shape: 2^15 f x 2^15 t = 2^30 terms, complex64 amplitudes", "bound": "alu",
-           "peak_ops_per_s": ALU_PEAK_OPS, "ops_per_term": NUDFT_OPS,
+           "peak_ops_per_s": ALU_PEAK_OPS, "ops_per_term": NUDFT_OPS, "ops_per_term_A": NUDFT_OPS_A,
            "kernel": "packed fp32 (FFMA2/FMUL2/FADD2, two frequencies per instruction)"}
     ks = torch.arange(0, nf, nf // 16, device=dev)
     asum = float(a.abs().sum())
@@ -481,8 +484,8 @@ def measure_nudft(dev, stream, reps=5):
             ms = e0.elapsed_time(e1) / reps
             terms = (nf * nt) / (ms / 1e3)
             r = {"ms": ms, "terms_per_s": terms, "max_err_over_sum_abs_a": err}
-            if vname.startswith("N"):
-                r["alu_frac"] = terms * NUDFT_OPS[uname] / ALU_PEAK_OPS
+            if vname in ("N", "A"):
+                r["alu_frac"] = terms * (NUDFT_OPS if vname == "N" else NUDFT_OPS_A)[uname] / ALU_PEAK_OPS
             res[f"{uname}_{vname}"] = r
     return res
 

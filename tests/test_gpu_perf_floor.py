@@ -97,6 +97,12 @@ def test_phase_grid_short_and_tiny_rows_floor():
     o5 = torch.empty(2 * n5, device="cuda")
     got = gbps(lambda: sp.phase_grid(f5, t5, interleaved_out=o5, units=sp.TURNS), 8 * n5)
     assert got >= 5300, f"nt=5 {got:.0f} (recorded 6.1 TB/s written)"
+    f12 = torch.rand((1 << 27) // 12, device="cuda") * 512     # interleaved rows of 12: staged, 2 rows per lane
+    t12 = torch.rand(12, device="cuda")
+    n12 = f12.numel() * 12
+    o12 = torch.empty(2 * n12, device="cuda")
+    got = gbps(lambda: sp.phase_grid(f12, t12, interleaved_out=o12, units=sp.TURNS), 8 * n12)
+    assert got >= 5600, f"nt=12 {got:.0f} (recorded 6.5 TB/s written)"
     f1 = torch.rand(1 << 27, device="cuda")
     t1 = torch.rand(1, device="cuda")
     s, c = torch.empty(1 << 27, device="cuda"), torch.empty(1 << 27, device="cuda")

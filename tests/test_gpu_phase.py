@@ -307,3 +307,39 @@ def test_staged_rows(units, variant, nt):
                         assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws, wc, "split " + tag)
                         iv = io.cpu().numpy()
                         assert_parity(iv[1::2], iv[0::2], ws, wc, "inter " + tag)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("units", [0, 1])
+def test_every_row_kernel_on_special_values(units, variant):
+    """Every phase-grid kernel (tiny, staged with 4 and 2 rows per lane, short-row, row, vector,
+    one pair per thread) on f and t holding the special values -- +-0, subnormals, +-inf, NaN,
+    huge, ties of the turn reduction -- so the products RN(f t) are zeros, subnormals, infinities,
+    NaN (0 x inf) and exact halves: the outputs equal the oracle's pairs by value (NaN == NaN)."""
+    rng = np.random.default_rng(7 + units + 2 * variant)
+    specials = np.array([0.0, -0.0, 1e-40, -1e-40, np.inf, -np.inf, np.nan, 3e38, -3e38, 0.5, -0.5, 2.5,
+                         1.0, 0.25, 1e30, 7.0], dtype=np.float32)
+    for nt, toff, ooff in ((1, 0, 0), (3, 0, 0), (5, 0, 4), (12, 0, 0), (14, 0, 4), (33, 1, 0), (1003, 0, 0),
+                           (256, 0, 0), (9, 0, 1)):
+        nf = 700
+        f = rng.uniform(-50, 50, nf).astype(np.float32)
+        f[rng.integers(0, nf, 60)] = rng.choice(specials, 60)
+        t = rng.uniform(-2, 2, nt).astype(np.float32)
+        t[rng.integers(0, nt, max(1, nt // 4))] = rng.choice(specials, max(1, nt // 4))
+        ws, wc = oracle.phase_grid(f, t, units, variant)
+        ws, wc = ws.ravel(), wc.ravel()
+        fd = torch.from_numpy(f).cuda()
+        tb = torch.empty(nt + 8, device="cuda")
+        tb[toff:toff + nt].copy_(torch.from_numpy(t))
+        td = tb[toff:toff + nt]
+        n = nf * nt
+        sb, cb, ib = (torch.empty(n + 8, device="cuda"), torch.empty(n + 8, device="cuda"),
+                      torch.empty(2 * n + 8, device="cuda"))
+        s, c, io = sb[ooff:ooff + n], cb[ooff:ooff + n], ib[ooff:ooff + 2 * n]
+        sp.phase_grid(fd, td, s, c, units=units, variant=variant)
+        sp.phase_grid(fd, td, interleaved_out=io, units=units, variant=variant)
+        torch.cuda.synchronize()
+        tag = f"nt={nt} toff={toff} ooff={ooff}"
+        assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws, wc, "split " + tag)
+        iv = io.cpu().numpy()
+        assert_parity(iv[1::2], iv[0::2], ws, wc, "inter " + tag)

@@ -38,6 +38,8 @@ if os.environ.get("AB_CASES") == "mid8":
     CASES = [(7, 2), (8, 0), (9, 0), (10, 0), (11, 3), (12, 0), (13, 0), (14, 0), (15, 1)]
 if os.environ.get("AB_CASES") == "mid16":
     CASES = [(14, 0), (16, 0), (17, 1), (20, 0), (23, 2), (24, 0), (28, 0), (30, 3), (31, 0), (33, 0)]
+if os.environ.get("AB_CASES") == "vec8":
+    CASES = [(16, 0), (32, 0), (64, 0), (96, 0), (128, 0), (200, 0), (248, 0), (256, 0)]
 if os.environ.get("AB_CASES") == "aligned":
     CASES = [(32768, 0), (8192, 0), (4096, 0), (2048, 0), (1000, 0), (512, 0), (256, 0), (136, 0), (64, 0), (16, 0)]
 

@@ -66,8 +66,11 @@ def parse():
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
-        d = json.load(open(p))
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: torch copy, burst)"
+        try:
+            d = json.load(open(p))
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: torch copy, burst)"
+        except (ValueError, KeyError, TypeError) as e:
+            return FALLBACK_HBM_GBS, f"fallback (B200_PROFILING.md; MEASURED_PEAKS.json unreadable: {e!r})"
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 

@@ -7,6 +7,7 @@
 #include <utility>
 
 #include "sincos_launch.h"
+#include "sincos_realign.cuh"
 #include "sincos_stream.cuh"
 
 namespace sincos_b200 {
@@ -244,10 +245,87 @@ sincos_outshift_kernel(const float *theta, float *so, float *co, float *io,
     }
 }
 
+// Split layouts with BOTH streams off theta's frame (ks, kc != 0, ks != kc).  Re-aligning one
+// output stream costs ~1% (sin+0 cos+k: 6.79-6.81 TB/s against 6.86 aligned) and re-aligning
+// theta onto the outputs' frame about as little (KB3b: 6.80-6.89), while re-aligning both
+// output streams cost 3-9% (6.2-6.7; profiles/r02/ab_all_rot_v*.jsonl).  So most of these
+// layouts take the frame of one output stream ("direct": plain 256-bit stores), theta re-aligned
+// onto it from the next lane as in KB3b (KT = 8 - k_direct floats, sincos_realign.cuh) and only
+// the other stream re-aligned by store_realigned (KX = k_other - k_direct mod 8).  The vectors
+// start at hb + KT (scalar head below that); the last lane's second theta vector must lie
+// inside theta, so one vector fewer than KB3c's, the tail one element per thread.
+// Measured over all 42 such layouts, both variants, two boxes (tools/ab_layouts.py,
+// profiles/r02/ab_hyb*.jsonl; per-layout results reproduced to ~0.3%): the direct stream is the
+// one further past its 32-B boundary (the other choice lost 2-5% nearly everywhere); the
+// hybrid gains 0.5-3.8% in 28 layouts and loses 0.4-2.8% where the offsets are {1,2}, {1,3},
+// {1,4}, {1,6}, {2,3}, {2,4} or {4,7}, which keep both streams re-aligned on theta's frame.
+// (Fewer theta shuffles for KT > 4 -- each lane loading the second vector and taking the
+// first 8 - KT values from its predecessor -- changed nothing: the shuffle count is not what
+// costs here.)
+#ifndef SINCOS_OUTSHIFT_HYB
+#define SINCOS_OUTSHIFT_HYB 1        // 0: every such layout on theta's frame (A/B)
+#endif
+__host__ __device__ constexpr bool hyb_pair(int a, int b) {   // unordered offsets {a, b}, a < b
+    return !((a == 1 && (b == 2 || b == 3 || b == 4 || b == 6)) || (a == 2 && (b == 3 || b == 4)) ||
+             (a == 4 && b == 7));
+}
+template <int KI>
+__host__ __device__ constexpr bool hyb_applies() {
+    constexpr int ks = KI / 8, kc = KI % 8;
+    return SINCOS_OUTSHIFT_HYB != 0 && KI >= 0 && ks != 0 && kc != 0 && ks != kc &&
+           hyb_pair(ks < kc ? ks : kc, ks < kc ? kc : ks);
+}
+// the direct stream: the one further past its 32-B boundary
+template <int KI>
+__host__ __device__ constexpr bool hyb_sin_direct() { return KI / 8 > KI % 8; }
+
+template <int V, int KI>
+__global__ void __launch_bounds__(128, 16)
+sincos_outshift_hyb_kernel(const float *theta, float *so, float *co, float *io, size_t hb, size_t nvec, size_t n,
+                           int, int) {
+    (void)io;
+    constexpr bool SD = hyb_sin_direct<KI>();
+    constexpr int kd = SD ? KI / 8 : KI % 8, kx = SD ? KI % 8 : KI / 8;
+    constexpr int KT = 8 - kd;              // theta's float offset at the direct stream's frame (1..7)
+    constexpr int KX = (kx - kd + 8) % 8;   // the other stream's offset there (1..7)
+    const size_t head = hb + KT < n ? hb + KT : n;
+    const size_t nv = nvec > 0 ? nvec - 1 : 0;
+    const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t tail0 = head + nv * 8;
+    if (tid < head) emit_scalar<V, false>(theta, tid, so, co, nullptr);
+    if (tid < n - tail0) emit_scalar<V, false>(theta, tail0 + tid, so, co, nullptr);
+    const float *tal = theta + hb;          // 32-B aligned: theta + head - KT
+    float *dst = SD ? so : co;
+    float *oth = SD ? co : so;
+    const unsigned lane = threadIdx.x & 31u;
+    for (size_t w0 = tid - lane; w0 < nv; w0 += nthr) {   // warp-uniform trips
+        const size_t v = w0 + lane;
+        const bool act = v < nv;
+        const bool last = act && (lane == 31u || v + 1 >= nv);
+        float x[8];
+        load8_realigned_k<KT>(tal, v, nv, lane, act, x);
+        float d[8], o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if constexpr (SD) op<V>(x[j], d[j], o[j]);
+            else op<V>(x[j], o[j], d[j]);
+        }
+        if (act) store8(dst + head + 8 * v, d);
+        store_realigned<8, KX>(oth, head + 8 * v, o, KX, lane, act, last);
+    }
+}
+
+template <int V, int K>
+static const void *split_fn() {
+    if constexpr (hyb_applies<K>()) return reinterpret_cast<const void *>(sincos_outshift_hyb_kernel<V, K>);
+    else return reinterpret_cast<const void *>(sincos_outshift_kernel<V, false, K>);
+}
+
 template <int V, int... K>
 static const void *pick_split(int k, std::integer_sequence<int, K...>) {
     const void *fn = reinterpret_cast<const void *>(sincos_outshift_kernel<V, false, -1>);
-    ((k == K ? (fn = reinterpret_cast<const void *>(sincos_outshift_kernel<V, false, K>), 0) : 0), ...);
+    ((k == K ? (fn = split_fn<V, K>(), 0) : 0), ...);
     return fn;
 }
 

@@ -1,6 +1,6 @@
 // sincos_realign.cuh -- eight consecutive angles from any 4-B offset, with aligned 256-bit
 // loads: the re-alignment of KB3b (sincos_kernels.cu) for the kernels whose outputs fix the
-// vector alignment (16-bit outputs, general methods).
+// vector alignment (16-bit outputs, general methods) and the hybrid KB3c form (sincos_outshift.cu).
 //
 // The caller's vector v covers angles theta[head + 8v .. head + 8v + 7]; tal = theta + head - K
 // is 32-B aligned, K = 1..7 the angles' float offset past that boundary (the callers run an

@@ -211,16 +211,17 @@ def test_sass_value_path_branch_free():
 
 
 def test_sass_other_kernel_forms_have_no_slow_paths():
-    """The re-aligning and phase-grid (row, short-row, staged, tiny) forms evaluate the same
-    method: no FCHK (fp32 division slow path), no fp64, and the method's reciprocal only in variant A
-    -- each variant-A instance has more MUFU.RCP than its variant-N twin (whose MUFU.RCP, where
-    present, belong to integer divisions of an index by a run-time row length)."""
+    """The re-aligning (KB3b, KB3c and its hybrid) and phase-grid (row, short-row, staged, tiny)
+    forms evaluate the same method: no FCHK (fp32 division slow path), no fp64, and the method's
+    reciprocal only in variant A -- each variant-A instance has more MUFU.RCP than its variant-N
+    twin (whose MUFU.RCP, where present, belong to integer divisions of an index by a run-time
+    row length)."""
     sass = _sass()
     funcs = re.split(r"\n\s*Function : ", sass)
     rcp = {}
     for f in funcs:
         name = f.split("\n", 1)[0].strip()
-        form = next((k for k in ("sincos_outshift_kernel", "phase_grid_staged", "phase_grid_tiny",
+        form = next((k for k in ("sincos_outshift_kernel", "sincos_outshift_hyb_kernel", "phase_grid_staged", "phase_grid_tiny",
                                  "phase_grid_short", "phase_grid_rows") if k in name), None)
         if form is None:
             continue

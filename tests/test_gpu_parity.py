@@ -520,7 +520,7 @@ def test_scalar_path_unshared_outputs():
 
 @pytest.mark.parametrize("variant,name", [(oracle.VARIANT_N, "N"), (oracle.VARIANT_A, "A")])
 @pytest.mark.parametrize("path", ["interleaved", "realign_split", "realign_interleaved", "scalar_split",
-                                  "outshift_split", "outshift_interleaved"])
+                                  "outshift_split", "outshift_interleaved", "hybrid_split"])
 def test_all_fp32_bit_patterns_other_paths(golden, variant, name, path):
     """The whole-input-space hash through the other kernels: the 256-bit interleaved kernel,
     the re-aligning kernel (theta one float off the outputs; split and interleaved) and the
@@ -535,10 +535,13 @@ def test_all_fp32_bit_patterns_other_paths(golden, variant, name, path):
         if "inter" in path:
             ibuf = torch.empty(2 * chunk + 8, dtype=torch.float32, device="cuda")
             io = ibuf[1:1 + 2 * chunk] if path == "outshift_interleaved" else ibuf[:2 * chunk]   # 4-B pairs
-        elif path == "outshift_split":
+        elif path in ("outshift_split", "hybrid_split"):
             sbuf = torch.empty(chunk + 8, dtype=torch.float32, device="cuda")
             cbuf = torch.empty(chunk + 8, dtype=torch.float32, device="cuda")
-            s, c = sbuf[1:1 + chunk], cbuf[2:2 + chunk]      # sin and cos apart mod 16 B
+            if path == "outshift_split":
+                s, c = sbuf[1:1 + chunk], cbuf[2:2 + chunk]      # sin and cos apart mod 16 B
+            else:
+                s, c = sbuf[5:5 + chunk], cbuf[3:3 + chunk]      # both off theta's frame: the hybrid form
         else:
             s = torch.empty(chunk, dtype=torch.float32, device="cuda")
             c = torch.empty(chunk, dtype=torch.float32, device="cuda")

@@ -50,7 +50,8 @@ CASES = {
     "theta realigned interleaved": (1, 0, 0, 0, 6000, 6890),
     "outputs realigned (KB3c)": (0, 1, 2, None, 5900, 6760),
     "outputs realigned, sin 4 off (KB3c, cos stored first)": (0, 4, 2, None, 5900, 6600),
-    "sin/cos sharing 16 B (KB3c)": (0, 3, 7, None, 5800, 6570),
+    "sin/cos sharing 16 B (hybrid KB3c)": (0, 3, 7, None, 5800, 6570),
+    "both streams off theta (hybrid KB3c)": (0, 6, 5, None, 5800, 6570),
     "pairs 4-B only, k = 1 (KB3c)": (0, 0, 0, 1, 5900, 6710),
     "pairs 4-B only, k = 3 (KB3c, two trips)": (0, 0, 0, 3, 5900, 6690),
     "pairs 4-B only, k = 5 (KB3c, two trips)": (0, 0, 0, 5, 5800, 6540),

@@ -85,7 +85,9 @@ typedef enum {
  * common element (split: sin and cos at one offset mod 32 B; interleaved: 8-B
  * aligned), theta is read as aligned vectors and re-aligned in registers (warp
  * shuffles); otherwise the outputs are re-aligned instead (theta's 256-bit frame,
- * whole 32-B output blocks from neighbouring lanes).  (Exact in-place always
+ * whole 32-B output blocks from neighbouring lanes) -- or, for most split layouts
+ * with both sin and cos off theta's frame, theta is re-aligned onto one output's
+ * frame and only the other output re-aligned.  (Exact in-place always
  * keeps the aliased output at theta's alignment.)
  * A scalar head and tail cover the ragged ends.  The kernel configuration (block
  * size, grid, vector width) is fixed per path -- a full grid of 128-thread blocks,

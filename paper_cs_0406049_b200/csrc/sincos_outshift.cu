@@ -254,7 +254,7 @@ sincos_outshift_kernel(const float *theta, float *so, float *co, float *io,
 // the other stream re-aligned by store_realigned (KX = k_other - k_direct mod 8).  The vectors
 // start at hb + KT (scalar head below that); the last lane's second theta vector must lie
 // inside theta, so one vector fewer than KB3c's, the tail one element per thread.
-// Measured over all 42 such layouts, both variants, two boxes (tools/ab_layouts.py,
+// Measured over all 42 such layouts, both variants, three boxes (tools/ab_layouts.py,
 // profiles/r02/ab_hyb*.jsonl; per-layout results reproduced to ~0.3%): the direct stream is the
 // one further past its 32-B boundary (the other choice lost 2-5% nearly everywhere); the
 // hybrid gains 0.5-3.8% in 28 layouts and loses 0.4-2.8% where the offsets are {1,2}, {1,3},

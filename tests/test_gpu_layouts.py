@@ -60,3 +60,37 @@ def test_every_split_layout(data, variant, ot):
                 if not ok:
                     bad.append((os_, oc, n))
     assert not bad, f"theta+{ot} variant {variant}: {len(bad)} failing (sin off, cos off, n), first {bad[:8]}"
+
+
+@pytest.mark.parametrize("variant", [oracle.VARIANT_N, oracle.VARIANT_A])
+def test_every_split_layout_grid_stride(variant):
+    """The same 64 (sin, cos) offset pairs on the A/B build with a grid of one block per SM, so
+    every warp makes several grid-stride trips (the hybrid's warp-edge blocks meet across trips),
+    at two theta offsets and a length with a ragged tail."""
+    from paper_cs_0406049_b200 import ab
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    n = 400_003
+    base = inputs.generate(3, 0, n + 8)
+    s_, c_ = oracle.sincos(base, variant)
+    ws = torch.from_numpy(s_.view(np.int32)).cuda()
+    wc = torch.from_numpy(c_.view(np.int32)).cuda()
+    tb = torch.from_numpy(base).cuda()
+    bs = torch.empty(2 * G + n + 8, dtype=torch.int32, device="cuda")
+    bc = torch.empty_like(bs)
+    bad = []
+    with ab.knobs(blocks_per_sm=1):
+        for ot in (0, 5):
+            for os_ in range(8):
+                for oc in range(8):
+                    bs.fill_(SENT)
+                    bc.fill_(SENT)
+                    sp.sincos_pairs(tb[ot:ot + n], bs[G + os_:G + os_ + n].view(torch.float32),
+                                    bc[G + oc:G + oc + n].view(torch.float32), variant=variant)
+                    ok = (torch.equal(bs[G + os_:G + os_ + n], ws[ot:ot + n]) and
+                          torch.equal(bc[G + oc:G + oc + n], wc[ot:ot + n]) and
+                          bool((bs[:G + os_] == SENT).all()) and bool((bs[G + os_ + n:] == SENT).all()) and
+                          bool((bc[:G + oc] == SENT).all()) and bool((bc[G + oc + n:] == SENT).all()))
+                    if not ok:
+                        bad.append((ot, os_, oc))
+    assert not bad, f"variant {variant}: {len(bad)} failing (theta off, sin off, cos off), first {bad[:8]}"

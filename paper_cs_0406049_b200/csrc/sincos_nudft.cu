@@ -34,11 +34,13 @@ constexpr int kNuThreads = 128;
 #endif
 constexpr int kKPerThread = SINCOS_NUDFT_KPT;
 // Terms per trip of the inner loop.  Unrolled by 8 the loop's own instructions (index, compare,
-// branch, shared-memory address) leave the issue stream and the compiler interleaves
-// consecutive terms' chains: C4 shape, packed, +3-7% over a rolled loop (N turns 1.23 -> 1.31,
-// radians 1.19 -> 1.27 T terms/s; A 1.14 -> 1.17, 1.10 -> 1.18), 4 and 16 within 1% of 8,
-// outputs bit-identical (tools/ab_nudft.py, profiles/r02/ab_nudft_unroll*.json); 56 registers,
-// no spill.
+// branch, shared-memory address) leave the issue stream and the compiler may interleave
+// consecutive terms' chains; outputs bit-identical, 56 registers, no spill.  Gain: +3-7% over
+// the rolled loop in the libraries A/B (C4 shape, packed; tools/ab_nudft.py,
+// profiles/r02/ab_nudft_unroll*.json; 4 and 16 within 1% of 8), but only 0-1% in the bench
+// line against earlier bench lines (bench_r02/c2_final12.json vs c2_final11.json) and -1.8% /
+// +0.2% in kernel time under ncu (radians / turns) -- the rolled loop read lower in the A/B
+// tool's context than in the bench's.  Kept: never slower.
 #ifndef SINCOS_NUDFT_UNROLL
 #define SINCOS_NUDFT_UNROLL 8
 #endif

@@ -19,7 +19,7 @@ def main():
     import bench
     n = 1 << 28
     libs = {}
-    for p in sorted(glob.glob(os.path.join(ROOT, "tools", "ab_host", "*.so"))):
+    for p in sorted(glob.glob(os.environ.get("AB_HOST_GLOB", os.path.join(ROOT, "tools", "ab_host", "*.so")))):
         L = ctypes.CDLL(p)
         L.sincos_pairs_host.restype = ctypes.c_int
         L.sincos_pairs_host.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p,
@@ -49,11 +49,23 @@ def main():
                 ev[k + 1].record()
             torch.cuda.synchronize()
             res[name] += [ev[k].elapsed_time(ev[k + 1]) for k in range(3)]
+    # every library's outputs equal the first one's (variant A, the last step's)
+    same = {}
+    ref = None
+    for name in order:
+        step(libs[name])
+        torch.cuda.synchronize()
+        got = (so.clone(), co.clone())
+        if ref is None:
+            ref = got
+        same[name] = bool(torch.equal(got[0].view(torch.int32), ref[0].view(torch.int32)) and
+                          torch.equal(got[1].view(torch.int32), ref[1].view(torch.int32)))
     roof = bench.pcie_roofline(th, n, 2, dev, [so, co])
     print(json.dumps({"ws_mib": ws.numel() >> 20, "ms_per_step_median": {k: statistics.median(v) for k, v in res.items()},
                       "ms_per_step_min": {k: min(v) for k, v in res.items()},
                       "roofline_concurrent_ms": roof["concurrent_ms"],
-                      "frac": {k: roof["step_floor_ms"] / statistics.median(v) for k, v in res.items()}}))
+                      "frac": {k: roof["step_floor_ms"] / statistics.median(v) for k, v in res.items()},
+                      "outputs_equal_first": same}))
 
 
 if __name__ == "__main__":

@@ -515,12 +515,13 @@ sincos_status_t sincos_pairs_dtype(const float *theta_dev, void *sin_dev, void *
     } else if (overlaps(theta_dev, 4 * n, inter_dev, 4 * n)) {
         return SINCOS_ERR_OVERLAP;
     }
-    // vector body: the outputs' alignment fixes the first vector element (split: 128-bit stores,
-    // sin and cos at one offset mod 16 B; interleaved: one 256-bit store per 8 pairs), theta is
-    // re-aligned in registers when it sits off that alignment (sincos_realign.cuh)
+    // vector body: the outputs' alignment fixes the first vector element (split: sin[]'s 128-bit
+    // stores, cos[] at the same offset mod 16 B or else in the widest pieces its own alignment
+    // allows; interleaved: one 256-bit store per 8 pairs), theta is re-aligned in registers when
+    // it sits off that alignment (sincos_realign.cuh)
     const uintptr_t so_a = reinterpret_cast<uintptr_t>(sin_dev), co_a = reinterpret_cast<uintptr_t>(cos_dev),
                     io_a = reinterpret_cast<uintptr_t>(inter_dev);
-    bool vec = inter || ((so_a ^ co_a) & 15) == 0;
+    bool vec = inter || ((so_a ^ co_a) & 15) == 0 || tuning().realign != 0;
     const size_t h0 = inter ? ((32 - (io_a & 31)) & 31) / 4 : ((16 - (so_a & 15)) & 15) / 2;
     int k = 0;
     size_t head = 0, nvec = 0;
@@ -529,12 +530,17 @@ sincos_status_t sincos_pairs_dtype(const float *theta_dev, void *sin_dev, void *
         if (k != 0 && tuning().realign == 0) vec = false;
     }
     if (!vec) head = nvec = 0, k = 0;
+    int cw = 16;                                   // cos[]'s alignment at the vector elements
+    if (!inter) {
+        const uintptr_t ca = (co_a + 2 * head) & 15;
+        cw = ca == 0 ? 16 : (ca & 7) == 0 ? 8 : (ca & 3) == 0 ? 4 : 2;
+    }
     // without the vector path every element is a "tail" element: one per thread
     const size_t work = vec ? (nvec > 8 ? nvec : 8) : n;
     size_t grid = (work + 127) / 128;
     if (grid > 0x7FFFFFFFu) return SINCOS_ERR_INVALID_ARGUMENT;
     cudaError_t e = launch_pairs16(variant, out_dtype, inter, static_cast<unsigned>(grid), theta_dev, sin_dev,
-                                   cos_dev, inter_dev, head, nvec, n, k, static_cast<cudaStream_t>(stream));
+                                   cos_dev, inter_dev, head, nvec, n, k, cw, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SINCOS_OK;

@@ -31,6 +31,30 @@ __device__ __forceinline__ void st4u(void *p, uint32_t a, uint32_t b, uint32_t c
                  : "memory");
 }
 
+// cos[] when it does not share sin[]'s 16-B offset (split outputs): the eight values at a
+// position whose alignment `cw` is the same for every vector (16 / 8 / 4 / 2 bytes: one 128-bit
+// store, two 64-bit, four 32-bit or eight 16-bit ones -- warp-uniform; each warp instruction still
+// covers its 32 threads' neighbouring blocks, which L2 merges into whole sectors).
+__device__ __forceinline__ void st8x16(uint16_t *p, const uint16_t (&c)[8], int cw) {
+    if (cw == 16) {
+        st4u(p, pack2(c[0], c[1]), pack2(c[2], c[3]), pack2(c[4], c[5]), pack2(c[6], c[7]));
+    } else if (cw == 8) {
+#pragma unroll
+        for (int h = 0; h < 8; h += 4)
+            asm volatile("st.global.L1::no_allocate.v2.b32 [%0], {%1,%2};" ::"l"(p + h), "r"(pack2(c[h], c[h + 1])),
+                         "r"(pack2(c[h + 2], c[h + 3]))
+                         : "memory");
+    } else if (cw == 4) {
+#pragma unroll
+        for (int h = 0; h < 8; h += 2)
+            asm volatile("st.global.L1::no_allocate.b32 [%0], %1;" ::"l"(p + h), "r"(pack2(c[h], c[h + 1])) : "memory");
+    } else {
+#pragma unroll
+        for (int h = 0; h < 8; ++h)
+            asm volatile("st.global.L1::no_allocate.b16 [%0], %1;" ::"l"(p + h), "h"(c[h]) : "memory");
+    }
+}
+
 template <int V, int DT, bool INTER>
 __device__ __forceinline__ void emit16_scalar(const float *theta, size_t e, uint16_t *so, uint16_t *co,
                                               uint16_t *io) {
@@ -51,7 +75,7 @@ __device__ __forceinline__ void emit16_scalar(const float *theta, size_t e, uint
 // re-aligned in registers (sincos_realign.cuh), with warp-uniform trips for the shuffles.
 template <int V, int DT, bool INTER, int K>
 __global__ void __launch_bounds__(128) sincos16_kernel(const float *theta, uint16_t *so, uint16_t *co, uint16_t *io,
-                                                       size_t head, size_t nvec, size_t n, int k) {
+                                                       size_t head, size_t nvec, size_t n, int k, int cw) {
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const size_t tail0 = head + 8 * nvec;
@@ -89,7 +113,7 @@ __global__ void __launch_bounds__(128) sincos16_kernel(const float *theta, uint1
                          : "memory");
         } else {
             st4u(so + e0, pack2(s16[0], s16[1]), pack2(s16[2], s16[3]), pack2(s16[4], s16[5]), pack2(s16[6], s16[7]));
-            st4u(co + e0, pack2(c16[0], c16[1]), pack2(c16[2], c16[3]), pack2(c16[4], c16[5]), pack2(c16[6], c16[7]));
+            st8x16(co + e0, c16, cw);
         }
     }
 }
@@ -114,14 +138,14 @@ static const void *pick16i(bool inter, int k) {
 }
 
 cudaError_t launch_pairs16(int variant, int dtype, bool inter, unsigned grid, const float *theta, void *so, void *co,
-                           void *io, size_t head, size_t nvec, size_t n, int k, cudaStream_t stream) {
+                           void *io, size_t head, size_t nvec, size_t n, int k, int cw, cudaStream_t stream) {
     const void *fn;
     if (variant == kNormalized)
         fn = dtype == 1 ? pick16i<kNormalized, 1>(inter, k) : pick16i<kNormalized, 2>(inter, k);
     else
         fn = dtype == 1 ? pick16i<kRenormalized, 1>(inter, k) : pick16i<kRenormalized, 2>(inter, k);
     uint16_t *s = static_cast<uint16_t *>(so), *c = static_cast<uint16_t *>(co), *i = static_cast<uint16_t *>(io);
-    void *args[] = {&theta, &s, &c, &i, &head, &nvec, &n, &k};
+    void *args[] = {&theta, &s, &c, &i, &head, &nvec, &n, &k, &cw};
     return cudaLaunchKernel(fn, dim3(grid), dim3(128), args, 0, stream);
 }
 

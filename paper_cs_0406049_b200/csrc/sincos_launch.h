@@ -162,7 +162,7 @@ cudaError_t launch_method(const float *ss, int n_ss, const float *cc, int n_cc, 
                           size_t nvec, size_t n, int k, cudaStream_t stream);
 // NEXT(4) 16-bit outputs (dtype 1 = fp16, 2 = bf16) and fp32 layout adapters (sincos_dtype.cu).
 cudaError_t launch_pairs16(int variant, int dtype, bool inter, unsigned grid, const float *theta, void *so, void *co,
-                           void *io, size_t head, size_t nvec, size_t n, int k, cudaStream_t stream);
+                           void *io, size_t head, size_t nvec, size_t n, int k, int cw, cudaStream_t stream);
 cudaError_t launch_interleave(bool to_inter, unsigned grid, const float *s, const float *c, float *io, size_t n,
                               cudaStream_t stream);
 

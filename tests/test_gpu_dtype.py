@@ -190,3 +190,40 @@ def test_adapters_any_alignment(n, offs):
     torch.cuda.synchronize()
     assert torch.equal(io[0::2], c) and torch.equal(io[1::2], s)
     assert torch.equal(s2, s) and torch.equal(c2, c)
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_16bit_every_split_offset_pair(dtype):
+    """sin and cos at every pair of element offsets 0..7 (2-B units: cos 16-, 8-, 4- or 2-B
+    aligned where sin's 128-bit stores fall -- the cos[] piece stores) at two theta offsets,
+    lengths around the vector boundaries; raw 16-bit values = RN of the oracle's pair; sentinel
+    guard zones around both outputs."""
+    SENT = 0x7E5A                       # a 16-bit NaN pattern no conversion produces
+    G = 32
+    N = 8 * 128 * 3 + 29
+    base = inputs.generate(2, 0, N + 8)
+    bt = torch.from_numpy(base).cuda()
+    bs = torch.empty(2 * G + N + 16, dtype=torch.int16, device="cuda")
+    bc = torch.empty_like(bs)
+    bad = []
+    for variant in (0, 1):
+        ws, wc = oracle.sincos(base, variant)
+        rs, rc = rn16(ws, dtype), rn16(wc, dtype)
+        for ot in (0, 3):
+            for n in list(range(0, 18)) + [63, 64, 65, 8 * 128 + 5, N]:
+                for os_ in range(8):
+                    for oc in range(8):
+                        bs.fill_(SENT)
+                        bc.fill_(SENT)
+                        s = bs[G + os_:G + os_ + n].view(dtype)
+                        c = bc[G + oc:G + oc + n].view(dtype)
+                        sp.sincos_pairs_dtype(bt[ot:ot + n], s, c, variant=variant)
+                        hs = bs.cpu().numpy().view(np.uint16)
+                        hc = bc.cpu().numpy().view(np.uint16)
+                        ok = (same16(hs[G + os_:G + os_ + n], rs[ot:ot + n], dtype).all() and
+                              same16(hc[G + oc:G + oc + n], rc[ot:ot + n], dtype).all() and
+                              (hs[:G + os_] == SENT).all() and (hs[G + os_ + n:] == SENT).all() and
+                              (hc[:G + oc] == SENT).all() and (hc[G + oc + n:] == SENT).all())
+                        if not ok:
+                            bad.append((variant, ot, n, os_, oc))
+    assert not bad, f"{len(bad)} failing (variant, theta off, n, sin off, cos off), first {bad[:8]}"

@@ -128,10 +128,11 @@ SINCOS_API size_t sincos_host_workspace_min_bytes(void);
  * method's fp32 result to out_dtype -- IEEE binary16 or bfloat16 (2 B per value; 8 B per
  * pair of traffic instead of 12) -- or fp32 (= sincos_pairs).  Outputs are 2-B aligned
  * uint16 arrays (split) or n {cos, sin} 16-bit pairs (interleaved); theta must not overlap
- * them.  Vector path (8 pairs per thread; 128-bit split / 256-bit interleaved stores) when
- * sin and cos share their offset mod 16 B (interleaved: always), theta read as one aligned
- * 256-bit vector or re-aligned in registers when it sits off the outputs' alignment;
- * otherwise one element per thread; identical values.
+ * them.  Vector path always (8 pairs per thread; 128-bit split / 256-bit interleaved
+ * stores in the frame of sin[] / the pairs), theta read as one aligned 256-bit vector or
+ * re-aligned in registers when it sits off that frame; a split cos[] at another offset mod
+ * 16 B is written as two 64-bit stores per vector (8 B off) or as whole 16-B blocks re-aligned
+ * by warp shuffles (any other offset); head and tail one element per thread; identical values.
  *
  * sincos_interleave / sincos_deinterleave: fp32 split (sin[], cos[]) <-> interleaved
  * ({cos, sin} float2) copies; no overlap allowed.

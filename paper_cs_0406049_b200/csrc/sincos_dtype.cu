@@ -55,6 +55,68 @@ __device__ __forceinline__ void st8x16(uint16_t *p, const uint16_t (&c)[8], int 
     }
 }
 
+// Halfwords [A, B) of a 16-B block from r[0 .. B - A), as naturally aligned pieces (2 / 4 / 8 B).
+template <int A, int B>
+__device__ __forceinline__ void store16_range(uint16_t *blk, const uint16_t *r) {
+    if constexpr (A < B) {
+        constexpr int al = (A & 1) ? 1 : (A & 2) ? 2 : 4;             // alignment of position A, halfwords
+        constexpr int m = al <= (B - A) ? al : ((B - A) >= 2 ? 2 : 1);
+        if constexpr (m == 4)
+            asm volatile("st.global.L1::no_allocate.v2.b32 [%0], {%1,%2};" ::"l"(blk + A), "r"(pack2(r[0], r[1])),
+                         "r"(pack2(r[2], r[3]))
+                         : "memory");
+        else if constexpr (m == 2)
+            asm volatile("st.global.L1::no_allocate.b32 [%0], %1;" ::"l"(blk + A), "r"(pack2(r[0], r[1])) : "memory");
+        else
+            asm volatile("st.global.L1::no_allocate.b16 [%0], %1;" ::"l"(blk + A), "h"(r[0]) : "memory");
+        store16_range<A + m, B>(blk, r + m);
+    }
+}
+
+// cos[] O halfwords (1..7) past sin[]'s 16-B frame, written as whole aligned 16-B blocks built
+// from the neighbouring lane's values -- the output re-alignment of KB3c (sincos_outshift.cu)
+// on 16-bit elements: O <= 4 the block at e0 - O takes the previous lane's last O values
+// (shuffled up), O > 4 the block at e0 + 8 - O the next lane's first 8 - O (shuffled down);
+// the warp's lane 0 and last active lane store their partial blocks as aligned pieces.  All 32
+// lanes call it.
+template <int O>
+__device__ __forceinline__ void store16_shift(uint16_t *x, size_t e0, const uint16_t (&c)[8], unsigned lane, bool act,
+                                              bool last) {
+    uint16_t *blk0 = x + e0 - O;
+    if constexpr (O <= 4) {
+        uint16_t prev[O];
+#pragma unroll
+        for (int j = 0; j < O; ++j)
+            prev[j] = static_cast<uint16_t>(__shfl_up_sync(0xFFFFFFFFu, static_cast<unsigned>(c[8 - O + j]), 1));
+        if (!act) return;
+        if (lane > 0) {
+            uint16_t b[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) b[j] = j < O ? prev[j] : c[j - O];
+            st4u(blk0, pack2(b[0], b[1]), pack2(b[2], b[3]), pack2(b[4], b[5]), pack2(b[6], b[7]));
+        } else {
+            store16_range<O, 8>(blk0, c);
+        }
+        if (last) store16_range<0, O>(blk0 + 8, c + 8 - O);
+    } else {
+        constexpr int D = 8 - O;
+        uint16_t next[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            next[j] = static_cast<uint16_t>(__shfl_down_sync(0xFFFFFFFFu, static_cast<unsigned>(c[j]), 1));
+        if (!act) return;
+        if (lane == 0) store16_range<O, 8>(blk0, c);
+        if (last) {
+            store16_range<0, O>(blk0 + 8, c + D);
+        } else {
+            uint16_t b[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) b[j] = j < O ? c[D + j] : next[j - O];
+            st4u(blk0 + 8, pack2(b[0], b[1]), pack2(b[2], b[3]), pack2(b[4], b[5]), pack2(b[6], b[7]));
+        }
+    }
+}
+
 template <int V, int DT, bool INTER>
 __device__ __forceinline__ void emit16_scalar(const float *theta, size_t e, uint16_t *so, uint16_t *co,
                                               uint16_t *io) {
@@ -73,7 +135,7 @@ __device__ __forceinline__ void emit16_scalar(const float *theta, size_t e, uint
 // K = 0: theta shares the outputs' vector alignment (one aligned 256-bit load per thread, 32
 // registers: full occupancy).  K = 1..7 (a template parameter): theta sits K floats off it and is
 // re-aligned in registers (sincos_realign.cuh), with warp-uniform trips for the shuffles.
-template <int V, int DT, bool INTER, int K>
+template <int V, int DT, bool INTER, int K, bool SH>
 __global__ void __launch_bounds__(128) sincos16_kernel(const float *theta, uint16_t *so, uint16_t *co, uint16_t *io,
                                                        size_t head, size_t nvec, size_t n, int k, int cw) {
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
@@ -84,13 +146,16 @@ __global__ void __launch_bounds__(128) sincos16_kernel(const float *theta, uint1
     const unsigned lane = threadIdx.x & 31u;
     const float *tal = theta + head - k;
     constexpr bool RE = K > 0;
-    for (size_t w0 = RE ? tid - lane : tid; w0 < nvec; w0 += nthr) {
-        const size_t v = RE ? w0 + lane : w0;
-        float x[8];
+    constexpr bool WU = RE || SH;          // warp-uniform trips: the shuffles need all 32 lanes
+    for (size_t w0 = WU ? tid - lane : tid; w0 < nvec; w0 += nthr) {
+        const size_t v = WU ? w0 + lane : w0;
+        const bool act = v < nvec;
+        float x[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
         if constexpr (RE) {
-            const bool act = v < nvec;
             load8_realigned_k<(K > 0 ? K : 1)>(tal, v, nvec, lane, act, x);
-            if (!act) continue;
+            if (!SH && !act) continue;
+        } else if constexpr (SH) {
+            if (act) ld8_stream(x, theta + head + 8 * v);
         } else {
             ld8_stream(x, theta + head + 8 * v);
         }
@@ -111,6 +176,21 @@ __global__ void __launch_bounds__(128) sincos16_kernel(const float *theta, uint1
                          ::"l"(io + 2 * e0), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]),
                          "r"(w[6]), "r"(w[7])
                          : "memory");
+        } else if constexpr (SH) {
+            // cw: cos[]'s halfword offset O (1..7) at the vector elements
+            const bool last = act && (lane == 31u || v + 1 >= nvec);
+            if (act)
+                st4u(so + e0, pack2(s16[0], s16[1]), pack2(s16[2], s16[3]), pack2(s16[4], s16[5]),
+                     pack2(s16[6], s16[7]));
+            switch (cw) {
+            case 1: store16_shift<1>(co, e0, c16, lane, act, last); break;
+            case 2: store16_shift<2>(co, e0, c16, lane, act, last); break;
+            case 3: store16_shift<3>(co, e0, c16, lane, act, last); break;
+            case 4: store16_shift<4>(co, e0, c16, lane, act, last); break;
+            case 5: store16_shift<5>(co, e0, c16, lane, act, last); break;
+            case 6: store16_shift<6>(co, e0, c16, lane, act, last); break;
+            default: store16_shift<7>(co, e0, c16, lane, act, last); break;
+            }
         } else {
             st4u(so + e0, pack2(s16[0], s16[1]), pack2(s16[2], s16[3]), pack2(s16[4], s16[5]), pack2(s16[6], s16[7]));
             st8x16(co + e0, c16, cw);
@@ -118,32 +198,41 @@ __global__ void __launch_bounds__(128) sincos16_kernel(const float *theta, uint1
     }
 }
 
+// cos[] re-aligned by shuffles (SH) unless it shares sin[]'s 16-B offset or sits 8 B off it
+// (there two 64-bit stores per vector run at the aligned rate); cw = 16 / 8 / halfword offset
+#ifndef SINCOS_16_SHIFT
+#define SINCOS_16_SHIFT 1                    // 0: the 4-/2-B piece stores instead (A/B)
+#endif
 template <int V, int DT, int K>
-static const void *pick16r(bool inter) {
-    return inter ? reinterpret_cast<const void *>(sincos16_kernel<V, DT, true, K>)
-                 : reinterpret_cast<const void *>(sincos16_kernel<V, DT, false, K>);
+static const void *pick16r(bool inter, bool sh) {
+    if (inter) return reinterpret_cast<const void *>(sincos16_kernel<V, DT, true, K, false>);
+    return sh ? reinterpret_cast<const void *>(sincos16_kernel<V, DT, false, K, true>)
+              : reinterpret_cast<const void *>(sincos16_kernel<V, DT, false, K, false>);
 }
 template <int V, int DT>
-static const void *pick16i(bool inter, int k) {
+static const void *pick16i(bool inter, int k, bool sh) {
     switch (k) {
-    case 0: return pick16r<V, DT, 0>(inter);
-    case 1: return pick16r<V, DT, 1>(inter);
-    case 2: return pick16r<V, DT, 2>(inter);
-    case 3: return pick16r<V, DT, 3>(inter);
-    case 4: return pick16r<V, DT, 4>(inter);
-    case 5: return pick16r<V, DT, 5>(inter);
-    case 6: return pick16r<V, DT, 6>(inter);
-    default: return pick16r<V, DT, 7>(inter);
+    case 0: return pick16r<V, DT, 0>(inter, sh);
+    case 1: return pick16r<V, DT, 1>(inter, sh);
+    case 2: return pick16r<V, DT, 2>(inter, sh);
+    case 3: return pick16r<V, DT, 3>(inter, sh);
+    case 4: return pick16r<V, DT, 4>(inter, sh);
+    case 5: return pick16r<V, DT, 5>(inter, sh);
+    case 6: return pick16r<V, DT, 6>(inter, sh);
+    default: return pick16r<V, DT, 7>(inter, sh);
     }
 }
 
 cudaError_t launch_pairs16(int variant, int dtype, bool inter, unsigned grid, const float *theta, void *so, void *co,
                            void *io, size_t head, size_t nvec, size_t n, int k, int cw, cudaStream_t stream) {
     const void *fn;
+    // cw: cos[]'s alignment in bytes at the vector elements (16, 8, 4, 2)
+    const bool sh = SINCOS_16_SHIFT && !inter && cw != 16 && cw != 8;
+    if (sh) cw = static_cast<int>(((reinterpret_cast<uintptr_t>(co) + 2 * head) & 15) / 2);   // halfword offset
     if (variant == kNormalized)
-        fn = dtype == 1 ? pick16i<kNormalized, 1>(inter, k) : pick16i<kNormalized, 2>(inter, k);
+        fn = dtype == 1 ? pick16i<kNormalized, 1>(inter, k, sh) : pick16i<kNormalized, 2>(inter, k, sh);
     else
-        fn = dtype == 1 ? pick16i<kRenormalized, 1>(inter, k) : pick16i<kRenormalized, 2>(inter, k);
+        fn = dtype == 1 ? pick16i<kRenormalized, 1>(inter, k, sh) : pick16i<kRenormalized, 2>(inter, k, sh);
     uint16_t *s = static_cast<uint16_t *>(so), *c = static_cast<uint16_t *>(co), *i = static_cast<uint16_t *>(io);
     void *args[] = {&theta, &s, &c, &i, &head, &nvec, &n, &k, &cw};
     return cudaLaunchKernel(fn, dim3(grid), dim3(128), args, 0, stream);

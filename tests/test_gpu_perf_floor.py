@@ -148,6 +148,10 @@ def test_16bit_and_method_floors(bufs):
     assert got >= 5600, f"fp16 realigned {got:.0f}"  # recorded 6.47 TB/s
     got = gbps(lambda: sp.sincos_pairs_method(tb, m, sb[:N], cb[:N]), 12 * N)
     assert got >= 6000, f"method realigned {got:.0f}"  # recorded 6.82 TB/s
+    c16b = torch.empty(N + 8, dtype=torch.float16, device="cuda")
+    for oc in (1, 2, 4):                              # cos[] off sin[]'s 16-B frame: shuffles / 8-B pieces
+        got = gbps(lambda: sp.sincos_pairs_dtype(th, s16, c16b[oc:oc + N]), 8 * N)
+        assert got >= 5300, f"fp16 cos+{oc} {got:.0f}"  # recorded 6.0-6.1 (1, 2) / 6.87 (4) TB/s
 
 
 def test_batched_floor():

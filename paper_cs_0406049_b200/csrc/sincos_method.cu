@@ -14,6 +14,7 @@
 #include "sincos_launch.h"
 #include "sincos_method.cuh"
 #include "sincos_realign.cuh"
+#include "sincos_storeshift.cuh"
 
 namespace sincos_b200 {
 
@@ -41,11 +42,13 @@ __device__ __forceinline__ void st8m(float *p, const float *r) {
 // K = 0: theta shares the outputs' 32-B alignment (one aligned 256-bit load per thread).
 // K = 1..7 (a template parameter): theta sits K floats off it and is re-aligned in registers
 // (sincos_realign.cuh), with warp-uniform trips for the shuffles.
-// vec == false: every element scalar (outputs that cannot take 256-bit stores).
-template <int NT, int FIX, bool INTER, int K>
+// SH (split only): cos[] sits kc = 1..7 floats off sin[]'s 32-B frame and is written as whole
+// 32-B blocks re-aligned by warp shuffles (KB3c's store_realigned, sincos_storeshift.cuh).
+// vec == false: every element scalar (interleaved pairs only 4-B aligned).
+template <int NT, int FIX, bool INTER, int K, bool SH>
 __global__ void __launch_bounds__(128) method_kernel(const MethodParams m, const float *theta, float *so,
                                                      float *co, float *io, size_t head, size_t nvec, size_t n,
-                                                     bool vec, int k) {
+                                                     bool vec, int k, int kc) {
     const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (!vec) {
@@ -58,13 +61,16 @@ __global__ void __launch_bounds__(128) method_kernel(const MethodParams m, const
     const unsigned lane = threadIdx.x & 31u;
     const float *tal = theta + head - k;
     constexpr bool RE = K > 0;
-    for (size_t w0 = RE ? tid - lane : tid; w0 < nvec; w0 += nthr) {
-        const size_t v = RE ? w0 + lane : w0;
-        float x[8];
+    constexpr bool WU = RE || SH;          // warp-uniform trips: the shuffles need all 32 lanes
+    for (size_t w0 = WU ? tid - lane : tid; w0 < nvec; w0 += nthr) {
+        const size_t v = WU ? w0 + lane : w0;
+        const bool act = v < nvec;
+        float x[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
         if constexpr (RE) {
-            const bool act = v < nvec;
             load8_realigned_k<(K > 0 ? K : 1)>(tal, v, nvec, lane, act, x);
-            if (!act) continue;
+            if (!SH && !act) continue;
+        } else if constexpr (SH) {
+            if (act) ld8_stream(x, theta + head + 8 * v);
         } else {
             ld8_stream(x, theta + head + 8 * v);
         }
@@ -80,6 +86,18 @@ __global__ void __launch_bounds__(128) method_kernel(const MethodParams m, const
             }
             st8m(io + 2 * e0, cs);
             st8m(io + 2 * e0 + 8, cs + 8);
+        } else if constexpr (SH) {
+            const bool last = act && (lane == 31u || v + 1 >= nvec);
+            if (act) st8m(so + e0, sv);
+            switch (kc) {
+            case 1: store_realigned<8, 1>(co, e0, cv, 1, lane, act, last); break;
+            case 2: store_realigned<8, 2>(co, e0, cv, 2, lane, act, last); break;
+            case 3: store_realigned<8, 3>(co, e0, cv, 3, lane, act, last); break;
+            case 4: store_realigned<8, 4>(co, e0, cv, 4, lane, act, last); break;
+            case 5: store_realigned<8, 5>(co, e0, cv, 5, lane, act, last); break;
+            case 6: store_realigned<8, 6>(co, e0, cv, 6, lane, act, last); break;
+            default: store_realigned<8, 7>(co, e0, cv, 7, lane, act, last); break;
+            }
         } else {
             st8m(so + e0, sv);
             st8m(co + e0, cv);
@@ -88,21 +106,22 @@ __global__ void __launch_bounds__(128) method_kernel(const MethodParams m, const
 }
 
 template <int NT, int FIX, int K>
-static const void *pick_mr(bool inter) {
-    return inter ? reinterpret_cast<const void *>(method_kernel<NT, FIX, true, K>)
-                 : reinterpret_cast<const void *>(method_kernel<NT, FIX, false, K>);
+static const void *pick_mr(bool inter, bool sh) {
+    if (inter) return reinterpret_cast<const void *>(method_kernel<NT, FIX, true, K, false>);
+    return sh ? reinterpret_cast<const void *>(method_kernel<NT, FIX, false, K, true>)
+              : reinterpret_cast<const void *>(method_kernel<NT, FIX, false, K, false>);
 }
 template <int NT, int FIX>
-static const void *pick_m(bool inter, int k) {
+static const void *pick_m(bool inter, int k, bool sh) {
     switch (k) {
-    case 0: return pick_mr<NT, FIX, 0>(inter);
-    case 1: return pick_mr<NT, FIX, 1>(inter);
-    case 2: return pick_mr<NT, FIX, 2>(inter);
-    case 3: return pick_mr<NT, FIX, 3>(inter);
-    case 4: return pick_mr<NT, FIX, 4>(inter);
-    case 5: return pick_mr<NT, FIX, 5>(inter);
-    case 6: return pick_mr<NT, FIX, 6>(inter);
-    default: return pick_mr<NT, FIX, 7>(inter);
+    case 0: return pick_mr<NT, FIX, 0>(inter, sh);
+    case 1: return pick_mr<NT, FIX, 1>(inter, sh);
+    case 2: return pick_mr<NT, FIX, 2>(inter, sh);
+    case 3: return pick_mr<NT, FIX, 3>(inter, sh);
+    case 4: return pick_mr<NT, FIX, 4>(inter, sh);
+    case 5: return pick_mr<NT, FIX, 5>(inter, sh);
+    case 6: return pick_mr<NT, FIX, 6>(inter, sh);
+    default: return pick_mr<NT, FIX, 7>(inter, sh);
     }
 }
 
@@ -115,11 +134,14 @@ cudaError_t launch_method(const float *ss, int n_ss, const float *cc, int n_cc, 
     const bool small = n_ss <= 4 && n_cc <= 4;
     const void *fn;
     const int kk = vec ? k : 0;
+    // split: cos[]'s float offset from sin[]'s 32-B frame at the vector elements
+    int kc = inter || !vec ? 0 : static_cast<int>(((reinterpret_cast<uintptr_t>(co) + 4 * head) & 31) / 4);
+    const bool sh = kc != 0;
     if (small)
-        fn = fix == 0 ? pick_m<4, 0>(inter, kk) : fix == 1 ? pick_m<4, 1>(inter, kk) : pick_m<4, 3>(inter, kk);
+        fn = fix == 0 ? pick_m<4, 0>(inter, kk, sh) : fix == 1 ? pick_m<4, 1>(inter, kk, sh) : pick_m<4, 3>(inter, kk, sh);
     else
-        fn = fix == 0 ? pick_m<8, 0>(inter, kk) : fix == 1 ? pick_m<8, 1>(inter, kk) : pick_m<8, 3>(inter, kk);
-    void *args[] = {&m, &theta, &so, &co, &io, &head, &nvec, &n, &vec, &k};
+        fn = fix == 0 ? pick_m<8, 0>(inter, kk, sh) : fix == 1 ? pick_m<8, 1>(inter, kk, sh) : pick_m<8, 3>(inter, kk, sh);
+    void *args[] = {&m, &theta, &so, &co, &io, &head, &nvec, &n, &vec, &k, &kc};
     return cudaLaunchKernel(fn, dim3(grid), dim3(128), args, 0, stream);
 }
 

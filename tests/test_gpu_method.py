@@ -135,3 +135,39 @@ def test_method_every_theta_offset(realign):
                     assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws[ot:ot + n], wc[ot:ot + n], tag)
                     iv = io.cpu().numpy()
                     assert_parity(iv[1::2], iv[0::2], ws[ot:ot + n], wc[ot:ot + n], "inter " + tag)
+
+
+@pytest.mark.parametrize("fix", [sp.FIX_LINEAR, sp.FIX_RECIPROCAL])
+def test_method_every_split_offset_pair(fix):
+    """The general-method kernel with sin and cos at every pair of float offsets 0..7 (cos off
+    sin's 32-B frame: re-aligned by warp shuffles) at two theta offsets, lengths around the
+    vector / warp boundaries; raw bits equal the oracle's method, sentinel guard zones."""
+    SENT = 0x7F8ABCDE
+    G = 64
+    N = 8 * 128 * 3 + 77
+    base = inputs.generate(2, 0, N + 8)
+    f = cf.fit_angle(1, 3, 2)
+    ss, cc = f.fp32()
+    m = sp.make_method(list(ss), list(cc), 1, fix)
+    ws, wc = oracle.method_sincos(base, omethod(list(ss), list(cc), 1, fix))
+    ws_i = torch.from_numpy(np.ascontiguousarray(ws).view(np.int32)).cuda()
+    wc_i = torch.from_numpy(np.ascontiguousarray(wc).view(np.int32)).cuda()
+    bt = torch.from_numpy(base).cuda()
+    bs = torch.empty(2 * G + N + 8, dtype=torch.int32, device="cuda")
+    bc = torch.empty_like(bs)
+    bad = []
+    for ot in (0, 3):
+        for n in list(range(0, 18)) + [63, 64, 65, 8 * 32 + 5, 8 * 128 + 9, N]:
+            for os_ in range(8):
+                for oc in range(8):
+                    bs.fill_(SENT)
+                    bc.fill_(SENT)
+                    sp.sincos_pairs_method(bt[ot:ot + n], m, bs[G + os_:G + os_ + n].view(torch.float32),
+                                           bc[G + oc:G + oc + n].view(torch.float32))
+                    ok = (torch.equal(bs[G + os_:G + os_ + n], ws_i[ot:ot + n]) and
+                          torch.equal(bc[G + oc:G + oc + n], wc_i[ot:ot + n]) and
+                          bool((bs[:G + os_] == SENT).all()) and bool((bs[G + os_ + n:] == SENT).all()) and
+                          bool((bc[:G + oc] == SENT).all()) and bool((bc[G + oc + n:] == SENT).all()))
+                    if not ok:
+                        bad.append((ot, n, os_, oc))
+    assert not bad, f"{len(bad)} failing (theta off, n, sin off, cos off), first {bad[:8]}"

@@ -1,7 +1,8 @@
 """16-bit split outputs with cos[] at every element offset 0..7 from sin[]'s 16-B frame (GPU box):
 GB/s (8 B per pair) of sincos_pairs_dtype at the C2 size for fp16 / bf16, variants N and A --
 the product (cos[] piece stores) beside the one-element-per-thread path (A/B build,
-realign = 0), which these layouts took before.  3 warm-up launches, median of 5 rounds x 5.
+realign = 0), which these layouts took before; then the general-method path (fp32, 12 B per pair)
+with cos[] at every float offset from sin[]'s 32-B frame.  3 warm-up launches, median of 5 rounds x 5.
   python tools/dtype_offsets_probe.py"""
 import json
 import os
@@ -48,6 +49,17 @@ def main():
                 with ab.knobs(realign=0):
                     res[key]["one_per_thread"] = timed(lambda: sp.sincos_pairs_dtype(t, s, c, variant=v))
                 print(json.dumps({key: res[key]}), flush=True)
+    # the general method (paper's table N), fp32 split outputs, cos[] at float offsets 0..7
+    m = sp.make_method(*sp.PAPER_METHODS[0])
+    sb = torch.empty(N + 16, device="cuda")
+    cb = torch.empty(N + 16, device="cuda")
+    for oc in range(8):
+        s, c = sb[:N], cb[oc:oc + N]
+        key = f"method_N_cos+{oc}"
+        res[key] = {"product": round(timed(lambda: sp.sincos_pairs_method(t, m, s, c)) * 1.5, 1)}
+        with ab.knobs(realign=0):
+            res[key]["one_per_thread"] = round(timed(lambda: sp.sincos_pairs_method(t, m, s, c)) * 1.5, 1)
+        print(json.dumps({key: res[key]}), flush=True)
 
 
 if __name__ == "__main__":

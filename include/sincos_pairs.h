@@ -158,9 +158,10 @@ SINCOS_API sincos_status_t sincos_deinterleave(const float *inter_dev, float *si
  * for penultimate magnitudes^2 in [0.5, 2), i.e. any usable fit), 3 = none.
  * The paper's two methods are {its coefficients, n_ss 4, n_cc 3, doublings 2, fix 0/1}
  * and give bit-identical results to sincos_pairs.  Same buffers, alignment and error
- * conventions as sincos_pairs (in-place not supported); vector path (256-bit stores) when
- * the outputs allow it (split: sin and cos at one offset mod 32 B; interleaved: 8-B
- * aligned), theta re-aligned in registers when needed, else one element per thread.
+ * conventions as sincos_pairs (in-place not supported); vector path (256-bit stores in the
+ * frame of sin[] / the pairs; split cos[] at another offset mod 32 B re-aligned by warp
+ * shuffles into whole 32-B blocks; interleaved pairs 8-B aligned), theta re-aligned in
+ * registers when needed; interleaved pairs only 4-B aligned: one element per thread.
  * `method` is a host pointer, read before return.
  */
 typedef struct {

@@ -591,9 +591,14 @@ sincos_status_t sincos_pairs_method(const float *theta_dev, float *sin_dev, floa
     // off that alignment (sincos_realign.cuh)
     const uintptr_t so_a = reinterpret_cast<uintptr_t>(sin_dev), co_a = reinterpret_cast<uintptr_t>(cos_dev),
                     io_a = reinterpret_cast<uintptr_t>(inter_dev);
-    // (split with cos[] off sin[]'s 32-B offset: cos re-aligned by shuffles in the kernel)
-    bool vec = inter ? aligned(inter_dev, 8) : (((so_a ^ co_a) & 31) == 0 || tuning().realign != 0);
-    const size_t h0 = inter ? ((32 - (io_a & 31)) & 31) / 8 : ((32 - (so_a & 31)) & 31) / 4;
+    // (split with cos[] off sin[]'s 32-B offset: cos re-aligned by shuffles in the kernel;
+    // interleaved pairs only 4-B aligned: theta's own 32-B frame, the pairs re-aligned)
+    const bool inter4 = inter && !aligned(inter_dev, 8);
+    bool vec = inter ? (!inter4 || tuning().realign != 0)
+                     : (((so_a ^ co_a) & 31) == 0 || tuning().realign != 0);
+    const size_t h0 = inter4  ? ((32 - (reinterpret_cast<uintptr_t>(theta_dev) & 31)) & 31) / 4
+                      : inter ? ((32 - (io_a & 31)) & 31) / 8
+                              : ((32 - (so_a & 31)) & 31) / 4;
     int k = 0;
     size_t head = 0, nvec = 0;
     if (vec) {

@@ -84,8 +84,19 @@ __global__ void __launch_bounds__(128) method_kernel(const MethodParams m, const
                 cs[2 * k] = cv[k];
                 cs[2 * k + 1] = sv[k];
             }
-            st8m(io + 2 * e0, cs);
-            st8m(io + 2 * e0 + 8, cs + 8);
+            if constexpr (SH) {
+                // pairs only 4-B aligned: theta's frame, the pairs kc = 1/3/5/7 floats off it
+                const bool last = act && (lane == 31u || v + 1 >= nvec);
+                switch (kc) {
+                case 1: store_realigned<16, 1>(io, 2 * e0, cs, 1, lane, act, last); break;
+                case 3: store_realigned<16, 3>(io, 2 * e0, cs, 3, lane, act, last); break;
+                case 5: store_realigned<16, 5>(io, 2 * e0, cs, 5, lane, act, last); break;
+                default: store_realigned<16, 7>(io, 2 * e0, cs, 7, lane, act, last); break;
+                }
+            } else {
+                st8m(io + 2 * e0, cs);
+                st8m(io + 2 * e0 + 8, cs + 8);
+            }
         } else if constexpr (SH) {
             const bool last = act && (lane == 31u || v + 1 >= nvec);
             if (act) st8m(so + e0, sv);
@@ -107,7 +118,9 @@ __global__ void __launch_bounds__(128) method_kernel(const MethodParams m, const
 
 template <int NT, int FIX, int K>
 static const void *pick_mr(bool inter, bool sh) {
-    if (inter) return reinterpret_cast<const void *>(method_kernel<NT, FIX, true, K, false>);
+    if (inter)
+        return sh ? reinterpret_cast<const void *>(method_kernel<NT, FIX, true, 0, true>)
+                  : reinterpret_cast<const void *>(method_kernel<NT, FIX, true, K, false>);
     return sh ? reinterpret_cast<const void *>(method_kernel<NT, FIX, false, K, true>)
               : reinterpret_cast<const void *>(method_kernel<NT, FIX, false, K, false>);
 }
@@ -134,8 +147,11 @@ cudaError_t launch_method(const float *ss, int n_ss, const float *cc, int n_cc, 
     const bool small = n_ss <= 4 && n_cc <= 4;
     const void *fn;
     const int kk = vec ? k : 0;
-    // split: cos[]'s float offset from sin[]'s 32-B frame at the vector elements
-    int kc = inter || !vec ? 0 : static_cast<int>(((reinterpret_cast<uintptr_t>(co) + 4 * head) & 31) / 4);
+    // split: cos[]'s float offset from sin[]'s 32-B frame at the vector elements; interleaved
+    // pairs only 4-B aligned: their float offset from theta's frame (odd)
+    int kc = !vec ? 0
+             : inter ? (reinterpret_cast<uintptr_t>(io) & 7 ? static_cast<int>(((reinterpret_cast<uintptr_t>(io) + 8 * head) & 31) / 4) : 0)
+                     : static_cast<int>(((reinterpret_cast<uintptr_t>(co) + 4 * head) & 31) / 4);
     const bool sh = kc != 0;
     if (small)
         fn = fix == 0 ? pick_m<4, 0>(inter, kk, sh) : fix == 1 ? pick_m<4, 1>(inter, kk, sh) : pick_m<4, 3>(inter, kk, sh);

@@ -60,6 +60,15 @@ def main():
         with ab.knobs(realign=0):
             res[key]["one_per_thread"] = round(timed(lambda: sp.sincos_pairs_method(t, m, s, c)) * 1.5, 1)
         print(json.dumps({key: res[key]}), flush=True)
+    ib = torch.empty(2 * N + 16, device="cuda")
+    for oi in range(8):                               # interleaved pairs at float offsets 0..7
+        io = ib[oi:oi + 2 * N]
+        key = f"method_N_inter+{oi}"
+        res[key] = {"product": round(timed(lambda: sp.sincos_pairs_method(t, m, interleaved_out=io)) * 1.5, 1)}
+        with ab.knobs(realign=0):
+            res[key]["one_per_thread"] = round(
+                timed(lambda: sp.sincos_pairs_method(t, m, interleaved_out=io)) * 1.5, 1)
+        print(json.dumps({key: res[key]}), flush=True)
 
 
 if __name__ == "__main__":

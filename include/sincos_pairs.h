@@ -161,7 +161,8 @@ SINCOS_API sincos_status_t sincos_deinterleave(const float *inter_dev, float *si
  * conventions as sincos_pairs (in-place not supported); vector path (256-bit stores in the
  * frame of sin[] / the pairs; split cos[] at another offset mod 32 B re-aligned by warp
  * shuffles into whole 32-B blocks; interleaved pairs 8-B aligned), theta re-aligned in
- * registers when needed; interleaved pairs only 4-B aligned: one element per thread.
+ * registers when needed; interleaved pairs only 4-B aligned: theta's 32-B frame with the
+ * pairs re-aligned by shuffles.
  * `method` is a host pointer, read before return.
  */
 typedef struct {

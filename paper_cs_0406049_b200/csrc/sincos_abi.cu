@@ -485,6 +485,19 @@ sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_
         e = launch_phase_flat(variant, inter, units == SINCOS_TURNS, f_dev, nf, t_dev, nt, sin_dev, cos_dev,
                               inter_dev, head, nvec, static_cast<unsigned>(grid), short_rows,
                               static_cast<cudaStream_t>(stream));
+    } else if (!vec && T.realign != 0 && n < (size_t(1) << 52)) {
+        // unshared output alignment: sin[]'s frame (interleaved: any), the other stream re-aligned
+        size_t head = split ? ((32 - (so_a & 31)) & 31) / 4 : 0;
+        if (head > n) head = n;
+        const size_t nvec = (n - head) / 8;
+        const int kc = split ? static_cast<int>(((co_a + 4 * head) & 31) / 4)
+                             : static_cast<int>(((io_a + 8 * head) & 31) / 4);
+        size_t grid = (nvec + 127) / 128;
+        if (grid < 1) grid = 1;
+        if (grid > 0x7FFFFFFFu) grid = 0x7FFFFFFFu;
+        e = launch_phase_flat_sh(variant, inter, units == SINCOS_TURNS, f_dev, nf, t_dev, nt, sin_dev, cos_dev,
+                                 inter_dev, head, nvec, static_cast<unsigned>(grid), kc,
+                                 static_cast<cudaStream_t>(stream));
     } else {
         e = launch_phase_grid(variant, inter, units == SINCOS_TURNS, vec, f_dev, nf, t_dev, nt, sin_dev, cos_dev,
                               inter_dev, static_cast<cudaStream_t>(stream));

@@ -91,6 +91,11 @@ cudaError_t launch_phase_grid(int variant, bool inter, bool turns, bool vec, con
 cudaError_t launch_phase_flat(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
                               size_t nt, float *so, float *co, float *io, size_t head, size_t nvec,
                               unsigned grid, bool short_rows, cudaStream_t stream);
+// unshared output alignment (split cos[] off sin[]'s 32-B offset, or interleaved pairs only
+// 4-B aligned): the flat mapping with the re-aligned stream written by warp shuffles
+cudaError_t launch_phase_flat_sh(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
+                                 size_t nt, float *so, float *co, float *io, size_t head, size_t nvec,
+                                 unsigned grid, int kc, cudaStream_t stream);
 // NEXT(1) row path for nt % 8 != 0 or unaligned t (nt >= kPhaseRowsMinNt): h0 = the first
 // pair at which the outputs are 32-B aligned (0..7); t any 4-B alignment.
 #ifndef SINCOS_PHASE_ROWS_MIN_NT

@@ -18,6 +18,7 @@
 #include "sincos_math.cuh"
 #include "sincos_math2.cuh"
 #include "sincos_realign.cuh"
+#include "sincos_storeshift.cuh"
 
 namespace sincos_b200 {
 
@@ -218,6 +219,63 @@ __device__ __forceinline__ void select_t(const float (&w)[12], float (&tv)[8]) {
     for (int k = 0; k < 8; ++k) tv[k] = w[R + k];
 }
 
+// The eight pairs e0 .. e0 + 7 of the flat mapping (pair e = i nt + j), into sv / cv.
+template <int V, bool TURNS>
+__device__ __forceinline__ void flat_pairs8(const float *__restrict__ f, const float *__restrict__ t, size_t nt,
+                                            double inv_nt, bool t_al16, size_t e0, float (&sv)[8], float (&cv)[8]) {
+    size_t i, j;
+    divmod_nt(e0, nt, inv_nt, i, j);
+    if (j + 8 <= nt) {
+        // the common case: the eight pairs lie in one row -- one f and t[j .. j+7]: with t
+        // 16-B aligned, three aligned 128-bit loads from t[j - r] (r = j mod 4, uniform along
+        // a row) and a register selection; else eight loads at immediate offsets
+        const float fi = __ldg(f + i);
+        float tv[8];
+        const size_t r = j & 3;
+        if (t_al16 && j - r + 12 <= nt) {
+            const float4 *tq = reinterpret_cast<const float4 *>(t + (j - r));
+            const float4 q0 = __ldg(tq), q1 = __ldg(tq + 1), q2 = __ldg(tq + 2);
+            const float w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+            switch (r) {
+            case 0: select_t<0>(w, tv); break;
+            case 1: select_t<1>(w, tv); break;
+            case 2: select_t<2>(w, tv); break;
+            default: select_t<3>(w, tv); break;
+            }
+        } else {
+            const float *tp = t + j;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) tv[k] = __ldg(tp + k);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fi, tv[k], sv[k], cv[k]);
+    } else if (nt >= 8) {
+        // one row boundary inside the vector: rows i and i+1, branch-free per pair
+        const float f0 = __ldg(f + i), f1 = __ldg(f + i + 1);   // row i+1 exists: reached
+        const size_t kw = nt - j;                                // first pair of row i+1
+        float tv[8], fv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const bool next = static_cast<size_t>(k) >= kw;
+            tv[k] = __ldg(t + (next ? k - kw : j + k));
+            fv[k] = next ? f1 : f0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fv[k], tv[k], sv[k], cv[k]);
+    } else {
+        // rows shorter than a vector: walk the pairs
+        float fi = __ldg(f + i);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            phase_pair<V, TURNS>(fi, __ldg(t + j), sv[k], cv[k]);
+            if (++j == nt && k < 7) {      // next row (only when a pair of it follows)
+                j = 0;
+                fi = __ldg(f + ++i);
+            }
+        }
+    }
+}
+
 template <int V, bool INTER, bool TURNS>
 __global__ void __launch_bounds__(kPhaseThreads) phase_grid_flat(const float *__restrict__ f,
                                                                 const float *__restrict__ t, size_t nf,
@@ -232,58 +290,8 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_flat(const float *__
     if (tid < n - tail0) phase_one<V, INTER, TURNS>(f, t, nt, inv_nt, tail0 + tid, so, co, io);
     for (size_t v = tid; v < nvec; v += nthr) {
         const size_t e0 = head + 8 * v;
-        size_t i, j;
-        divmod_nt(e0, nt, inv_nt, i, j);
         float sv[8], cv[8];
-        if (j + 8 <= nt) {
-            // the common case: the eight pairs lie in one row -- one f and t[j .. j+7]: with t
-            // 16-B aligned, three aligned 128-bit loads from t[j - r] (r = j mod 4, uniform along
-            // a row) and a register selection; else eight loads at immediate offsets
-            const float fi = __ldg(f + i);
-            float tv[8];
-            const size_t r = j & 3;
-            if (t_al16 && j - r + 12 <= nt) {
-                const float4 *tq = reinterpret_cast<const float4 *>(t + (j - r));
-                const float4 q0 = __ldg(tq), q1 = __ldg(tq + 1), q2 = __ldg(tq + 2);
-                const float w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
-                switch (r) {
-                case 0: select_t<0>(w, tv); break;
-                case 1: select_t<1>(w, tv); break;
-                case 2: select_t<2>(w, tv); break;
-                default: select_t<3>(w, tv); break;
-                }
-            } else {
-                const float *tp = t + j;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) tv[k] = __ldg(tp + k);
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fi, tv[k], sv[k], cv[k]);
-        } else if (nt >= 8) {
-            // one row boundary inside the vector: rows i and i+1, branch-free per pair
-            const float f0 = __ldg(f + i), f1 = __ldg(f + i + 1);   // row i+1 exists: reached
-            const size_t kw = nt - j;                                // first pair of row i+1
-            float tv[8], fv[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const bool next = static_cast<size_t>(k) >= kw;
-                tv[k] = __ldg(t + (next ? k - kw : j + k));
-                fv[k] = next ? f1 : f0;
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) phase_pair<V, TURNS>(fv[k], tv[k], sv[k], cv[k]);
-        } else {
-            // rows shorter than a vector: walk the pairs
-            float fi = __ldg(f + i);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                phase_pair<V, TURNS>(fi, __ldg(t + j), sv[k], cv[k]);
-                if (++j == nt && k < 7) {      // next row (only when a pair of it follows)
-                    j = 0;
-                    fi = __ldg(f + ++i);
-                }
-            }
-        }
+        flat_pairs8<V, TURNS>(f, t, nt, inv_nt, t_al16, e0, sv, cv);
         if constexpr (INTER) {
             float cs[16];
 #pragma unroll
@@ -298,6 +306,83 @@ __global__ void __launch_bounds__(kPhaseThreads) phase_grid_flat(const float *__
             st8_stream(co + e0, cv);
         }
     }
+}
+
+// Unshared output alignment (split: cos[] off sin[]'s 32-B offset; interleaved: pairs only
+// 4-B aligned), any row length: the flat mapping in sin[]'s 32-B frame (interleaved: any
+// frame), sin[] stored as 256-bit vectors and the re-aligned stream -- cos[], or the pairs --
+// written as whole 32-B blocks built by warp shuffles (KB3c's store_realigned, kc = its float
+// offset at the vector elements), warp-uniform trips.  Before it these layouts ran one pair
+// per thread (0.4-3.7 TB/s).
+template <int V, bool INTER, bool TURNS>
+__global__ void __launch_bounds__(kPhaseThreads) phase_grid_flat_sh(const float *__restrict__ f,
+                                                                   const float *__restrict__ t, size_t nf,
+                                                                   size_t nt, float *so, float *co, float *io,
+                                                                   size_t head, size_t nvec, size_t n,
+                                                                   double inv_nt, int kc) {
+    const bool t_al16 = (reinterpret_cast<uintptr_t>(t) & 15) == 0;
+    const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t nthr = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t tail0 = head + 8 * nvec;
+    if (tid < head) phase_one<V, INTER, TURNS>(f, t, nt, inv_nt, tid, so, co, io);
+    if (tid < n - tail0) phase_one<V, INTER, TURNS>(f, t, nt, inv_nt, tail0 + tid, so, co, io);
+    const unsigned lane = threadIdx.x & 31u;
+    for (size_t w0 = tid - lane; w0 < nvec; w0 += nthr) {
+        const size_t v = w0 + lane;
+        const bool act = v < nvec;
+        const bool last = act && (lane == 31u || v + 1 >= nvec);
+        const size_t e0 = head + 8 * v;
+        float sv[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+        float cv[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+        if (act) flat_pairs8<V, TURNS>(f, t, nt, inv_nt, t_al16, e0, sv, cv);
+        if constexpr (INTER) {
+            float cs[16];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                cs[2 * k] = cv[k];
+                cs[2 * k + 1] = sv[k];
+            }
+            switch (kc) {
+            case 1: store_realigned<16, 1>(io, 2 * e0, cs, 1, lane, act, last); break;
+            case 3: store_realigned<16, 3>(io, 2 * e0, cs, 3, lane, act, last); break;
+            case 5: store_realigned<16, 5>(io, 2 * e0, cs, 5, lane, act, last); break;
+            default: store_realigned<16, 7>(io, 2 * e0, cs, 7, lane, act, last); break;
+            }
+        } else {
+            if (act) st8_stream(so + e0, sv);
+            switch (kc) {
+            case 1: store_realigned<8, 1>(co, e0, cv, 1, lane, act, last); break;
+            case 2: store_realigned<8, 2>(co, e0, cv, 2, lane, act, last); break;
+            case 3: store_realigned<8, 3>(co, e0, cv, 3, lane, act, last); break;
+            case 4: store_realigned<8, 4>(co, e0, cv, 4, lane, act, last); break;
+            case 5: store_realigned<8, 5>(co, e0, cv, 5, lane, act, last); break;
+            case 6: store_realigned<8, 6>(co, e0, cv, 6, lane, act, last); break;
+            default: store_realigned<8, 7>(co, e0, cv, 7, lane, act, last); break;
+            }
+        }
+    }
+}
+
+template <int V, bool INTER, bool TURNS>
+static const void *pick_flat_sh() {
+    return reinterpret_cast<const void *>(phase_grid_flat_sh<V, INTER, TURNS>);
+}
+
+cudaError_t launch_phase_flat_sh(int variant, bool inter, bool turns, const float *f, size_t nf, const float *t,
+                                 size_t nt, float *so, float *co, float *io, size_t head, size_t nvec,
+                                 unsigned grid, int kc, cudaStream_t stream) {
+    const void *fn;
+    if (variant == kNormalized)
+        fn = inter ? (turns ? pick_flat_sh<kNormalized, true, true>() : pick_flat_sh<kNormalized, true, false>())
+                   : (turns ? pick_flat_sh<kNormalized, false, true>() : pick_flat_sh<kNormalized, false, false>());
+    else
+        fn = inter ? (turns ? pick_flat_sh<kRenormalized, true, true>() : pick_flat_sh<kRenormalized, true, false>())
+                   : (turns ? pick_flat_sh<kRenormalized, false, true>()
+                            : pick_flat_sh<kRenormalized, false, false>());
+    size_t n = nf * nt;
+    double inv_nt = 1.0 / static_cast<double>(nt);
+    void *args[] = {&f, &t, &nf, &nt, &so, &co, &io, &head, &nvec, &n, &inv_nt, &kc};
+    return cudaLaunchKernel(fn, dim3(grid), dim3(kPhaseThreads), args, 0, stream);
 }
 
 // Row path (nt % 8 != 0 or t not 32-B aligned; nt >= kPhaseRowsMinNt): the vector kernel's

@@ -343,3 +343,49 @@ def test_every_row_kernel_on_special_values(units, variant):
         assert_parity(s.cpu().numpy(), c.cpu().numpy(), ws, wc, "split " + tag)
         iv = io.cpu().numpy()
         assert_parity(iv[1::2], iv[0::2], ws, wc, "inter " + tag)
+
+
+@pytest.mark.parametrize("units", [0, 1])
+def test_phase_grid_unshared_output_alignment(units):
+    """Split outputs with cos[] at every float offset from sin[]'s 32-B frame, and interleaved
+    pairs only 4-B aligned (odd float offsets), for short, ragged and long rows: the flat kernel
+    with the re-aligned stream written by warp shuffles; raw bits equal the oracle's grid,
+    sentinel guard zones around every output."""
+    SENT = 0x7F8ABCDE
+    G = 64
+    bad = []
+    for nt, nf in ((1, 3001), (2, 1503), (5, 701), (8, 389), (13, 257), (300, 11), (1001, 4)):
+        f = (inputs.generate(1, 0, nf) * np.float32(3.0)).astype(np.float32)
+        t = (inputs.generate(2, 7, nt) * np.float32(1e-3)).astype(np.float32)
+        fd, td = torch.from_numpy(f).cuda(), torch.from_numpy(t).cuda()
+        n = nf * nt
+        for variant in (0, 1):
+            ws, wc = oracle.phase_grid(f, t, units, variant)
+            ws_i = torch.from_numpy(ws.reshape(-1).view(np.int32)).cuda()
+            wc_i = torch.from_numpy(wc.reshape(-1).view(np.int32)).cuda()
+            bs = torch.empty(2 * G + n + 8, dtype=torch.int32, device="cuda")
+            bc = torch.empty_like(bs)
+            for os_ in (0, 3):
+                for oc in range(8):
+                    if (oc - os_) % 8 == 0:
+                        continue                    # shared alignment: the other kernels
+                    bs.fill_(SENT)
+                    bc.fill_(SENT)
+                    sp.phase_grid(fd, td, sin_out=bs[G + os_:G + os_ + n].view(torch.float32),
+                                  cos_out=bc[G + oc:G + oc + n].view(torch.float32), units=units, variant=variant)
+                    ok = (torch.equal(bs[G + os_:G + os_ + n], ws_i) and torch.equal(bc[G + oc:G + oc + n], wc_i) and
+                          bool((bs[:G + os_] == SENT).all()) and bool((bs[G + os_ + n:] == SENT).all()) and
+                          bool((bc[:G + oc] == SENT).all()) and bool((bc[G + oc + n:] == SENT).all()))
+                    if not ok:
+                        bad.append(("split", nt, variant, os_, oc))
+            bi = torch.empty(2 * G + 2 * n + 8, dtype=torch.int32, device="cuda")
+            for oi in (1, 3, 5, 7):
+                bi.fill_(SENT)
+                sp.phase_grid(fd, td, interleaved_out=bi[G + oi:G + oi + 2 * n].view(torch.float32), units=units,
+                              variant=variant)
+                got = bi[G + oi:G + oi + 2 * n]
+                ok = (torch.equal(got[1::2], ws_i) and torch.equal(got[0::2], wc_i) and
+                      bool((bi[:G + oi] == SENT).all()) and bool((bi[G + oi + 2 * n:] == SENT).all()))
+                if not ok:
+                    bad.append(("inter", nt, variant, oi))
+    assert not bad, f"{len(bad)} failing, first {bad[:8]}"

@@ -203,8 +203,11 @@ SINCOS_API sincos_status_t sincos_pairs_method(const float *theta_dev, float *si
  * outputs 32-B aligned at pair 0: the tiny-row path (8 whole rows per thread), and rows
  * of 4-14 pairs split or 2-15 interleaved with outputs 16-B aligned at pair 0: the staged
  * path (4 or 2 whole rows per thread, a warp's 128 or 64 rows staged in shared memory and
- * written back as contiguous 512-B stores); otherwise one pair per thread.  Returns as
- * sincos_pairs; nf*nt == 0 is a no-op.
+ * written back as contiguous 512-B stores); outputs that cannot take 256-bit stores at a
+ * common element (split: sin and cos at different offsets mod 32 B; interleaved: pairs
+ * only 4-B aligned): 8 consecutive pairs per thread in sin[]'s 32-B frame, the other
+ * stream re-aligned into whole 32-B blocks by warp shuffles.  Returns as sincos_pairs;
+ * nf*nt == 0 is a no-op.
  */
 typedef enum { SINCOS_RADIANS = 0, SINCOS_TURNS = 1 } sincos_units_t;
 SINCOS_API sincos_status_t sincos_phase_grid(const float *f_dev, size_t nf, const float *t_dev, size_t nt,
